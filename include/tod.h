@@ -1,0 +1,195 @@
+/*
+ * tod.h — C ABI of the B200-native exact kNN / LOF hot path of TOD
+ * (Zhao et al., "TOD: GPU-accelerated Outlier Detection via Tensor Operations",
+ * arXiv 2110.14007).  Implemented in paper_2110_14007_b200/csrc (CUDA sm_100a),
+ * built as paper_2110_14007_b200/libtod.so.
+ *
+ * Citations are PAPER.md line numbers (P:nnn) of /root/reference/PAPER.md and
+ * DESIGN.md section names.
+ *
+ * Problem statement: given X in R^{n x d} (rows = samples) without
+ * labels, output outlier scores O in R^n, higher = more outlying, "roughly
+ * deterministic and irrespective of the underlying system".  Here the scores
+ * are EXACT: neighbour indices equal the fp64 brute-force oracle bit for bit
+ * (DESIGN.md "Parity contract").
+ *
+ * Conventions for every entry point
+ * ---------------------------------
+ *  - Every call returns tod_status; TOD_OK == 0.  No C++ exception crosses
+ *    the ABI.  On error the contents of output buffers are unspecified, and
+ *    tod_last_message(ctx) returns a one-line human-readable reason.
+ *  - Pointers may be DEVICE memory (cudaMalloc / torch CUDA tensors on the
+ *    context's device) or HOST memory (pageable or pinned); the library
+ *    detects which with cudaPointerGetAttributes and stages host buffers
+ *    through its own device workspace (host<->device copies are inside the
+ *    call).  Device pointers must be on cfg->device.
+ *  - Layout: all matrices are row-major and contiguous.  X is fp32 n x d;
+ *    per-row outputs are [q_count] and per-neighbour outputs [q_count x k].
+ *  - Ownership: the caller owns X and every output buffer; X is read-only.
+ *    The library owns only its workspace (allocated lazily, grown on demand,
+ *    freed by tod_destroy).
+ *  - Synchronisation: the call enqueues work on the context stream and
+ *    synchronises that stream before returning, so results are valid on
+ *    return.  A context must not be used by two threads at once.
+ *  - Self-join semantics (P:270 kNN = cdist -> topk; DESIGN.md readings
+ *    A3/A4/A13): row i's neighbours are all j != i (self excluded by INDEX,
+ *    duplicates of i remain valid neighbours), ordered by the exact fp64
+ *    squared distance D64(i,j) (DESIGN.md "Oracle" O1), ties broken by the
+ *    smaller index, k smallest kept.
+ */
+#ifndef TOD_H_
+#define TOD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TOD_ABI_VERSION 1
+
+typedef enum {
+  TOD_OK = 0,
+  TOD_E_ARG = -1,          /* null/misaligned pointer, bad enum, inconsistent sizes */
+  TOD_E_NONFINITE = -2,    /* NaN or Inf in X (checked on device before any output) */
+  TOD_E_RANGE = -3,        /* k < 1, k > n-1 (k > n for queries), n > 2^31-1, d < 1 or d > 4096, q range outside [0,n) */
+  TOD_E_NOMEM = -4,        /* workspace allocation failed */
+  TOD_E_CUDA = -5,         /* a CUDA runtime error (message has cudaGetErrorString) */
+  TOD_E_UNSUPPORTED = -7,  /* valid request this build cannot serve (message says why) */
+  TOD_E_INTERNAL = -8      /* invariant violated inside the library (a bug) */
+} tod_status;
+
+/* Low-precision format of the first (tensor-core) pass — the "input
+ * quantization" step (i) of provable quantization. */
+typedef enum {
+  TOD_FMT_AUTO = 0,   /* planner's choice: FP32 SIMT for small d, else FP16 */
+  TOD_FMT_FP16 = 1,   /* tcgen05 kind::f16, power-of-two scaled fp16 operands, fp32 accumulate */
+  TOD_FMT_BF16 = 2,   /* tcgen05 kind::f16 with bf16 operands, fp32 accumulate */
+  TOD_FMT_FP32 = 3    /* CUDA-core fp32 difference-form tile path (no quantization) */
+} tod_format;
+
+/* Flags for tod_config.flags. */
+#define TOD_F_NO_CERTIFY   0x1u  /* testing: treat every row as uncertified -> fp64 brute-force tier */
+#define TOD_F_TIMING       0x2u  /* record per-phase CUDA-event times in tod_stats */
+
+typedef struct {
+  int32_t device;          /* CUDA device ordinal */
+  int32_t format;          /* tod_format */
+  int32_t kprime;          /* K' candidates kept per row by the low-precision pass; 0 = auto */
+  uint32_t flags;          /* TOD_F_* */
+  void* stream;            /* cudaStream_t to run on; NULL = the library's own non-blocking stream */
+  int32_t chunks;          /* reference chunks S per query tile (load balance); 0 = auto */
+  int32_t reserved;
+} tod_config;
+
+typedef struct {
+  int64_t rows;            /* query rows answered */
+  int64_t certified;       /* rows whose top-k was certified by the low-precision pass (P:342-343 step iii) */
+  int64_t fallback_rows;   /* rows recomputed by the fp64 brute-force tier ("recalculate on the subset") */
+  int32_t kprime;          /* K' used */
+  int32_t format;          /* tod_format actually used */
+  int32_t chunks;          /* S used */
+  int32_t dpad;            /* padded feature count of the tensor-core operands */
+  double scale;            /* power-of-two scale s applied before quantization (1 for FP32) */
+  double max_abs_err;      /* largest per-row pass-1 error term (E_i + quantization), scaled units */
+  float ms_stage, ms_prep, ms_main, ms_certify, ms_fallback, ms_lof, ms_total;  /* with TOD_F_TIMING */
+  int64_t kernel_launches; /* kernels launched by this call */
+} tod_stats;
+
+/* Per-neighbour and per-row outputs of the kNN functional operator (P:270,
+ * P:448-455) and the kNN outlier scores (Table 1; reading A1: both the
+ * k-th-neighbour distance and the mean kNN distance).  Every pointer is
+ * nullable; non-null ones are filled for the q_count query rows. */
+typedef struct {
+  int64_t* idx;         /* [q_count x k] neighbour indices, ascending (D64, index) */
+  float* dist;          /* [q_count x k] Euclidean distance fp32(sqrt_RN(D64)) */
+  double* dist64;       /* [q_count x k] sqrt_RN(D64) in fp64 (bit-identical to the oracle) */
+  float* score_kth;     /* [q_count] fp32(dist64[:, k-1]) */
+  float* score_mean;    /* [q_count] fp32((sum_m dist64[:, m], sequential in m) / k) */
+  double* kdist64;      /* [q_count] dist64[:, k-1] (k-distance; input of the LOF stage) */
+} tod_knn_out;
+
+typedef struct tod_ctx tod_ctx;
+
+/* Create a context bound to cfg->device.  cfg may be NULL (all defaults). */
+tod_status tod_create(const tod_config* cfg, tod_ctx** out);
+
+/* Free the context and its workspace.  NULL is a no-op. */
+tod_status tod_destroy(tod_ctx* ctx);
+
+/* Static string for a status code. */
+const char* tod_status_str(tod_status s);
+
+/* Reason for the last non-OK status returned on ctx ("" if none). */
+const char* tod_last_message(const tod_ctx* ctx);
+
+/* ABI version (TOD_ABI_VERSION) and build string (arch, git describe). */
+int32_t tod_abi_version(void);
+const char* tod_build_info(void);
+
+/*
+ * tod_knn — exact kNN self-join with fused distance + top-K' (P:452-459 operator
+ * fusion; Eq. 3 P:350-355 for the tensor-core distance form) and re-derived
+ * provable quantization.
+ *
+ *   X        fp32 [n x d] row-major, the whole dataset (references = all rows).
+ *   q_begin, q_count   query rows [q_begin, q_begin+q_count) of X answered by
+ *            this call (a process in a multi-GPU job passes its shard; a single
+ *            process passes 0, n).  0 <= q_begin, q_begin+q_count <= n.
+ *   k        1 <= k <= n-1.
+ *   out      per-row outputs for the q_count rows (see tod_knn_out), may be NULL
+ *            (then nothing is written — useful only for timing).
+ *   stats    nullable.
+ * Errors: TOD_E_RANGE, TOD_E_NONFINITE, TOD_E_ARG, TOD_E_NOMEM, TOD_E_CUDA,
+ * TOD_E_UNSUPPORTED (e.g. d > 4096).
+ */
+tod_status tod_knn(tod_ctx* ctx, const float* X, int64_t n, int32_t d, int32_t k,
+                   int64_t q_begin, int64_t q_count, const tod_knn_out* out,
+                   tod_stats* stats);
+
+/*
+ * tod_lof — Local Outlier Factor over the whole dataset in one process
+ * (Table 1 P:158, P:184 citing Breunig et al. 2000; DESIGN.md "Oracle" O4 and
+ * readings A5/A6):
+ *   kdist(o) = dist(o, o_k);  reach(p,o) = max(kdist(o), dist(p,o));
+ *   lrd(p) = k / sum_m reach(p, o_m)   (+inf when the sum is 0);
+ *   LOF(p) = (sum_m lrd(o_m)) / (k * lrd(p))   (1 when lrd(p) = +inf),
+ * fp64 throughout, rounded to fp32 on output.
+ *   lof, lrd  [n] fp32, nullable (lrd = +inf allowed).
+ *   knn_out   nullable; if given, also receives the kNN outputs for all n rows.
+ */
+tod_status tod_lof(tod_ctx* ctx, const float* X, int64_t n, int32_t d, int32_t k,
+                   float* lof, float* lrd, const tod_knn_out* knn_out, tod_stats* stats);
+
+/*
+ * Sharded LOF stages, for SPMD multi-GPU jobs (one process per GPU):
+ * each rank runs tod_knn on its rows (with dist64 and kdist64), all-gathers
+ * kdist64 to kdist64_all[n], calls tod_lof_lrd, all-gathers lrd64 to
+ * lrd64_all[n], then calls tod_lof_finish.  Bit-identical to tod_lof.
+ *
+ * tod_lof_lrd:    lrd64_out[r] = k / sum_m max(kdist64_all[idx[r,m]], dist64[r,m])
+ *                 for r < q_count (idx, dist64: [q_count x k] from tod_knn).
+ * tod_lof_finish: lof_out[r] = fp32(LOF) with lrd(p) = lrd64_all[q_begin+r] and
+ *                 neighbour lrds from lrd64_all; lrd_out[r] = fp32(lrd) (nullable).
+ */
+tod_status tod_lof_lrd(tod_ctx* ctx, int64_t n, int32_t k, int64_t q_count,
+                       const int64_t* idx, const double* dist64, const double* kdist64_all,
+                       double* lrd64_out);
+tod_status tod_lof_finish(tod_ctx* ctx, int64_t n, int32_t k, int64_t q_begin, int64_t q_count,
+                          const int64_t* idx, const double* lrd64_all, float* lof_out,
+                          float* lrd_out);
+
+/*
+ * tod_knn_query — test-set scoring (the detector's decision_function on new
+ * rows): kNN of each row of Q [nq x d] among the rows of
+ * X [n x d], nothing excluded, 1 <= k <= n.  Same ordering and outputs as
+ * tod_knn (indices refer to rows of X).
+ */
+tod_status tod_knn_query(tod_ctx* ctx, const float* Q, int64_t nq, const float* X, int64_t n,
+                         int32_t d, int32_t k, const tod_knn_out* out, tod_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOD_H_ */

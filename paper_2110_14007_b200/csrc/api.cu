@@ -1,0 +1,653 @@
+// api.cu — the C ABI of include/tod.h: argument validation, planning
+// (format, K', chunking), workspace management, host<->device staging, and
+// the launch sequence of the hot path:
+//   prep (K1) -> fused distance + top-K' (K2 tcgen05 | K2s SIMT) ->
+//   fp64 re-rank + certificate (K3) -> fp64 brute-force fallback (K4) ->
+//   [LOF stage (K5)].
+// Every step runs in this library's CUDA kernels; there is no CPU path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/tod.h"
+#include "internal.h"
+
+#ifndef TOD_BUILD_INFO
+#define TOD_BUILD_INFO "libtod sm_100a"
+#endif
+
+using namespace tod;
+
+namespace {
+
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct Workspace {
+  Buf bufs[32];
+  void release() {
+    for (auto& b : bufs) {
+      if (b.p) cudaFree(b.p);
+      b = Buf{};
+    }
+  }
+};
+
+enum BufId {
+  B_X = 0, B_Q, B_IMG_B, B_NRM_B, B_A2_B, B_E_B, B_IMG_A, B_NRM_A, B_A2_A, B_E_A, B_MU, B_PART,
+  B_G, B_CIDX, B_CV, B_FAIL, B_SMALL, B_IDX, B_DIST, B_DIST64, B_KTH, B_MEAN, B_KD64,
+  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_NBUF
+};
+
+}  // namespace
+
+struct tod_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  tod_config cfg{};
+  int num_sms = 148;
+  std::string msg;
+  Workspace ws;
+  cudaEvent_t ev[8] = {};
+};
+
+namespace {
+
+tod_status fail(tod_ctx* ctx, tod_status s, const char* fmt, ...) {
+  if (ctx) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    ctx->msg = buf;
+  }
+  return s;
+}
+
+#define TOD_CUDA(call)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? TOD_E_NOMEM : TOD_E_CUDA,       \
+                  "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+tod_status ensure(tod_ctx* ctx, int id, size_t bytes, void** out) {
+  Buf& b = ctx->ws.bufs[id];
+  if (bytes == 0) bytes = 16;
+  if (b.bytes < bytes) {
+    if (b.p) cudaFree(b.p);
+    b = Buf{};
+    cudaError_t e = cudaMalloc(&b.p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ctx, TOD_E_NOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    }
+    b.bytes = bytes;
+  }
+  *out = b.p;
+  return TOD_OK;
+}
+
+#define TOD_TRY(expr)                  \
+  do {                                 \
+    tod_status s_ = (expr);            \
+    if (s_ != TOD_OK) return s_;       \
+  } while (0)
+
+// Is p device memory of this context's device?  Host (pageable/pinned) -> false.
+bool is_device_ptr(const void* p, int device) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) && a.device == device;
+}
+
+int roundup(int x, int m) { return (x + m - 1) / m * m; }
+
+struct Plan {
+  int fmt;       // 1 fp16, 2 bf16, 3 fp32 simt
+  int kind;      // PASS_TC / PASS_SIMT
+  int dpad;
+  int kp;
+  int S;
+};
+
+tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k, Plan* p) {
+  int fmt = ctx->cfg.format;
+  if (fmt < 0 || fmt > 3) return fail(ctx, TOD_E_ARG, "bad format %d", fmt);
+  if (fmt == TOD_FMT_AUTO) fmt = d < 16 ? TOD_FMT_FP32 : TOD_FMT_FP16;
+  p->fmt = fmt;
+  p->kind = fmt == TOD_FMT_FP32 ? PASS_SIMT : PASS_TC;
+  if (p->kind == PASS_TC) {
+    if (d > 128)
+      return fail(ctx, TOD_E_UNSUPPORTED, "tensor-core pass supports d <= 128 in this build (d=%d)", d);
+    p->dpad = d <= 16 ? 16 : d <= 32 ? 32 : d <= 64 ? 64 : 128;
+  } else {
+    if (d > 64) return fail(ctx, TOD_E_UNSUPPORTED, "fp32 SIMT pass supports d <= 64 (d=%d)", d);
+    p->dpad = d;
+  }
+  int kp = ctx->cfg.kprime;
+  const int kmax_list = p->kind == PASS_TC ? 64 : 128;
+  if (kp <= 0) {
+    if (fmt == TOD_FMT_FP16) kp = roundup(std::max(2 * k, k + 28), 16);
+    else if (fmt == TOD_FMT_BF16) kp = roundup(std::max(6 * k, k + 40), 16);
+    else kp = roundup(std::max(k + 8, 16), 8);
+    kp = std::min(kp, kmax_list);
+  }
+  if (kp < k) kp = k;  // never fewer candidates than outputs
+  if (kp > kmax_list)
+    return fail(ctx, TOD_E_UNSUPPORTED, "K'=%d exceeds this pass's list capacity %d (k=%d)", kp,
+                kmax_list, k);
+  p->kp = kp;
+  int S = ctx->cfg.chunks;
+  if (S <= 0) {
+    if (p->kind == PASS_TC) {
+      const int64_t qtiles = (q_count + 127) / 128 + 1;
+      const int64_t btiles = (n_ref + 255) / 256;
+      double best = 1e30;
+      S = 1;
+      for (int s = 1; s <= 4; ++s) {
+        if (s * kp > 256 || btiles / s < 4) break;
+        const double items = (double)(qtiles * s);
+        const double waves = std::ceil(items / ctx->num_sms);
+        const double eff = items / (waves * ctx->num_sms);
+        const double cost = (1.0 / eff) * (1.0 + 0.02 * (s - 1));
+        if (cost < best - 1e-9) {
+          best = cost;
+          S = s;
+        }
+      }
+    } else {
+      const int64_t qtiles = (q_count + 127) / 128;
+      S = 1;
+      while (qtiles * S < 2 * ctx->num_sms && (S + 1) * kp <= 256 && n_ref / (S + 1) >= 256) ++S;
+    }
+  }
+  if (S < 1 || S * kp > 256) return fail(ctx, TOD_E_ARG, "bad chunk count S=%d (K'=%d)", S, kp);
+  p->S = S;
+  return TOD_OK;
+}
+
+struct Timer {
+  tod_ctx* ctx;
+  bool on;
+  int n = 0;
+  void mark() {
+    if (on && n < 8) cudaEventRecord(ctx->ev[n++], ctx->stream);
+  }
+  float between(int a, int b) {
+    if (!on || b >= n) return 0.f;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev[a], ctx->ev[b]);
+    return ms;
+  }
+};
+
+struct SmallDev {
+  PrepGlobals g;
+  int32_t fail_count;
+  int32_t pad;
+  double max_err;
+};
+
+// Core: all pointers device.  Q == nullptr => self-join over X, rows
+// [q_begin, q_begin+q_count).  Else queries Q[0..q_count) against X.
+tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, int64_t q_begin,
+                   int64_t q_count, int d, int k, KnnOutDev out, tod_stats* stats, Timer& tm,
+                   int* launches) {
+  const bool self = dQ == nullptr;
+  Plan plan;
+  TOD_TRY(make_plan(ctx, n, q_count, d, k, &plan));
+  cudaStream_t st = ctx->stream;
+
+  void* p;
+  TOD_TRY(ensure(ctx, B_SMALL, sizeof(SmallDev), &p));
+  SmallDev* small = static_cast<SmallDev*>(p);
+  TOD_CUDA(cudaMemsetAsync(small, 0, sizeof(SmallDev), st));
+  PrepGlobals* g = &small->g;
+
+  Cands cands;
+  cands.kp = plan.kp;
+  cands.S = plan.S;
+  TOD_TRY(ensure(ctx, B_CIDX, (size_t)std::max<int64_t>(q_count, 1) * plan.S * plan.kp * 4, &p));
+  cands.idx = static_cast<int32_t*>(p);
+  TOD_TRY(ensure(ctx, B_CV, (size_t)std::max<int64_t>(q_count, 1) * plan.S * 4, &p));
+  cands.v = static_cast<float*>(p);
+  TOD_TRY(ensure(ctx, B_FAIL, (size_t)std::max<int64_t>(q_count, 1) * 4, &p));
+  int32_t* fail_rows = static_cast<int32_t*>(p);
+
+  CertParams cp{};
+  cp.kind = plan.kind;
+  cp.d = d;
+  cp.dpad = plan.dpad;
+  cp.s = 1.0;
+  cp.g = g;
+  cp.force_fail = (ctx->cfg.flags & TOD_F_NO_CERTIFY) ? 1 : 0;
+
+  tm.mark();  // 1: prep start
+  if (plan.kind == PASS_TC) {
+    const int64_t n_pad = (n + 255) / 256 * 256;
+    const int64_t qn_pad = self ? n_pad : (q_count + 255) / 256 * 256;
+    const int rb = std::min(128, plan.dpad * 2);
+    auto make_img = [&](int id_img, int id_nrm, int id_a2, int id_e, int64_t rows,
+                        int64_t rows_pad, Image* img) -> tod_status {
+      void* q;
+      img->n = rows;
+      img->n_pad = rows_pad;
+      img->dpad = plan.dpad;
+      img->rb = rb;
+      img->nkb = plan.dpad * 2 / rb;
+      img->layout = rb == 128 ? 2 : (rb == 64 ? 4 : 6);
+      TOD_TRY(ensure(ctx, id_img, (size_t)rows_pad * plan.dpad * 2, &q));
+      img->data = static_cast<uint16_t*>(q);
+      TOD_TRY(ensure(ctx, id_nrm, (size_t)rows_pad * 4, &q));
+      img->nrm32 = static_cast<float*>(q);
+      TOD_TRY(ensure(ctx, id_a2, (size_t)std::max<int64_t>(rows, 1) * 8, &q));
+      img->a2 = static_cast<double*>(q);
+      TOD_TRY(ensure(ctx, id_e, (size_t)std::max<int64_t>(rows, 1) * 8, &q));
+      img->e = static_cast<double*>(q);
+      return TOD_OK;
+    };
+    Image B, A;
+    TOD_TRY(make_img(B_IMG_B, B_NRM_B, B_A2_B, B_E_B, n, n_pad, &B));
+    if (self) {
+      A = B;
+    } else {
+      TOD_TRY(make_img(B_IMG_A, B_NRM_A, B_A2_A, B_E_A, q_count, qn_pad, &A));
+    }
+    const int stat_blocks = (int)((n + 1023) / 1024);
+    TOD_TRY(ensure(ctx, B_MU, (size_t)d * 8, &p));
+    double* mu = static_cast<double*>(p);
+    TOD_TRY(ensure(ctx, B_PART, (size_t)stat_blocks * d * 8, &p));
+    double* part = static_cast<double*>(p);
+    TOD_CUDA(launch_prep_stats(dX, n, d, mu, part, stat_blocks, g, st, launches));
+    TOD_CUDA(launch_prep_absmax(dX, n, d, mu, g, st, launches));
+    if (!self) {
+      TOD_CUDA(launch_finite_check(dQ, q_count, d, g, st, launches));
+      TOD_CUDA(launch_prep_absmax(dQ, q_count, d, mu, g, st, launches));
+    }
+    TOD_CUDA(launch_prep_scale(g, plan.fmt, st, launches));
+    TOD_CUDA(launch_prep_quant(dX, n, d, mu, g, g, plan.fmt, B, true, st, launches));
+    if (!self) TOD_CUDA(launch_prep_quant(dQ, q_count, d, mu, g, g, plan.fmt, A, false, st, launches));
+    cp.qa2 = self ? B.a2 + q_begin : A.a2;
+    cp.qe = self ? B.e + q_begin : A.e;
+    tm.mark();  // 2: main start
+    TOD_CUDA(launch_knn_tc(A, B, self ? q_begin : 0, q_count, self, plan.fmt, cands, ctx->num_sms,
+                           st, launches));
+  } else {
+    TOD_CUDA(launch_finite_check(dX, n, d, g, st, launches));
+    if (!self) TOD_CUDA(launch_finite_check(dQ, q_count, d, g, st, launches));
+    tm.mark();  // 2
+    TOD_CUDA(launch_knn_simt(dQ, q_begin, q_count, dX, n, d, self, cands, st, launches));
+  }
+  tm.mark();  // 3: certify start
+  TOD_CUDA(launch_rerank(dQ, q_begin, q_count, dX, n, d, k, self, cands, cp, out, fail_rows,
+                         &small->fail_count, &small->max_err, st, launches));
+  tm.mark();  // 4: fallback start
+  SmallDev h{};
+  TOD_CUDA(cudaMemcpyAsync(&h, small, sizeof(SmallDev), cudaMemcpyDeviceToHost, st));
+  TOD_CUDA(cudaStreamSynchronize(st));
+  if (h.g.nonfinite) return fail(ctx, TOD_E_NONFINITE, "X (or Q) contains NaN or Inf");
+  if (h.fail_count > 0)
+    TOD_CUDA(launch_fallback(dQ, q_begin, dX, n, d, k, self, fail_rows, h.fail_count, out, st,
+                             launches));
+  tm.mark();  // 5: end of kNN
+  if (stats) {
+    stats->rows = q_count;
+    stats->certified = q_count - h.fail_count;
+    stats->fallback_rows = h.fail_count;
+    stats->kprime = plan.kp;
+    stats->format = plan.fmt;
+    stats->chunks = plan.S;
+    stats->dpad = plan.dpad;
+    stats->scale = plan.kind == PASS_TC ? h.g.s : 1.0;
+    stats->max_abs_err = h.max_err;
+  }
+  return TOD_OK;
+}
+
+// Resolve a caller buffer: device pointer as is, host pointer -> staging buffer.
+template <class T>
+tod_status dev_view(tod_ctx* ctx, T* user, size_t count, int id, T** dev, bool* staged) {
+  *staged = false;
+  if (!user) {
+    *dev = nullptr;
+    return TOD_OK;
+  }
+  if (is_device_ptr(user, ctx->device)) {
+    *dev = user;
+    return TOD_OK;
+  }
+  void* p;
+  TOD_TRY(ensure(ctx, id, count * sizeof(T), &p));
+  *dev = static_cast<T*>(p);
+  *staged = true;
+  return TOD_OK;
+}
+
+tod_status validate_common(tod_ctx* ctx, int64_t n, int32_t d, int32_t k) {
+  if (!ctx) return TOD_E_ARG;
+  if (n < 1 || n > INT32_MAX) return fail(ctx, TOD_E_RANGE, "n=%lld outside [1, 2^31-1]", (long long)n);
+  if (d < 1 || d > 4096) return fail(ctx, TOD_E_RANGE, "d=%d outside [1, 4096]", d);
+  if (k < 1) return fail(ctx, TOD_E_RANGE, "k=%d < 1", k);
+  return TOD_OK;
+}
+
+struct OutStage {
+  KnnOutDev dev{};
+  bool st_idx = false, st_dist = false, st_d64 = false, st_kth = false, st_mean = false,
+       st_kd = false;
+};
+
+tod_status stage_outputs(tod_ctx* ctx, const tod_knn_out* o, int64_t q, int k, OutStage* s) {
+  tod_knn_out z{};
+  if (!o) o = &z;
+  const size_t qk = (size_t)q * k;
+  TOD_TRY(dev_view(ctx, o->idx, qk, B_IDX, &s->dev.idx, &s->st_idx));
+  TOD_TRY(dev_view(ctx, o->dist, qk, B_DIST, &s->dev.dist, &s->st_dist));
+  TOD_TRY(dev_view(ctx, o->dist64, qk, B_DIST64, &s->dev.dist64, &s->st_d64));
+  TOD_TRY(dev_view(ctx, o->score_kth, (size_t)q, B_KTH, &s->dev.score_kth, &s->st_kth));
+  TOD_TRY(dev_view(ctx, o->score_mean, (size_t)q, B_MEAN, &s->dev.score_mean, &s->st_mean));
+  TOD_TRY(dev_view(ctx, o->kdist64, (size_t)q, B_KD64, &s->dev.kdist64, &s->st_kd));
+  return TOD_OK;
+}
+
+tod_status unstage_outputs(tod_ctx* ctx, const tod_knn_out* o, int64_t q, int k, const OutStage& s) {
+  if (!o) return TOD_OK;
+  const size_t qk = (size_t)q * k;
+  cudaStream_t st = ctx->stream;
+  if (s.st_idx) TOD_CUDA(cudaMemcpyAsync(o->idx, s.dev.idx, qk * 8, cudaMemcpyDeviceToHost, st));
+  if (s.st_dist) TOD_CUDA(cudaMemcpyAsync(o->dist, s.dev.dist, qk * 4, cudaMemcpyDeviceToHost, st));
+  if (s.st_d64) TOD_CUDA(cudaMemcpyAsync(o->dist64, s.dev.dist64, qk * 8, cudaMemcpyDeviceToHost, st));
+  if (s.st_kth) TOD_CUDA(cudaMemcpyAsync(o->score_kth, s.dev.score_kth, q * 4, cudaMemcpyDeviceToHost, st));
+  if (s.st_mean) TOD_CUDA(cudaMemcpyAsync(o->score_mean, s.dev.score_mean, q * 4, cudaMemcpyDeviceToHost, st));
+  if (s.st_kd) TOD_CUDA(cudaMemcpyAsync(o->kdist64, s.dev.kdist64, q * 8, cudaMemcpyDeviceToHost, st));
+  return TOD_OK;
+}
+
+tod_status stage_input(tod_ctx* ctx, const float* user, size_t count, int id, const float** dev) {
+  if (!user) return fail(ctx, TOD_E_ARG, "null input pointer");
+  if (is_device_ptr(user, ctx->device)) {
+    *dev = user;
+    return TOD_OK;
+  }
+  void* p;
+  TOD_TRY(ensure(ctx, id, count * 4, &p));
+  TOD_CUDA(cudaMemcpyAsync(p, user, count * 4, cudaMemcpyHostToDevice, ctx->stream));
+  *dev = static_cast<const float*>(p);
+  return TOD_OK;
+}
+
+void finish_stats(tod_stats* stats, Timer& tm, int launches, int i_lof_end) {
+  if (!stats) return;
+  stats->kernel_launches = launches;
+  stats->ms_stage = tm.between(0, 1);
+  stats->ms_prep = tm.between(1, 2);
+  stats->ms_main = tm.between(2, 3);
+  stats->ms_certify = tm.between(3, 4);
+  stats->ms_fallback = tm.between(4, 5);
+  stats->ms_lof = i_lof_end > 0 ? tm.between(5, i_lof_end) : 0.f;
+  stats->ms_total = tm.between(0, tm.n - 1);
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t tod_abi_version(void) { return TOD_ABI_VERSION; }
+const char* tod_build_info(void) { return TOD_BUILD_INFO; }
+
+const char* tod_status_str(tod_status s) {
+  switch (s) {
+    case TOD_OK: return "TOD_OK";
+    case TOD_E_ARG: return "TOD_E_ARG: invalid argument";
+    case TOD_E_NONFINITE: return "TOD_E_NONFINITE: NaN or Inf in input";
+    case TOD_E_RANGE: return "TOD_E_RANGE: size or k out of range";
+    case TOD_E_NOMEM: return "TOD_E_NOMEM: device allocation failed";
+    case TOD_E_CUDA: return "TOD_E_CUDA: CUDA runtime error";
+    case TOD_E_UNSUPPORTED: return "TOD_E_UNSUPPORTED: not supported by this build";
+    case TOD_E_INTERNAL: return "TOD_E_INTERNAL: internal error";
+  }
+  return "unknown tod_status";
+}
+
+const char* tod_last_message(const tod_ctx* ctx) { return ctx ? ctx->msg.c_str() : ""; }
+
+tod_status tod_create(const tod_config* cfg, tod_ctx** out) {
+  if (!out) return TOD_E_ARG;
+  *out = nullptr;
+  tod_ctx* ctx = new (std::nothrow) tod_ctx();
+  if (!ctx) return TOD_E_NOMEM;
+  if (cfg) ctx->cfg = *cfg;
+  ctx->device = ctx->cfg.device;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0 || ctx->device < 0 || ctx->device >= ndev) {
+    cudaGetLastError();
+    delete ctx;
+    return TOD_E_CUDA;
+  }
+  cudaDeviceProp prop;
+  if (cudaSetDevice(ctx->device) != cudaSuccess ||
+      cudaGetDeviceProperties(&prop, ctx->device) != cudaSuccess) {
+    delete ctx;
+    return TOD_E_CUDA;
+  }
+  if (prop.major != 10 || prop.minor != 0) {
+    delete ctx;
+    return TOD_E_UNSUPPORTED;  // built for sm_100a only
+  }
+  ctx->num_sms = prop.multiProcessorCount;
+  if (ctx->cfg.stream) {
+    ctx->stream = static_cast<cudaStream_t>(ctx->cfg.stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete ctx;
+      return TOD_E_CUDA;
+    }
+    ctx->own_stream = true;
+  }
+  for (auto& ev : ctx->ev) cudaEventCreate(&ev);
+  *out = ctx;
+  return TOD_OK;
+}
+
+tod_status tod_destroy(tod_ctx* ctx) {
+  if (!ctx) return TOD_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  ctx->ws.release();
+  for (auto& ev : ctx->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return TOD_OK;
+}
+
+tod_status tod_knn(tod_ctx* ctx, const float* X, int64_t n, int32_t d, int32_t k, int64_t q_begin,
+                   int64_t q_count, const tod_knn_out* out, tod_stats* stats) {
+  TOD_TRY(validate_common(ctx, n, d, k));
+  if (n < 2 || k > n - 1) return fail(ctx, TOD_E_RANGE, "need 1 <= k <= n-1 (n=%lld k=%d)", (long long)n, k);
+  if (q_begin < 0 || q_count < 0 || q_begin + q_count > n)
+    return fail(ctx, TOD_E_RANGE, "query rows [%lld, %lld) outside [0, %lld)", (long long)q_begin,
+                (long long)(q_begin + q_count), (long long)n);
+  TOD_CUDA(cudaSetDevice(ctx->device));
+  if (stats) memset(stats, 0, sizeof *stats);
+  Timer tm{ctx, (ctx->cfg.flags & TOD_F_TIMING) != 0};
+  int launches = 0;
+  tm.mark();  // 0
+  const float* dX;
+  TOD_TRY(stage_input(ctx, X, (size_t)n * d, B_X, &dX));
+  OutStage os;
+  TOD_TRY(stage_outputs(ctx, out, q_count, k, &os));
+  if (q_count > 0) TOD_TRY(run_knn(ctx, dX, n, nullptr, q_begin, q_count, d, k, os.dev, stats, tm, &launches));
+  TOD_TRY(unstage_outputs(ctx, out, q_count, k, os));
+  tm.mark();
+  TOD_CUDA(cudaStreamSynchronize(ctx->stream));
+  finish_stats(stats, tm, launches, 0);
+  ctx->msg.clear();
+  return TOD_OK;
+}
+
+tod_status tod_knn_query(tod_ctx* ctx, const float* Q, int64_t nq, const float* X, int64_t n,
+                         int32_t d, int32_t k, const tod_knn_out* out, tod_stats* stats) {
+  TOD_TRY(validate_common(ctx, n, d, k));
+  if (k > n) return fail(ctx, TOD_E_RANGE, "need 1 <= k <= n (n=%lld k=%d)", (long long)n, k);
+  if (nq < 0 || nq > INT32_MAX) return fail(ctx, TOD_E_RANGE, "nq=%lld out of range", (long long)nq);
+  TOD_CUDA(cudaSetDevice(ctx->device));
+  if (stats) memset(stats, 0, sizeof *stats);
+  Timer tm{ctx, (ctx->cfg.flags & TOD_F_TIMING) != 0};
+  int launches = 0;
+  tm.mark();
+  const float *dX, *dQ;
+  TOD_TRY(stage_input(ctx, X, (size_t)n * d, B_X, &dX));
+  if (nq > 0) TOD_TRY(stage_input(ctx, Q, (size_t)nq * d, B_Q, &dQ));
+  OutStage os;
+  TOD_TRY(stage_outputs(ctx, out, nq, k, &os));
+  if (nq > 0) TOD_TRY(run_knn(ctx, dX, n, dQ, 0, nq, d, k, os.dev, stats, tm, &launches));
+  TOD_TRY(unstage_outputs(ctx, out, nq, k, os));
+  tm.mark();
+  TOD_CUDA(cudaStreamSynchronize(ctx->stream));
+  finish_stats(stats, tm, launches, 0);
+  ctx->msg.clear();
+  return TOD_OK;
+}
+
+tod_status tod_lof(tod_ctx* ctx, const float* X, int64_t n, int32_t d, int32_t k, float* lof,
+                   float* lrd, const tod_knn_out* knn_out, tod_stats* stats) {
+  TOD_TRY(validate_common(ctx, n, d, k));
+  if (n < 2 || k > n - 1) return fail(ctx, TOD_E_RANGE, "need 1 <= k <= n-1 (n=%lld k=%d)", (long long)n, k);
+  TOD_CUDA(cudaSetDevice(ctx->device));
+  if (stats) memset(stats, 0, sizeof *stats);
+  Timer tm{ctx, (ctx->cfg.flags & TOD_F_TIMING) != 0};
+  int launches = 0;
+  tm.mark();
+  const float* dX;
+  TOD_TRY(stage_input(ctx, X, (size_t)n * d, B_X, &dX));
+  OutStage os;
+  TOD_TRY(stage_outputs(ctx, knn_out, n, k, &os));
+  // LOF needs idx, dist64 and kdist64 on the device even if the caller did not ask.
+  void* p;
+  if (!os.dev.idx) {
+    TOD_TRY(ensure(ctx, B_IDX, (size_t)n * k * 8, &p));
+    os.dev.idx = static_cast<int64_t*>(p);
+  }
+  if (!os.dev.dist64) {
+    TOD_TRY(ensure(ctx, B_DIST64, (size_t)n * k * 8, &p));
+    os.dev.dist64 = static_cast<double*>(p);
+  }
+  if (!os.dev.kdist64) {
+    TOD_TRY(ensure(ctx, B_KD64, (size_t)n * 8, &p));
+    os.dev.kdist64 = static_cast<double*>(p);
+  }
+  TOD_TRY(run_knn(ctx, dX, n, nullptr, 0, n, d, k, os.dev, stats, tm, &launches));
+  TOD_TRY(ensure(ctx, B_LRD64, (size_t)n * 8, &p));
+  double* lrd64 = static_cast<double*>(p);
+  float *dlof, *dlrd;
+  bool st_lof, st_lrd;
+  TOD_TRY(dev_view(ctx, lof, (size_t)n, B_LOF, &dlof, &st_lof));
+  TOD_TRY(dev_view(ctx, lrd, (size_t)n, B_LRD32, &dlrd, &st_lrd));
+  TOD_CUDA(launch_lof_lrd(n, k, os.dev.idx, os.dev.dist64, os.dev.kdist64, lrd64, ctx->stream, &launches));
+  TOD_CUDA(launch_lof_finish(0, n, k, os.dev.idx, lrd64, dlof, dlrd, ctx->stream, &launches));
+  tm.mark();  // 6: LOF end
+  TOD_TRY(unstage_outputs(ctx, knn_out, n, k, os));
+  if (st_lof) TOD_CUDA(cudaMemcpyAsync(lof, dlof, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  if (st_lrd) TOD_CUDA(cudaMemcpyAsync(lrd, dlrd, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  tm.mark();
+  TOD_CUDA(cudaStreamSynchronize(ctx->stream));
+  finish_stats(stats, tm, launches, 6);
+  ctx->msg.clear();
+  return TOD_OK;
+}
+
+tod_status tod_lof_lrd(tod_ctx* ctx, int64_t n, int32_t k, int64_t q_count, const int64_t* idx,
+                       const double* dist64, const double* kdist64_all, double* lrd64_out) {
+  if (!ctx) return TOD_E_ARG;
+  if (n < 2 || k < 1 || k > n - 1 || q_count < 0 || q_count > n)
+    return fail(ctx, TOD_E_RANGE, "bad sizes n=%lld k=%d q=%lld", (long long)n, k, (long long)q_count);
+  if (!idx || !dist64 || !kdist64_all || !lrd64_out) return fail(ctx, TOD_E_ARG, "null pointer");
+  TOD_CUDA(cudaSetDevice(ctx->device));
+  int launches = 0;
+  const size_t qk = (size_t)q_count * k;
+  // stage (host -> device) as needed
+  const int64_t* di = idx;
+  const double *dd = dist64, *dk = kdist64_all;
+  double* dl = lrd64_out;
+  void* p;
+  cudaStream_t st = ctx->stream;
+  if (!is_device_ptr(idx, ctx->device)) {
+    TOD_TRY(ensure(ctx, B_IDX, qk * 8, &p));
+    TOD_CUDA(cudaMemcpyAsync(p, idx, qk * 8, cudaMemcpyHostToDevice, st));
+    di = static_cast<int64_t*>(p);
+  }
+  if (!is_device_ptr(dist64, ctx->device)) {
+    TOD_TRY(ensure(ctx, B_DIST64, qk * 8, &p));
+    TOD_CUDA(cudaMemcpyAsync(p, dist64, qk * 8, cudaMemcpyHostToDevice, st));
+    dd = static_cast<double*>(p);
+  }
+  if (!is_device_ptr(kdist64_all, ctx->device)) {
+    TOD_TRY(ensure(ctx, B_KDALL, (size_t)n * 8, &p));
+    TOD_CUDA(cudaMemcpyAsync(p, kdist64_all, n * 8, cudaMemcpyHostToDevice, st));
+    dk = static_cast<double*>(p);
+  }
+  const bool st_out = !is_device_ptr(lrd64_out, ctx->device);
+  if (st_out) {
+    TOD_TRY(ensure(ctx, B_LRD64, (size_t)std::max<int64_t>(q_count, 1) * 8, &p));
+    dl = static_cast<double*>(p);
+  }
+  TOD_CUDA(launch_lof_lrd(q_count, k, di, dd, dk, dl, st, &launches));
+  if (st_out) TOD_CUDA(cudaMemcpyAsync(lrd64_out, dl, q_count * 8, cudaMemcpyDeviceToHost, st));
+  TOD_CUDA(cudaStreamSynchronize(st));
+  return TOD_OK;
+}
+
+tod_status tod_lof_finish(tod_ctx* ctx, int64_t n, int32_t k, int64_t q_begin, int64_t q_count,
+                          const int64_t* idx, const double* lrd64_all, float* lof_out,
+                          float* lrd_out) {
+  if (!ctx) return TOD_E_ARG;
+  if (n < 2 || k < 1 || k > n - 1 || q_begin < 0 || q_count < 0 || q_begin + q_count > n)
+    return fail(ctx, TOD_E_RANGE, "bad sizes");
+  if (!idx || !lrd64_all) return fail(ctx, TOD_E_ARG, "null pointer");
+  TOD_CUDA(cudaSetDevice(ctx->device));
+  int launches = 0;
+  const size_t qk = (size_t)q_count * k;
+  cudaStream_t st = ctx->stream;
+  void* p;
+  const int64_t* di = idx;
+  const double* dl = lrd64_all;
+  if (!is_device_ptr(idx, ctx->device)) {
+    TOD_TRY(ensure(ctx, B_IDX, qk * 8, &p));
+    TOD_CUDA(cudaMemcpyAsync(p, idx, qk * 8, cudaMemcpyHostToDevice, st));
+    di = static_cast<int64_t*>(p);
+  }
+  if (!is_device_ptr(lrd64_all, ctx->device)) {
+    TOD_TRY(ensure(ctx, B_KDALL, (size_t)n * 8, &p));
+    TOD_CUDA(cudaMemcpyAsync(p, lrd64_all, n * 8, cudaMemcpyHostToDevice, st));
+    dl = static_cast<double*>(p);
+  }
+  float *dlof, *dlrd;
+  bool st_lof, st_lrd;
+  TOD_TRY(dev_view(ctx, lof_out, (size_t)q_count, B_LOF, &dlof, &st_lof));
+  TOD_TRY(dev_view(ctx, lrd_out, (size_t)q_count, B_LRD32, &dlrd, &st_lrd));
+  TOD_CUDA(launch_lof_finish(q_begin, q_count, k, di, dl, dlof, dlrd, st, &launches));
+  if (st_lof) TOD_CUDA(cudaMemcpyAsync(lof_out, dlof, q_count * 4, cudaMemcpyDeviceToHost, st));
+  if (st_lrd) TOD_CUDA(cudaMemcpyAsync(lrd_out, dlrd, q_count * 4, cudaMemcpyDeviceToHost, st));
+  TOD_CUDA(cudaStreamSynchronize(st));
+  return TOD_OK;
+}
+
+}  // extern "C"

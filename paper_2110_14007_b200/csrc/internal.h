@@ -1,0 +1,102 @@
+// internal.h — shared structs and kernel launchers of libtod (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace tod {
+
+// Quantized operand image of a row set in HBM ("input quantization", step (i)
+// of provable quantization).  16-bit elements, laid out exactly as
+// the tcgen05 K-major swizzled shared-memory tiles, so a contiguous bulk copy
+// of rows [r0, r0+R) of one K-region lands as a ready UMMA operand:
+//   nkb regions (one per 64-element K block, or 1 when dpad < 64),
+//   region kb = n_pad rows x rb bytes, rb = min(128, 2*dpad), row r at r*rb,
+//   16-byte chunks XOR-swizzled within each 8-row atom (Swizzle<B,4,3>).
+struct Image {
+  uint16_t* data = nullptr;
+  float* nrm32 = nullptr;   // [n_pad] fp32(||xhat_r||^2), +inf for padding rows
+  double* a2 = nullptr;     // [n]     ||xhat_r||^2 in fp64
+  double* e = nullptr;      // [n]     upper bound on ||xhat_r - s(x_r - mu)||
+  int64_t n = 0, n_pad = 0;
+  int dpad = 0, rb = 0, nkb = 0, layout = 0;  // layout: 2=SW128, 4=SW64, 6=SW32
+  __host__ __device__ size_t region_bytes() const { return (size_t)n_pad * rb; }
+};
+
+// Global prep scalars, device resident.
+struct PrepGlobals {
+  double s;          // power-of-two scale
+  double amax2;      // max_j ||xhat_j||^2 over references
+  double emax;       // max_j e_j over references
+  unsigned long long absmax_bits;  // max |x - mu| (fp64 bits) over queries and references
+  int nonfinite;     // any NaN/Inf seen in X (or Q)
+  int pad;
+};
+
+// Candidate lists written by the pass-1 kernels: per (query row, chunk) K'
+// column indices (-1 = empty) and the threshold v (keys of non-kept >= v).
+struct Cands {
+  int32_t* idx = nullptr;   // [q_count][S][kp]
+  float* v = nullptr;       // [q_count][S]
+  int kp = 0, S = 0;
+};
+
+enum PassKind : int { PASS_TC = 0, PASS_SIMT = 1 };
+
+// ---- prep.cu
+cudaError_t launch_prep_stats(const float* X, int64_t n, int d, double* mu, double* partial,
+                              int partial_blocks, PrepGlobals* g, cudaStream_t st, int* launches);
+cudaError_t launch_prep_absmax(const float* X, int64_t n, int d, const double* mu, PrepGlobals* g,
+                               cudaStream_t st, int* launches);
+cudaError_t launch_prep_scale(PrepGlobals* g, int fmt, cudaStream_t st, int* launches);
+cudaError_t launch_prep_quant(const float* X, int64_t n, int d, const double* mu,
+                              const PrepGlobals* g, PrepGlobals* g_out_max, int fmt, Image img,
+                              bool update_max, cudaStream_t st, int* launches);
+cudaError_t launch_finite_check(const float* X, int64_t n, int d, PrepGlobals* g, cudaStream_t st,
+                                int* launches);
+
+// ---- knn_tc.cu  (tcgen05 fused distance + top-K')
+int tc_smem_bytes(int dpad, int kp);
+cudaError_t launch_knn_tc(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
+                          bool self_join, int fmt, Cands c, int num_sms, cudaStream_t st,
+                          int* launches);
+
+// ---- knn_simt.cu  (CUDA-core fp32 difference-form fused distance + top-K')
+cudaError_t launch_knn_simt(const float* Q, int64_t q_begin, int64_t q_count, const float* X,
+                            int64_t n, int d, bool self_join, Cands c, cudaStream_t st,
+                            int* launches);
+
+// ---- rerank.cu  (fp64 re-rank + certificate, fp64 brute-force fallback)
+struct CertParams {
+  int kind;        // PassKind
+  int d, dpad;
+  double s;        // scale (tensor path)
+  const PrepGlobals* g;  // device: amax2, emax (tensor path)
+  const double* qa2;     // query ||xhat||^2 (tensor path)
+  const double* qe;      // query residual bound (tensor path)
+  int force_fail;        // TOD_F_NO_CERTIFY
+};
+struct KnnOutDev {
+  int64_t* idx;
+  float* dist;
+  double* dist64;
+  float* score_kth;
+  float* score_mean;
+  double* kdist64;
+};
+cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, const float* X,
+                          int64_t n, int d, int k, bool self_join, Cands c, CertParams cp,
+                          KnnOutDev out, int32_t* fail_rows, int32_t* fail_count,
+                          double* max_err, cudaStream_t st, int* launches);
+cudaError_t launch_fallback(const float* Q, int64_t q_begin, const float* X, int64_t n, int d,
+                            int k, bool self_join, const int32_t* fail_rows, int nfail,
+                            KnnOutDev out, cudaStream_t st, int* launches);
+
+// ---- lof.cu
+cudaError_t launch_lof_lrd(int64_t q_count, int k, const int64_t* idx, const double* dist64,
+                           const double* kdist64_all, double* lrd64_out, cudaStream_t st,
+                           int* launches);
+cudaError_t launch_lof_finish(int64_t q_begin, int64_t q_count, int k, const int64_t* idx,
+                              const double* lrd64_all, float* lof_out, float* lrd_out,
+                              cudaStream_t st, int* launches);
+
+}  // namespace tod

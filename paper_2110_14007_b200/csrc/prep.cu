@@ -1,0 +1,234 @@
+// prep.cu — K1: input quantization for the tensor-core pass (provable
+// quantization step (i), §5.2), re-derived (DESIGN.md
+// "Prep"): global translation mu (column mean, fp64, deterministic order),
+// power-of-two scale s, x' = s*(x - mu), xhat = RN16(x'), written straight into
+// the swizzled UMMA operand image; per-row fp64 ||xhat||^2, fp32 norm for the
+// epilogue, and a rigorous per-row residual bound e_i >= ||xhat_i - x'_i||.
+// The paper's per-column min-max scaling to [0,1] is NOT applied: it
+// changes Euclidean neighbourhoods (reading A11).  All kernels are HBM-bound.
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#include <math_constants.h>
+
+#include "internal.h"
+
+namespace tod {
+
+namespace {
+
+constexpr int kStatThreads = 256;
+constexpr int kRowsPerStatBlock = 1024;
+
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long* addr, double v) {
+  // Non-negative doubles order like their bit patterns.
+  atomicMax(addr, (unsigned long long)__double_as_longlong(v));
+}
+
+// Column partial sums over a fixed row range per block (fixed order => the
+// result depends only on (X, n, d), never on timing).  Also the finite check.
+__global__ void k_colsum_partial(const float* __restrict__ X, int64_t n, int d,
+                                 double* __restrict__ partial, PrepGlobals* g) {
+  __shared__ double red[kStatThreads];
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  const int t = threadIdx.x;
+  const int nphase = d <= kStatThreads ? kStatThreads / d : 1;
+  const int64_t r0 = (int64_t)blockIdx.x * kRowsPerStatBlock;
+  const int64_t r1 = min(n, r0 + kRowsPerStatBlock);
+  int mybad = 0;
+  for (int cbase = 0; cbase < d; cbase += (d <= kStatThreads ? d : kStatThreads)) {
+    const int c = d <= kStatThreads ? (t % d) : (cbase + t);
+    const int rp = d <= kStatThreads ? (t / d) : 0;
+    double s = 0.0;
+    const bool active = (rp < nphase) && (c < d);
+    if (active) {
+      for (int64_t r = r0 + rp; r < r1; r += nphase) {
+        const float v = X[r * d + c];
+        mybad |= !isfinite(v);
+        s += (double)v;
+      }
+    }
+    red[t] = active ? s : 0.0;
+    __syncthreads();
+    if (d <= kStatThreads) {
+      if (t < d) {
+        double acc = 0.0;
+        for (int p = 0; p < nphase; ++p) acc += red[p * d + t];
+        partial[(int64_t)blockIdx.x * d + t] = acc;
+      }
+    } else if (c < d) {
+      partial[(int64_t)blockIdx.x * d + c] = red[t];
+    }
+    __syncthreads();
+    if (d <= kStatThreads) break;
+  }
+  if (mybad) bad = 1;
+  __syncthreads();
+  if (t == 0 && bad) atomicOr(&g->nonfinite, 1);
+}
+
+__global__ void k_colmean(const double* __restrict__ partial, int blocks, int64_t n, int d,
+                          double* __restrict__ mu) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= d) return;
+  double acc = 0.0;
+  for (int b = 0; b < blocks; ++b) acc += partial[(int64_t)b * d + c];
+  mu[c] = acc / (double)n;
+}
+
+__global__ void k_finite(const float* __restrict__ X, int64_t total, PrepGlobals* g) {
+  int bad = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(X[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&g->nonfinite, 1);
+}
+
+__global__ void k_absmax(const float* __restrict__ X, int64_t n, int d,
+                         const double* __restrict__ mu, PrepGlobals* g) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double m = 0.0;
+  for (int64_t r = warp; r < n; r += nwarps)
+    for (int c = lane; c < d; c += 32) m = fmax(m, fabs((double)X[r * d + c] - mu[c]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) atomic_max_nonneg(&g->absmax_bits, m);
+}
+
+// s = 2^e with max|s*(x-mu)| in [2^14, 2^15) for fp16 (fp16 max finite 65504,
+// so no operand can overflow and products/sums stay far inside fp32 range).
+// bf16 shares fp32's exponent range: s = 1.
+__global__ void k_scale(PrepGlobals* g, int fmt) {
+  const double amax = __longlong_as_double((long long)g->absmax_bits);
+  double s = 1.0;
+  if (fmt == 1 && amax > 0.0) {
+    int ex;
+    frexp(amax, &ex);  // amax in [2^(ex-1), 2^ex)
+    s = ldexp(1.0, 15 - ex);
+  }
+  g->s = s;
+}
+
+template <int FMT>
+__device__ __forceinline__ uint16_t rn16(double t) {
+  if (FMT == 1) return __half_as_ushort(__double2half(t));
+  return __bfloat16_as_ushort(__double2bfloat16(t));
+}
+template <int FMT>
+__device__ __forceinline__ double widen16(uint16_t h) {
+  if (FMT == 1) return (double)__half2float(__ushort_as_half(h));
+  return (double)__bfloat162float(__ushort_as_bfloat16(h));
+}
+
+// One warp per row (rows [0, n_pad)); padding rows get zeros and nrm32 = +inf.
+template <int FMT>
+__global__ void k_quant(const float* __restrict__ X, int64_t n, int d,
+                        const double* __restrict__ mu, const PrepGlobals* __restrict__ g,
+                        PrepGlobals* gmax, Image img, int update_max) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= img.n_pad) return;
+  const double s = g->s;
+  const int epr = img.rb / 2;  // elements per row per region
+  const unsigned M = img.layout == 2 ? 7u : (img.layout == 4 ? 3u : 1u);
+  uint8_t* base = reinterpret_cast<uint8_t*>(img.data);
+  double a2 = 0.0, r2 = 0.0, tt = 0.0;
+  const bool real = r < n;
+  for (int p = lane; p < img.dpad / 2; p += 32) {
+    const int c0 = 2 * p, c1 = 2 * p + 1;
+    double t0 = 0.0, t1 = 0.0;
+    if (real && c0 < d) t0 = ((double)X[r * d + c0] - mu[c0]) * s;
+    if (real && c1 < d) t1 = ((double)X[r * d + c1] - mu[c1]) * s;
+    const uint16_t h0 = rn16<FMT>(t0), h1 = rn16<FMT>(t1);
+    const double q0 = widen16<FMT>(h0), q1 = widen16<FMT>(h1);
+    a2 += q0 * q0 + q1 * q1;
+    r2 += (q0 - t0) * (q0 - t0) + (q1 - t1) * (q1 - t1);
+    tt += t0 * t0 + t1 * t1;
+    const int kb = c0 / epr;
+    const uint64_t o = (uint64_t)r * img.rb + (uint64_t)(c0 % epr) * 2u;
+    const uint64_t phys = o ^ (((o >> 7) & M) << 4);
+    *reinterpret_cast<uint32_t*>(base + (size_t)kb * img.region_bytes() + phys) =
+        (uint32_t)h0 | ((uint32_t)h1 << 16);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+    tt += __shfl_xor_sync(0xffffffffu, tt, o);
+  }
+  if (lane == 0) {
+    if (!real) {
+      img.nrm32[r] = CUDART_INF_F;
+      return;
+    }
+    img.nrm32[r] = __double2float_rn(a2);
+    img.a2[r] = a2;
+    // e >= ||xhat - t|| + ||t - s(x - mu)||: fp64 rounding of the residual sum
+    // (relative <= (d+4) 2^-53, doubled) plus the rounding of fl64(x - mu)
+    // (<= 2^-53 |x - mu| per element, doubled), then a final 2^-50 margin.
+    const double eps = 1.1102230246251565e-16;  // 2^-53
+    const double e = (sqrt(r2) * (1.0 + 2.0 * (d + 4) * eps) + 2.0 * eps * sqrt(tt) * (1.0 + 1e-6)) *
+                     (1.0 + 8.0 * eps);
+    img.e[r] = e;
+    if (update_max) {
+      atomic_max_nonneg(reinterpret_cast<unsigned long long*>(&gmax->amax2), a2);
+      atomic_max_nonneg(reinterpret_cast<unsigned long long*>(&gmax->emax), e);
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_prep_stats(const float* X, int64_t n, int d, double* mu, double* partial,
+                              int partial_blocks, PrepGlobals* g, cudaStream_t st, int* launches) {
+  const int blocks = (int)((n + kRowsPerStatBlock - 1) / kRowsPerStatBlock);
+  if (blocks > partial_blocks) return cudaErrorInvalidValue;
+  k_colsum_partial<<<blocks, kStatThreads, 0, st>>>(X, n, d, partial, g);
+  k_colmean<<<(d + 127) / 128, 128, 0, st>>>(partial, blocks, n, d, mu);
+  *launches += 2;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finite_check(const float* X, int64_t n, int d, PrepGlobals* g, cudaStream_t st,
+                                int* launches) {
+  const int64_t total = n * (int64_t)d;
+  const int64_t want = (total + 255) / 256;
+  const int blocks = (int)(want < 148 * 8 ? want : 148 * 8);
+  k_finite<<<max(blocks, 1), 256, 0, st>>>(X, total, g);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prep_absmax(const float* X, int64_t n, int d, const double* mu, PrepGlobals* g,
+                               cudaStream_t st, int* launches) {
+  const int64_t total = n * (int64_t)d;
+  const int64_t want = (total + 255) / 256;
+  const int blocks = (int)(want < 148 * 8 ? want : 148 * 8);
+  k_absmax<<<max(blocks, 1), 256, 0, st>>>(X, n, d, mu, g);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prep_scale(PrepGlobals* g, int fmt, cudaStream_t st, int* launches) {
+  k_scale<<<1, 1, 0, st>>>(g, fmt);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prep_quant(const float* X, int64_t n, int d, const double* mu,
+                              const PrepGlobals* g, PrepGlobals* gmax, int fmt, Image img,
+                              bool update_max, cudaStream_t st, int* launches) {
+  const int64_t threads = img.n_pad * 32;
+  const int blocks = (int)((threads + 255) / 256);
+  if (fmt == 1)
+    k_quant<1><<<blocks, 256, 0, st>>>(X, n, d, mu, g, gmax, img, update_max ? 1 : 0);
+  else
+    k_quant<2><<<blocks, 256, 0, st>>>(X, n, d, mu, g, gmax, img, update_max ? 1 : 0);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+}  // namespace tod

@@ -1,0 +1,251 @@
+"""Thin ctypes binding over libtod.so (include/tod.h).  Argument marshalling
+only: every step of the hot path runs in the library's CUDA kernels.  There is
+no CPU fallback — if libtod.so is missing or no sm_100 GPU is present, calls
+raise.
+
+Accepts torch tensors (CUDA on the context's device, or CPU) and numpy arrays
+(host).  Outputs are allocated like the input: CUDA tensors for CUDA input,
+numpy arrays for host input (then the library stages the copies inside the
+call, which is what bench.py's e2e leg measures).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtod.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "tod.h")
+
+TOD_OK = 0
+STATUS = {0: "TOD_OK", -1: "TOD_E_ARG", -2: "TOD_E_NONFINITE", -3: "TOD_E_RANGE",
+          -4: "TOD_E_NOMEM", -5: "TOD_E_CUDA", -7: "TOD_E_UNSUPPORTED", -8: "TOD_E_INTERNAL"}
+FORMATS = {"auto": 0, "fp16": 1, "bf16": 2, "fp32": 3}
+F_NO_CERTIFY = 0x1
+F_TIMING = 0x2
+
+
+class TodError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__("%s: %s" % (STATUS.get(status, str(status)), msg))
+        self.status = status
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("format", ctypes.c_int32), ("kprime", ctypes.c_int32),
+                ("flags", ctypes.c_uint32), ("stream", ctypes.c_void_p), ("chunks", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("rows", ctypes.c_int64), ("certified", ctypes.c_int64),
+                ("fallback_rows", ctypes.c_int64), ("kprime", ctypes.c_int32),
+                ("format", ctypes.c_int32), ("chunks", ctypes.c_int32), ("dpad", ctypes.c_int32),
+                ("scale", ctypes.c_double), ("max_abs_err", ctypes.c_double),
+                ("ms_stage", ctypes.c_float), ("ms_prep", ctypes.c_float),
+                ("ms_main", ctypes.c_float), ("ms_certify", ctypes.c_float),
+                ("ms_fallback", ctypes.c_float), ("ms_lof", ctypes.c_float),
+                ("ms_total", ctypes.c_float), ("kernel_launches", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class KnnOut(ctypes.Structure):
+    _fields_ = [("idx", ctypes.c_void_p), ("dist", ctypes.c_void_p), ("dist64", ctypes.c_void_p),
+                ("score_kth", ctypes.c_void_p), ("score_mean", ctypes.c_void_p),
+                ("kdist64", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libtod.so; raise (loudly) if it is missing.  Never falls back."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError("libtod.so not built (%s); run __graft_entry__.build()" % path)
+    lib = ctypes.CDLL(path)
+    P, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    sig = {
+        "tod_create": ([ctypes.POINTER(Config), ctypes.POINTER(P)], ctypes.c_int),
+        "tod_destroy": ([P], ctypes.c_int),
+        "tod_status_str": ([ctypes.c_int], ctypes.c_char_p),
+        "tod_last_message": ([P], ctypes.c_char_p),
+        "tod_abi_version": ([], I32),
+        "tod_build_info": ([], ctypes.c_char_p),
+        "tod_knn": ([P, P, I64, I32, I32, I64, I64, ctypes.POINTER(KnnOut), ctypes.POINTER(Stats)],
+                    ctypes.c_int),
+        "tod_knn_query": ([P, P, I64, P, I64, I32, I32, ctypes.POINTER(KnnOut),
+                           ctypes.POINTER(Stats)], ctypes.c_int),
+        "tod_lof": ([P, P, I64, I32, I32, P, P, ctypes.POINTER(KnnOut), ctypes.POINTER(Stats)],
+                    ctypes.c_int),
+        "tod_lof_lrd": ([P, I64, I32, I64, P, P, P, P], ctypes.c_int),
+        "tod_lof_finish": ([P, I64, I32, I64, I64, P, P, P, P], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def header_symbols(header: str = HEADER):
+    """Function names declared in include/tod.h."""
+    with open(header) as f:
+        txt = f.read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(tod_[a-z_0-9]+)\s*\(", txt)))
+
+
+def _is_torch(x):
+    return type(x).__module__.startswith("torch")
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if _is_torch(x):
+        return x.data_ptr()
+    return x.ctypes.data
+
+
+def _as_f32_2d(x):
+    if _is_torch(x):
+        import torch
+        if x.dtype != torch.float32 or x.dim() != 2:
+            raise ValueError("X must be a 2-D float32 tensor")
+        return x.contiguous()
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    if x.ndim != 2:
+        raise ValueError("X must be 2-D")
+    return x
+
+
+def _empty_like_host_or_dev(ref, shape, dtype_np):
+    if _is_torch(ref):
+        import torch
+        tmap = {np.int64: torch.int64, np.float32: torch.float32, np.float64: torch.float64}
+        return torch.empty(shape, dtype=tmap[dtype_np], device=ref.device)
+    return np.empty(shape, dtype=dtype_np)
+
+
+@dataclass
+class KnnResult:
+    idx: object
+    dist: object
+    dist64: object
+    score_kth: object
+    score_mean: object
+    kdist64: object
+    stats: dict
+
+
+class Context:
+    """Owns a tod_ctx (device workspace + stream binding)."""
+
+    def __init__(self, device: int = 0, fmt: str = "auto", kprime: int = 0, chunks: int = 0,
+                 flags: int = 0, stream=None):
+        self.lib = load_library()
+        cfg = Config(device=device, format=FORMATS[fmt], kprime=kprime, flags=flags,
+                     stream=stream, chunks=chunks, reserved=0)
+        h = ctypes.c_void_p()
+        st = self.lib.tod_create(ctypes.byref(cfg), ctypes.byref(h))
+        if st != TOD_OK:
+            raise TodError(st, "tod_create(device=%d) failed" % device)
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.tod_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _check(self, st):
+        if st != TOD_OK:
+            msg = self.lib.tod_last_message(self.h)
+            raise TodError(st, msg.decode() if msg else "")
+
+    def _alloc_knn(self, ref, q, k, want):
+        o = {}
+        o["idx"] = _empty_like_host_or_dev(ref, (q, k), np.int64) if "idx" in want else None
+        o["dist"] = _empty_like_host_or_dev(ref, (q, k), np.float32) if "dist" in want else None
+        o["dist64"] = _empty_like_host_or_dev(ref, (q, k), np.float64) if "dist64" in want else None
+        o["score_kth"] = _empty_like_host_or_dev(ref, (q,), np.float32) if "score_kth" in want else None
+        o["score_mean"] = _empty_like_host_or_dev(ref, (q,), np.float32) if "score_mean" in want else None
+        o["kdist64"] = _empty_like_host_or_dev(ref, (q,), np.float64) if "kdist64" in want else None
+        ko = KnnOut(*[_ptr(o[f]) for f, _ in KnnOut._fields_])
+        return o, ko
+
+    ALL = ("idx", "dist", "dist64", "score_kth", "score_mean", "kdist64")
+
+    def knn(self, X, k: int, q_begin: int = 0, q_count=None, want=ALL) -> KnnResult:
+        """tod_knn: exact kNN self-join for rows [q_begin, q_begin+q_count) of X."""
+        X = _as_f32_2d(X)
+        n, d = X.shape
+        if q_count is None:
+            q_count = n - q_begin
+        o, ko = self._alloc_knn(X, q_count, k, want)
+        s = Stats()
+        self._check(self.lib.tod_knn(self.h, _ptr(X), n, d, k, q_begin, q_count, ctypes.byref(ko),
+                                     ctypes.byref(s)))
+        return KnnResult(**o, stats=s.as_dict())
+
+    def knn_query(self, Q, X, k: int, want=ALL) -> KnnResult:
+        """tod_knn_query: kNN of rows of Q among rows of X (no exclusion)."""
+        Q = _as_f32_2d(Q)
+        X = _as_f32_2d(X)
+        if Q.shape[1] != X.shape[1]:
+            raise ValueError("dimension mismatch")
+        o, ko = self._alloc_knn(X, Q.shape[0], k, want)
+        s = Stats()
+        self._check(self.lib.tod_knn_query(self.h, _ptr(Q), Q.shape[0], _ptr(X), X.shape[0],
+                                           X.shape[1], k, ctypes.byref(ko), ctypes.byref(s)))
+        return KnnResult(**o, stats=s.as_dict())
+
+    def lof(self, X, k: int, want_knn=()):
+        """tod_lof: returns (lof fp32[n], lrd fp32[n], KnnResult|None, stats)."""
+        X = _as_f32_2d(X)
+        n, d = X.shape
+        lof = _empty_like_host_or_dev(X, (n,), np.float32)
+        lrd = _empty_like_host_or_dev(X, (n,), np.float32)
+        o, ko = self._alloc_knn(X, n, k, want_knn)
+        s = Stats()
+        self._check(self.lib.tod_lof(self.h, _ptr(X), n, d, k, _ptr(lof), _ptr(lrd),
+                                     ctypes.byref(ko) if want_knn else None, ctypes.byref(s)))
+        res = KnnResult(**o, stats=s.as_dict()) if want_knn else None
+        return lof, lrd, res, s.as_dict()
+
+    def lof_lrd(self, n: int, k: int, idx, dist64, kdist64_all):
+        q = idx.shape[0]
+        out = _empty_like_host_or_dev(idx, (q,), np.float64)
+        self._check(self.lib.tod_lof_lrd(self.h, n, k, q, _ptr(idx), _ptr(dist64),
+                                         _ptr(kdist64_all), _ptr(out)))
+        return out
+
+    def lof_finish(self, n: int, k: int, q_begin: int, idx, lrd64_all):
+        q = idx.shape[0]
+        lof = _empty_like_host_or_dev(idx, (q,), np.float32)
+        lrd = _empty_like_host_or_dev(idx, (q,), np.float32)
+        self._check(self.lib.tod_lof_finish(self.h, n, k, q_begin, q, _ptr(idx), _ptr(lrd64_all),
+                                            _ptr(lof), _ptr(lrd)))
+        return lof, lrd

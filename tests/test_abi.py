@@ -1,0 +1,75 @@
+"""CPU-side checks of the C-ABI boundary: the library loads, exports every
+symbol include/tod.h declares, and its host-only entry points behave.  No
+compute calls (there is no GPU here)."""
+import ctypes
+import os
+import re
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2110_14007_b200 import build
+    build.build()
+    import paper_2110_14007_b200 as pkg
+    return pkg.load_library()
+
+
+def test_header_declares_expected_entry_points():
+    import paper_2110_14007_b200 as pkg
+    syms = pkg.header_symbols()
+    for s in ("tod_create", "tod_destroy", "tod_knn", "tod_lof", "tod_lof_lrd", "tod_lof_finish",
+              "tod_knn_query", "tod_status_str", "tod_last_message", "tod_abi_version",
+              "tod_build_info"):
+        assert s in syms
+
+
+def test_library_exports_every_header_symbol(lib):
+    import paper_2110_14007_b200 as pkg
+    out = subprocess.check_output(["nm", "-D", "--defined-only", pkg.LIB_PATH], text=True)
+    exported = set(re.findall(r" T (tod_\w+)", out))
+    missing = set(pkg.header_symbols()) - exported
+    assert not missing, missing
+
+
+def test_status_strings_and_version(lib):
+    for code in (0, -1, -2, -3, -4, -5, -7, -8):
+        assert lib.tod_status_str(code).startswith(b"TOD_")
+    assert lib.tod_abi_version() == 1
+    assert b"sm_100a" in lib.tod_build_info()
+
+
+def test_sass_contains_tcgen05_and_bulk_copy(lib):
+    import paper_2110_14007_b200 as pkg
+    sass = subprocess.check_output(["cuobjdump", "-sass", pkg.LIB_PATH], text=True)
+    for mnemonic in ("UTCHMMA", "LDTM", "UBLKCP"):
+        assert mnemonic in sass, mnemonic
+    assert "HMMA." not in sass.replace("UTCHMMA", "")   # no legacy mma.sync path
+
+
+def test_create_fails_cleanly_without_gpu(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    h = ctypes.c_void_p()
+    assert lib.tod_create(None, ctypes.byref(h)) == -5   # TOD_E_CUDA, no crash
+    assert lib.tod_destroy(None) == 0
+
+
+def test_product_package_never_imports_oracle():
+    code = ("import sys; sys.path.insert(0, %r); import paper_2110_14007_b200 as p; "
+            "import paper_2110_14007_b200.dist; "
+            "assert 'oracle' not in sys.modules, 'oracle imported'; print('ok')" % ROOT)
+    assert subprocess.check_output([sys.executable, "-c", code], text=True).strip() == "ok"
+    pkg_dir = os.path.join(ROOT, "paper_2110_14007_b200")
+    for dp, _, fs in os.walk(pkg_dir):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dp, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", txt, re.M), f
+                assert "knn_oracle" not in txt and "liboracle" not in txt, f

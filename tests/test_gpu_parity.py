@@ -1,0 +1,208 @@
+"""GPU parity: libtod.so (through the C ABI) vs the CPU oracle, element by element
+on the same seeded inputs.  Bar (BASELINE.json north_star, DESIGN.md "Parity
+contract"): neighbour indices bit-exact (order included); fp32 scores within
+1e-5 relative (they are in fact bit-identical because the re-rank evaluates the
+oracle's own fp64 formula, so the tests demand exact equality and report the
+relative error on failure)."""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2110_14007_b200 import build
+    build.build()
+    import paper_2110_14007_b200 as p
+    return p
+
+
+def _ctx(pkg, **kw):
+    return pkg.Context(device=0, **kw)
+
+
+def _np(x):
+    return x.cpu().numpy() if hasattr(x, "cpu") else np.asarray(x)
+
+
+def _check_rows(res, X, k, rows, q_begin=0, ref=None):
+    """Compare GPU outputs of global rows `rows` with the oracle."""
+    if ref is None:
+        ref = oracle.knn(X, k, rows=rows)
+    ri, rd = ref
+    loc = np.asarray(rows) - q_begin
+    gi = _np(res.idx)[loc]
+    bad = np.nonzero((gi != ri).any(1))[0]
+    assert bad.size == 0, "rows %s: gpu %s oracle %s" % (np.asarray(rows)[bad[:3]], gi[bad[:1]], ri[bad[:1]])
+    assert np.array_equal(_np(res.dist64)[loc], np.sqrt(rd))
+    kth, mean = oracle.scores(rd)
+    g_kth, g_mean = _np(res.score_kth)[loc], _np(res.score_mean)[loc]
+    rel = np.max(np.abs(g_mean - mean) / np.maximum(np.abs(mean), 1e-30)) if mean.size else 0
+    assert np.array_equal(g_kth, kth) and np.array_equal(g_mean, mean), "rel err %g" % rel
+    assert np.array_equal(_np(res.dist)[loc], np.sqrt(rd).astype(np.float32))
+
+
+# ----------------------------------------------------------- configs[0] (C1)
+def test_c1_full_bitexact(pkg):
+    X = datagen.gaussian_mixture(1000, 10, seed=0)
+    with _ctx(pkg) as ctx:
+        res = ctx.knn(torch.from_numpy(X).cuda(), 10)
+    _check_rows(res, X, 10, np.arange(1000))
+    assert res.stats["certified"] + res.stats["fallback_rows"] == 1000
+
+
+@pytest.mark.parametrize("n,d,k,fmt", [
+    (3000, 32, 20, "fp16"),     # C2 shape, small n, several tiles + ragged tail
+    (2999, 64, 10, "fp16"),     # C3 shape, ragged
+    (1000, 16, 10, "fp16"),     # SW32 operand layout
+    (1500, 100, 12, "fp16"),    # dpad 128 (two K regions), d not a multiple of 16
+    (2500, 64, 10, "bf16"),
+    (777, 10, 5, "fp32"),
+    (2000, 40, 30, "fp32"),
+    (257, 33, 7, "fp16"),       # one query tile more than a reference tile
+])
+def test_knn_full_parity(pkg, n, d, k, fmt):
+    X = datagen.gaussian_mixture(n, d, seed=n + d)
+    with _ctx(pkg, fmt=fmt) as ctx:
+        res = ctx.knn(torch.from_numpy(X).cuda(), k)
+    _check_rows(res, X, k, np.arange(n))
+    st = res.stats
+    assert st["rows"] == n
+    if fmt != "bf16":
+        assert st["certified"] >= 0.95 * n, st
+
+
+def test_forced_fallback_tier(pkg):
+    X = datagen.gaussian_mixture(1200, 24, seed=5)
+    with _ctx(pkg, flags=pkg.F_NO_CERTIFY) as ctx:
+        res = ctx.knn(torch.from_numpy(X).cuda(), 9)
+    assert res.stats["fallback_rows"] == 1200
+    _check_rows(res, X, 9, np.arange(1200))
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "fp32"])
+def test_ties_lattice_and_duplicates(pkg, fmt):
+    X = datagen.lattice(2000, 20, seed=3, extent=2)
+    X = datagen.with_duplicates(X, frac=0.05, seed=4)
+    with _ctx(pkg, fmt=fmt) as ctx:
+        res = ctx.knn(torch.from_numpy(X).cuda(), 12)
+    _check_rows(res, X, 12, np.arange(2000))
+
+
+def test_translated_far_from_origin(pkg):
+    # cancellation stress for the norm expansion: |x| >> pairwise distances
+    X = datagen.uniform(2000, 32, seed=2, offset=1000.0)
+    with _ctx(pkg, fmt="fp16") as ctx:
+        res = ctx.knn(torch.from_numpy(X).cuda(), 10)
+    _check_rows(res, X, 10, np.arange(2000))
+
+
+def test_query_range_and_chunk_invariance(pkg):
+    X = datagen.gaussian_mixture(4000, 32, seed=8)
+    Xd = torch.from_numpy(X).cuda()
+    outs = []
+    for chunks, kp in ((1, 0), (3, 0), (2, 64), (1, 48)):
+        with _ctx(pkg, chunks=chunks, kprime=kp) as ctx:
+            outs.append(ctx.knn(Xd, 20, q_begin=1000, q_count=1700))
+    for o in outs[1:]:
+        assert torch.equal(o.idx, outs[0].idx) and torch.equal(o.dist64, outs[0].dist64)
+    _check_rows(outs[0], X, 20, np.arange(1000, 2700), q_begin=1000)
+
+
+def test_host_pointer_path_matches_device(pkg):
+    X = datagen.gaussian_mixture(2500, 48, seed=11)
+    with _ctx(pkg) as ctx:
+        dev = ctx.knn(torch.from_numpy(X).cuda(), 15)
+        host = ctx.knn(X, 15)
+    assert np.array_equal(host.idx, _np(dev.idx))
+    assert np.array_equal(host.score_mean, _np(dev.score_mean))
+
+
+def test_lof_full_bitexact(pkg):
+    X = datagen.gaussian_mixture(3000, 32, seed=21)
+    k = 20
+    with _ctx(pkg) as ctx:
+        lof, lrd, res, st = ctx.lof(torch.from_numpy(X).cuda(), k, want_knn=("idx",))
+    ri, rd = oracle.knn(X, k)
+    olrd, olof = oracle.lof_from_knn(ri, rd)
+    assert np.array_equal(_np(res.idx), ri)
+    assert np.array_equal(_np(lof), olof.astype(np.float32))
+    assert np.array_equal(_np(lrd), olrd.astype(np.float32))
+
+
+def test_lof_duplicates_inf_lrd(pkg):
+    X = np.repeat(datagen.gaussian_mixture(50, 8, seed=1), 4, axis=0)   # 4 copies each
+    with _ctx(pkg) as ctx:
+        lof, lrd, _, _ = ctx.lof(torch.from_numpy(X).cuda(), 3)
+    ri, rd = oracle.knn(X, 3)
+    olrd, olof = oracle.lof_from_knn(ri, rd)
+    assert np.all(np.isinf(_np(lrd))) and np.all(_np(lof) == 1.0)
+    assert np.array_equal(_np(lof), olof.astype(np.float32))
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "fp32"])
+def test_knn_query_parity(pkg, fmt):
+    X = datagen.gaussian_mixture(3000, 24, seed=31)
+    Q = datagen.gaussian_mixture(700, 24, seed=32)
+    Q[:10] = X[:10]     # exact duplicates of references: distance 0
+    with _ctx(pkg, fmt=fmt) as ctx:
+        res = ctx.knn_query(torch.from_numpy(Q).cuda(), torch.from_numpy(X).cuda(), 11)
+    ri, rd = oracle.knn_query(Q, X, 11)
+    assert np.array_equal(_np(res.idx), ri)
+    assert np.array_equal(_np(res.dist64), np.sqrt(rd))
+
+
+def test_error_paths(pkg):
+    X = datagen.gaussian_mixture(100, 8, seed=0)
+    with _ctx(pkg) as ctx:
+        for k in (0, 100):
+            with pytest.raises(pkg.TodError) as e:
+                ctx.knn(torch.from_numpy(X).cuda(), k)
+            assert e.value.status == -3
+        Y = X.copy()
+        Y[5, 3] = np.nan
+        with pytest.raises(pkg.TodError) as e:
+            ctx.knn(torch.from_numpy(Y).cuda(), 5)
+        assert e.value.status == -2
+        r = ctx.knn(torch.from_numpy(X).cuda(), 99)    # k = n-1: every other row
+        assert sorted(_np(r.idx)[0].tolist()) == list(range(1, 100))
+
+
+# ------------------------------------------------ BASELINE full-size configs
+def _sample_rows(n, labels, m, seed):
+    rng = np.random.default_rng(seed)
+    out_rows = np.nonzero(labels)[0]
+    rows = np.concatenate([rng.choice(n, m - m // 4, replace=False),
+                           rng.choice(out_rows, m // 4, replace=False), [0, n - 1]])
+    return np.unique(rows)
+
+
+def test_c2_full_size_sampled(pkg):
+    # configs[1]: kNN + LOF, n=100,000, d=32, k=20 on 1xB200 (bench launch config)
+    X, lab = datagen.gaussian_mixture(100_000, 32, seed=0, return_labels=True)
+    k = 20
+    with _ctx(pkg) as ctx:
+        lof, lrd, res, st = ctx.lof(torch.from_numpy(X).cuda(), k,
+                                    want_knn=("idx", "dist", "dist64", "score_kth", "score_mean"))
+    rows = _sample_rows(100_000, lab, 48, seed=1)
+    _check_rows(res, X, k, rows)
+    lr = oracle.lof_rows(X, k, rows[:3])
+    assert np.array_equal(_np(lof)[rows[:3]], lr["lof"].astype(np.float32))
+    assert st["certified"] >= 0.99 * 100_000, st
+
+
+def test_c3_full_size_sampled_bf16(pkg):
+    # configs[2]: n=1,000,000, d=64, k=10, bf16 provable-quantization path
+    X, lab = datagen.gaussian_mixture(1_000_000, 64, seed=0, return_labels=True)
+    k = 10
+    with _ctx(pkg, fmt="bf16") as ctx:
+        res = ctx.knn(torch.from_numpy(X).cuda(), k)
+    rows = _sample_rows(1_000_000, lab, 16, seed=2)
+    _check_rows(res, X, k, rows)
