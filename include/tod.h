@@ -72,6 +72,7 @@ typedef enum {
 /* Flags for tod_config.flags. */
 #define TOD_F_NO_CERTIFY   0x1u  /* testing: treat every row as uncertified -> fp64 brute-force tier */
 #define TOD_F_TIMING       0x2u  /* record per-phase CUDA-event times in tod_stats */
+#define TOD_F_DEBUG_NULL_EPILOGUE 0x100u  /* profiling only: pass 1 skips its epilogue (results invalid) */
 
 typedef struct {
   int32_t device;          /* CUDA device ordinal */
@@ -80,7 +81,8 @@ typedef struct {
   uint32_t flags;          /* TOD_F_* */
   void* stream;            /* cudaStream_t to run on; NULL = the library's own non-blocking stream */
   int32_t chunks;          /* reference chunks S per query tile (load balance); 0 = auto */
-  int32_t reserved;
+  int32_t epilogue_split;  /* tensor-core pass: epilogue warps per TMEM lane quarter (1 or 2; 2 splits each
+                              tile's columns into two per-row lists of K'/2+8); 0 = auto */
 } tod_config;
 
 typedef struct {

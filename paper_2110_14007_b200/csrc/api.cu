@@ -41,9 +41,9 @@ struct Workspace {
 };
 
 enum BufId {
-  B_X = 0, B_Q, B_IMG_B, B_NRM_B, B_A2_B, B_E_B, B_IMG_A, B_NRM_A, B_A2_A, B_E_A, B_MU, B_PART,
+  B_X = 0, B_Q, B_IMG_B, B_A2_B, B_E_B, B_IMG_A, B_A2_A, B_E_A, B_MU, B_PART,
   B_G, B_CIDX, B_CV, B_FAIL, B_SMALL, B_IDX, B_DIST, B_DIST64, B_KTH, B_MEAN, B_KD64,
-  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_NBUF
+  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_NBUF
 };
 
 }  // namespace
@@ -124,6 +124,7 @@ struct Plan {
   int dpad;
   int kp;
   int S;
+  int lists;     // candidate lists per row (TC: epilogue split; SIMT: S)
 };
 
 tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k, Plan* p) {
@@ -143,7 +144,7 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
   int kp = ctx->cfg.kprime;
   const int kmax_list = p->kind == PASS_TC ? 64 : 128;
   if (kp <= 0) {
-    if (fmt == TOD_FMT_FP16) kp = roundup(std::max(2 * k, k + 28), 16);
+    if (fmt == TOD_FMT_FP16) kp = roundup(k + 24, 8);
     else if (fmt == TOD_FMT_BF16) kp = roundup(std::max(6 * k, k + 40), 16);
     else kp = roundup(std::max(k + 8, 16), 8);
     kp = std::min(kp, kmax_list);
@@ -154,30 +155,47 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
                 kmax_list, k);
   p->kp = kp;
   int S = ctx->cfg.chunks;
-  if (S <= 0) {
-    if (p->kind == PASS_TC) {
-      const int64_t qtiles = (q_count + 127) / 128 + 1;
-      const int64_t btiles = (n_ref + 255) / 256;
+  if (p->kind == PASS_TC) {
+    // Reference chunks: each chunk's operand image should stay L2-resident
+    // while all CTAs sweep it (chunk-major work order), and the (query tile x
+    // chunk) items should fill the last wave of the persistent grid.
+    // Epilogue split: two warps per TMEM lane quarter, each with its own
+    // per-row list of K'' = K'/2 + 8 candidates over half of every tile.
+    int sp = ctx->cfg.epilogue_split;
+    const int kh = roundup(kp / 2 + 8, 8);
+    if (sp <= 0 || sp > 2) sp = tc_split_fits(p->dpad, kh) ? 2 : 1;
+    if (sp == 2 && !tc_split_fits(p->dpad, kh)) sp = 1;
+    p->lists = sp;
+    if (sp == 2) p->kp = kh;
+    const int64_t qtiles = (q_count + 127) / 128 + 1;
+    const int64_t btiles = (n_ref + 255) / 256;
+    const double img_bytes = (double)btiles * 256 * (p->dpad + 16) * 2;
+    const int s_min = std::max(1, (int)std::ceil(img_bytes / (48.0 * 1024 * 1024)));
+    if (S <= 0) {
       double best = 1e30;
-      S = 1;
-      for (int s = 1; s <= 4; ++s) {
-        if (s * kp > 256 || btiles / s < 4) break;
+      S = s_min;
+      for (int s = s_min; s <= s_min + 8; ++s) {
+        if (btiles / s < 8) break;
         const double items = (double)(qtiles * s);
         const double waves = std::ceil(items / ctx->num_sms);
-        const double eff = items / (waves * ctx->num_sms);
-        const double cost = (1.0 / eff) * (1.0 + 0.02 * (s - 1));
-        if (cost < best - 1e-9) {
+        const double cost = waves / items * (1.0 + 0.003 * (s - s_min));
+        if (cost < best - 1e-12) {
           best = cost;
           S = s;
         }
       }
-    } else {
+    }
+    if (S < 1 || S > btiles) return fail(ctx, TOD_E_ARG, "bad chunk count S=%d", S);
+  } else {
+    p->lists = 0;  // set below
+    if (S <= 0) {
       const int64_t qtiles = (q_count + 127) / 128;
       S = 1;
       while (qtiles * S < 2 * ctx->num_sms && (S + 1) * kp <= 256 && n_ref / (S + 1) >= 256) ++S;
     }
+    if (S < 1 || S * kp > 256) return fail(ctx, TOD_E_ARG, "bad chunk count S=%d (K'=%d)", S, kp);
+    p->lists = S;
   }
-  if (S < 1 || S * kp > 256) return fail(ctx, TOD_E_ARG, "bad chunk count S=%d (K'=%d)", S, kp);
   p->S = S;
   return TOD_OK;
 }
@@ -223,10 +241,20 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
   Cands cands;
   cands.kp = plan.kp;
   cands.S = plan.S;
-  TOD_TRY(ensure(ctx, B_CIDX, (size_t)std::max<int64_t>(q_count, 1) * plan.S * plan.kp * 4, &p));
+  cands.lists = plan.lists;
+  cands.dbg = (int)((ctx->cfg.flags >> 8) & 0xFF);
+  TOD_TRY(ensure(ctx, B_CIDX, (size_t)std::max<int64_t>(q_count, 1) * cands.lists * plan.kp * 4, &p));
   cands.idx = static_cast<int32_t*>(p);
-  TOD_TRY(ensure(ctx, B_CV, (size_t)std::max<int64_t>(q_count, 1) * plan.S * 4, &p));
+  TOD_TRY(ensure(ctx, B_CV, (size_t)std::max<int64_t>(q_count, 1) * cands.lists * 4, &p));
   cands.v = static_cast<float*>(p);
+  if (plan.kind == PASS_TC && plan.S > 1) {
+    const int64_t nqt = (q_begin + q_count + 127) / 128 - q_begin / 128;
+    TOD_TRY(ensure(ctx, B_STLIST, (size_t)nqt * plan.lists * plan.kp * 128 * 8, &p));
+    cands.st_list = static_cast<uint2*>(p);
+    TOD_TRY(ensure(ctx, B_STDONE, (size_t)nqt * 4, &p));   // >= query groups
+    cands.st_done = static_cast<int*>(p);
+    TOD_CUDA(cudaMemsetAsync(cands.st_done, 0, (size_t)nqt * 4, st));
+  }
   TOD_TRY(ensure(ctx, B_FAIL, (size_t)std::max<int64_t>(q_count, 1) * 4, &p));
   int32_t* fail_rows = static_cast<int32_t*>(p);
 
@@ -241,10 +269,14 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
   tm.mark();  // 1: prep start
   if (plan.kind == PASS_TC) {
     const int64_t n_pad = (n + 255) / 256 * 256;
-    const int64_t qn_pad = self ? n_pad : (q_count + 255) / 256 * 256;
+    // query image rows: the 128-row query tiles covering [q_begin, q_begin+q_count)
+    const int64_t a_row0 = self ? (q_begin / 128) * 128 : 0;
+    const int64_t a_rows = self ? std::min<int64_t>(n, (q_begin + q_count + 127) / 128 * 128) - a_row0
+                                : q_count;
+    const int64_t a_pad = (a_rows + 255) / 256 * 256;
     const int rb = std::min(128, plan.dpad * 2);
-    auto make_img = [&](int id_img, int id_nrm, int id_a2, int id_e, int64_t rows,
-                        int64_t rows_pad, Image* img) -> tod_status {
+    auto make_img = [&](int id_img, int id_a2, int id_e, int64_t rows, int64_t rows_pad,
+                        Image* img) -> tod_status {
       void* q;
       img->n = rows;
       img->n_pad = rows_pad;
@@ -252,10 +284,8 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
       img->rb = rb;
       img->nkb = plan.dpad * 2 / rb;
       img->layout = rb == 128 ? 2 : (rb == 64 ? 4 : 6);
-      TOD_TRY(ensure(ctx, id_img, (size_t)rows_pad * plan.dpad * 2, &q));
+      TOD_TRY(ensure(ctx, id_img, img->total_bytes(), &q));
       img->data = static_cast<uint16_t*>(q);
-      TOD_TRY(ensure(ctx, id_nrm, (size_t)rows_pad * 4, &q));
-      img->nrm32 = static_cast<float*>(q);
       TOD_TRY(ensure(ctx, id_a2, (size_t)std::max<int64_t>(rows, 1) * 8, &q));
       img->a2 = static_cast<double*>(q);
       TOD_TRY(ensure(ctx, id_e, (size_t)std::max<int64_t>(rows, 1) * 8, &q));
@@ -263,12 +293,8 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
       return TOD_OK;
     };
     Image B, A;
-    TOD_TRY(make_img(B_IMG_B, B_NRM_B, B_A2_B, B_E_B, n, n_pad, &B));
-    if (self) {
-      A = B;
-    } else {
-      TOD_TRY(make_img(B_IMG_A, B_NRM_A, B_A2_A, B_E_A, q_count, qn_pad, &A));
-    }
+    TOD_TRY(make_img(B_IMG_B, B_A2_B, B_E_B, n, n_pad, &B));
+    TOD_TRY(make_img(B_IMG_A, B_A2_A, B_E_A, a_rows, a_pad, &A));
     const int stat_blocks = (int)((n + 1023) / 1024);
     TOD_TRY(ensure(ctx, B_MU, (size_t)d * 8, &p));
     double* mu = static_cast<double*>(p);
@@ -280,11 +306,12 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
       TOD_CUDA(launch_finite_check(dQ, q_count, d, g, st, launches));
       TOD_CUDA(launch_prep_absmax(dQ, q_count, d, mu, g, st, launches));
     }
-    TOD_CUDA(launch_prep_scale(g, plan.fmt, st, launches));
-    TOD_CUDA(launch_prep_quant(dX, n, d, mu, g, g, plan.fmt, B, true, st, launches));
-    if (!self) TOD_CUDA(launch_prep_quant(dQ, q_count, d, mu, g, g, plan.fmt, A, false, st, launches));
-    cp.qa2 = self ? B.a2 + q_begin : A.a2;
-    cp.qe = self ? B.e + q_begin : A.e;
+    TOD_CUDA(launch_prep_scale(g, plan.fmt, plan.dpad, st, launches));
+    TOD_CUDA(launch_prep_quant(dX, n, d, mu, g, plan.fmt, B, 0, st, launches));
+    const float* qsrc = self ? dX + a_row0 * d : dQ;
+    TOD_CUDA(launch_prep_quant(qsrc, a_rows, d, mu, g, plan.fmt, A, 1, st, launches));
+    cp.qa2 = A.a2 + (self ? q_begin - a_row0 : 0);
+    cp.qe = A.e + (self ? q_begin - a_row0 : 0);
     tm.mark();  // 2: main start
     TOD_CUDA(launch_knn_tc(A, B, self ? q_begin : 0, q_count, self, plan.fmt, cands, ctx->num_sms,
                            st, launches));
@@ -295,6 +322,19 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     TOD_CUDA(launch_knn_simt(dQ, q_begin, q_count, dX, n, d, self, cands, st, launches));
   }
   tm.mark();  // 3: certify start
+  if (cands.dbg) {  // profiling aid: pass 1 only, outputs invalid
+    TOD_CUDA(cudaStreamSynchronize(st));
+    tm.mark();
+    tm.mark();
+    if (stats) {
+      stats->rows = q_count;
+      stats->kprime = plan.kp;
+      stats->format = plan.fmt;
+      stats->chunks = plan.S;
+      stats->dpad = plan.dpad;
+    }
+    return TOD_OK;
+  }
   TOD_CUDA(launch_rerank(dQ, q_begin, q_count, dX, n, d, k, self, cands, cp, out, fail_rows,
                          &small->fail_count, &small->max_err, st, launches));
   tm.mark();  // 4: fallback start
@@ -302,9 +342,11 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
   TOD_CUDA(cudaMemcpyAsync(&h, small, sizeof(SmallDev), cudaMemcpyDeviceToHost, st));
   TOD_CUDA(cudaStreamSynchronize(st));
   if (h.g.nonfinite) return fail(ctx, TOD_E_NONFINITE, "X (or Q) contains NaN or Inf");
-  if (h.fail_count > 0)
-    TOD_CUDA(launch_fallback(dQ, q_begin, dX, n, d, k, self, fail_rows, h.fail_count, out, st,
-                             launches));
+  if (h.fail_count > 0) {
+    TOD_TRY(ensure(ctx, B_FBPART, fallback_workspace(h.fail_count, k, n, ctx->num_sms), &p));
+    TOD_CUDA(launch_fallback(dQ, q_begin, dX, n, d, k, self, fail_rows, h.fail_count, out, p,
+                             ctx->num_sms, st, launches));
+  }
   tm.mark();  // 5: end of kNN
   if (stats) {
     stats->rows = q_count;

@@ -6,20 +6,25 @@
 namespace tod {
 
 // Quantized operand image of a row set in HBM ("input quantization", step (i)
-// of provable quantization).  16-bit elements, laid out exactly as
-// the tcgen05 K-major swizzled shared-memory tiles, so a contiguous bulk copy
-// of rows [r0, r0+R) of one K-region lands as a ready UMMA operand:
-//   nkb regions (one per 64-element K block, or 1 when dpad < 64),
-//   region kb = n_pad rows x rb bytes, rb = min(128, 2*dpad), row r at r*rb,
-//   16-byte chunks XOR-swizzled within each 8-row atom (Swizzle<B,4,3>).
+// of provable quantization).  16-bit elements laid out exactly as
+// tcgen05 K-major swizzled shared-memory tiles, so a contiguous bulk copy of
+// rows [r0, r0+R) of one K region lands as a ready UMMA operand.  K = dpad + 16:
+//   main regions kb = 0..nkb-1: 64-element K blocks (or one block of dpad < 64
+//     elements), n_pad rows x rb bytes, rb = min(128, 2*dpad), swizzle
+//     SW128/SW64/SW32 (16-byte chunks XOR-swizzled within 8-row atoms);
+//   extra region (16 elements, 32-byte rows, SW32): the fp16/bf16 pieces of
+//     ||xhat_j||^2 (reference image "B") or the power-of-two constants that
+//     multiply them (query image "A"), so the tensor core itself produces
+//     w_ij = ||xhat_j||^2 - 2 xhat_i.xhat_j (the A image stores -2 xhat_i).
 struct Image {
   uint16_t* data = nullptr;
-  float* nrm32 = nullptr;   // [n_pad] fp32(||xhat_r||^2), +inf for padding rows
-  double* a2 = nullptr;     // [n]     ||xhat_r||^2 in fp64
-  double* e = nullptr;      // [n]     upper bound on ||xhat_r - s(x_r - mu)||
+  double* a2 = nullptr;     // [n] ||xhat_r||^2 in fp64 (B: references; A: queries)
+  double* e = nullptr;      // [n] upper bound on ||xhat_r - s(x_r - mu)||
   int64_t n = 0, n_pad = 0;
   int dpad = 0, rb = 0, nkb = 0, layout = 0;  // layout: 2=SW128, 4=SW64, 6=SW32
   __host__ __device__ size_t region_bytes() const { return (size_t)n_pad * rb; }
+  __host__ __device__ size_t extra_offset() const { return (size_t)nkb * n_pad * rb; }
+  __host__ __device__ size_t total_bytes() const { return extra_offset() + (size_t)n_pad * 32; }
 };
 
 // Global prep scalars, device resident.
@@ -27,17 +32,24 @@ struct PrepGlobals {
   double s;          // power-of-two scale
   double amax2;      // max_j ||xhat_j||^2 over references
   double emax;       // max_j e_j over references
+  double repmax;     // max_j |sum_q c_q p_jq - ||xhat_j||^2| (norm-piece representation error)
   unsigned long long absmax_bits;  // max |x - mu| (fp64 bits) over queries and references
   int nonfinite;     // any NaN/Inf seen in X (or Q)
   int pad;
 };
 
-// Candidate lists written by the pass-1 kernels: per (query row, chunk) K'
+// Candidate lists written by the pass-1 kernels: per (query row, list) K'
 // column indices (-1 = empty) and the threshold v (keys of non-kept >= v).
+// The tensor-core kernel keeps ONE list per row across all S reference chunks
+// (state parked in st_list between chunks); the SIMT kernel writes S lists.
 struct Cands {
-  int32_t* idx = nullptr;   // [q_count][S][kp]
-  float* v = nullptr;       // [q_count][S]
-  int kp = 0, S = 0;
+  int32_t* idx = nullptr;   // [q_count][lists][kp]
+  float* v = nullptr;       // [q_count][lists]
+  int kp = 0, S = 0;        // S = reference chunks
+  int lists = 1;            // lists per row (TC: epilogue split 1|2; SIMT: S)
+  uint2* st_list = nullptr; // TC: [q tiles][kp][128] parked (key, index) state
+  int* st_done = nullptr;   // TC: [q tiles] chunks completed
+  int dbg = 0;  // profiling aid bits (TOD_F_DEBUG_*), 0 in production
 };
 
 enum PassKind : int { PASS_TC = 0, PASS_SIMT = 1 };
@@ -47,15 +59,16 @@ cudaError_t launch_prep_stats(const float* X, int64_t n, int d, double* mu, doub
                               int partial_blocks, PrepGlobals* g, cudaStream_t st, int* launches);
 cudaError_t launch_prep_absmax(const float* X, int64_t n, int d, const double* mu, PrepGlobals* g,
                                cudaStream_t st, int* launches);
-cudaError_t launch_prep_scale(PrepGlobals* g, int fmt, cudaStream_t st, int* launches);
-cudaError_t launch_prep_quant(const float* X, int64_t n, int d, const double* mu,
-                              const PrepGlobals* g, PrepGlobals* g_out_max, int fmt, Image img,
-                              bool update_max, cudaStream_t st, int* launches);
+cudaError_t launch_prep_scale(PrepGlobals* g, int fmt, int dpad, cudaStream_t st, int* launches);
+// side 0 = reference image B (xhat | norm pieces; updates amax2/emax/repmax),
+// side 1 = query image A (-2 xhat | constants).
+cudaError_t launch_prep_quant(const float* X, int64_t n, int d, const double* mu, PrepGlobals* g,
+                              int fmt, Image img, int side, cudaStream_t st, int* launches);
 cudaError_t launch_finite_check(const float* X, int64_t n, int d, PrepGlobals* g, cudaStream_t st,
                                 int* launches);
 
 // ---- knn_tc.cu  (tcgen05 fused distance + top-K')
-int tc_smem_bytes(int dpad, int kp);
+int tc_split_fits(int dpad, int kp);  // 1 if the SPLIT=2 epilogue fits in smem with K''=kp
 cudaError_t launch_knn_tc(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                           bool self_join, int fmt, Cands c, int num_sms, cudaStream_t st,
                           int* launches);
@@ -87,9 +100,11 @@ cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, cons
                           int64_t n, int d, int k, bool self_join, Cands c, CertParams cp,
                           KnnOutDev out, int32_t* fail_rows, int32_t* fail_count,
                           double* max_err, cudaStream_t st, int* launches);
+int fallback_slices(int nfail, int64_t n, int num_sms);
+size_t fallback_workspace(int nfail, int k, int64_t n, int num_sms);
 cudaError_t launch_fallback(const float* Q, int64_t q_begin, const float* X, int64_t n, int d,
                             int k, bool self_join, const int32_t* fail_rows, int nfail,
-                            KnnOutDev out, cudaStream_t st, int* launches);
+                            KnnOutDev out, void* ws, int num_sms, cudaStream_t st, int* launches);
 
 // ---- lof.cu
 cudaError_t launch_lof_lrd(int64_t q_count, int k, const int64_t* idx, const double* dist64,

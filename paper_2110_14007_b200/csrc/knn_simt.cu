@@ -30,8 +30,7 @@ __global__ void __launch_bounds__(kRowsQ)
                int32_t* __restrict__ cand_idx, float* __restrict__ cand_v) {
   extern __shared__ float smem_f[];
   float* sR = smem_f;                                       // [kRowsR][DMAX]
-  float* sLv = sR + kRowsR * DMAX;                          // [(kp+P)][128]
-  int* sLi = reinterpret_cast<int*>(sLv + (kp + kPend) * kRowsQ);
+  uint2* sL = reinterpret_cast<uint2*>(sR + kRowsR * DMAX);  // [(kp+P)][128] (key, index)
   const int t = threadIdx.x;
   const int64_t qtile = blockIdx.x / S;
   const int c = blockIdx.x % S;
@@ -45,7 +44,7 @@ __global__ void __launch_bounds__(kRowsQ)
   const int self = self_join ? (int)gi : -1;
 
   RowTopK<kRowsQ> L;
-  L.init(sLv, sLi, t, kp);
+  L.init(sL, t, kp);
   const int64_t j_lo = n * c / S, j_hi = n * (c + 1) / S;
   for (int64_t j0 = j_lo; j0 < j_hi; j0 += kRowsR) {
     const int rows = (int)(j_hi - j0 < kRowsR ? j_hi - j0 : kRowsR);
@@ -78,8 +77,8 @@ __global__ void __launch_bounds__(kRowsQ)
       const float m = fminf(fminf(fminf(w[0], w[1]), fminf(w[2], w[3])),
                             fminf(fminf(w[4], w[5]), fminf(w[6], w[7])));
       if (__any_sync(0xffffffffu, m < L.thr)) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) L.offer(w[e], (int)(j0 + jb + e), self);
+        L.reserve_group();
+        L.offer_group(w, (int)(j0 + jb), self);
       }
     }
   }
@@ -90,7 +89,7 @@ __global__ void __launch_bounds__(kRowsQ)
 template <int DMAX>
 cudaError_t launch_s(const float* Q, int64_t q_begin, int64_t q_count, const float* X, int64_t n,
                      int d, bool self_join, Cands c, cudaStream_t st) {
-  const size_t smem = (size_t)kRowsR * DMAX * 4 + (size_t)(c.kp + kPend) * kRowsQ * 8;
+  const size_t smem = (size_t)kRowsR * DMAX * 4 + (size_t)(c.kp + RowTopK<kRowsQ>::kPend) * kRowsQ * 8;
   auto kern = k_knn_simt<DMAX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -1,28 +1,39 @@
 // knn_tc.cu — K2: the hot loop.  Fused tile distance + running per-row top-K'
 // on 5th-generation tensor cores (tcgen05, sm_100a).
 //
-// What it computes: for every query row i of a 128-row
-// query tile and every reference column j of the chunk's 256-column tiles,
-//     G_ij  = xhat_i . xhat_j                (tcgen05.mma kind::f16, fp32 in TMEM)
-//     w_ij  = fl32(n_j - 2 G_ij)             (one FFMA; n_j = fp32 ||xhat_j||^2)
-// which is Eq. (3)'s right-hand side ||X_i||^2 + ||X_j||^2 - 2 X_i^T X_j
-// (§5.3) minus the row-constant ||X_i||^2 (ranking within
-// a row does not need it), and keeps the K' smallest w per row (operator
-// fusion of cdist and topk: the n x n matrix is never stored).
-// Self is excluded by index (reading A3).
+// What it computes: for every query row i and every
+// reference column j,
+//     w_ij = ||xhat_j||^2 - 2 xhat_i . xhat_j          (one fp32 TMEM value)
+// i.e. Eq. (3)'s right-hand side ||X_i||^2 + ||X_j||^2 - 2 X_i^T X_j (PAPER.md
+// §5.3) minus the row constant ||X_i||^2, which a row's ranking does
+// not need.  The whole of w comes out of the tensor core: the operand images
+// carry an extra 16-wide K block in which the query side holds power-of-two
+// constants c_q and the reference side the 16-bit pieces p_jq of ||xhat_j||^2
+// (sum_q c_q p_jq = ||xhat_j||^2 to ~2^-33), and the query side stores
+// -2 xhat_i.  The epilogue is then a pure min-tree + vote per 8 columns; it
+// keeps the K' smallest w per row (operator fusion of cdist and topk,
+// the n x n matrix is never stored).  Self is excluded by index
+// (reading A3); padding columns are masked.
 //
-// Structure (one CTA per SM, persistent over (query tile, chunk) work items):
-//   warp 0     producer: bulk async copies (TMA engine) of the resident query
-//              tile A, the reference tiles B (ring of NSTAGE stages) and their
-//              norms (ring of 4), completion on mbarriers (complete_tx).
-//   warp 1     TMEM allocator + single-thread MMA issuer: DPAD/16 MMAs of
-//              128 x BN x 16 per reference tile into one of two TMEM
-//              accumulators (double buffered: MMA of tile t+1 overlaps the
-//              epilogue of tile t); tcgen05.commit frees smem stages and
-//              publishes accumulators.
-//   warps 2-5  epilogue: thread = query row (TMEM lane), tcgen05.ld 32 columns
-//              at a time, FFMA + running min per 8 columns, warp vote against
-//              the per-row threshold; rare hits go to the RowTopK list.
+// Work decomposition ("automatic batching" re-derived): items are
+// (query group of QT 128-row tiles) x (reference chunk c of S), in chunk-major
+// order so that all CTAs sweep the same L2-resident chunk of the reference
+// image at the same time; a row's top-K' state is parked in HBM between its
+// chunks (st_list / st_done), so chunking adds no candidates and no re-rank
+// work.  The query image A holds only the rows of query tiles [qt0, qt1).
+//
+// Structure (one CTA per SM, persistent):
+//   warp 0     producer: bulk async copies (TMA engine, UBLKCP) of the QT
+//              resident query tiles and the reference tiles B (ring of
+//              nstage stages), completion on mbarriers (complete_tx).
+//   warp 1     TMEM allocator + single-thread MMA issuer: per reference tile,
+//              for each of the QT query tiles, (DPAD+16)/16 MMAs 128 x BN x 16
+//              into one of two TMEM accumulators (double buffered: the MMA of
+//              tile t+1 overlaps the epilogue of tile t).  With QT = 2 each B
+//              tile feeds 256 query rows, halving L2->SM traffic per pair.
+//   warps 2+   epilogue, 4 per query tile: thread = query row (TMEM lane),
+//              tcgen05.ld 32 columns at a time (double-buffered), 3-input min
+//              trees, one warp OR-reduction per tile; rare hits -> RowTopK.
 // Operands arrive pre-quantized and pre-swizzled (prep.cu writes the exact
 // K-major SWIZZLE_{32,64,128}B smem image), so a plain contiguous bulk copy
 // replaces tensor-map TMA.
@@ -40,91 +51,124 @@ namespace tod {
 namespace {
 
 constexpr int kBM = 128;
-constexpr int kThreads = 192;
-constexpr int kNormSlots = 4;
-
-template <int DPAD>
-struct TcCfg {
-  static constexpr int RB = DPAD * 2 < 128 ? DPAD * 2 : 128;  // bytes per row per K region
-  static constexpr int NKB = DPAD * 2 / RB;                  // K regions
-  static constexpr int LAYOUT = RB == 128 ? 2 : (RB == 64 ? 4 : 6);
-  static constexpr int SBO = 8 * RB;
-  static constexpr int BN = DPAD <= 64 ? 256 : 128;
-  static constexpr int KSTEPS = DPAD / 16;
-  static constexpr int NSTAGE = DPAD <= 32 ? 4 : (DPAD == 64 ? 3 : 3);
-  static constexpr int A_BYTES = kBM * DPAD * 2;
-  static constexpr int B_BYTES = BN * DPAD * 2;
-  static constexpr int TMEM_COLS = 2 * BN;  // two accumulators
-};
+constexpr int kExtraRB = 32;     // bytes per row of the 16-wide extra K block
+constexpr int kSmemMax = 232448; // 227 KB opt-in per block
 
 __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
 
-template <int DPAD>
-__host__ __device__ constexpr int smem_layout_bytes(int kp, int* off_b, int* off_n, int* off_lv,
-                                                    int* off_li, int* off_bar) {
-  using C = TcCfg<DPAD>;
-  int o = 0;
-  o += C::A_BYTES;
-  o = align_up(o, 1024);
+// SPLIT = epilogue warps per TMEM lane quarter.  With SPLIT = 2 each tile's
+// columns are split in two halves, each with its own warp (2 warps per SM
+// sub-partition for latency hiding) and its own per-row top-K'' list; the
+// re-rank takes the union of the two lists (v = min of the two thresholds).
+template <int DPAD, int SPLIT>
+struct TcCfg {
+  static constexpr int QT = 1;
+  static constexpr int RB = DPAD * 2 < 128 ? DPAD * 2 : 128;  // bytes per row per main K region
+  static constexpr int NKB = DPAD * 2 / RB;                  // main K regions
+  static constexpr int LAYOUT = RB == 128 ? 2 : (RB == 64 ? 4 : 6);
+  static constexpr int SBO = 8 * RB;
+  static constexpr int BN = DPAD <= 64 ? 256 : 128;
+  static constexpr int BH = BN / SPLIT;                      // columns per epilogue warp
+  static constexpr int KSTEPS = DPAD / 16;                   // main K steps (+1 extra)
+  static constexpr int MAX_STAGE = 4;
+  static constexpr int NROWS = kBM;                          // query rows per CTA item
+  static constexpr int NLIST = kBM * SPLIT;                  // lists per CTA item
+  static constexpr int PEND = 16;                            // pending slots per list (group entries)
+  static constexpr int EPI_WARPS = 4 * SPLIT;
+  static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+  static constexpr int A_ONE = kBM * (DPAD + 16) * 2;        // one query tile
+  static constexpr int A_STRIDE = align_up(A_ONE, 1024);
+  static constexpr int A_EXTRA = kBM * NKB * RB;             // offset of a tile's extra block
+  static constexpr int B_BYTES = BN * (DPAD + 16) * 2;
+  static constexpr int B_STRIDE = align_up(B_BYTES, 1024);
+  static constexpr int B_EXTRA = BN * NKB * RB;
+  static constexpr int NACC = 2;                             // accumulators in TMEM
+  static constexpr int TMEM_COLS = NACC * BN;
+  static_assert(TMEM_COLS <= 512, "TMEM overflow");
+};
+
+template <int DPAD, int SPLIT>
+__host__ __device__ constexpr int smem_layout_bytes(int kp, int nstage, int* off_b, int* off_l,
+                                                    int* off_bar) {
+  using C = TcCfg<DPAD, SPLIT>;
+  int o = C::A_STRIDE;
   *off_b = o;
-  o += C::NSTAGE * C::B_BYTES;
-  *off_n = o;
-  o += kNormSlots * C::BN * 4;
-  *off_lv = o;
-  o += (kp + kPend) * kBM * 4;
-  *off_li = o;
-  o += (kp + kPend) * kBM * 4;
+  o += nstage * C::B_STRIDE;
+  *off_l = o;
+  o += (kp + C::PEND) * C::NLIST * 8;
   o = align_up(o, 8);
   *off_bar = o;
-  o += 8 * (2 * C::NSTAGE + 2 + 2 * kNormSlots + 4) + 16;
+  o += 8 * (2 * C::MAX_STAGE + 2 + 2 * C::NACC) + 16;
   return o + 1024;  // slack for aligning the dynamic smem base to 1024
 }
 
-template <int DPAD, int FMT>
-__global__ void __launch_bounds__(kThreads, 1)
-    k_knn_tc(const uint8_t* __restrict__ a_img, size_t a_region, const uint8_t* __restrict__ b_img,
-             size_t b_region, const float* __restrict__ b_nrm, int64_t b_tiles, int64_t qt0,
-             int64_t n_qtiles, int64_t q_begin, int64_t q_end, int self_join, int S, int kp,
-             int32_t* __restrict__ cand_idx, float* __restrict__ cand_v) {
-  using C = TcCfg<DPAD>;
+// Deepest B pipeline (<= 4 stages) that fits; 0 if even 2 stages do not fit.
+template <int DPAD, int SPLIT>
+int pick_stages(int kp) {
+  int a, b, c;
+  for (int ns = TcCfg<DPAD, SPLIT>::MAX_STAGE; ns >= 2; --ns)
+    if (smem_layout_bytes<DPAD, SPLIT>(kp, ns, &a, &b, &c) <= kSmemMax) return ns;
+  return 0;
+}
+
+// 4-bit mask of the 8-column groups of a 32-column chunk whose minimum < thr.
+__device__ __forceinline__ unsigned group_bits(const float (&v)[32], float thr) {
+  unsigned gm = 0;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const float* vg = v + 8 * g;
+    const float m = fminf(fminf(fminf(vg[0], vg[1]), vg[2]),
+                          fminf(fminf(vg[3], vg[4]), fminf(fminf(vg[5], vg[6]), vg[7])));
+    gm |= (m < thr) ? (1u << g) : 0u;
+  }
+  return gm;
+}
+
+// Self column and padding columns (>= n_ref) become +inf: never kept.
+__device__ __noinline__ void mask_cols(float (&v)[32], int jb, int self, int64_t n_ref) {
+#pragma unroll
+  for (int e = 0; e < 32; ++e) v[e] = (jb + e == self || jb + e >= n_ref) ? CUDART_INF_F : v[e];
+}
+
+template <int DPAD, int FMT, int SPLIT>
+__global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
+    k_knn_tc(const uint8_t* __restrict__ a_img, size_t a_region, size_t a_extra,
+             const uint8_t* __restrict__ b_img, size_t b_region, size_t b_extra, int64_t b_tiles,
+             int64_t n_ref, int64_t qt0, int64_t n_qtiles, int64_t q_begin, int64_t q_end,
+             int self_join, int S, int kp, int nstage, int dbg, int32_t* __restrict__ cand_idx,
+             float* __restrict__ cand_v, uint2* __restrict__ st_list, int* __restrict__ st_done) {
+  using C = TcCfg<DPAD, SPLIT>;
+  constexpr int QT = C::QT;
+  using List = RowTopK<C::NLIST, C::PEND>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  int off_b, off_n, off_lv, off_li, off_bar;
-  smem_layout_bytes<DPAD>(kp, &off_b, &off_n, &off_lv, &off_li, &off_bar);
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  int off_b, off_l, off_bar;
+  smem_layout_bytes<DPAD, SPLIT>(kp, nstage, &off_b, &off_l, &off_bar);
   uint8_t* sA = smem;
   uint8_t* sB = smem + off_b;
-  float* sN = reinterpret_cast<float*>(smem + off_n);
-  float* sLv = reinterpret_cast<float*>(smem + off_lv);
-  int* sLi = reinterpret_cast<int*>(smem + off_li);
+  uint2* sL = reinterpret_cast<uint2*>(smem + off_l);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + off_bar);
-  uint64_t* full = bars;                        // [NSTAGE]
-  uint64_t* empty = bars + C::NSTAGE;           // [NSTAGE]
-  uint64_t* a_full = bars + 2 * C::NSTAGE;      // [1]
+  uint64_t* full = bars;                        // [nstage]
+  uint64_t* empty = bars + C::MAX_STAGE;        // [nstage]
+  uint64_t* a_full = bars + 2 * C::MAX_STAGE;   // [1]
   uint64_t* a_empty = a_full + 1;               // [1]
-  uint64_t* n_full = a_empty + 1;               // [kNormSlots]
-  uint64_t* n_empty = n_full + kNormSlots;      // [kNormSlots]
-  uint64_t* t_full = n_empty + kNormSlots;      // [2]
-  uint64_t* t_empty = t_full + 2;               // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
+  uint64_t* t_full = a_empty + 1;               // [NACC]
+  uint64_t* t_empty = t_full + C::NACC;         // [NACC]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + C::NACC);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < C::NSTAGE; ++i) {
+    for (int i = 0; i < nstage; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
     mbar_init(a_full, 1);
     mbar_init(a_empty, 1);
-    for (int i = 0; i < kNormSlots; ++i) {
-      mbar_init(&n_full[i], 1);
-      mbar_init(&n_empty[i], 4);
-    }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < C::NACC; ++i) {
       mbar_init(&t_full[i], 1);
-      mbar_init(&t_empty[i], 4);
+      mbar_init(&t_empty[i], C::EPI_WARPS);
     }
     fence_mbar_init();
   }
@@ -134,43 +178,43 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int64_t n_items = n_qtiles * S;
+  const int64_t n_groups = n_qtiles;  // one query tile per item
+  const int64_t n_items = n_groups * S;
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ producer
       int stage = 0;
       uint32_t phase = 0;
-      int ns = 0;
-      uint32_t nphase = 0;
       uint32_t aphase = 0;
       for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const int64_t qt = qt0 + item / S;
-        const int c = (int)(item % S);
+        const int64_t qg = item % n_groups;
+        const int c = (int)(item / n_groups);
         const int64_t t_lo = b_tiles * c / S, t_hi = b_tiles * (c + 1) / S;
         mbar_wait(a_empty, aphase ^ 1);
         aphase ^= 1;
-        mbar_arrive_expect_tx(a_full, C::A_BYTES);
-        for (int kb = 0; kb < C::NKB; ++kb)
-          bulk_g2s(sA + kb * kBM * C::RB, a_img + kb * a_region + qt * (int64_t)kBM * C::RB,
-                   kBM * C::RB, a_full);
+        mbar_arrive_expect_tx(a_full, QT * C::A_ONE);
+        for (int s = 0; s < QT; ++s) {
+          const int64_t qtl = qg * QT + s;  // local query tile (A image rows qtl*128..)
+          uint8_t* dstA = sA + s * C::A_STRIDE;
+          for (int kb = 0; kb < C::NKB; ++kb)
+            bulk_g2s(dstA + kb * kBM * C::RB, a_img + kb * a_region + qtl * (int64_t)kBM * C::RB,
+                     kBM * C::RB, a_full);
+          bulk_g2s(dstA + C::A_EXTRA, a_img + a_extra + qtl * (int64_t)kBM * kExtraRB,
+                   kBM * kExtraRB, a_full);
+        }
         for (int64_t t = t_lo; t < t_hi; ++t) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::B_BYTES);
-          uint8_t* dst = sB + stage * C::B_BYTES;
+          uint8_t* dst = sB + stage * C::B_STRIDE;
           for (int kb = 0; kb < C::NKB; ++kb)
             bulk_g2s(dst + kb * C::BN * C::RB, b_img + kb * b_region + t * (int64_t)C::BN * C::RB,
                      C::BN * C::RB, &full[stage]);
-          if (++stage == C::NSTAGE) {
+          bulk_g2s(dst + C::B_EXTRA, b_img + b_extra + t * (int64_t)C::BN * kExtraRB,
+                   C::BN * kExtraRB, &full[stage]);
+          if (++stage == nstage) {
             stage = 0;
             phase ^= 1;
-          }
-          mbar_wait(&n_empty[ns], nphase ^ 1);
-          mbar_arrive_expect_tx(&n_full[ns], C::BN * 4);
-          bulk_g2s(sN + ns * C::BN, b_nrm + t * C::BN, C::BN * 4, &n_full[ns]);
-          if (++ns == kNormSlots) {
-            ns = 0;
-            nphase ^= 1;
           }
         }
       }
@@ -184,38 +228,46 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
-      uint32_t aphase_acc = 0;
+      uint32_t acc_phase = 0;
       uint32_t aphase = 0;
       for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const int c = (int)(item % S);
+        const int c = (int)(item / n_groups);
         const int64_t t_lo = b_tiles * c / S, t_hi = b_tiles * (c + 1) / S;
         mbar_wait(a_full, aphase);
         aphase ^= 1;
         tc_fence_after();
         for (int64_t t = t_lo; t < t_hi; ++t) {
-          mbar_wait(&t_empty[acc], aphase_acc ^ 1);
-          tc_fence_after();
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t d_tmem = tmem_base + acc * C::BN;
-          const uint32_t bst = b_base + stage * C::B_BYTES;
+          const uint32_t bst = b_base + stage * C::B_STRIDE;
 #pragma unroll
-          for (int ks = 0; ks < C::KSTEPS; ++ks) {
-            const int kb = (ks * 32) / C::RB;
-            const int koff = (ks * 32) % C::RB;
-            const uint64_t ad = smem_desc(a_base + kb * kBM * C::RB + koff, C::SBO, C::LAYOUT);
-            const uint64_t bd = smem_desc(bst + kb * C::BN * C::RB + koff, C::SBO, C::LAYOUT);
-            tc_mma_f16(d_tmem, ad, bd, IDESC, ks > 0 ? 1u : 0u);
+          for (int s = 0; s < QT; ++s) {
+            const int ai = acc * QT + s;
+            mbar_wait(&t_empty[ai], acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + ai * C::BN;
+            const uint32_t ast = a_base + s * C::A_STRIDE;
+#pragma unroll
+            for (int ks = 0; ks < C::KSTEPS; ++ks) {
+              const int kb = (ks * 32) / C::RB;
+              const int koff = (ks * 32) % C::RB;
+              const uint64_t ad = smem_desc(ast + kb * kBM * C::RB + koff, C::SBO, C::LAYOUT);
+              const uint64_t bd = smem_desc(bst + kb * C::BN * C::RB + koff, C::SBO, C::LAYOUT);
+              tc_mma_f16(d_tmem, ad, bd, IDESC, ks > 0 ? 1u : 0u);
+            }
+            // extra K block: ||xhat_j||^2 pieces x constants (SW32, 8-row atoms of 256 B)
+            tc_mma_f16(d_tmem, smem_desc(ast + C::A_EXTRA, 8 * kExtraRB, 6),
+                       smem_desc(bst + C::B_EXTRA, 8 * kExtraRB, 6), IDESC, 1u);
+            tc_commit(&t_full[ai]);
           }
           tc_commit(&empty[stage]);
-          tc_commit(&t_full[acc]);
-          if (++stage == C::NSTAGE) {
+          if (++stage == nstage) {
             stage = 0;
             phase ^= 1;
           }
           if (++acc == 2) {
             acc = 0;
-            aphase_acc ^= 1;
+            acc_phase ^= 1;
           }
         }
         tc_commit(a_empty);
@@ -223,73 +275,119 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ---------------------------------------------------------------- epilogue
+    const int ew = warp - 2;          // epilogue warp index
+    const int half = ew / 4;          // column half of each tile (SPLIT = 2)
     const int q = warp & 3;           // TMEM lane quarter this warp may access
     const int t = q * 32 + lane;      // row within the query tile
-    RowTopK<kBM> L;
-    L.init(sLv, sLi, t, kp);
+    const int li = half * kBM + t;    // list slot (row, half)
+    List L;
+    L.init(sL, li, kp);
     int acc = 0;
-    uint32_t aphase_acc = 0;
-    int ns = 0;
-    uint32_t nphase = 0;
+    uint32_t acc_phase = 0;
+    constexpr int NCH = C::BH / 32;   // 32-column chunks per warp per tile (even)
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int64_t qt = qt0 + item / S;
-      const int c = (int)(item % S);
+      const int64_t qg = item % n_groups;
+      const int c = (int)(item / n_groups);  // reference chunk (chunk-major order)
       const int64_t t_lo = b_tiles * c / S, t_hi = b_tiles * (c + 1) / S;
-      const int64_t row = qt * kBM + t;
+      const int64_t qtl = qg;                // local query tile
+      const int64_t row = (qt0 + qtl) * kBM + t;
       const int self = self_join ? (int)row : -1;
+      // state layout: [query tile][half][slot][row]
+      const int64_t st_base = ((qtl * SPLIT + half) * (int64_t)kp) * kBM + t;
+      if (c > 0) {
+        // Resume this (row, half)'s top-K'' after chunk c-1 (state parked in HBM).
+        if (threadIdx.x == 64) {
+          while (ld_acquire_gpu(st_done + qg) < c) __nanosleep(256);
+        }
+        named_bar(1, 32 * C::EPI_WARPS);
+        int fill = 0;
+        for (int e = 0; e < kp; ++e) {
+          const uint2 kv = __ldcg(st_list + st_base + e * kBM);
+          sts_kv(L.base + e * List::S, __uint_as_float(kv.x), (int)kv.y);
+          fill += (int)kv.y >= 0;
+        }
+        L.fill = fill;
+        L.thr = fill == kp ? lds_kv(L.base + (kp - 1) * List::S).x : CUDART_INF_F;
+      }
       for (int64_t tt = t_lo; tt < t_hi; ++tt) {
-        mbar_wait(&t_full[acc], aphase_acc);
+        mbar_wait(&t_full[acc], acc_phase);
         tc_fence_after();
-        mbar_wait(&n_full[ns], nphase);
-        const float* nrm = sN + ns * C::BN;
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::BN;
-        const int j0 = (int)(tt * C::BN);
+        const uint32_t taddr =
+            tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::BN + half * C::BH;
+        const int j0 = (int)(tt * C::BN) + half * C::BH;
+        if (!(dbg & 1)) {
+          // Masking is needed only on the last (padded) tile and on tiles that
+          // contain some lane's own column: warp-uniform decision per tile.
+          const bool diag = self_join && (self >= j0) && (self < j0 + C::BH);
+          const bool masked = __any_sync(0xffffffffu, diag) || (j0 + C::BH > n_ref);
+          // Group-min pass (every tile): for each 8-column group, a 3-input
+          // min tree; a group whose minimum is below thr is appended to the
+          // row's list as (min, group index) with predicated stores -- no
+          // branches on the data.  The re-rank expands a kept group to its
+          // 8 columns.
+          const int gbase = j0 >> 3;
+          auto groups = [&](const float(&v)[32], int ch) {
+            float m[4];
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              const float* vg = v + 8 * g;
+              m[g] = fminf(fminf(fminf(vg[0], vg[1]), vg[2]),
+                           fminf(fminf(vg[3], vg[4]), fminf(fminf(vg[5], vg[6]), vg[7])));
+            }
+            const float th = L.thr;
+            L.reserve(4);
+#pragma unroll
+            for (int g = 0; g < 4; ++g) L.append_if(m[g] < th, m[g], gbase + ch * 4 + g);
+          };
+          if (!masked) {
+            float va[32], vb[32];
+            tmem_ld32(taddr, va);
+#pragma unroll
+            for (int ch = 0; ch < NCH; ch += 2) {
+              tmem_ld_wait();
+              tmem_ld32(taddr + (ch + 1) * 32, vb);
+              groups(va, ch);
+              tmem_ld_wait();
+              if (ch + 2 < NCH) tmem_ld32(taddr + (ch + 2) * 32, va);
+              groups(vb, ch + 1);
+            }
+          } else {
 #pragma unroll 1
-        for (int ch = 0; ch < C::BN / 32; ++ch) {
-          float v[32];
-          tmem_ld32(taddr + ch * 32, v);
-          tmem_ld_wait();
-          const float4* n4 = reinterpret_cast<const float4*>(nrm + ch * 32);
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            const float4 na = n4[2 * g], nb = n4[2 * g + 1];
-            float w[8];
-            w[0] = fmaf(-2.f, v[8 * g + 0], na.x);
-            w[1] = fmaf(-2.f, v[8 * g + 1], na.y);
-            w[2] = fmaf(-2.f, v[8 * g + 2], na.z);
-            w[3] = fmaf(-2.f, v[8 * g + 3], na.w);
-            w[4] = fmaf(-2.f, v[8 * g + 4], nb.x);
-            w[5] = fmaf(-2.f, v[8 * g + 5], nb.y);
-            w[6] = fmaf(-2.f, v[8 * g + 6], nb.z);
-            w[7] = fmaf(-2.f, v[8 * g + 7], nb.w);
-            const float m = fminf(fminf(fminf(w[0], w[1]), fminf(w[2], w[3])),
-                                  fminf(fminf(w[4], w[5]), fminf(w[6], w[7])));
-            if (__any_sync(0xffffffffu, m < L.thr)) {
-              const int jb = j0 + ch * 32 + 8 * g;
-#pragma unroll
-              for (int e = 0; e < 8; ++e) L.offer(w[e], jb + e, self);
+            for (int ch = 0; ch < NCH; ++ch) {
+              float v[32];
+              tmem_ld32(taddr + ch * 32, v);
+              tmem_ld_wait();
+              mask_cols(v, j0 + ch * 32, self, n_ref);
+              groups(v, ch);
             }
           }
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&t_empty[acc]);
-          mbar_arrive(&n_empty[ns]);
-        }
+        if (lane == 0) mbar_arrive(&t_empty[acc]);
         if (++acc == 2) {
           acc = 0;
-          aphase_acc ^= 1;
-        }
-        if (++ns == kNormSlots) {
-          ns = 0;
-          nphase ^= 1;
+          acc_phase ^= 1;
         }
       }
-      const bool write = row >= q_begin && row < q_end;
-      const int64_t r = row - q_begin;
-      const float v = L.finish(cand_idx + (write ? (r * S + c) * kp : 0), write);
-      if (write) cand_v[r * S + c] = v;
+      if (c < S - 1) {
+        // Park this list's state for chunk c+1 (coalesced [slot][row] layout).
+        if (__any_sync(0xffffffffu, L.pa != L.base + kp * List::S)) L.merge();
+        for (int e = 0; e < kp; ++e) {
+          const float2 kv = e < L.fill ? lds_kv(L.base + e * List::S)
+                                       : make_float2(CUDART_INF_F, __int_as_float(-1));
+          st_list[st_base + e * kBM] =
+              make_uint2(__float_as_uint(kv.x), (unsigned)__float_as_int(kv.y));
+        }
+        __threadfence();
+        named_bar(1, 32 * C::EPI_WARPS);
+        if (threadIdx.x == 64) st_release_gpu(st_done + qg, c + 1);
+      } else {
+        const bool write = row >= q_begin && row < q_end;
+        const int64_t r = row - q_begin;
+        const float v = L.finish(cand_idx + (write ? (r * SPLIT + half) * kp : 0), write);
+        if (write) cand_v[r * SPLIT + half] = v;
+      }
       L.reset();
     }
   }
@@ -301,13 +399,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int DPAD, int FMT>
+template <int DPAD, int FMT, int SPLIT>
 cudaError_t launch_t(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                      bool self_join, Cands c, int num_sms, cudaStream_t st) {
-  using C = TcCfg<DPAD>;
-  int ob, on, olv, oli, obar;
-  const int smem = smem_layout_bytes<DPAD>(c.kp, &ob, &on, &olv, &oli, &obar);
-  auto kern = k_knn_tc<DPAD, FMT>;
+  using C = TcCfg<DPAD, SPLIT>;
+  const int nstage = pick_stages<DPAD, SPLIT>(c.kp);
+  if (nstage == 0) return cudaErrorInvalidValue;
+  int ob, ol, obar;
+  const int smem = smem_layout_bytes<DPAD, SPLIT>(c.kp, nstage, &ob, &ol, &obar);
+  auto kern = k_knn_tc<DPAD, FMT, SPLIT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t qt0 = q_begin / kBM;
@@ -315,27 +415,34 @@ cudaError_t launch_t(const Image& A, const Image& B, int64_t q_begin, int64_t q_
   const int64_t n_items = (qt1 - qt0) * c.S;
   const int grid = (int)std::min<int64_t>(num_sms, n_items);
   if (grid <= 0) return cudaSuccess;
-  kern<<<grid, kThreads, smem, st>>>(
-      reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(),
-      reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.nrm32, B.n_pad / C::BN, qt0,
-      qt1 - qt0, q_begin, q_begin + q_count, self_join ? 1 : 0, c.S, c.kp, c.idx, c.v);
+  if (c.S > 1 && (!c.st_list || !c.st_done)) return cudaErrorInvalidValue;
+  if (c.lists != SPLIT) return cudaErrorInvalidValue;
+  kern<<<grid, C::THREADS, smem, st>>>(
+      reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(), A.extra_offset(),
+      reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
+      B.n_pad / C::BN, B.n, qt0, qt1 - qt0, q_begin, q_begin + q_count, self_join ? 1 : 0, c.S,
+      c.kp, nstage, c.dbg, c.idx, c.v, c.st_list, c.st_done);
   return cudaGetLastError();
+}
+
+template <int DPAD, int FMT>
+cudaError_t launch_d(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
+                     bool self_join, Cands c, int num_sms, cudaStream_t st) {
+  if (c.lists == 2) return launch_t<DPAD, FMT, 2>(A, B, q_begin, q_count, self_join, c, num_sms, st);
+  return launch_t<DPAD, FMT, 1>(A, B, q_begin, q_count, self_join, c, num_sms, st);
 }
 
 }  // namespace
 
-int tc_smem_bytes(int dpad, int kp) {
-  int a, b, c, d, e;
+int tc_split_fits(int dpad, int kp) {
   switch (dpad) {
-    case 16: return smem_layout_bytes<16>(kp, &a, &b, &c, &d, &e);
-    case 32: return smem_layout_bytes<32>(kp, &a, &b, &c, &d, &e);
-    case 64: return smem_layout_bytes<64>(kp, &a, &b, &c, &d, &e);
-    case 128: return smem_layout_bytes<128>(kp, &a, &b, &c, &d, &e);
+    case 16: return pick_stages<16, 2>(kp) > 0;
+    case 32: return pick_stages<32, 2>(kp) > 0;
+    case 64: return pick_stages<64, 2>(kp) > 0;
+    case 128: return pick_stages<128, 2>(kp) > 0;
   }
-  return -1;
+  return 0;
 }
-
-int tc_block_n(int dpad) { return dpad <= 64 ? 256 : 128; }
 
 cudaError_t launch_knn_tc(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                           bool self_join, int fmt, Cands c, int num_sms, cudaStream_t st,
@@ -343,8 +450,8 @@ cudaError_t launch_knn_tc(const Image& A, const Image& B, int64_t q_begin, int64
   *launches += 1;
 #define TOD_TC_CASE(D)                                                                      \
   case D:                                                                                  \
-    return fmt == 1 ? launch_t<D, 1>(A, B, q_begin, q_count, self_join, c, num_sms, st)    \
-                    : launch_t<D, 2>(A, B, q_begin, q_count, self_join, c, num_sms, st);
+    return fmt == 1 ? launch_d<D, 1>(A, B, q_begin, q_count, self_join, c, num_sms, st)    \
+                    : launch_d<D, 2>(A, B, q_begin, q_count, self_join, c, num_sms, st);
   switch (A.dpad) {
     TOD_TC_CASE(16)
     TOD_TC_CASE(32)

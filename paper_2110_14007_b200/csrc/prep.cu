@@ -98,16 +98,19 @@ __global__ void k_absmax(const float* __restrict__ X, int64_t n, int d,
   if (lane == 0) atomic_max_nonneg(&g->absmax_bits, m);
 }
 
-// s = 2^e with max|s*(x-mu)| in [2^14, 2^15) for fp16 (fp16 max finite 65504,
-// so no operand can overflow and products/sums stay far inside fp32 range).
-// bf16 shares fp32's exponent range: s = 1.
-__global__ void k_scale(PrepGlobals* g, int fmt) {
+// s = 2^e with max|s*(x-mu)| in [2^(E-1), 2^E), E = floor((30 - log2 dpad)/2),
+// so every ||xhat||^2 <= dpad * 2^(2E) <= 2^30: the fp16 norm pieces below stay
+// in range (fp16 max 65504) and all fp32 accumulations stay far from overflow.
+__global__ void k_scale(PrepGlobals* g, int fmt, int dpad) {
   const double amax = __longlong_as_double((long long)g->absmax_bits);
+  int lg = 0;
+  while ((1 << lg) < dpad) ++lg;
+  const int E = (30 - lg) / 2;
   double s = 1.0;
-  if (fmt == 1 && amax > 0.0) {
+  if (amax > 0.0) {
     int ex;
     frexp(amax, &ex);  // amax in [2^(ex-1), 2^ex)
-    s = ldexp(1.0, 15 - ex);
+    s = ldexp(1.0, E - ex);
   }
   g->s = s;
 }
@@ -123,16 +126,30 @@ __device__ __forceinline__ double widen16(uint16_t h) {
   return (double)__bfloat162float(__ushort_as_bfloat16(h));
 }
 
-// One warp per row (rows [0, n_pad)); padding rows get zeros and nrm32 = +inf.
+// Power-of-two constants c_q of the norm pieces (query side of the extra K
+// block).  fp16 (11-bit significand): 3 pieces, 2^15, 2^4, 2^-7; bf16 (8-bit):
+// 4 pieces, 2^22, 2^14, 2^6, 2^-2.  sum_q c_q p_jq reproduces ||xhat_j||^2
+// <= 2^30 to ~2^-33 (fp16) / 2^-32 (bf16) relative; the exact residual is
+// measured per row (repmax) and enters the certificate.
+template <int FMT>
+struct Pieces {
+  static constexpr int NP = FMT == 1 ? 3 : 4;
+  __device__ static double c(int q) {
+    return FMT == 1 ? ldexp(1.0, 15 - 11 * q) : ldexp(1.0, 22 - 8 * q);
+  }
+};
+
+// One warp per row (rows [0, n_pad)).  side 0 = reference image B:
+// [xhat | norm pieces]; side 1 = query image A: [-2 xhat | constants].
+// Padding rows are zero (the epilogue masks padding columns).
 template <int FMT>
 __global__ void k_quant(const float* __restrict__ X, int64_t n, int d,
-                        const double* __restrict__ mu, const PrepGlobals* __restrict__ g,
-                        PrepGlobals* gmax, Image img, int update_max) {
+                        const double* __restrict__ mu, PrepGlobals* g, Image img, int side) {
   const int lane = threadIdx.x & 31;
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (r >= img.n_pad) return;
   const double s = g->s;
-  const int epr = img.rb / 2;  // elements per row per region
+  const int epr = img.rb / 2;  // elements per row per main region
   const unsigned M = img.layout == 2 ? 7u : (img.layout == 4 ? 3u : 1u);
   uint8_t* base = reinterpret_cast<uint8_t*>(img.data);
   double a2 = 0.0, r2 = 0.0, tt = 0.0;
@@ -147,11 +164,16 @@ __global__ void k_quant(const float* __restrict__ X, int64_t n, int d,
     a2 += q0 * q0 + q1 * q1;
     r2 += (q0 - t0) * (q0 - t0) + (q1 - t1) * (q1 - t1);
     tt += t0 * t0 + t1 * t1;
+    uint16_t w0 = h0, w1 = h1;
+    if (side == 1) {  // -2 xhat: exact (power-of-two scaling, no overflow by k_scale)
+      w0 = rn16<FMT>(-2.0 * q0);
+      w1 = rn16<FMT>(-2.0 * q1);
+    }
     const int kb = c0 / epr;
     const uint64_t o = (uint64_t)r * img.rb + (uint64_t)(c0 % epr) * 2u;
     const uint64_t phys = o ^ (((o >> 7) & M) << 4);
     *reinterpret_cast<uint32_t*>(base + (size_t)kb * img.region_bytes() + phys) =
-        (uint32_t)h0 | ((uint32_t)h1 << 16);
+        (uint32_t)w0 | ((uint32_t)w1 << 16);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -159,24 +181,57 @@ __global__ void k_quant(const float* __restrict__ X, int64_t n, int d,
     r2 += __shfl_xor_sync(0xffffffffu, r2, o);
     tt += __shfl_xor_sync(0xffffffffu, tt, o);
   }
-  if (lane == 0) {
-    if (!real) {
-      img.nrm32[r] = CUDART_INF_F;
-      return;
+  if (lane != 0) return;
+  // extra K block (16 elements, 32-byte rows, SW32 swizzle: bit 4 ^= bit 7)
+  uint16_t ex[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) ex[q] = 0;
+  double rep = 0.0;
+  if (side == 1) {
+#pragma unroll
+    for (int q = 0; q < Pieces<FMT>::NP; ++q) ex[q] = rn16<FMT>(Pieces<FMT>::c(q));
+  } else if (real) {
+    double rres = a2;
+#pragma unroll
+    for (int q = 0; q < Pieces<FMT>::NP; ++q) {
+      const double cq = Pieces<FMT>::c(q);
+      ex[q] = rn16<FMT>(rres / cq);
+      rres = rres - cq * widen16<FMT>(ex[q]);  // exact: cq is a power of two
     }
-    img.nrm32[r] = __double2float_rn(a2);
-    img.a2[r] = a2;
-    // e >= ||xhat - t|| + ||t - s(x - mu)||: fp64 rounding of the residual sum
-    // (relative <= (d+4) 2^-53, doubled) plus the rounding of fl64(x - mu)
-    // (<= 2^-53 |x - mu| per element, doubled), then a final 2^-50 margin.
-    const double eps = 1.1102230246251565e-16;  // 2^-53
-    const double e = (sqrt(r2) * (1.0 + 2.0 * (d + 4) * eps) + 2.0 * eps * sqrt(tt) * (1.0 + 1e-6)) *
-                     (1.0 + 8.0 * eps);
-    img.e[r] = e;
-    if (update_max) {
-      atomic_max_nonneg(reinterpret_cast<unsigned long long*>(&gmax->amax2), a2);
-      atomic_max_nonneg(reinterpret_cast<unsigned long long*>(&gmax->emax), e);
-    }
+    // |rres| is the representation error w.r.t. the fp64 a2; a2 itself is
+    // within (d+2) 2^-53 a2 of the exact ||xhat||^2.
+    rep = fabs(rres) * (1.0 + 1e-6) + (double)(d + 4) * 2.220446049250313e-16 * a2;
+  }
+  {
+    const uint64_t o0 = (uint64_t)r * 32u;
+    uint8_t* eb = base + img.extra_offset();
+    uint4 lo, hi;
+    lo.x = ex[0] | ((uint32_t)ex[1] << 16);
+    lo.y = ex[2] | ((uint32_t)ex[3] << 16);
+    lo.z = ex[4] | ((uint32_t)ex[5] << 16);
+    lo.w = ex[6] | ((uint32_t)ex[7] << 16);
+    hi.x = ex[8] | ((uint32_t)ex[9] << 16);
+    hi.y = ex[10] | ((uint32_t)ex[11] << 16);
+    hi.z = ex[12] | ((uint32_t)ex[13] << 16);
+    hi.w = ex[14] | ((uint32_t)ex[15] << 16);
+    const uint64_t p0 = o0 ^ (((o0 >> 7) & 1u) << 4);
+    const uint64_t p1 = (o0 + 16) ^ ((((o0 + 16) >> 7) & 1u) << 4);
+    *reinterpret_cast<uint4*>(eb + p0) = lo;
+    *reinterpret_cast<uint4*>(eb + p1) = hi;
+  }
+  if (!real) return;
+  img.a2[r] = a2;
+  // e >= ||xhat - t|| + ||t - s(x - mu)||: fp64 rounding of the residual sum
+  // (relative <= (d+4) 2^-53, doubled) plus the rounding of fl64(x - mu)
+  // (<= 2^-53 |x - mu| per element, doubled), then a final margin.
+  const double eps = 1.1102230246251565e-16;  // 2^-53
+  const double e = (sqrt(r2) * (1.0 + 2.0 * (d + 4) * eps) + 2.0 * eps * sqrt(tt) * (1.0 + 1e-6)) *
+                   (1.0 + 8.0 * eps);
+  img.e[r] = e;
+  if (side == 0) {
+    atomic_max_nonneg(reinterpret_cast<unsigned long long*>(&g->amax2), a2);
+    atomic_max_nonneg(reinterpret_cast<unsigned long long*>(&g->emax), e);
+    atomic_max_nonneg(reinterpret_cast<unsigned long long*>(&g->repmax), rep);
   }
 }
 
@@ -212,21 +267,20 @@ cudaError_t launch_prep_absmax(const float* X, int64_t n, int d, const double* m
   return cudaGetLastError();
 }
 
-cudaError_t launch_prep_scale(PrepGlobals* g, int fmt, cudaStream_t st, int* launches) {
-  k_scale<<<1, 1, 0, st>>>(g, fmt);
+cudaError_t launch_prep_scale(PrepGlobals* g, int fmt, int dpad, cudaStream_t st, int* launches) {
+  k_scale<<<1, 1, 0, st>>>(g, fmt, dpad);
   *launches += 1;
   return cudaGetLastError();
 }
 
-cudaError_t launch_prep_quant(const float* X, int64_t n, int d, const double* mu,
-                              const PrepGlobals* g, PrepGlobals* gmax, int fmt, Image img,
-                              bool update_max, cudaStream_t st, int* launches) {
+cudaError_t launch_prep_quant(const float* X, int64_t n, int d, const double* mu, PrepGlobals* g,
+                              int fmt, Image img, int side, cudaStream_t st, int* launches) {
   const int64_t threads = img.n_pad * 32;
   const int blocks = (int)((threads + 255) / 256);
   if (fmt == 1)
-    k_quant<1><<<blocks, 256, 0, st>>>(X, n, d, mu, g, gmax, img, update_max ? 1 : 0);
+    k_quant<1><<<blocks, 256, 0, st>>>(X, n, d, mu, g, img, side);
   else
-    k_quant<2><<<blocks, 256, 0, st>>>(X, n, d, mu, g, gmax, img, update_max ? 1 : 0);
+    k_quant<2><<<blocks, 256, 0, st>>>(X, n, d, mu, g, img, side);
   *launches += 1;
   return cudaGetLastError();
 }

@@ -2,7 +2,7 @@
 // "verification", §5.2) and K4 fallback ("recalculate ...
 // only on the subset of X where the verification fails").
 //
-// K3, one warp per query row: the K' (x S chunks) candidates of pass 1 are
+// K3, one warp per query row: the K' (x lists) candidates of pass 1 are
 // re-ranked with the EXACT fp64 distance of the oracle's definition
 // (O1: sequential sum over c of fl64(x_ic - x_jc)^2, explicit
 // __dsub_rn/__dmul_rn/__dadd_rn so nvcc cannot contract to FMA), sorted by
@@ -25,7 +25,7 @@ namespace tod {
 namespace {
 
 constexpr int kRerankWarps = 8;
-constexpr int kMaxCands = 256;   // S * K' per row
+constexpr int kMaxCands = 256;   // lists * K' per row
 constexpr int kMaxK = 128;
 
 // O1, bit-identical to the oracle (no FMA, ascending c, from +0.0).
@@ -68,6 +68,59 @@ __device__ void write_row(const KnnOutDev& out, int64_t r, int k, const double* 
       out.score_mean[r] = __double2float_rn(__ddiv_rn(acc, (double)k));
     }
   }
+}
+
+// The certificate: true iff every reference the
+// pass did not keep has exact squared distance > dk (the k-th re-ranked D64),
+// so the oracle's top-k lies inside the kept set.  `vmin` is the threshold
+// below which pass 1 kept everything it was offered.  *err receives the
+// pass-1 error term used (diagnostics).
+__device__ bool row_certified(const CertParams& cp, int64_t r, float vmin, double dk, double* err) {
+  const double u53 = 1.1102230246251565e-16;
+  const double vv = (double)vmin;
+  bool cert = false;
+  if (vmin == CUDART_INF_F) return true;  // every reference was offered and kept
+  if (cp.kind == PASS_TC) {
+    // Tensor-core pass (fp16/bf16 operands, fp32 accumulation; the norm
+    // ||xhat_j||^2 enters as pieces p_jq times constants c_q in an extra K
+    // block).  With w_ij = ||xhat_j||^2 - 2 xhat_i.xhat_j exact: every product
+    // is exact in fp32, so
+    //   |w~_ij - w_ij| <= gamma_m(u) sum_k |A_ik B_jk| + rep_j
+    //                  <= gamma (2 a_i a_max + 1.002 amax2) + repmax  =: E_i
+    // (Cauchy-Schwarz on the dot part; sum_q |c_q p_jq| <= 1.002 ||xhat_j||^2).
+    // A9: accumulation modelled order-free with m = 2 (dpad + 16), u = 2^-22.
+    // Non-kept j have w~_ij >= v, so ||xhat_i - xhat_j||^2 >= a_i^2 + v - E_i;
+    // the residuals e_i, e_j <= emax then bound the exact distance.
+    const double a2i = cp.qa2[r];
+    const double ei = cp.qe[r];
+    const double amax2 = cp.g->amax2;
+    const double emax = cp.g->emax;
+    const double rep = cp.g->repmax;
+    const double ai = sqrt(a2i) * (1.0 + 4 * u53);
+    const double am = sqrt(amax2) * (1.0 + 4 * u53);
+    const double gam = gamma_up(2.0 * (cp.dpad + 16), 2.384185791015625e-07 /*2^-22*/);
+    const double E = (gam * (2.0 * ai * am + 1.002 * amax2) + rep) * (1.0 + 1e-6) + 1e-300;
+    const double slack = (cp.d + 8) * 2.0 * u53 * (fabs(a2i) + fabs(vv) + E);
+    const double R2 = a2i + vv - E - slack;
+    *err = E + slack;
+    if (R2 > 0.0) {
+      const double Rh = sqrt(R2) * (1.0 - 2.0 * u53);
+      const double LB = (Rh - ei - emax) * (1.0 - 8.0 * u53);
+      if (LB > 0.0) {
+        const double lbo = LB / cp.g->s;  // s = 2^e: exact
+        const double lb2 = lbo * lbo * (1.0 - 8.0 * u53);
+        cert = dk < lb2 * (1.0 - gamma_up(cp.d + 2, u53));
+      }
+    }
+  } else {
+    // fp32 difference-form pass: D~ <= D (1 + gamma_{d+2}(2^-24)) + tiny.
+    const double g32 = gamma_up(cp.d + 2, 5.9604644775390625e-08);
+    const double lb2 =
+        (vv - (cp.d + 2) * 1.1754943508222875e-38 /*2^-126*/) / (1.0 + g32) * (1.0 - 8.0 * u53);
+    *err = vv * g32;
+    if (lb2 > 0.0) cert = dk < lb2 * (1.0 - gamma_up(cp.d + 2, u53));
+  }
+  return cert;
 }
 
 __global__ void __launch_bounds__(kRerankWarps * 32)
@@ -117,52 +170,147 @@ __global__ void __launch_bounds__(kRerankWarps * 32)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nv_local += __shfl_xor_sync(0xffffffffu, nv_local, o);
   __syncwarp();
-  bool cert = false;
   double err = 0.0;
-  if (nv_local >= k) {
-    const double dk = s_sk[w][k - 1];
-    const double u53 = 1.1102230246251565e-16;
-    const double vv = (double)vmin;
-    if (vmin == CUDART_INF_F) {
-      cert = true;  // every reference was offered and kept: nothing outside
-    } else if (cp.kind == PASS_TC) {
-      // Tensor-core pass (fp16/bf16 operands, fp32 accumulation), DESIGN.md
-      // "Certificate": |w~_ij - w_ij| <= E_i for every reference j, with
-      // w_ij = ||xhat_j||^2 - 2 xhat_i.xhat_j exact, so non-kept j satisfy
-      // ||xhat_i - xhat_j||^2 >= a_i^2 + v - E_i, then the triangle inequality
-      // through the residuals e_i, e_j <= emax.
-      const double a2i = cp.qa2[r];
-      const double ei = cp.qe[r];
-      const double amax2 = cp.g->amax2;
-      const double emax = cp.g->emax;
-      const double ai = sqrt(a2i) * (1.0 + 4 * u53);
-      const double am = sqrt(amax2) * (1.0 + 4 * u53);
-      const double gam = gamma_up(2.0 * cp.dpad, 2.384185791015625e-07 /*2^-22*/);
-      const double E = (1.1920928955078125e-07 /*2^-23*/ * amax2 + 2.0 * gam * ai * am +
-                        5.9604644775390625e-08 /*2^-24*/ * (amax2 + 2.0 * ai * am)) *
-                           (1.0 + 9.5367431640625e-07 /*2^-20*/) +
-                       1e-300;
-      const double slack = (cp.d + 8) * 2.0 * u53 * (fabs(a2i) + fabs(vv) + E);
-      const double R2 = a2i + vv - E - slack;
-      err = E + slack;
-      if (R2 > 0.0) {
-        const double Rh = sqrt(R2) * (1.0 - 2.0 * u53);
-        const double LB = (Rh - ei - emax) * (1.0 - 8.0 * u53);
-        if (LB > 0.0) {
-          const double lbo = LB / cp.g->s;  // s = 2^e: exact
-          const double lb2 = lbo * lbo * (1.0 - 8.0 * u53);
-          cert = dk < lb2 * (1.0 - gamma_up(cp.d + 2, u53));
+  bool cert = nv_local >= k && row_certified(cp, r, vmin, s_sk[w][k - 1], &err);
+  if (cp.force_fail) cert = false;
+  if (lane == 0 && err > 0.0)
+    atomicMax(max_err_bits, (unsigned long long)__double_as_longlong(err));
+  if (cert) {
+    write_row(out, r, k, s_sk[w], s_si[w], lane, 32);
+  } else if (lane == 0) {
+    const int slot = atomicAdd(fail_count, 1);
+    fail_rows[slot] = (int32_t)r;
+  }
+}
+
+
+// ------------------------------------------------------- group candidates
+// Tensor-core pass candidates are 8-column groups (list entries hold the
+// group index g = column / 8 and the group's minimum w).  Every column of every
+// kept group is re-ranked; columns outside kept groups have w~ >= v (their
+// group's minimum is >= v), so the same certificate applies.
+constexpr int kGrpWarps = 4;
+constexpr int kGrpCPL = 20;                 // candidate columns per lane
+constexpr int kGrpMaxCols = 32 * kGrpCPL;   // 640 = lists * K'' * 8 max
+
+// Dynamic smem per warp: 4 groups x 8 rows x (d+1) floats (row stride d+1
+// words: lanes reading the same c of different rows hit distinct banks).
+__global__ void __launch_bounds__(kGrpWarps * 32)
+    k_rerank_groups(const float* __restrict__ Q, int64_t q_begin, int64_t q_count,
+                    const float* __restrict__ X, int64_t n, int d, int k, int self_join,
+                    const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_v,
+                    int kp, int lists, CertParams cp, KnnOutDev out,
+                    int32_t* __restrict__ fail_rows, int32_t* __restrict__ fail_count,
+                    unsigned long long* __restrict__ max_err_bits) {
+  extern __shared__ float s_rows[];
+  __shared__ double s_sk[kGrpWarps][kMaxK];
+  __shared__ int s_si[kGrpWarps][kMaxK];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * kGrpWarps + w;
+  if (r >= q_count) return;
+  const int ld = d + 1;
+  float* rows = s_rows + (size_t)w * 32 * ld;   // 32 candidate rows of this warp
+  double* xq = reinterpret_cast<double*>(s_rows + (size_t)kGrpWarps * 32 * ld) + (size_t)w * d;
+  const int64_t gi = q_begin + r;
+  const float* xi = self_join ? X + gi * d : Q + r * d;
+  for (int c = lane; c < d; c += 32) xq[c] = (double)xi[c];
+  __syncwarp();
+  const int G = lists * kp;       // group slots
+  double key[kGrpCPL];
+  int id[kGrpCPL];
+  int nv = 0;
+#pragma unroll
+  for (int s = 0; s < kGrpCPL; ++s) {
+    key[s] = CUDART_INF;
+    id[s] = INT32_MAX;
+    if (s * 4 < G) {  // warp-uniform: 4 groups (32 columns) per step
+      // lane -> (group slot 4s + lane/8, column lane%8)
+      const int gslot = s * 4 + (lane >> 3);
+      const int g = gslot < G ? cand_idx[r * G + gslot] : -1;
+      // cooperative, coalesced staging of the 4 groups' 8 consecutive rows
+      // (8*d contiguous floats per group; float4 when d % 4 == 0)
+#pragma unroll 1
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const int gq = __shfl_sync(0xffffffffu, g, q4 * 8);
+        if (gq < 0) continue;
+        const int64_t j0 = (int64_t)gq * 8;
+        const int nrows = (int)(n - j0 < 8 ? n - j0 : 8);
+        const float* src = X + j0 * d;
+        float* dst = rows + q4 * 8 * ld;
+        if ((d & 3) == 0) {
+          const int d4 = d >> 2;
+          const float4* src4 = reinterpret_cast<const float4*>(src);
+          for (int e4 = lane; e4 < nrows * d4; e4 += 32) {
+            const int rr = e4 / d4, c4 = e4 - rr * d4;
+            const float4 vv = __ldg(src4 + e4);
+            float* o = dst + rr * ld + 4 * c4;
+            o[0] = vv.x;
+            o[1] = vv.y;
+            o[2] = vv.z;
+            o[3] = vv.w;
+          }
+        } else {
+          for (int e = lane; e < nrows * d; e += 32) {
+            const int rr = e / d, cc = e - rr * d;
+            dst[rr * ld + cc] = __ldg(src + e);
+          }
         }
       }
-    } else {
-      // fp32 difference-form pass: D~ <= D (1 + gamma_{d+2}(2^-24)) + tiny.
-      const double g32 = gamma_up(cp.d + 2, 5.9604644775390625e-08);
-      const double lb2 =
-          (vv - (cp.d + 2) * 1.1754943508222875e-38 /*2^-126*/) / (1.0 + g32) * (1.0 - 8.0 * u53);
-      err = vv * g32;
-      if (lb2 > 0.0) cert = dk < lb2 * (1.0 - gamma_up(cp.d + 2, u53));
+      __syncwarp();
+      const int64_t j = (int64_t)g * 8 + (lane & 7);
+      if (g >= 0 && j < n && !(self_join && j == gi)) {
+        // O1, bit-identical to the oracle (no FMA, ascending c, from +0.0).
+        const float* xj = rows + lane * ld;
+        double acc = 0.0;
+        for (int c = 0; c < d; ++c) {
+          const double t = __dsub_rn(xq[c], (double)xj[c]);
+          acc = __dadd_rn(acc, __dmul_rn(t, t));
+        }
+        key[s] = acc;
+        id[s] = (int)j;
+        ++nv;
+      }
+      __syncwarp();
     }
   }
+  float vmin = CUDART_INF_F;
+  for (int c = 0; c < lists; ++c) vmin = fminf(vmin, cand_v[r * lists + c]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nv += __shfl_xor_sync(0xffffffffu, nv, o);
+  // k rounds of warp-wide lexicographic argmin over (D64, index).
+  const int kk = nv < k ? nv : k;
+  for (int m = 0; m < kk; ++m) {
+    double bk = key[0];
+    int bi = id[0];
+#pragma unroll
+    for (int s = 1; s < kGrpCPL; ++s)
+      if (key_less(key[s], id[s], bk, bi)) {
+        bk = key[s];
+        bi = id[s];
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (key_less(ok, oi, bk, bi)) {
+        bk = ok;
+        bi = oi;
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < kGrpCPL; ++s)
+      if (id[s] == bi) {
+        key[s] = CUDART_INF;
+        id[s] = INT32_MAX;
+      }
+    if (lane == 0) {
+      s_sk[w][m] = bk;
+      s_si[w][m] = bi;
+    }
+  }
+  __syncwarp();
+  double err = 0.0;
+  bool cert = nv >= k && row_certified(cp, r, vmin, s_sk[w][k - 1], &err);
   if (cp.force_fail) cert = false;
   if (lane == 0 && err > 0.0)
     atomicMax(max_err_bits, (unsigned long long)__double_as_longlong(err));
@@ -175,42 +323,51 @@ __global__ void __launch_bounds__(kRerankWarps * 32)
 }
 
 // ---------------------------------------------------------------- fallback
+// Brute-force fp64 tier for rows the certificate could not prove ("recalculate
+// on the subset").  Phase 1: grid (P slices x failing rows); block
+// (p, f) scans the reference slice p for row f with the oracle's D64 formula,
+// per-thread sorted top-k, block k-way merge -> k partial results.  Phase 2:
+// one block per failing row merges the P sorted partial lists.  Spreading a
+// row over P SMs makes a handful of failures cost one pass over X, not one
+// SM's bandwidth.
 constexpr int kFbThreads = 256;
 
 template <int KMAX>
 __global__ void __launch_bounds__(kFbThreads)
-    k_fallback(const float* __restrict__ Q, int64_t q_begin, const float* __restrict__ X,
-               int64_t n, int d, int k, int self_join, const int32_t* __restrict__ fail_rows,
-               KnnOutDev out) {
+    k_fallback_part(const float* __restrict__ Q, int64_t q_begin, const float* __restrict__ X,
+                    int64_t n, int d, int k, int self_join, const int32_t* __restrict__ fail_rows,
+                    int P, double* __restrict__ part_key, int* __restrict__ part_id) {
   __shared__ double s_hk[kFbThreads / 32];
   __shared__ int s_hi[kFbThreads / 32];
   __shared__ int s_ht[kFbThreads / 32];
-  __shared__ double s_key[KMAX];
-  __shared__ int s_id[KMAX];
   __shared__ int s_win;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int64_t r = fail_rows[blockIdx.x];
+  const int p = blockIdx.x, f = blockIdx.y;
+  const int64_t r = fail_rows[f];
   const int64_t gi = q_begin + r;
   const float* xi = self_join ? X + gi * d : Q + r * d;
+  const int64_t j_lo = n * p / P, j_hi = n * (p + 1) / P;
   double lk[KMAX];
   int li[KMAX];
   int cnt = 0;
-  for (int64_t j = t; j < n; j += kFbThreads) {
+  for (int64_t j = j_lo + t; j < j_hi; j += kFbThreads) {
     if (self_join && j == gi) continue;
     const double key = d64_row(xi, X + j * d, d);
     const int jj = (int)j;
     if (cnt < k || key_less(key, jj, lk[cnt - 1], li[cnt - 1])) {
-      int p = cnt < k ? cnt : k - 1;
-      while (p > 0 && key_less(key, jj, lk[p - 1], li[p - 1])) {
-        lk[p] = lk[p - 1];
-        li[p] = li[p - 1];
-        --p;
+      int q = cnt < k ? cnt : k - 1;
+      while (q > 0 && key_less(key, jj, lk[q - 1], li[q - 1])) {
+        lk[q] = lk[q - 1];
+        li[q] = li[q - 1];
+        --q;
       }
-      lk[p] = key;
-      li[p] = jj;
+      lk[q] = key;
+      li[q] = jj;
       if (cnt < k) ++cnt;
     }
   }
+  double* ok_out = part_key + ((int64_t)f * P + p) * k;
+  int* oi_out = part_id + ((int64_t)f * P + p) * k;
   // Block k-way merge: k rounds of lexicographic argmin over list heads.
   int head = 0;
   for (int m = 0; m < k; ++m) {
@@ -238,6 +395,58 @@ __global__ void __launch_bounds__(kFbThreads)
       int b = 0;
       for (int q = 1; q < kFbThreads / 32; ++q)
         if (key_less(s_hk[q], s_hi[q], s_hk[b], s_hi[b])) b = q;
+      ok_out[m] = s_hk[b];
+      oi_out[m] = s_hi[b];
+      s_win = s_ht[b];
+    }
+    __syncthreads();
+    if (t == s_win) ++head;
+    __syncthreads();
+  }
+}
+
+constexpr int kFbMaxP = 64;
+
+__global__ void __launch_bounds__(kFbMaxP)
+    k_fallback_merge(int k, const int32_t* __restrict__ fail_rows, int P,
+                     const double* __restrict__ part_key, const int* __restrict__ part_id,
+                     KnnOutDev out) {
+  __shared__ double s_key[kMaxK];
+  __shared__ int s_id[kMaxK];
+  __shared__ double s_hk[kFbMaxP / 32];
+  __shared__ int s_hi[kFbMaxP / 32];
+  __shared__ int s_ht[kFbMaxP / 32];
+  __shared__ int s_win;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int f = blockIdx.x;
+  const double* pk = part_key + ((int64_t)f * P + t) * k;
+  const int* pi = part_id + ((int64_t)f * P + t) * k;
+  int head = 0;
+  for (int m = 0; m < k; ++m) {
+    double hk = (t < P && head < k) ? pk[head] : CUDART_INF;
+    int hi = (t < P && head < k) ? pi[head] : INT32_MAX;
+    int ht = t;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ok = __shfl_xor_sync(0xffffffffu, hk, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, hi, o);
+      const int ot = __shfl_xor_sync(0xffffffffu, ht, o);
+      if (key_less(ok, oi, hk, hi)) {
+        hk = ok;
+        hi = oi;
+        ht = ot;
+      }
+    }
+    if (lane == 0) {
+      s_hk[w] = hk;
+      s_hi[w] = hi;
+      s_ht[w] = ht;
+    }
+    __syncthreads();
+    if (t == 0) {
+      int b = 0;
+      for (int q = 1; q < kFbMaxP / 32; ++q)
+        if (key_less(s_hk[q], s_hi[q], s_hk[b], s_hi[b])) b = q;
       s_key[m] = s_hk[b];
       s_id[m] = s_hi[b];
       s_win = s_ht[b];
@@ -246,7 +455,7 @@ __global__ void __launch_bounds__(kFbThreads)
     if (t == s_win) ++head;
     __syncthreads();
   }
-  if (w == 0) write_row(out, r, k, s_key, s_id, lane, 32);
+  if (w == 0) write_row(out, fail_rows[f], k, s_key, s_id, lane, 32);
 }
 
 }  // namespace
@@ -255,32 +464,64 @@ cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, cons
                           int64_t n, int d, int k, bool self_join, Cands c, CertParams cp,
                           KnnOutDev out, int32_t* fail_rows, int32_t* fail_count,
                           double* max_err, cudaStream_t st, int* launches) {
-  if (c.S * c.kp > kMaxCands || k > kMaxK) return cudaErrorInvalidValue;
+  if (k > kMaxK) return cudaErrorInvalidValue;
+  if (cp.kind == PASS_TC) {  // group candidates
+    if (c.lists * c.kp * 8 > kGrpMaxCols) return cudaErrorInvalidValue;
+    const int64_t gb = (q_count + kGrpWarps - 1) / kGrpWarps;
+    if (gb == 0) return cudaSuccess;
+    const size_t smem = (size_t)kGrpWarps * 32 * (d + 1) * 4 + 8 + (size_t)kGrpWarps * d * 8;
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(k_rerank_groups,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_rerank_groups<<<(unsigned)gb, kGrpWarps * 32, smem, st>>>(
+        Q, q_begin, q_count, X, n, d, k, self_join ? 1 : 0, c.idx, c.v, c.kp, c.lists, cp, out,
+        fail_rows, fail_count, reinterpret_cast<unsigned long long*>(max_err));
+    *launches += 1;
+    return cudaGetLastError();
+  }
+  if (c.lists * c.kp > kMaxCands) return cudaErrorInvalidValue;
   const int64_t blocks = (q_count + kRerankWarps - 1) / kRerankWarps;
   if (blocks == 0) return cudaSuccess;
   k_rerank<<<(unsigned)blocks, kRerankWarps * 32, 0, st>>>(
-      Q, q_begin, q_count, X, n, d, k, self_join ? 1 : 0, c.idx, c.v, c.kp, c.S, cp, out,
+      Q, q_begin, q_count, X, n, d, k, self_join ? 1 : 0, c.idx, c.v, c.kp, c.lists, cp, out,
       fail_rows, fail_count, reinterpret_cast<unsigned long long*>(max_err));
   *launches += 1;
   return cudaGetLastError();
 }
 
+size_t fallback_workspace(int nfail, int k, int64_t n, int num_sms) {
+  const int P = fallback_slices(nfail, n, num_sms);
+  return (size_t)nfail * P * k * (sizeof(double) + sizeof(int));
+}
+
+int fallback_slices(int nfail, int64_t n, int num_sms) {
+  int P = (4 * num_sms + nfail - 1) / nfail;
+  P = P > kFbMaxP ? kFbMaxP : P;
+  while (P > 1 && n / P < 2048) --P;
+  return P < 1 ? 1 : P;
+}
+
 cudaError_t launch_fallback(const float* Q, int64_t q_begin, const float* X, int64_t n, int d,
                             int k, bool self_join, const int32_t* fail_rows, int nfail,
-                            KnnOutDev out, cudaStream_t st, int* launches) {
+                            KnnOutDev out, void* ws, int num_sms, cudaStream_t st, int* launches) {
   if (nfail <= 0) return cudaSuccess;
-  *launches += 1;
+  if (k > kMaxK) return cudaErrorInvalidValue;
+  const int P = fallback_slices(nfail, n, num_sms);
+  double* pk = static_cast<double*>(ws);
+  int* pi = reinterpret_cast<int*>(pk + (size_t)nfail * P * k);
+  const dim3 grid(P, nfail);
   if (k <= 32)
-    k_fallback<32><<<nfail, kFbThreads, 0, st>>>(Q, q_begin, X, n, d, k, self_join ? 1 : 0,
-                                                 fail_rows, out);
+    k_fallback_part<32><<<grid, kFbThreads, 0, st>>>(Q, q_begin, X, n, d, k, self_join ? 1 : 0,
+                                                     fail_rows, P, pk, pi);
   else if (k <= 64)
-    k_fallback<64><<<nfail, kFbThreads, 0, st>>>(Q, q_begin, X, n, d, k, self_join ? 1 : 0,
-                                                 fail_rows, out);
-  else if (k <= kMaxK)
-    k_fallback<kMaxK><<<nfail, kFbThreads, 0, st>>>(Q, q_begin, X, n, d, k, self_join ? 1 : 0,
-                                                    fail_rows, out);
+    k_fallback_part<64><<<grid, kFbThreads, 0, st>>>(Q, q_begin, X, n, d, k, self_join ? 1 : 0,
+                                                     fail_rows, P, pk, pi);
   else
-    return cudaErrorInvalidValue;
+    k_fallback_part<kMaxK><<<grid, kFbThreads, 0, st>>>(Q, q_begin, X, n, d, k,
+                                                        self_join ? 1 : 0, fail_rows, P, pk, pi);
+  k_fallback_merge<<<nfail, kFbMaxP, 0, st>>>(k, fail_rows, P, pk, pi, out);
+  *launches += 2;
   return cudaGetLastError();
 }
 

@@ -1,47 +1,54 @@
 // topk_list.cuh — per-row running top-K' (K' smallest keys with their column
-// indices) kept by ONE thread for ONE query row, inside the fused
-// distance epilogue.  This is the "topk on each cdist batch, local candidates
-// merged so the result is still exact" of operator fusion (§6.1,
-// P:452-455), re-derived for a thread-per-row TMEM/register layout.
+// indices) kept by ONE thread for ONE query row, inside the fused distance
+// epilogue.  This is the "topk on each cdist batch, local candidates merged so
+// the result is still exact" of operator fusion (§6.1),
+// re-derived for a thread-per-row TMEM/register layout.
 //
-// Storage: shared memory, column-per-thread ([slot][NT] with NT threads), so a
-// warp touching "its" slot e hits 32 consecutive words (conflict-free).
-//   slots [0, kp)        the kept list, sorted ascending by key
-//   slots [kp, kp+P)     an append-only pending buffer
-// The fast path (per distance) is one compare against `thr` (the current
-// K'-th smallest key, +inf while the list is not full).  Hits are appended to
-// the pending buffer; when any lane of the warp fills its buffer the whole
-// warp merges in lock step: bitonic-sort the P pending entries in registers,
-// then an in-place backward merge into the sorted list, truncated at kp.
+// Storage: shared memory, column-per-thread: slot e of thread t is the 8-byte
+// (key, index) pair at base + (e*NT + t)*8, so 32 lanes touching their own
+// slots (any e per lane) hit distinct bank pairs (the slot stride NT*8 bytes
+// is a multiple of 256).
+//   slots [0, kp)          the kept list, sorted ascending by key
+//   slots [kp, kp+P)       an append-only pending buffer
+// The fast path compares keys against `thr` (the current K'-th smallest key,
+// +inf while the list is not full); hits are appended with one predicated
+// 64-bit store.  When any lane's pending buffer might overflow, the warp
+// merges in lock step: bitonic sort of the pending entries in registers, then
+// an in-place backward merge into the sorted list, truncated at kp.
 //
 // Invariant used by the certificate: every column
-// offered to a row and not in its final list has key >= v, where v = the final
+// offered to a row and not in its final list has key >= v, where v is the final
 // thr (the K'-th kept key, or +inf when fewer than K' were ever offered).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include "ptx.cuh"
+
 namespace tod {
 
-constexpr int kPend = 16;  // P: pending slots per row
+constexpr int kPendGroup = 8;   // appends per group between overflow checks
 
-// Merge one row's pending buffer into its sorted list (see header comment).
-// Returns (new fill, new thr).  A free __noinline__ function with scalar
-// arguments so that the caller's RowTopK state stays in registers.
-template <int NT>
-__device__ __noinline__ float2 merge_row(float* lv, int* li, int kp, int fill, int pcnt) {
+// Merge one row's pending buffer into its sorted list.  `base` is the shared
+// address of this thread's slot 0.  Returns (new fill as int bits, new thr).
+// __noinline__ with scalar arguments so the caller's state stays in registers.
+template <int NT, int kPend>
+__device__ __noinline__ float2 merge_row(uint32_t base, int kp, int fill, int pcnt) {
+  constexpr uint32_t S = NT * 8;  // byte stride between slots
   if (pcnt == 0) {
-    const float t = (fill == kp) ? lv[(kp - 1) * NT] : CUDART_INF_F;
+    const float t = (fill == kp) ? lds_kv(base + (kp - 1) * S).x : CUDART_INF_F;
     return make_float2(__int_as_float(fill), t);
   }
+  const uint32_t pb = base + kp * S;
   float pv[kPend];
   int pi[kPend];
 #pragma unroll
   for (int p = 0; p < kPend; ++p) {
     const bool live = p < pcnt;
-    pv[p] = live ? lv[(kp + p) * NT] : CUDART_INF_F;
-    pi[p] = live ? li[(kp + p) * NT] : -1;
+    const float2 e = live ? lds_kv(pb + p * S) : make_float2(CUDART_INF_F, __int_as_float(-1));
+    pv[p] = e.x;
+    pi[p] = __float_as_int(e.y);
   }
   // Bitonic sort ascending (fully unrolled: stays in registers).
 #pragma unroll
@@ -65,96 +72,94 @@ __device__ __noinline__ float2 merge_row(float* lv, int* li, int kp, int fill, i
     }
   }
 #pragma unroll
-  for (int p = 0; p < kPend; ++p) {
-    if (p < pcnt) {
-      lv[(kp + p) * NT] = pv[p];
-      li[(kp + p) * NT] = pi[p];
-    }
-  }
+  for (int p = 0; p < kPend; ++p)
+    if (p < pcnt) sts_kv(pb + p * S, pv[p], pi[p]);
   // Backward in-place merge of list[0,fill) and pending[0,pcnt) (both
   // ascending) into list[0, min(fill+pcnt, kp)).  Once the pending run is
   // exhausted the remaining list prefix is already in place (o == i).
   int i = fill - 1, j = pcnt - 1;
   int o = fill + pcnt - 1;
-  float Lv = i >= 0 ? lv[i * NT] : -CUDART_INF_F;
-  int Li = i >= 0 ? li[i * NT] : -1;
-  float Pv = lv[(kp + j) * NT];
-  int Pi = li[(kp + j) * NT];
+  float2 L = i >= 0 ? lds_kv(base + i * S) : make_float2(-CUDART_INF_F, 0.f);
+  float2 P = lds_kv(pb + j * S);
   while (j >= 0) {
-    const bool takeL = (i >= 0) && (Lv > Pv);
+    const bool takeL = (i >= 0) && (L.x > P.x);
     if (o < kp) {
-      lv[o * NT] = takeL ? Lv : Pv;
-      li[o * NT] = takeL ? Li : Pi;
+      const float2 t = takeL ? L : P;
+      sts_kv(base + o * S, t.x, __float_as_int(t.y));
     }
     if (takeL) {
       --i;
-      if (i >= 0) {
-        Lv = lv[i * NT];
-        Li = li[i * NT];
-      }
+      if (i >= 0) L = lds_kv(base + i * S);
     } else {
       --j;
-      if (j >= 0) {
-        Pv = lv[(kp + j) * NT];
-        Pi = li[(kp + j) * NT];
-      }
+      if (j >= 0) P = lds_kv(pb + j * S);
     }
     --o;
   }
   fill = min(fill + pcnt, kp);
-  const float t = (fill == kp) ? lv[(kp - 1) * NT] : CUDART_INF_F;
+  const float t = (fill == kp) ? lds_kv(base + (kp - 1) * S).x : CUDART_INF_F;
   return make_float2(__int_as_float(fill), t);
 }
 
-template <int NT>
+// NT: rows (threads) sharing the slot array; P: pending slots per row.
+template <int NT, int P = 32>
 struct RowTopK {
-  float* lv;  // &vals[0][t]
-  int* li;    // &idx[0][t]
+  static constexpr int kPend = P;
+  static constexpr uint32_t S = NT * 8;
+  uint32_t base;  // shared address of slot 0 of this thread
+  uint32_t pa;    // shared address of the next pending slot
   int kp;
   int fill;
-  int pcnt;
   float thr;
 
-  __device__ __forceinline__ void init(float* vals, int* idxs, int t, int kprime) {
-    lv = vals + t;
-    li = idxs + t;
+  // `pairs` is the [(kp + kPend) * NT] array of 8-byte (key, index) pairs.
+  __device__ __forceinline__ void init(uint2* pairs, int t, int kprime) {
+    base = smem_u32(pairs + t);
     kp = kprime;
-    fill = 0;
-    pcnt = 0;
-    thr = CUDART_INF_F;
+    reset();
   }
   __device__ __forceinline__ void reset() {
     fill = 0;
-    pcnt = 0;
+    pa = base + kp * S;
     thr = CUDART_INF_F;
   }
+  __device__ __forceinline__ int pcnt() const { return (int)((pa - base) / S) - kp; }
   __device__ __forceinline__ void append(float v, int j) {
-    lv[(kp + pcnt) * NT] = v;
-    li[(kp + pcnt) * NT] = j;
-    ++pcnt;
+    sts_kv(pa, v, j);
+    pa += S;
   }
-
-  // Whole warp must call (lanes with pcnt == 0 participate as no-ops).
+  // Whole warp must call (lanes with no pending entries are no-ops).
   __device__ __forceinline__ void merge() {
-    const float2 r = merge_row<NT>(lv, li, kp, fill, pcnt);
+    const float2 r = merge_row<NT, P>(base, kp, fill, pcnt());
     fill = __float_as_int(r.x);
     thr = r.y;
-    pcnt = 0;
+    pa = base + kp * S;
   }
-
-  // Offer (key, column) unless column == self; merge when any lane is full.
-  // Whole warp must call with uniform control flow.
-  __device__ __forceinline__ void offer(float key, int col, int self) {
-    if (key < thr && col != self) append(key, col);
-    if (__any_sync(0xffffffffu, pcnt == kPend)) merge();
+  // Make room for up to kPendGroup appends.  Whole warp, uniform control flow.
+  __device__ __forceinline__ void reserve_group() { reserve(kPendGroup); }
+  // Make room for up to `r` appends.  Whole warp, uniform control flow.
+  __device__ __forceinline__ void reserve(int r) {
+    const uint32_t limit = base + (kp + kPend - r) * S;
+    if (__any_sync(0xffffffffu, pa > limit)) merge();
   }
-
-  // Flush pending and write the list: out_idx[0..kp) (-1 for empty slots) and
+  // Predicated append (branch-free in SASS).
+  __device__ __forceinline__ void append_if(bool p, float v, int j) {
+    if (p) append(v, j);
+  }
+  // Offer up to kPendGroup (key, column) pairs: keys below thr and columns !=
+  // self are appended (predicated stores, no branches on the data).
+  __device__ __forceinline__ void offer_group(const float (&w)[kPendGroup], int col0, int self) {
+#pragma unroll
+    for (int e = 0; e < kPendGroup; ++e)
+      if (w[e] < thr && col0 + e != self) append(w[e], col0 + e);
+  }
+  // Flush pending and write the list: out_idx[0..kp) (-1 for empty slots);
   // returns v (the certificate threshold).  Whole warp must call.
   __device__ __forceinline__ float finish(int* out_idx, bool write) {
-    if (__any_sync(0xffffffffu, pcnt > 0)) merge();
+    if (__any_sync(0xffffffffu, pa != base + kp * S)) merge();
     if (write) {
-      for (int e = 0; e < kp; ++e) out_idx[e] = e < fill ? li[e * NT] : -1;
+      for (int e = 0; e < kp; ++e)
+        out_idx[e] = e < fill ? __float_as_int(lds_kv(base + e * S).y) : -1;
     }
     return thr;
   }

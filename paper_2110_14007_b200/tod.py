@@ -38,7 +38,7 @@ class TodError(RuntimeError):
 class Config(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("format", ctypes.c_int32), ("kprime", ctypes.c_int32),
                 ("flags", ctypes.c_uint32), ("stream", ctypes.c_void_p), ("chunks", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("epilogue_split", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -152,10 +152,10 @@ class Context:
     """Owns a tod_ctx (device workspace + stream binding)."""
 
     def __init__(self, device: int = 0, fmt: str = "auto", kprime: int = 0, chunks: int = 0,
-                 flags: int = 0, stream=None):
+                 flags: int = 0, stream=None, split: int = 0):
         self.lib = load_library()
         cfg = Config(device=device, format=FORMATS[fmt], kprime=kprime, flags=flags,
-                     stream=stream, chunks=chunks, reserved=0)
+                     stream=stream, chunks=chunks, epilogue_split=split)
         h = ctypes.c_void_p()
         st = self.lib.tod_create(ctypes.byref(cfg), ctypes.byref(h))
         if st != TOD_OK:

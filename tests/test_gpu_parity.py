@@ -108,8 +108,8 @@ def test_query_range_and_chunk_invariance(pkg):
     X = datagen.gaussian_mixture(4000, 32, seed=8)
     Xd = torch.from_numpy(X).cuda()
     outs = []
-    for chunks, kp in ((1, 0), (3, 0), (2, 64), (1, 48)):
-        with _ctx(pkg, chunks=chunks, kprime=kp) as ctx:
+    for chunks, kp, sp in ((1, 0, 1), (3, 0, 2), (2, 64, 0), (1, 48, 2), (5, 40, 1), (4, 32, 2)):
+        with _ctx(pkg, chunks=chunks, kprime=kp, split=sp) as ctx:
             outs.append(ctx.knn(Xd, 20, q_begin=1000, q_count=1700))
     for o in outs[1:]:
         assert torch.equal(o.idx, outs[0].idx) and torch.equal(o.dist64, outs[0].dist64)
