@@ -43,7 +43,7 @@ struct Workspace {
 enum BufId {
   B_X = 0, B_Q, B_IMG_B, B_A2_B, B_E_B, B_IMG_A, B_A2_A, B_E_A, B_MU, B_PART,
   B_G, B_CIDX, B_CV, B_FAIL, B_SMALL, B_IDX, B_DIST, B_DIST64, B_KTH, B_MEAN, B_KD64,
-  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_NBUF
+  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_NBUF
 };
 
 }  // namespace
@@ -247,6 +247,10 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
   cands.idx = static_cast<int32_t*>(p);
   TOD_TRY(ensure(ctx, B_CV, (size_t)std::max<int64_t>(q_count, 1) * cands.lists * 4, &p));
   cands.v = static_cast<float*>(p);
+  if (plan.kind == PASS_TC) {
+    TOD_TRY(ensure(ctx, B_CKEY, (size_t)std::max<int64_t>(q_count, 1) * cands.lists * plan.kp * 4, &p));
+    cands.key = static_cast<float*>(p);
+  }
   if (plan.kind == PASS_TC && plan.S > 1) {
     const int64_t nqt = (q_begin + q_count + 127) / 128 - q_begin / 128;
     TOD_TRY(ensure(ctx, B_STLIST, (size_t)nqt * plan.lists * plan.kp * 128 * 8, &p));

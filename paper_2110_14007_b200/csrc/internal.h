@@ -45,6 +45,7 @@ struct PrepGlobals {
 struct Cands {
   int32_t* idx = nullptr;   // [q_count][lists][kp]
   float* v = nullptr;       // [q_count][lists]
+  float* key = nullptr;     // TC: [q_count][lists][kp] group-min w~ of each kept group (ascending)
   int kp = 0, S = 0;        // S = reference chunks
   int lists = 1;            // lists per row (TC: epilogue split 1|2; SIMT: S)
   uint2* st_list = nullptr; // TC: [q tiles][kp][128] parked (key, index) state

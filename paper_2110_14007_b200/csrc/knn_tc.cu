@@ -136,7 +136,8 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
              const uint8_t* __restrict__ b_img, size_t b_region, size_t b_extra, int64_t b_tiles,
              int64_t n_ref, int64_t qt0, int64_t n_qtiles, int64_t q_begin, int64_t q_end,
              int self_join, int S, int kp, int nstage, int dbg, int32_t* __restrict__ cand_idx,
-             float* __restrict__ cand_v, uint2* __restrict__ st_list, int* __restrict__ st_done) {
+             float* __restrict__ cand_v, float* __restrict__ cand_key, uint2* __restrict__ st_list,
+             int* __restrict__ st_done) {
   using C = TcCfg<DPAD, SPLIT>;
   constexpr int QT = C::QT;
   using List = RowTopK<C::NLIST, C::PEND>;
@@ -385,7 +386,8 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
       } else {
         const bool write = row >= q_begin && row < q_end;
         const int64_t r = row - q_begin;
-        const float v = L.finish(cand_idx + (write ? (r * SPLIT + half) * kp : 0), write);
+        const int64_t co = write ? (r * SPLIT + half) * kp : 0;
+        const float v = L.finish(cand_idx + co, write, cand_key + co);
         if (write) cand_v[r * SPLIT + half] = v;
       }
       L.reset();
@@ -421,7 +423,7 @@ cudaError_t launch_t(const Image& A, const Image& B, int64_t q_begin, int64_t q_
       reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(), A.extra_offset(),
       reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
       B.n_pad / C::BN, B.n, qt0, qt1 - qt0, q_begin, q_begin + q_count, self_join ? 1 : 0, c.S,
-      c.kp, nstage, c.dbg, c.idx, c.v, c.st_list, c.st_done);
+      c.kp, nstage, c.dbg, c.idx, c.v, c.key, c.st_list, c.st_done);
   return cudaGetLastError();
 }
 

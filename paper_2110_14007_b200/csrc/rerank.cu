@@ -70,16 +70,12 @@ __device__ void write_row(const KnnOutDev& out, int64_t r, int k, const double* 
   }
 }
 
-// The certificate: true iff every reference the
-// pass did not keep has exact squared distance > dk (the k-th re-ranked D64),
-// so the oracle's top-k lies inside the kept set.  `vmin` is the threshold
-// below which pass 1 kept everything it was offered.  *err receives the
-// pass-1 error term used (diagnostics).
-__device__ bool row_certified(const CertParams& cp, int64_t r, float vmin, double dk, double* err) {
+// Lower bound, in original units, on the exact squared distance rho^2 of row r
+// to ANY reference column whose pass-1 key is >= w.  Returns a
+// value <= 0 when no positive bound exists.  *err receives the pass-1 error
+// term (diagnostics).
+__device__ double lb2_from_key(const CertParams& cp, int64_t r, double w, double* err) {
   const double u53 = 1.1102230246251565e-16;
-  const double vv = (double)vmin;
-  bool cert = false;
-  if (vmin == CUDART_INF_F) return true;  // every reference was offered and kept
   if (cp.kind == PASS_TC) {
     // Tensor-core pass (fp16/bf16 operands, fp32 accumulation; the norm
     // ||xhat_j||^2 enters as pieces p_jq times constants c_q in an extra K
@@ -89,8 +85,8 @@ __device__ bool row_certified(const CertParams& cp, int64_t r, float vmin, doubl
     //                  <= gamma (2 a_i a_max + 1.002 amax2) + repmax  =: E_i
     // (Cauchy-Schwarz on the dot part; sum_q |c_q p_jq| <= 1.002 ||xhat_j||^2).
     // A9: accumulation modelled order-free with m = 2 (dpad + 16), u = 2^-22.
-    // Non-kept j have w~_ij >= v, so ||xhat_i - xhat_j||^2 >= a_i^2 + v - E_i;
-    // the residuals e_i, e_j <= emax then bound the exact distance.
+    // w~_ij >= w gives ||xhat_i - xhat_j||^2 >= a_i^2 + w - E_i; the residuals
+    // e_i, e_j <= emax then bound the exact distance (triangle inequality).
     const double a2i = cp.qa2[r];
     const double ei = cp.qe[r];
     const double amax2 = cp.g->amax2;
@@ -100,27 +96,30 @@ __device__ bool row_certified(const CertParams& cp, int64_t r, float vmin, doubl
     const double am = sqrt(amax2) * (1.0 + 4 * u53);
     const double gam = gamma_up(2.0 * (cp.dpad + 16), 2.384185791015625e-07 /*2^-22*/);
     const double E = (gam * (2.0 * ai * am + 1.002 * amax2) + rep) * (1.0 + 1e-6) + 1e-300;
-    const double slack = (cp.d + 8) * 2.0 * u53 * (fabs(a2i) + fabs(vv) + E);
-    const double R2 = a2i + vv - E - slack;
+    const double slack = (cp.d + 8) * 2.0 * u53 * (fabs(a2i) + fabs(w) + E);
+    const double R2 = a2i + w - E - slack;
     *err = E + slack;
-    if (R2 > 0.0) {
-      const double Rh = sqrt(R2) * (1.0 - 2.0 * u53);
-      const double LB = (Rh - ei - emax) * (1.0 - 8.0 * u53);
-      if (LB > 0.0) {
-        const double lbo = LB / cp.g->s;  // s = 2^e: exact
-        const double lb2 = lbo * lbo * (1.0 - 8.0 * u53);
-        cert = dk < lb2 * (1.0 - gamma_up(cp.d + 2, u53));
-      }
-    }
-  } else {
-    // fp32 difference-form pass: D~ <= D (1 + gamma_{d+2}(2^-24)) + tiny.
-    const double g32 = gamma_up(cp.d + 2, 5.9604644775390625e-08);
-    const double lb2 =
-        (vv - (cp.d + 2) * 1.1754943508222875e-38 /*2^-126*/) / (1.0 + g32) * (1.0 - 8.0 * u53);
-    *err = vv * g32;
-    if (lb2 > 0.0) cert = dk < lb2 * (1.0 - gamma_up(cp.d + 2, u53));
+    if (!(R2 > 0.0)) return -1.0;
+    const double Rh = sqrt(R2) * (1.0 - 2.0 * u53);
+    const double LB = (Rh - ei - emax) * (1.0 - 8.0 * u53);
+    if (!(LB > 0.0)) return -1.0;
+    const double lbo = LB / cp.g->s;  // s = 2^e: exact
+    return lbo * lbo * (1.0 - 8.0 * u53);
   }
-  return cert;
+  // fp32 difference-form pass: D~ <= rho^2 (1 + gamma_{d+2}(2^-24)) + tiny.
+  const double g32 = gamma_up(cp.d + 2, 5.9604644775390625e-08);
+  *err = w * g32;
+  return (w - (cp.d + 2) * 1.1754943508222875e-38 /*2^-126*/) / (1.0 + g32) * (1.0 - 8.0 * u53);
+}
+
+// The certificate: true iff every reference the pass did not keep has oracle
+// distance D64 > dk (the k-th re-ranked D64), so the oracle's top-k lies inside
+// the kept set.  `vmin` is the key threshold below which pass 1 kept
+// everything it was offered.  D64 >= rho^2 (1 - gamma_{d+2}(2^-53)).
+__device__ bool row_certified(const CertParams& cp, int64_t r, float vmin, double dk, double* err) {
+  if (vmin == CUDART_INF_F) return true;  // every reference was offered and kept
+  const double lb2 = lb2_from_key(cp, r, (double)vmin, err);
+  return lb2 > 0.0 && dk < lb2 * (1.0 - gamma_up(cp.d + 2, 1.1102230246251565e-16));
 }
 
 __global__ void __launch_bounds__(kRerankWarps * 32)
@@ -190,132 +189,183 @@ __global__ void __launch_bounds__(kRerankWarps * 32)
 // kept group is re-ranked; columns outside kept groups have w~ >= v (their
 // group's minimum is >= v), so the same certificate applies.
 constexpr int kGrpWarps = 4;
-constexpr int kGrpCPL = 20;                 // candidate columns per lane
-constexpr int kGrpMaxCols = 32 * kGrpCPL;   // 640 = lists * K'' * 8 max
+constexpr int kGrpMaxG = 128;   // lists * K'' group slots per row
 
-// Dynamic smem per warp: 4 groups x 8 rows x (d+1) floats (row stride d+1
-// words: lanes reading the same c of different rows hit distinct banks).
+// Warp-wide bitonic sort (ascending by (key, id)) of one element per lane.
+__device__ __forceinline__ void warp_sort32(double& key, int& id, int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const double ok = __shfl_xor_sync(0xffffffffu, key, j);
+      const int oi = __shfl_xor_sync(0xffffffffu, id, j);
+      const bool up = (lane & k) == 0;
+      const bool lower = (lane & j) == 0;
+      // keep the smaller in the lower lane of an ascending pair
+      const bool other_less = key_less(ok, oi, key, id);
+      const bool take = (lower == up) ? other_less : !other_less;
+      if (take) {
+        key = ok;
+        id = oi;
+      }
+    }
+  }
+}
+
+// Group candidates, pruned: the kept groups of all lists are
+// visited in ascending order of their pass-1 minimum; before each batch of 4
+// groups, if the lower bound implied by that minimum (lb2_from_key) already
+// exceeds the current k-th exact distance, every remaining group is provably
+// farther and the scan stops.  Visited groups are expanded to their 8 columns
+// and re-ranked with the oracle formula; a running top-k (by (D64, index)) is
+// merged batch by batch.
 __global__ void __launch_bounds__(kGrpWarps * 32)
     k_rerank_groups(const float* __restrict__ Q, int64_t q_begin, int64_t q_count,
                     const float* __restrict__ X, int64_t n, int d, int k, int self_join,
-                    const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_v,
-                    int kp, int lists, CertParams cp, KnnOutDev out,
-                    int32_t* __restrict__ fail_rows, int32_t* __restrict__ fail_count,
-                    unsigned long long* __restrict__ max_err_bits) {
-  extern __shared__ float s_rows[];
-  __shared__ double s_sk[kGrpWarps][kMaxK];
-  __shared__ int s_si[kGrpWarps][kMaxK];
+                    const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_key,
+                    const float* __restrict__ cand_v, int kp, int lists, CertParams cp,
+                    KnnOutDev out, int32_t* __restrict__ fail_rows,
+                    int32_t* __restrict__ fail_count, unsigned long long* __restrict__ max_err_bits) {
+  __shared__ float s_gk[kGrpWarps][kGrpMaxG];     // group keys, merged ascending
+  __shared__ int s_gi[kGrpWarps][kGrpMaxG];       // group indices
+  __shared__ double s_tk[kGrpWarps][2][kMaxK];    // running top-k (double buffered)
+  __shared__ int s_ti[kGrpWarps][2][kMaxK];
+  __shared__ double s_bk[kGrpWarps][32];          // sorted batch
+  __shared__ int s_bi[kGrpWarps][32];
+  extern __shared__ double s_xq[];                // [warps][d] query row in fp64
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * kGrpWarps + w;
   if (r >= q_count) return;
-  const int ld = d + 1;
-  float* rows = s_rows + (size_t)w * 32 * ld;   // 32 candidate rows of this warp
-  double* xq = reinterpret_cast<double*>(s_rows + (size_t)kGrpWarps * 32 * ld) + (size_t)w * d;
   const int64_t gi = q_begin + r;
   const float* xi = self_join ? X + gi * d : Q + r * d;
+  double* xq = s_xq + (size_t)w * d;
   for (int c = lane; c < d; c += 32) xq[c] = (double)xi[c];
-  __syncwarp();
-  const int G = lists * kp;       // group slots
-  double key[kGrpCPL];
-  int id[kGrpCPL];
-  int nv = 0;
-#pragma unroll
-  for (int s = 0; s < kGrpCPL; ++s) {
-    key[s] = CUDART_INF;
-    id[s] = INT32_MAX;
-    if (s * 4 < G) {  // warp-uniform: 4 groups (32 columns) per step
-      // lane -> (group slot 4s + lane/8, column lane%8)
-      const int gslot = s * 4 + (lane >> 3);
-      const int g = gslot < G ? cand_idx[r * G + gslot] : -1;
-      // cooperative, coalesced staging of the 4 groups' 8 consecutive rows
-      // (8*d contiguous floats per group; float4 when d % 4 == 0)
-#pragma unroll 1
-      for (int q4 = 0; q4 < 4; ++q4) {
-        const int gq = __shfl_sync(0xffffffffu, g, q4 * 8);
-        if (gq < 0) continue;
-        const int64_t j0 = (int64_t)gq * 8;
-        const int nrows = (int)(n - j0 < 8 ? n - j0 : 8);
-        const float* src = X + j0 * d;
-        float* dst = rows + q4 * 8 * ld;
-        if ((d & 3) == 0) {
-          const int d4 = d >> 2;
-          const float4* src4 = reinterpret_cast<const float4*>(src);
-          for (int e4 = lane; e4 < nrows * d4; e4 += 32) {
-            const int rr = e4 / d4, c4 = e4 - rr * d4;
-            const float4 vv = __ldg(src4 + e4);
-            float* o = dst + rr * ld + 4 * c4;
-            o[0] = vv.x;
-            o[1] = vv.y;
-            o[2] = vv.z;
-            o[3] = vv.w;
-          }
-        } else {
-          for (int e = lane; e < nrows * d; e += 32) {
-            const int rr = e / d, cc = e - rr * d;
-            dst[rr * ld + cc] = __ldg(src + e);
-          }
-        }
+  const int G = lists * kp;
+  // ---- merge the (ascending) lists into one ascending order of group keys
+  float* gk = s_gk[w];
+  int* gid = s_gi[w];
+  for (int e = lane; e < G; e += 32) {
+    const int a = e / kp, pos = e - a * kp;
+    const float key = cand_key[r * G + e];
+    const int g = cand_idx[r * G + e];
+    int rank = pos;
+    if (lists == 2) {  // rank among the other list (ties: list 0 first)
+      const float* other = cand_key + r * G + (1 - a) * kp;
+      int lo = 0, hi = kp;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const float om = other[mid];
+        if (a == 0 ? (om < key) : (om <= key)) lo = mid + 1;
+        else hi = mid;
       }
-      __syncwarp();
-      const int64_t j = (int64_t)g * 8 + (lane & 7);
-      if (g >= 0 && j < n && !(self_join && j == gi)) {
-        // O1, bit-identical to the oracle (no FMA, ascending c, from +0.0).
-        const float* xj = rows + lane * ld;
-        double acc = 0.0;
-        for (int c = 0; c < d; ++c) {
-          const double t = __dsub_rn(xq[c], (double)xj[c]);
-          acc = __dadd_rn(acc, __dmul_rn(t, t));
-        }
-        key[s] = acc;
-        id[s] = (int)j;
-        ++nv;
-      }
-      __syncwarp();
+      rank += lo;
     }
+    gk[rank] = key;
+    gid[rank] = g;
   }
   float vmin = CUDART_INF_F;
   for (int c = 0; c < lists; ++c) vmin = fminf(vmin, cand_v[r * lists + c]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) nv += __shfl_xor_sync(0xffffffffu, nv, o);
-  // k rounds of warp-wide lexicographic argmin over (D64, index).
-  const int kk = nv < k ? nv : k;
-  for (int m = 0; m < kk; ++m) {
-    double bk = key[0];
-    int bi = id[0];
-#pragma unroll
-    for (int s = 1; s < kGrpCPL; ++s)
-      if (key_less(key[s], id[s], bk, bi)) {
-        bk = key[s];
-        bi = id[s];
-      }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (key_less(ok, oi, bk, bi)) {
-        bk = ok;
-        bi = oi;
-      }
-    }
-#pragma unroll
-    for (int s = 0; s < kGrpCPL; ++s)
-      if (id[s] == bi) {
-        key[s] = CUDART_INF;
-        id[s] = INT32_MAX;
-      }
-    if (lane == 0) {
-      s_sk[w][m] = bk;
-      s_si[w][m] = bi;
-    }
-  }
   __syncwarp();
+  const double gamma64 = gamma_up(cp.d + 2, 1.1102230246251565e-16);
+  int cnt = 0;            // entries in the running top-k
+  int buf = 0;
+  double dk = CUDART_INF;  // current k-th exact distance (valid when cnt == k)
   double err = 0.0;
-  bool cert = nv >= k && row_certified(cp, r, vmin, s_sk[w][k - 1], &err);
+  for (int b = 0; b < G; b += 4) {
+    const int g0 = gid[b];
+    if (g0 < 0) break;  // empty slots sort last (key +inf)
+    if (cnt == k) {
+      double e2;
+      const double lb2 = lb2_from_key(cp, r, (double)gk[b], &e2);
+      if (lb2 > 0.0 && dk < lb2 * (1.0 - gamma64)) break;  // all remaining groups are farther
+    }
+    // expand 4 groups -> 32 columns, one per lane
+    const int gs = b + (lane >> 3);
+    const int g = gs < G ? gid[gs] : -1;
+    const int64_t j = (int64_t)g * 8 + (lane & 7);
+    double key = CUDART_INF;
+    int id = INT32_MAX;
+    if (g >= 0 && j < n && !(self_join && j == gi)) {
+      const float* xj = X + j * d;
+      double acc = 0.0;  // O1, bit-identical to the oracle (no FMA, ascending c)
+      if ((d & 3) == 0) {
+        const float4* x4 = reinterpret_cast<const float4*>(xj);
+        for (int c4 = 0; c4 < (d >> 2); ++c4) {
+          const float4 v = __ldg(x4 + c4);
+          double t = __dsub_rn(xq[4 * c4 + 0], (double)v.x);
+          acc = __dadd_rn(acc, __dmul_rn(t, t));
+          t = __dsub_rn(xq[4 * c4 + 1], (double)v.y);
+          acc = __dadd_rn(acc, __dmul_rn(t, t));
+          t = __dsub_rn(xq[4 * c4 + 2], (double)v.z);
+          acc = __dadd_rn(acc, __dmul_rn(t, t));
+          t = __dsub_rn(xq[4 * c4 + 3], (double)v.w);
+          acc = __dadd_rn(acc, __dmul_rn(t, t));
+        }
+      } else {
+        for (int c = 0; c < d; ++c) {
+          const double t = __dsub_rn(xq[c], (double)__ldg(xj + c));
+          acc = __dadd_rn(acc, __dmul_rn(t, t));
+        }
+      }
+      key = acc;
+      id = (int)j;
+    }
+    // merge the sorted batch into the running top-k (merge path by ranks)
+    warp_sort32(key, id, lane);
+    const double* tk = s_tk[w][buf];
+    const int* ti = s_ti[w][buf];
+    double* nk = s_tk[w][buf ^ 1];
+    int* ni = s_ti[w][buf ^ 1];
+    const unsigned valid = __ballot_sync(0xffffffffu, id != INT32_MAX);
+    const int nb = __popc(valid);  // valid batch entries are the first nb lanes
+    s_bk[w][lane] = key;
+    s_bi[w][lane] = id;
+    __syncwarp();
+    // batch element (lane) position = lane + #(list entries less than it)
+    if (lane < nb) {
+      int lo = 0, hi = cnt;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (key_less(tk[mid], ti[mid], key, id)) lo = mid + 1;
+        else hi = mid;
+      }
+      const int p = lane + lo;
+      if (p < k) {
+        nk[p] = key;
+        ni[p] = id;
+      }
+    }
+    // list element e position = e + #(batch elements less than it)
+    for (int e = lane; e < cnt; e += 32) {
+      const double ek = tk[e];
+      const int ei = ti[e];
+      int lo = 0, hi = nb;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const double bk = s_bk[w][mid];
+        const int bi = s_bi[w][mid];
+        if (key_less(bk, bi, ek, ei)) lo = mid + 1;
+        else hi = mid;
+      }
+      const int p = e + lo;
+      if (p < k) {
+        nk[p] = ek;
+        ni[p] = ei;
+      }
+    }
+    cnt = min(k, cnt + nb);
+    buf ^= 1;
+    __syncwarp();
+    if (cnt == k) dk = s_tk[w][buf][k - 1];
+  }
+  double e1 = 0.0;
+  bool cert = cnt == k && row_certified(cp, r, vmin, s_tk[w][buf][k - 1], &e1);
+  err = e1;
   if (cp.force_fail) cert = false;
   if (lane == 0 && err > 0.0)
     atomicMax(max_err_bits, (unsigned long long)__double_as_longlong(err));
   if (cert) {
-    write_row(out, r, k, s_sk[w], s_si[w], lane, 32);
+    write_row(out, r, k, s_tk[w][buf], s_ti[w][buf], lane, 32);
   } else if (lane == 0) {
     const int slot = atomicAdd(fail_count, 1);
     fail_rows[slot] = (int32_t)r;
@@ -466,17 +516,17 @@ cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, cons
                           double* max_err, cudaStream_t st, int* launches) {
   if (k > kMaxK) return cudaErrorInvalidValue;
   if (cp.kind == PASS_TC) {  // group candidates
-    if (c.lists * c.kp * 8 > kGrpMaxCols) return cudaErrorInvalidValue;
+    if (c.lists * c.kp > kGrpMaxG || c.lists > 2 || !c.key) return cudaErrorInvalidValue;
     const int64_t gb = (q_count + kGrpWarps - 1) / kGrpWarps;
     if (gb == 0) return cudaSuccess;
-    const size_t smem = (size_t)kGrpWarps * 32 * (d + 1) * 4 + 8 + (size_t)kGrpWarps * d * 8;
-    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    const size_t smem = (size_t)kGrpWarps * d * 8;
+    if (smem > 160 * 1024) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(k_rerank_groups,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_rerank_groups<<<(unsigned)gb, kGrpWarps * 32, smem, st>>>(
-        Q, q_begin, q_count, X, n, d, k, self_join ? 1 : 0, c.idx, c.v, c.kp, c.lists, cp, out,
-        fail_rows, fail_count, reinterpret_cast<unsigned long long*>(max_err));
+        Q, q_begin, q_count, X, n, d, k, self_join ? 1 : 0, c.idx, c.key, c.v, c.kp, c.lists, cp,
+        out, fail_rows, fail_count, reinterpret_cast<unsigned long long*>(max_err));
     *launches += 1;
     return cudaGetLastError();
   }

@@ -155,11 +155,14 @@ struct RowTopK {
   }
   // Flush pending and write the list: out_idx[0..kp) (-1 for empty slots);
   // returns v (the certificate threshold).  Whole warp must call.
-  __device__ __forceinline__ float finish(int* out_idx, bool write) {
+  __device__ __forceinline__ float finish(int* out_idx, bool write, float* out_key = nullptr) {
     if (__any_sync(0xffffffffu, pa != base + kp * S)) merge();
     if (write) {
-      for (int e = 0; e < kp; ++e)
-        out_idx[e] = e < fill ? __float_as_int(lds_kv(base + e * S).y) : -1;
+      for (int e = 0; e < kp; ++e) {
+        const float2 kv = e < fill ? lds_kv(base + e * S) : make_float2(CUDART_INF_F, 0.f);
+        out_idx[e] = e < fill ? __float_as_int(kv.y) : -1;
+        if (out_key) out_key[e] = kv.x;
+      }
     }
     return thr;
   }
