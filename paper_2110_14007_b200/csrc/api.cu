@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -43,7 +44,7 @@ struct Workspace {
 enum BufId {
   B_X = 0, B_Q, B_IMG_B, B_A2_B, B_E_B, B_IMG_A, B_A2_A, B_E_A, B_MU, B_PART,
   B_G, B_CIDX, B_CV, B_FAIL, B_SMALL, B_IDX, B_DIST, B_DIST64, B_KTH, B_MEAN, B_KD64,
-  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_NBUF
+  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_NBUF
 };
 
 }  // namespace
@@ -243,6 +244,11 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
   cands.S = plan.S;
   cands.lists = plan.lists;
   cands.dbg = (int)((ctx->cfg.flags >> 8) & 0xFF);
+  if (cands.dbg & 8) {
+    TOD_TRY(ensure(ctx, B_TRACE, 4096 * 8 * sizeof(long long), &p));
+    cands.trace = static_cast<long long*>(p);
+    TOD_CUDA(cudaMemsetAsync(p, 0, 4096 * 8 * sizeof(long long), st));
+  }
   TOD_TRY(ensure(ctx, B_CIDX, (size_t)std::max<int64_t>(q_count, 1) * cands.lists * plan.kp * 4, &p));
   cands.idx = static_cast<int32_t*>(p);
   TOD_TRY(ensure(ctx, B_CV, (size_t)std::max<int64_t>(q_count, 1) * cands.lists * 4, &p));
@@ -326,7 +332,20 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     TOD_CUDA(launch_knn_simt(dQ, q_begin, q_count, dX, n, d, self, cands, st, launches));
   }
   tm.mark();  // 3: certify start
-  if (cands.dbg) {  // profiling aid: pass 1 only, outputs invalid
+  if (cands.trace) {  // profiling aid: dump CTA 0's per-tile timestamps
+    static long long host_trace[4096 * 8];
+    TOD_CUDA(cudaMemcpyAsync(host_trace, cands.trace, sizeof host_trace, cudaMemcpyDeviceToHost, st));
+    TOD_CUDA(cudaStreamSynchronize(st));
+    const char* path = getenv("TOD_TRACE_FILE");
+    if (path) {
+      FILE* f = fopen(path, "wb");
+      if (f) {
+        fwrite(host_trace, sizeof host_trace, 1, f);
+        fclose(f);
+      }
+    }
+  }
+  if (cands.dbg & ~8) {  // profiling aid: pass 1 only, outputs invalid
     TOD_CUDA(cudaStreamSynchronize(st));
     tm.mark();
     tm.mark();

@@ -51,6 +51,7 @@ struct Cands {
   uint2* st_list = nullptr; // TC: [q tiles][kp][128] parked (key, index) state
   int* st_done = nullptr;   // TC: [q tiles] chunks completed
   int dbg = 0;  // profiling aid bits (TOD_F_DEBUG_*), 0 in production
+  long long* trace = nullptr;  // TOD_F_DEBUG_TRACE: [4096 tiles][8] clock64 stamps of CTA 0
 };
 
 enum PassKind : int { PASS_TC = 0, PASS_SIMT = 1 };

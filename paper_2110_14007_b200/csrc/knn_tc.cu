@@ -53,6 +53,10 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kExtraRB = 32;     // bytes per row of the 16-wide extra K block
 constexpr int kSmemMax = 232448; // 227 KB opt-in per block
+constexpr int kTraceTiles = 4096;
+#ifndef TOD_SMALL_BN
+#define TOD_SMALL_BN 128
+#endif // TOD_F_DEBUG_TRACE: per-tile timestamps of CTA 0
 
 __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
 
@@ -67,7 +71,9 @@ struct TcCfg {
   static constexpr int NKB = DPAD * 2 / RB;                  // main K regions
   static constexpr int LAYOUT = RB == 128 ? 2 : (RB == 64 ? 4 : 6);
   static constexpr int SBO = 8 * RB;
-  static constexpr int BN = DPAD <= 64 ? 256 : 128;
+  // d <= 32: short MMAs, so use 4 accumulators of 128 columns (deeper MMA/epilogue
+  // pipeline); d = 64: 2 accumulators of 256 (fewer, longer MMAs; half the smem reads).
+  static constexpr int BN = DPAD == 64 ? 256 : (DPAD == 128 ? 128 : TOD_SMALL_BN);
   static constexpr int BH = BN / SPLIT;                      // columns per epilogue warp
   static constexpr int KSTEPS = DPAD / 16;                   // main K steps (+1 extra)
   static constexpr int MAX_STAGE = 4;
@@ -82,7 +88,7 @@ struct TcCfg {
   static constexpr int B_BYTES = BN * (DPAD + 16) * 2;
   static constexpr int B_STRIDE = align_up(B_BYTES, 1024);
   static constexpr int B_EXTRA = BN * NKB * RB;
-  static constexpr int NACC = 2;                             // accumulators in TMEM
+  static constexpr int NACC = 512 / BN;                      // accumulators in TMEM
   static constexpr int TMEM_COLS = NACC * BN;
   static_assert(TMEM_COLS <= 512, "TMEM overflow");
 };
@@ -137,7 +143,7 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
              int64_t n_ref, int64_t qt0, int64_t n_qtiles, int64_t q_begin, int64_t q_end,
              int self_join, int S, int kp, int nstage, int dbg, int32_t* __restrict__ cand_idx,
              float* __restrict__ cand_v, float* __restrict__ cand_key, uint2* __restrict__ st_list,
-             int* __restrict__ st_done) {
+             int* __restrict__ st_done, long long* __restrict__ trace) {
   using C = TcCfg<DPAD, SPLIT>;
   constexpr int QT = C::QT;
   using List = RowTopK<C::NLIST, C::PEND>;
@@ -192,7 +198,7 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
         const int64_t qg = item % n_groups;
         const int c = (int)(item / n_groups);
         const int64_t t_lo = b_tiles * c / S, t_hi = b_tiles * (c + 1) / S;
-        mbar_wait(a_empty, aphase ^ 1);
+        mbar_wait_backoff(a_empty, aphase ^ 1);
         aphase ^= 1;
         mbar_arrive_expect_tx(a_full, QT * C::A_ONE);
         for (int s = 0; s < QT; ++s) {
@@ -205,7 +211,7 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
                    kBM * kExtraRB, a_full);
         }
         for (int64_t t = t_lo; t < t_hi; ++t) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait_backoff(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::B_BYTES);
           uint8_t* dst = sB + stage * C::B_STRIDE;
           for (int kb = 0; kb < C::NKB; ++kb)
@@ -231,20 +237,24 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       uint32_t aphase = 0;
+      int ntr = 0;
       for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
         const int c = (int)(item / n_groups);
         const int64_t t_lo = b_tiles * c / S, t_hi = b_tiles * (c + 1) / S;
-        mbar_wait(a_full, aphase);
+        mbar_wait_backoff(a_full, aphase);
         aphase ^= 1;
         tc_fence_after();
         for (int64_t t = t_lo; t < t_hi; ++t) {
-          mbar_wait(&full[stage], phase);
+          const bool tr = trace && blockIdx.x == 0 && ntr < kTraceTiles;
+          if (tr) trace[ntr * 8 + 0] = clock64();
+          mbar_wait_backoff(&full[stage], phase);
           tc_fence_after();
+          if (tr) trace[ntr * 8 + 1] = clock64();
           const uint32_t bst = b_base + stage * C::B_STRIDE;
 #pragma unroll
           for (int s = 0; s < QT; ++s) {
             const int ai = acc * QT + s;
-            mbar_wait(&t_empty[ai], acc_phase ^ 1);
+            mbar_wait_backoff(&t_empty[ai], acc_phase ^ 1);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + ai * C::BN;
             const uint32_t ast = a_base + s * C::A_STRIDE;
@@ -262,11 +272,13 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
             tc_commit(&t_full[ai]);
           }
           tc_commit(&empty[stage]);
+          if (tr) trace[ntr * 8 + 2] = clock64();
+          ++ntr;
           if (++stage == nstage) {
             stage = 0;
             phase ^= 1;
           }
-          if (++acc == 2) {
+          if (++acc == C::NACC) {
             acc = 0;
             acc_phase ^= 1;
           }
@@ -285,6 +297,7 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
     L.init(sL, li, kp);
     int acc = 0;
     uint32_t acc_phase = 0;
+    int etr = 0;
     constexpr int NCH = C::BH / 32;   // 32-column chunks per warp per tile (even)
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t qg = item % n_groups;
@@ -311,8 +324,11 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
         L.thr = fill == kp ? lds_kv(L.base + (kp - 1) * List::S).x : CUDART_INF_F;
       }
       for (int64_t tt = t_lo; tt < t_hi; ++tt) {
+        const bool tr = trace && blockIdx.x == 0 && warp == 2 && lane == 0 && etr < kTraceTiles;
+        if (tr) trace[etr * 8 + 3] = clock64();
         mbar_wait(&t_full[acc], acc_phase);
         tc_fence_after();
+        if (tr) trace[etr * 8 + 4] = clock64();
         const uint32_t taddr =
             tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::BN + half * C::BH;
         const int j0 = (int)(tt * C::BN) + half * C::BH;
@@ -346,11 +362,13 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
 #pragma unroll
             for (int ch = 0; ch < NCH; ch += 2) {
               tmem_ld_wait();
-              tmem_ld32(taddr + (ch + 1) * 32, vb);
+              if (ch + 1 < NCH) tmem_ld32(taddr + (ch + 1) * 32, vb);
               groups(va, ch);
-              tmem_ld_wait();
-              if (ch + 2 < NCH) tmem_ld32(taddr + (ch + 2) * 32, va);
-              groups(vb, ch + 1);
+              if (ch + 1 < NCH) {
+                tmem_ld_wait();
+                if (ch + 2 < NCH) tmem_ld32(taddr + (ch + 2) * 32, va);
+                groups(vb, ch + 1);
+              }
             }
           } else {
 #pragma unroll 1
@@ -365,8 +383,10 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
         }
         tc_fence_before();
         __syncwarp();
+        if (tr) trace[etr * 8 + 5] = clock64();
+        ++etr;
         if (lane == 0) mbar_arrive(&t_empty[acc]);
-        if (++acc == 2) {
+        if (++acc == C::NACC) {
           acc = 0;
           acc_phase ^= 1;
         }
@@ -423,7 +443,7 @@ cudaError_t launch_t(const Image& A, const Image& B, int64_t q_begin, int64_t q_
       reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(), A.extra_offset(),
       reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
       B.n_pad / C::BN, B.n, qt0, qt1 - qt0, q_begin, q_begin + q_count, self_join ? 1 : 0, c.S,
-      c.kp, nstage, c.dbg, c.idx, c.v, c.key, c.st_list, c.st_done);
+      c.kp, nstage, c.dbg, c.idx, c.v, c.key, c.st_list, c.st_done, c.trace);
   return cudaGetLastError();
 }
 

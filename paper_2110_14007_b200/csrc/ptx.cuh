@@ -44,6 +44,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// Same, for single-thread roles (producer, MMA issuer) that share an SM
+// sub-partition with epilogue warps: back off between polls so the spin does
+// not steal their issue slots.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) __nanosleep(64);
+}
 
 // ------------------------------------------------- bulk async copy (TMA engine)
 // Global -> shared, completion reported as transaction bytes on `bar`.
