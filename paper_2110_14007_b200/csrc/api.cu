@@ -160,14 +160,22 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
     // Reference chunks: each chunk's operand image should stay L2-resident
     // while all CTAs sweep it (chunk-major work order), and the (query tile x
     // chunk) items should fill the last wave of the persistent grid.
-    // Epilogue split: two warps per TMEM lane quarter, each with its own
-    // per-row list of K'' = K'/2 + 8 candidates over half of every tile.
+    // Epilogue split: 1, 2 or 4 warps per TMEM lane quarter, each with its own
+    // per-row list over its part of every tile (K'' = K' for 1 part,
+    // K'/2 + 8 for 2, K'/4 + 4 for 4; the re-rank takes the union).
+    auto khalf = [&](int sp) { return sp == 1 ? kp : (sp == 2 ? roundup(kp / 2 + 8, 4) : roundup(kp / 4 + 4, 4)); };
     int sp = ctx->cfg.epilogue_split;
-    const int kh = roundup(kp / 2 + 8, 8);
-    if (sp <= 0 || sp > 2) sp = tc_split_fits(p->dpad, kh) ? 2 : 1;
-    if (sp == 2 && !tc_split_fits(p->dpad, kh)) sp = 1;
+    if (sp != 1 && sp != 2 && sp != 4) {
+      sp = 1;
+      for (int cand : {4, 2})
+        if (tc_split_fits(p->dpad, khalf(cand), cand)) {
+          sp = cand;
+          break;
+        }
+    }
+    if (sp != 1 && !tc_split_fits(p->dpad, khalf(sp), sp)) sp = 1;
     p->lists = sp;
-    if (sp == 2) p->kp = kh;
+    p->kp = khalf(sp);
     const int64_t qtiles = (q_count + 127) / 128 + 1;
     const int64_t btiles = (n_ref + 255) / 256;
     const double img_bytes = (double)btiles * 256 * (p->dpad + 16) * 2;

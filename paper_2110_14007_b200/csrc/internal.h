@@ -70,7 +70,7 @@ cudaError_t launch_finite_check(const float* X, int64_t n, int d, PrepGlobals* g
                                 int* launches);
 
 // ---- knn_tc.cu  (tcgen05 fused distance + top-K')
-int tc_split_fits(int dpad, int kp);  // 1 if the SPLIT=2 epilogue fits in smem with K''=kp
+int tc_split_fits(int dpad, int kp, int split);  // 1 if the split epilogue fits in smem with K''=kp
 cudaError_t launch_knn_tc(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                           bool self_join, int fmt, Cands c, int num_sms, cudaStream_t st,
                           int* launches);

@@ -55,7 +55,7 @@ constexpr int kExtraRB = 32;     // bytes per row of the 16-wide extra K block
 constexpr int kSmemMax = 232448; // 227 KB opt-in per block
 constexpr int kTraceTiles = 4096;
 #ifndef TOD_SMALL_BN
-#define TOD_SMALL_BN 128
+#define TOD_SMALL_BN 256
 #endif // TOD_F_DEBUG_TRACE: per-tile timestamps of CTA 0
 
 __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
@@ -79,7 +79,7 @@ struct TcCfg {
   static constexpr int MAX_STAGE = 4;
   static constexpr int NROWS = kBM;                          // query rows per CTA item
   static constexpr int NLIST = kBM * SPLIT;                  // lists per CTA item
-  static constexpr int PEND = 16;                            // pending slots per list (group entries)
+  static constexpr int PEND = SPLIT == 4 ? 16 : (DPAD <= 32 ? 32 : 24);  // pending slots per list
   static constexpr int EPI_WARPS = 4 * SPLIT;
   static constexpr int THREADS = 64 + 32 * EPI_WARPS;
   static constexpr int A_ONE = kBM * (DPAD + 16) * 2;        // one query tile
@@ -147,6 +147,9 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
   using C = TcCfg<DPAD, SPLIT>;
   constexpr int QT = C::QT;
   using List = RowTopK<C::NLIST, C::PEND>;
+  // Reserve pending room once per tile when a tile's worst case fits in half
+  // the pending run; otherwise per 32-column chunk.
+  constexpr bool kTileReserve = C::BH / 8 <= C::PEND / 2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   int off_b, off_l, off_bar;
@@ -189,17 +192,18 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
   const int64_t n_items = n_groups * S;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ producer
-      int stage = 0;
-      uint32_t phase = 0;
-      uint32_t aphase = 0;
-      for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const int64_t qg = item % n_groups;
-        const int c = (int)(item / n_groups);
-        const int64_t t_lo = b_tiles * c / S, t_hi = b_tiles * (c + 1) / S;
-        mbar_wait_backoff(a_empty, aphase ^ 1);
-        aphase ^= 1;
+    // -------------------------------------------------------------- producer
+    // The whole warp runs the loop (converged); one elected lane issues.
+    int stage = 0;
+    uint32_t phase = 0;
+    uint32_t aphase = 0;
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int64_t qg = item % n_groups;
+      const int c = (int)(item / n_groups);
+      const int64_t t_lo = b_tiles * c / S, t_hi = b_tiles * (c + 1) / S;
+      mbar_wait_backoff(a_empty, aphase ^ 1);
+      aphase ^= 1;
+      if (elect_one()) {
         mbar_arrive_expect_tx(a_full, QT * C::A_ONE);
         for (int s = 0; s < QT; ++s) {
           const int64_t qtl = qg * QT + s;  // local query tile (A image rows qtl*128..)
@@ -210,8 +214,11 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
           bulk_g2s(dstA + C::A_EXTRA, a_img + a_extra + qtl * (int64_t)kBM * kExtraRB,
                    kBM * kExtraRB, a_full);
         }
-        for (int64_t t = t_lo; t < t_hi; ++t) {
-          mbar_wait_backoff(&empty[stage], phase ^ 1);
+      }
+      __syncwarp();
+      for (int64_t t = t_lo; t < t_hi; ++t) {
+        mbar_wait_backoff(&empty[stage], phase ^ 1);
+        if (elect_one()) {
           mbar_arrive_expect_tx(&full[stage], C::B_BYTES);
           uint8_t* dst = sB + stage * C::B_STRIDE;
           for (int kb = 0; kb < C::NKB; ++kb)
@@ -219,77 +226,87 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
                      C::BN * C::RB, &full[stage]);
           bulk_g2s(dst + C::B_EXTRA, b_img + b_extra + t * (int64_t)C::BN * kExtraRB,
                    C::BN * kExtraRB, &full[stage]);
-          if (++stage == nstage) {
-            stage = 0;
-            phase ^= 1;
-          }
+        }
+        __syncwarp();
+        if (++stage == nstage) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------------------------------------------------- MMA issuer
-      constexpr uint32_t IDESC = idesc_f16(kBM, C::BN, FMT == 1 ? 0u : 1u);
-      const uint32_t a_base = smem_u32(sA);
-      const uint32_t b_base = smem_u32(sB);
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      uint32_t aphase = 0;
-      int ntr = 0;
-      for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const int c = (int)(item / n_groups);
-        const int64_t t_lo = b_tiles * c / S, t_hi = b_tiles * (c + 1) / S;
-        mbar_wait_backoff(a_full, aphase);
-        aphase ^= 1;
+    // ------------------------------------------------------------ MMA issuer
+    // Whole warp converged in the loop; descriptors precomputed (a shared-
+    // memory descriptor advances by (bytes >> 4) in its low field); one elected
+    // lane issues the MMAs and the commits that track them.
+    constexpr uint32_t IDESC = idesc_f16(kBM, C::BN, FMT == 1 ? 0u : 1u);
+    constexpr int NK = C::KSTEPS + 1;
+    const uint32_t a_base = smem_u32(sA);
+    const uint32_t b_base = smem_u32(sB);
+    uint64_t adesc[NK], bdesc[NK];
+#pragma unroll
+    for (int ks = 0; ks < C::KSTEPS; ++ks) {
+      const int kb = (ks * 32) / C::RB;
+      const int koff = (ks * 32) % C::RB;
+      adesc[ks] = smem_desc(a_base + kb * kBM * C::RB + koff, C::SBO, C::LAYOUT);
+      bdesc[ks] = smem_desc(b_base + kb * C::BN * C::RB + koff, C::SBO, C::LAYOUT);
+    }
+    adesc[C::KSTEPS] = smem_desc(a_base + C::A_EXTRA, 8 * kExtraRB, 6);
+    bdesc[C::KSTEPS] = smem_desc(b_base + C::B_EXTRA, 8 * kExtraRB, 6);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    uint32_t aphase = 0;
+    int ntr = 0;
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int c = (int)(item / n_groups);
+      const int64_t t_lo = b_tiles * c / S, t_hi = b_tiles * (c + 1) / S;
+      mbar_wait(a_full, aphase);
+      aphase ^= 1;
+      tc_fence_after();
+      for (int64_t t = t_lo; t < t_hi; ++t) {
+        const bool tr = trace && blockIdx.x == 0 && lane == 0 && ntr < kTraceTiles;
+        if (tr) trace[ntr * 8 + 0] = clock64();
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        for (int64_t t = t_lo; t < t_hi; ++t) {
-          const bool tr = trace && blockIdx.x == 0 && ntr < kTraceTiles;
-          if (tr) trace[ntr * 8 + 0] = clock64();
-          mbar_wait_backoff(&full[stage], phase);
+        if (tr) trace[ntr * 8 + 1] = clock64();
+        const uint64_t bst = (uint64_t)((stage * C::B_STRIDE) >> 4);
+#pragma unroll
+        for (int s = 0; s < QT; ++s) {
+          const int ai = acc * QT + s;
+          mbar_wait(&t_empty[ai], acc_phase ^ 1);
           tc_fence_after();
-          if (tr) trace[ntr * 8 + 1] = clock64();
-          const uint32_t bst = b_base + stage * C::B_STRIDE;
+          const uint32_t d_tmem = tmem_base + ai * C::BN;
+          const uint64_t ast = (uint64_t)((s * C::A_STRIDE) >> 4);
+          if (elect_one()) {
 #pragma unroll
-          for (int s = 0; s < QT; ++s) {
-            const int ai = acc * QT + s;
-            mbar_wait_backoff(&t_empty[ai], acc_phase ^ 1);
-            tc_fence_after();
-            const uint32_t d_tmem = tmem_base + ai * C::BN;
-            const uint32_t ast = a_base + s * C::A_STRIDE;
-#pragma unroll
-            for (int ks = 0; ks < C::KSTEPS; ++ks) {
-              const int kb = (ks * 32) / C::RB;
-              const int koff = (ks * 32) % C::RB;
-              const uint64_t ad = smem_desc(ast + kb * kBM * C::RB + koff, C::SBO, C::LAYOUT);
-              const uint64_t bd = smem_desc(bst + kb * C::BN * C::RB + koff, C::SBO, C::LAYOUT);
-              tc_mma_f16(d_tmem, ad, bd, IDESC, ks > 0 ? 1u : 0u);
-            }
-            // extra K block: ||xhat_j||^2 pieces x constants (SW32, 8-row atoms of 256 B)
-            tc_mma_f16(d_tmem, smem_desc(ast + C::A_EXTRA, 8 * kExtraRB, 6),
-                       smem_desc(bst + C::B_EXTRA, 8 * kExtraRB, 6), IDESC, 1u);
+            for (int ks = 0; ks < NK; ++ks)
+              tc_mma_f16(d_tmem, adesc[ks] + ast, bdesc[ks] + bst, IDESC, ks > 0 ? 1u : 0u);
             tc_commit(&t_full[ai]);
           }
-          tc_commit(&empty[stage]);
-          if (tr) trace[ntr * 8 + 2] = clock64();
-          ++ntr;
-          if (++stage == nstage) {
-            stage = 0;
-            phase ^= 1;
-          }
-          if (++acc == C::NACC) {
-            acc = 0;
-            acc_phase ^= 1;
-          }
+          __syncwarp();
         }
-        tc_commit(a_empty);
+        if (elect_one()) tc_commit(&empty[stage]);
+        __syncwarp();
+        if (tr) trace[ntr * 8 + 2] = clock64();
+        ++ntr;
+        if (++stage == nstage) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (++acc == C::NACC) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
       }
+      if (elect_one()) tc_commit(a_empty);
+      __syncwarp();
     }
   } else {
     // ---------------------------------------------------------------- epilogue
     const int ew = warp - 2;          // epilogue warp index
-    const int half = ew / 4;          // column half of each tile (SPLIT = 2)
+    const int half = ew / 4;          // column part of each tile (0..SPLIT-1)
     const int q = warp & 3;           // TMEM lane quarter this warp may access
     const int t = q * 32 + lane;      // row within the query tile
     const int li = half * kBM + t;    // list slot (row, half)
@@ -323,6 +340,7 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
         L.fill = fill;
         L.thr = fill == kp ? lds_kv(L.base + (kp - 1) * List::S).x : CUDART_INF_F;
       }
+      if (kTileReserve) L.reserve(C::BH / 8);
       for (int64_t tt = t_lo; tt < t_hi; ++tt) {
         const bool tr = trace && blockIdx.x == 0 && warp == 2 && lane == 0 && etr < kTraceTiles;
         if (tr) trace[etr * 8 + 3] = clock64();
@@ -352,22 +370,31 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
                            fminf(fminf(vg[3], vg[4]), fminf(fminf(vg[5], vg[6]), vg[7])));
             }
             const float th = L.thr;
-            L.reserve(4);
+            if (!kTileReserve) L.reserve(4);
 #pragma unroll
             for (int g = 0; g < 4; ++g) L.append_if(m[g] < th, m[g], gbase + ch * 4 + g);
           };
           if (!masked) {
-            float va[32], vb[32];
-            tmem_ld32(taddr, va);
+            // 64 columns per TMEM load, waited on immediately: no register of
+            // an in-flight tcgen05.ld may be touched (spilled, saved across a
+            // call) before tcgen05.wait::ld, so nothing is kept in flight
+            // across other work.  Latency is hidden by the other epilogue warps.
+            if constexpr (NCH % 2 == 0) {
 #pragma unroll
-            for (int ch = 0; ch < NCH; ch += 2) {
-              tmem_ld_wait();
-              if (ch + 1 < NCH) tmem_ld32(taddr + (ch + 1) * 32, vb);
-              groups(va, ch);
-              if (ch + 1 < NCH) {
+              for (int ch = 0; ch < NCH; ch += 2) {
+                float v[64];
+                tmem_ld64(taddr + ch * 32, v);
                 tmem_ld_wait();
-                if (ch + 2 < NCH) tmem_ld32(taddr + (ch + 2) * 32, va);
-                groups(vb, ch + 1);
+                groups(*reinterpret_cast<const float(*)[32]>(v), ch);
+                groups(*reinterpret_cast<const float(*)[32]>(v + 32), ch + 1);
+              }
+            } else {
+#pragma unroll
+              for (int ch = 0; ch < NCH; ++ch) {
+                float v[32];
+                tmem_ld32(taddr + ch * 32, v);
+                tmem_ld_wait();
+                groups(v, ch);
               }
             }
           } else {
@@ -389,6 +416,17 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
         if (++acc == C::NACC) {
           acc = 0;
           acc_phase ^= 1;
+        }
+        // Room for the next tile's appends (at most one per 8-column group).
+        // Merging only here, between tiles, keeps no TMEM values live across
+        // the call, and all epilogue warps tend to merge at the same tile.
+        if (kTileReserve) {
+          const long long m0 = tr ? clock64() : 0;
+          L.reserve(C::BH / 8);
+          if (tr) {
+            trace[(etr - 1) * 8 + 6] = clock64() - m0;  // merge (or check) cycles after this tile
+            trace[(etr - 1) * 8 + 7] = (long long)(L.pa - (L.base + kp * List::S)) / List::S;
+          }
         }
       }
       if (c < S - 1) {
@@ -450,19 +488,25 @@ cudaError_t launch_t(const Image& A, const Image& B, int64_t q_begin, int64_t q_
 template <int DPAD, int FMT>
 cudaError_t launch_d(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                      bool self_join, Cands c, int num_sms, cudaStream_t st) {
+  if (c.lists == 4) return launch_t<DPAD, FMT, 4>(A, B, q_begin, q_count, self_join, c, num_sms, st);
   if (c.lists == 2) return launch_t<DPAD, FMT, 2>(A, B, q_begin, q_count, self_join, c, num_sms, st);
   return launch_t<DPAD, FMT, 1>(A, B, q_begin, q_count, self_join, c, num_sms, st);
 }
 
 }  // namespace
 
-int tc_split_fits(int dpad, int kp) {
+int tc_split_fits(int dpad, int kp, int split) {
+#define TOD_FITS(D)                                                               \
+  case D:                                                                         \
+    return split == 4 ? pick_stages<D, 4>(kp) > 0                                 \
+                      : (split == 2 ? pick_stages<D, 2>(kp) > 0 : pick_stages<D, 1>(kp) > 0);
   switch (dpad) {
-    case 16: return pick_stages<16, 2>(kp) > 0;
-    case 32: return pick_stages<32, 2>(kp) > 0;
-    case 64: return pick_stages<64, 2>(kp) > 0;
-    case 128: return pick_stages<128, 2>(kp) > 0;
+    TOD_FITS(16)
+    TOD_FITS(32)
+    TOD_FITS(64)
+    TOD_FITS(128)
   }
+#undef TOD_FITS
   return 0;
 }
 

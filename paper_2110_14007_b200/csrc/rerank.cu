@@ -249,13 +249,14 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
     const float key = cand_key[r * G + e];
     const int g = cand_idx[r * G + e];
     int rank = pos;
-    if (lists == 2) {  // rank among the other list (ties: list 0 first)
-      const float* other = cand_key + r * G + (1 - a) * kp;
+    for (int b = 0; b < lists; ++b) {  // rank among the other lists (ties: lower list first)
+      if (b == a) continue;
+      const float* other = cand_key + r * G + b * kp;
       int lo = 0, hi = kp;
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
         const float om = other[mid];
-        if (a == 0 ? (om < key) : (om <= key)) lo = mid + 1;
+        if (b > a ? (om < key) : (om <= key)) lo = mid + 1;
         else hi = mid;
       }
       rank += lo;
@@ -516,7 +517,7 @@ cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, cons
                           double* max_err, cudaStream_t st, int* launches) {
   if (k > kMaxK) return cudaErrorInvalidValue;
   if (cp.kind == PASS_TC) {  // group candidates
-    if (c.lists * c.kp > kGrpMaxG || c.lists > 2 || !c.key) return cudaErrorInvalidValue;
+    if (c.lists * c.kp > kGrpMaxG || !c.key) return cudaErrorInvalidValue;
     const int64_t gb = (q_count + kGrpWarps - 1) / kGrpWarps;
     if (gb == 0) return cudaSuccess;
     const size_t smem = (size_t)kGrpWarps * d * 8;

@@ -41,22 +41,24 @@ __device__ __noinline__ float2 merge_row(uint32_t base, int kp, int fill, int pc
     return make_float2(__int_as_float(fill), t);
   }
   const uint32_t pb = base + kp * S;
-  float pv[kPend];
-  int pi[kPend];
+  // the bitonic network needs a power-of-two width: pad with +inf
+  constexpr int NP = kPend <= 8 ? 8 : (kPend <= 16 ? 16 : (kPend <= 32 ? 32 : 64));
+  float pv[NP];
+  int pi[NP];
 #pragma unroll
-  for (int p = 0; p < kPend; ++p) {
-    const bool live = p < pcnt;
+  for (int p = 0; p < NP; ++p) {
+    const bool live = p < kPend && p < pcnt;
     const float2 e = live ? lds_kv(pb + p * S) : make_float2(CUDART_INF_F, __int_as_float(-1));
     pv[p] = e.x;
     pi[p] = __float_as_int(e.y);
   }
   // Bitonic sort ascending (fully unrolled: stays in registers).
 #pragma unroll
-  for (int k = 2; k <= kPend; k <<= 1) {
+  for (int k = 2; k <= NP; k <<= 1) {
 #pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
 #pragma unroll
-      for (int i = 0; i < kPend; ++i) {
+      for (int i = 0; i < NP; ++i) {
         const int l = i ^ j;
         if (l > i) {
           const bool up = (i & k) == 0;
@@ -74,6 +76,7 @@ __device__ __noinline__ float2 merge_row(uint32_t base, int kp, int fill, int pc
 #pragma unroll
   for (int p = 0; p < kPend; ++p)
     if (p < pcnt) sts_kv(pb + p * S, pv[p], pi[p]);
+  static_assert(NP >= kPend, "network narrower than the pending run");
   // Backward in-place merge of list[0,fill) and pending[0,pcnt) (both
   // ascending) into list[0, min(fill+pcnt, kp)).  Once the pending run is
   // exhausted the remaining list prefix is already in place (o == i).
@@ -98,6 +101,74 @@ __device__ __noinline__ float2 merge_row(uint32_t base, int kp, int fill, int pc
   }
   fill = min(fill + pcnt, kp);
   const float t = (fill == kp) ? lds_kv(base + (kp - 1) * S).x : CUDART_INF_F;
+  return make_float2(__int_as_float(fill), t);
+}
+
+// Register-network merge for short lists (kp <= 32, P <= 32): load the sorted
+// list and the pending run into registers, bitonic-sort the pending run, take
+// the lower half of a half-cleaner between the list and the reversed pending
+// run (= the 32 smallest, bitonic) and sort it with five merge stages.  No
+// dependent shared-memory chains: ~350 compare-exchanges with full ILP.
+template <int NT, int kPend, int W>
+__device__ __noinline__ float2 merge_row_net(uint32_t base, int kp, int fill, int pcnt) {
+  constexpr uint32_t S = NT * 8;
+  static_assert(kPend <= W, "pending run longer than the network");
+  if (pcnt == 0) {
+    const float t = (fill == kp) ? lds_kv(base + (kp - 1) * S).x : CUDART_INF_F;
+    return make_float2(__int_as_float(fill), t);
+  }
+  float lk[W], pk[W];
+  int li[W], pi[W];
+#pragma unroll
+  for (int e = 0; e < W; ++e) {
+    const bool liv = e < fill;
+    const float2 a = liv ? lds_kv(base + e * S) : make_float2(CUDART_INF_F, __int_as_float(-1));
+    lk[e] = a.x;
+    li[e] = __float_as_int(a.y);
+    const bool piv = e < kPend && e < pcnt;
+    const float2 b = piv ? lds_kv(base + (kp + e) * S) : make_float2(CUDART_INF_F, __int_as_float(-1));
+    pk[e] = b.x;
+    pi[e] = __float_as_int(b.y);
+  }
+  auto cas = [](float& ka, int& ia, float& kb, int& ib, bool up) {
+    const bool sw = up ? (ka > kb) : (ka < kb);
+    const float tk = ka;
+    const int ti = ia;
+    ka = sw ? kb : ka;
+    ia = sw ? ib : ia;
+    kb = sw ? tk : kb;
+    ib = sw ? ti : ib;
+  };
+#pragma unroll
+  for (int k = 2; k <= W; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+      for (int i = 0; i < W; ++i) {
+        const int l = i ^ j;
+        if (l > i) cas(pk[i], pi[i], pk[l], pi[l], (i & k) == 0);
+      }
+  // half-cleaner: lower half = elementwise min of list and reversed pending
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    const bool take = pk[W - 1 - i] < lk[i];
+    lk[i] = take ? pk[W - 1 - i] : lk[i];
+    li[i] = take ? pi[W - 1 - i] : li[i];
+  }
+#pragma unroll
+  for (int j = W >> 1; j > 0; j >>= 1)
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      const int l = i ^ j;
+      if (l > i) cas(lk[i], li[i], lk[l], li[l], true);
+    }
+  fill = min(fill + pcnt, kp);
+  float t = CUDART_INF_F;
+#pragma unroll
+  for (int e = 0; e < W; ++e) {
+    if (e < fill) sts_kv(base + e * S, lk[e], li[e]);
+    t = (e == kp - 1 && fill == kp) ? lk[e] : t;
+  }
   return make_float2(__int_as_float(fill), t);
 }
 
@@ -130,7 +201,13 @@ struct RowTopK {
   }
   // Whole warp must call (lanes with no pending entries are no-ops).
   __device__ __forceinline__ void merge() {
-    const float2 r = merge_row<NT, P>(base, kp, fill, pcnt());
+    float2 r;
+    if (P <= 16 && kp <= 16)
+      r = merge_row_net<NT, (P <= 16 ? P : 16), 16>(base, kp, fill, pcnt());
+    else if (P <= 32 && kp <= 32)
+      r = merge_row_net<NT, (P <= 32 ? P : 32), 32>(base, kp, fill, pcnt());
+    else
+      r = merge_row<NT, P>(base, kp, fill, pcnt());
     fill = __float_as_int(r.x);
     thr = r.y;
     pa = base + kp * S;

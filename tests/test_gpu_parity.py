@@ -79,6 +79,20 @@ def test_knn_full_parity(pkg, n, d, k, fmt):
         assert st["certified"] >= 0.95 * n, st
 
 
+@pytest.mark.parametrize("d", [32, 64])
+@pytest.mark.parametrize("fmt", ["fp16", "bf16"])
+@pytest.mark.parametrize("split", [1, 2, 4])
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_epilogue_variants_parity(pkg, d, fmt, split, chunks):
+    # every epilogue layout (1/2/4 lists per row, pending widths 16/24/32,
+    # tile- and chunk-level reserves) and parked state across chunks
+    n, k = 2300, 10
+    X = datagen.gaussian_mixture(n, d, seed=77 + d)
+    with _ctx(pkg, fmt=fmt, split=split, chunks=chunks) as ctx:
+        res = ctx.knn(torch.from_numpy(X).cuda(), k)
+    _check_rows(res, X, k, np.arange(n))
+
+
 def test_forced_fallback_tier(pkg):
     X = datagen.gaussian_mixture(1200, 24, seed=5)
     with _ctx(pkg, flags=pkg.F_NO_CERTIFY) as ctx:

@@ -17,3 +17,8 @@ base = min(mma[0, 0], epi[0, 0])
 print("first tiles (cycles rel.): mma_start mma_full mma_done | epi_start epi_gotfull epi_done")
 for i in range(100, 112):
     print(i, mma[i] - base, "|", epi[i] - base)
+m = t[(t[:, 3] > 0) & (t[:, 5] > 0)][:, 6:8]
+if len(m):
+    big = m[:, 0] > 500
+    print("tile-boundary reserve: p50 %.0f cycles; merges (>500 cyc): %d of %d tiles, mean %.0f cycles; pending after p50 %.0f max %d"
+          % (np.median(m[:, 0]), big.sum(), len(m), m[big, 0].mean() if big.any() else 0, np.median(m[:, 1]), m[:, 1].max()))
