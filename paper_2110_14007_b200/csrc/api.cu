@@ -44,7 +44,7 @@ struct Workspace {
 enum BufId {
   B_X = 0, B_Q, B_IMG_B, B_A2_B, B_E_B, B_IMG_A, B_A2_A, B_E_A, B_MU, B_PART,
   B_G, B_CIDX, B_CV, B_FAIL, B_SMALL, B_IDX, B_DIST, B_DIST64, B_KTH, B_MEAN, B_KD64,
-  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_NBUF
+  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT, B_NBUF
 };
 
 }  // namespace
@@ -126,6 +126,10 @@ struct Plan {
   int kp;
   int S;
   int lists;     // candidate lists per row (TC: epilogue split; SIMT: S)
+  int two;       // TC: two-pass candidate selection (sample pass + append-only main pass)
+  int R;         // two-pass: sample stride over 256-column reference tiles
+  int main_S;    // two-pass: main-pass reference chunks
+  int cap;       // two-pass: main-pass buffer slots per (row, column half)
 };
 
 tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k, Plan* p) {
@@ -156,6 +160,27 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
                 kmax_list, k);
   p->kp = kp;
   int S = ctx->cfg.chunks;
+  p->two = 0;
+  p->R = 1;
+  p->main_S = 0;
+  p->cap = 0;
+  const int64_t bt256 = (n_ref + 255) / 256;
+  int64_t bt_v1 = 0;  // reference tiles seen by the v1 kernel (the sample pass: every R-th)
+  if (p->kind == PASS_TC && !(ctx->cfg.flags & TOD_F_PASS1_V1) && p->dpad <= 64 &&
+      tc3_fits(p->dpad) && bt256 >= 32) {
+    // Two-pass candidate selection: the sample pass keeps kps
+    // groups per row over every R-th tile; its threshold filters the main pass,
+    // which appends ~R*kps groups per row.  K' is the target count of kept
+    // groups; kps = 2K'/R leaves a wide margin for the sample's variance.
+    p->two = 1;
+    p->R = 8;
+    const int kps = std::min(64, std::max(8, roundup((2 * kp + p->R - 1) / p->R, 4)));
+    const double img_bytes = (double)bt256 * 256 * (p->dpad + 16) * 2;
+    p->main_S = std::max(1, (int)std::ceil(img_bytes / (48.0 * 1024 * 1024)));
+    p->cap = roundup(std::max(64, 2 * (p->R - 1) * kps), 32);
+    bt_v1 = (bt256 + p->R - 1) / p->R;
+  }
+  if (p->kind == PASS_TC && !p->two && p->dpad <= 64) bt_v1 = bt256;
   if (p->kind == PASS_TC) {
     // Reference chunks: each chunk's operand image should stay L2-resident
     // while all CTAs sweep it (chunk-major work order), and the (query tile x
@@ -163,21 +188,29 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
     // Epilogue split: 1, 2 or 4 warps per TMEM lane quarter, each with its own
     // per-row list over its part of every tile (K'' = K' for 1 part,
     // K'/2 + 8 for 2, K'/4 + 4 for 4; the re-rank takes the union).
-    auto khalf = [&](int sp) { return sp == 1 ? kp : (sp == 2 ? roundup(kp / 2 + 8, 4) : roundup(kp / 4 + 4, 4)); };
+    // Two-pass: the sample pass keeps ~2K'/R groups per row in total, split over
+    // the lists (its threshold is the minimum of the lists' thresholds).
+    auto khalf = [&](int sp) {
+      if (p->two) return std::max(4, roundup((2 * kp + p->R * sp - 1) / (p->R * sp), 4));
+      return sp == 1 ? kp : (sp == 2 ? roundup(kp / 2 + 8, 4) : roundup(kp / 4 + 4, 4));
+    };
     int sp = ctx->cfg.epilogue_split;
+    if (p->two && sp == 4) sp = 2;
     if (sp != 1 && sp != 2 && sp != 4) {
       sp = 1;
-      for (int cand : {4, 2})
+      for (int cand : {4, 2}) {
+        if (p->two && cand == 4) continue;
         if (tc_split_fits(p->dpad, khalf(cand), cand)) {
           sp = cand;
           break;
         }
+      }
     }
     if (sp != 1 && !tc_split_fits(p->dpad, khalf(sp), sp)) sp = 1;
     p->lists = sp;
     p->kp = khalf(sp);
     const int64_t qtiles = (q_count + 127) / 128 + 1;
-    const int64_t btiles = (n_ref + 255) / 256;
+    const int64_t btiles = bt_v1 > 0 ? bt_v1 : (n_ref + 255) / 256;
     const double img_bytes = (double)btiles * 256 * (p->dpad + 16) * 2;
     const int s_min = std::max(1, (int)std::ceil(img_bytes / (48.0 * 1024 * 1024)));
     if (S <= 0) {
@@ -248,9 +281,11 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
   PrepGlobals* g = &small->g;
 
   Cands cands;
+  MainPass mp;
   cands.kp = plan.kp;
   cands.S = plan.S;
   cands.lists = plan.lists;
+  cands.R = plan.R;
   cands.dbg = (int)((ctx->cfg.flags >> 8) & 0xFF);
   if (cands.dbg & 8) {
     TOD_TRY(ensure(ctx, B_TRACE, 4096 * 8 * sizeof(long long), &p));
@@ -331,8 +366,22 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     cp.qa2 = A.a2 + (self ? q_begin - a_row0 : 0);
     cp.qe = A.e + (self ? q_begin - a_row0 : 0);
     tm.mark();  // 2: main start
-    TOD_CUDA(launch_knn_tc(A, B, self ? q_begin : 0, q_count, self, plan.fmt, cands, ctx->num_sms,
-                           st, launches));
+    TOD_CUDA(launch_knn_tc(A, B, self ? q_begin : 0, q_count, self, plan.fmt, cands,
+                           ctx->num_sms, st, launches));
+    if (plan.two) {
+      mp.S = plan.main_S;
+      mp.R = plan.R;
+      mp.tau_v = cands.v;
+      mp.tau_lists = cands.lists;
+      mp.cap = plan.cap;
+      TOD_TRY(ensure(ctx, B_MBUF, (size_t)std::max<int64_t>(q_count, 1) * 2 * plan.cap * 8, &p));
+      mp.buf = static_cast<uint2*>(p);
+      TOD_TRY(ensure(ctx, B_MCNT, (size_t)std::max<int64_t>(q_count, 1) * 2 * 4, &p));
+      mp.cnt = static_cast<int*>(p);
+      TOD_CUDA(cudaMemsetAsync(mp.cnt, 0, (size_t)std::max<int64_t>(q_count, 1) * 2 * 4, st));
+      TOD_CUDA(launch_knn_tc3(A, B, self ? q_begin : 0, q_count, self, plan.fmt, mp,
+                              ctx->num_sms, cands.dbg, st, launches));
+    }
   } else {
     TOD_CUDA(launch_finite_check(dX, n, d, g, st, launches));
     if (!self) TOD_CUDA(launch_finite_check(dQ, q_count, d, g, st, launches));
@@ -366,7 +415,8 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     }
     return TOD_OK;
   }
-  TOD_CUDA(launch_rerank(dQ, q_begin, q_count, dX, n, d, k, self, cands, cp, out, fail_rows,
+  TOD_CUDA(launch_rerank(dQ, q_begin, q_count, dX, n, d, k, self, cands, plan.two ? &mp : nullptr,
+                         cp, out, fail_rows,
                          &small->fail_count, &small->max_err, st, launches));
   tm.mark();  // 4: fallback start
   SmallDev h{};

@@ -50,6 +50,7 @@ struct Cands {
   int lists = 1;            // lists per row (TC: epilogue split 1|2; SIMT: S)
   uint2* st_list = nullptr; // TC: [q tiles][kp][128] parked (key, index) state
   int* st_done = nullptr;   // TC: [q tiles] chunks completed
+  int R = 1;                // tile stride (sample pass: every R-th 256-column tile)
   int dbg = 0;  // profiling aid bits (TOD_F_DEBUG_*), 0 in production
   long long* trace = nullptr;  // TOD_F_DEBUG_TRACE: [4096 tiles][8] clock64 stamps of CTA 0
 };
@@ -75,6 +76,26 @@ cudaError_t launch_knn_tc(const Image& A, const Image& B, int64_t q_begin, int64
                           bool self_join, int fmt, Cands c, int num_sms, cudaStream_t st,
                           int* launches);
 
+// ---- knn_tc3.cu  (main pass: tcgen05 distance + fixed-threshold filter, append-only)
+// Two-pass candidate selection: the sample pass (launch_knn_tc with
+// Cands.R = R) keeps a small list per row over every R-th 256-column reference
+// tile; its threshold v is tau for the main pass, which appends every group of
+// the remaining tiles whose minimum is below tau to a per-(row, column half)
+// HBM buffer.
+struct MainPass {
+  int S = 1;                  // reference chunks (L2 locality)
+  int R = 0;                  // sample stride: tiles t % R == 0 are skipped (0 = none)
+  const float* tau_v = nullptr;  // [q_count][tau_lists] sample-list thresholds
+  int tau_lists = 1;
+  uint2* buf = nullptr;       // [q_count][2][cap] (key bits, group index)
+  int* cnt = nullptr;         // [q_count][2] appended counts (may exceed cap = overflow)
+  int cap = 0;
+};
+int tc3_fits(int dpad);
+cudaError_t launch_knn_tc3(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
+                           bool self_join, int fmt, const MainPass& m, int num_sms, int dbg,
+                           cudaStream_t st, int* launches);
+
 // ---- knn_simt.cu  (CUDA-core fp32 difference-form fused distance + top-K')
 cudaError_t launch_knn_simt(const float* Q, int64_t q_begin, int64_t q_count, const float* X,
                             int64_t n, int d, bool self_join, Cands c, cudaStream_t st,
@@ -99,7 +120,8 @@ struct KnnOutDev {
   double* kdist64;
 };
 cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, const float* X,
-                          int64_t n, int d, int k, bool self_join, Cands c, CertParams cp,
+                          int64_t n, int d, int k, bool self_join, Cands c, const MainPass* mp,
+                          CertParams cp,
                           KnnOutDev out, int32_t* fail_rows, int32_t* fail_count,
                           double* max_err, cudaStream_t st, int* launches);
 int fallback_slices(int nfail, int64_t n, int num_sms);

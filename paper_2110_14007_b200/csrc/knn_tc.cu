@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
     k_knn_tc(const uint8_t* __restrict__ a_img, size_t a_region, size_t a_extra,
              const uint8_t* __restrict__ b_img, size_t b_region, size_t b_extra, int64_t b_tiles,
              int64_t n_ref, int64_t qt0, int64_t n_qtiles, int64_t q_begin, int64_t q_end,
-             int self_join, int S, int kp, int nstage, int dbg, int32_t* __restrict__ cand_idx,
+             int self_join, int S, int R, int kp, int nstage, int dbg, int32_t* __restrict__ cand_idx,
              float* __restrict__ cand_v, float* __restrict__ cand_key, uint2* __restrict__ st_list,
              int* __restrict__ st_done, long long* __restrict__ trace) {
   using C = TcCfg<DPAD, SPLIT>;
@@ -222,9 +222,9 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
           mbar_arrive_expect_tx(&full[stage], C::B_BYTES);
           uint8_t* dst = sB + stage * C::B_STRIDE;
           for (int kb = 0; kb < C::NKB; ++kb)
-            bulk_g2s(dst + kb * C::BN * C::RB, b_img + kb * b_region + t * (int64_t)C::BN * C::RB,
+            bulk_g2s(dst + kb * C::BN * C::RB, b_img + kb * b_region + t * R * (int64_t)C::BN * C::RB,
                      C::BN * C::RB, &full[stage]);
-          bulk_g2s(dst + C::B_EXTRA, b_img + b_extra + t * (int64_t)C::BN * kExtraRB,
+          bulk_g2s(dst + C::B_EXTRA, b_img + b_extra + t * R * (int64_t)C::BN * kExtraRB,
                    C::BN * kExtraRB, &full[stage]);
         }
         __syncwarp();
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(TcCfg<DPAD, SPLIT>::THREADS, 1)
         if (tr) trace[etr * 8 + 4] = clock64();
         const uint32_t taddr =
             tmem_base + ((uint32_t)(q * 32) << 16) + acc * C::BN + half * C::BH;
-        const int j0 = (int)(tt * C::BN) + half * C::BH;
+        const int j0 = (int)(tt * R * C::BN) + half * C::BH;  // R > 1: strided sample tiles
         if (!(dbg & 1)) {
           // Masking is needed only on the last (padded) tile and on tiles that
           // contain some lane's own column: warp-uniform decision per tile.
@@ -480,8 +480,8 @@ cudaError_t launch_t(const Image& A, const Image& B, int64_t q_begin, int64_t q_
   kern<<<grid, C::THREADS, smem, st>>>(
       reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(), A.extra_offset(),
       reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
-      B.n_pad / C::BN, B.n, qt0, qt1 - qt0, q_begin, q_begin + q_count, self_join ? 1 : 0, c.S,
-      c.kp, nstage, c.dbg, c.idx, c.v, c.key, c.st_list, c.st_done, c.trace);
+      (B.n_pad / C::BN + c.R - 1) / c.R, B.n, qt0, qt1 - qt0, q_begin, q_begin + q_count,
+      self_join ? 1 : 0, c.S, c.R, c.kp, nstage, c.dbg, c.idx, c.v, c.key, c.st_list, c.st_done, c.trace);
   return cudaGetLastError();
 }
 

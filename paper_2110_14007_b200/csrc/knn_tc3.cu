@@ -1,0 +1,418 @@
+// knn_tc3.cu — K2 main pass (dpad <= 64): fused tile distance + threshold filter
+// on tcgen05 tensor cores, append-only.
+//
+// Arithmetic: the tensor core produces, per (query row i,
+// reference column j),
+//     w_ij = ||xhat_j||^2 - 2 xhat_i . xhat_j
+// i.e. Eq. (3)'s right-hand side minus the row constant (the norm
+// enters through an extra 16-wide K block).  Each 8-column group's minimum is
+// compared with the row's threshold tau_i and, when below, (min, group index)
+// is appended to the row's candidate buffer in HBM (operator fusion of cdist
+// and topk: the n x n matrix is never stored).
+//
+// tau_i comes from the SAMPLE pass (knn_tc.cu run on every R-th reference tile
+// with a small candidate list): it is that list's threshold, so every group
+// NOT appended anywhere -- sample or main -- has key >= tau_i, which is all the
+// certificate needs.  With tau_i
+// fixed for the whole pass there is no per-row set to maintain: the epilogue
+// is a pure stream (min trees, one compare, predicated shared-memory append),
+// and chunks of the same row may run concurrently (slots are reserved with one
+// atomicAdd per flush).
+//
+// Structure (one CTA per SM, persistent; items = query tile x reference
+// chunk, chunk-major so all SMs sweep the same L2-resident chunk):
+//   warp 0     producer: bulk async copies (TMA engine) of the query tile and
+//              a ring of 256-column reference tiles, mbarrier complete_tx.
+//   warp 1     TMEM allocator + MMA issuer: (dpad+16)/16 MMAs 128x256x16 per
+//              tile into one of two 256-column TMEM accumulators.
+//   warps 2-9  filter: warp (q, h) owns TMEM lane quarter q (32 rows) and
+//              column half h (128 columns) of every tile.
+#include <math_constants.h>
+
+#include <algorithm>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace tod {
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBN = 256;
+constexpr int kBH = 128;        // columns per filter warp per tile
+constexpr int kExtraRB = 32;
+constexpr int kFW = 8;
+constexpr int kThreads = 64 + 32 * kFW;
+constexpr int kSmemMax = 232448;
+constexpr int kMaxStage = 4;
+constexpr int kPend = 16;       // pending slots per row (checks every 8 groups)
+
+__host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
+
+template <int DPAD>
+struct Cfg3 {
+  static constexpr int RB = DPAD * 2 < 128 ? DPAD * 2 : 128;
+  static constexpr int NKB = DPAD * 2 / RB;
+  static constexpr int LAYOUT = RB == 128 ? 2 : (RB == 64 ? 4 : 6);
+  static constexpr int SBO = 8 * RB;
+  static constexpr int KSTEPS = DPAD / 16;
+  static constexpr int A_ONE = kBM * (DPAD + 16) * 2;
+  static constexpr int A_STRIDE = align_up(A_ONE, 1024);
+  static constexpr int A_EXTRA = kBM * NKB * RB;
+  static constexpr int B_BYTES = kBN * (DPAD + 16) * 2;
+  static constexpr int B_STRIDE = align_up(B_BYTES, 1024);
+  static constexpr int B_EXTRA = kBN * NKB * RB;
+};
+
+template <int DPAD>
+__host__ __device__ constexpr int smem3(int nstage, int* off_b, int* off_p, int* off_bar) {
+  using C = Cfg3<DPAD>;
+  int o = C::A_STRIDE;
+  *off_b = o;
+  o += nstage * C::B_STRIDE;
+  *off_p = o;
+  o += kFW * kPend * 32 * 8;
+  *off_bar = o;
+  o += 8 * (2 * kMaxStage + 2 + 4) + 16;
+  return o + 1024;
+}
+
+template <int DPAD>
+int pick_stages3() {
+  int a, b, c;
+  for (int ns = kMaxStage; ns >= 2; --ns)
+    if (smem3<DPAD>(ns, &a, &b, &c) <= kSmemMax) return ns;
+  return 0;
+}
+
+// Tiles of chunk c: [bt*c/S, bt*(c+1)/S) minus the sample tiles (t % R == 0;
+// R is a power of two, 0 = no sample pass).
+struct Seq {
+  int t, end;
+  int mask;
+  bool on;
+  __device__ __forceinline__ void begin(int64_t bt, int S, int R, int c) {
+    on = R > 0;
+    mask = R - 1;
+    t = (int)(bt * c / S);
+    end = (int)(bt * (c + 1) / S);
+    skip();
+  }
+  __device__ __forceinline__ void skip() {
+    if (on && (t & mask) == 0) ++t;
+  }
+  __device__ __forceinline__ bool more() const { return t < end; }
+  __device__ __forceinline__ void next() {
+    ++t;
+    skip();
+  }
+};
+
+__device__ __forceinline__ float min8(const float* v) {
+  return fminf(fminf(fminf(v[0], v[1]), v[2]),
+               fminf(fminf(v[3], v[4]), fminf(fminf(v[5], v[6]), v[7])));
+}
+
+template <int DPAD, int FMT, int DBG>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_knn_tc3(const uint8_t* __restrict__ a_img, size_t a_region, size_t a_extra,
+              const uint8_t* __restrict__ b_img, size_t b_region, size_t b_extra, int64_t b_tiles,
+              int64_t n_ref, int64_t qt0, int64_t n_qtiles, int64_t q_begin, int64_t q_end,
+              int self_join, int S, int R, int nstage,
+              const float* __restrict__ tau_v, int tau_lists,
+              uint2* __restrict__ mbuf, int* __restrict__ mcnt, int cap) {
+  using C = Cfg3<DPAD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  int off_b, off_p, off_bar;
+  smem3<DPAD>(nstage, &off_b, &off_p, &off_bar);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + off_b;
+  const uint32_t s_pend = smem_u32(smem + off_p);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + off_bar);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kMaxStage;
+  uint64_t* a_full = bars + 2 * kMaxStage;
+  uint64_t* a_empty = a_full + 1;
+  uint64_t* t_full = a_empty + 1;   // [2]
+  uint64_t* t_empty = t_full + 2;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nstage; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&t_full[i], 1);
+      mbar_init(&t_empty[i], kFW);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int64_t n_items = n_qtiles * S;
+
+  if (warp == 0) {
+    // -------------------------------------------------------------- producer
+    int stage = 0;
+    uint32_t phase = 0, aphase = 0;
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int64_t qtl = item % n_qtiles;
+      const int c = (int)(item / n_qtiles);
+      Seq ts;
+      ts.begin(b_tiles, S, R, c);
+      int issued = 0;
+      bool a_done = false;
+      auto load_a = [&]() {
+        mbar_wait_backoff(a_empty, aphase ^ 1);
+        aphase ^= 1;
+        if (elect_one()) {
+          mbar_arrive_expect_tx(a_full, C::A_ONE);
+          for (int kb = 0; kb < C::NKB; ++kb)
+            bulk_g2s(sA + kb * kBM * C::RB, a_img + kb * a_region + qtl * (int64_t)kBM * C::RB,
+                     kBM * C::RB, a_full);
+          bulk_g2s(sA + C::A_EXTRA, a_img + a_extra + qtl * (int64_t)kBM * kExtraRB,
+                   kBM * kExtraRB, a_full);
+        }
+        __syncwarp();
+        a_done = true;
+      };
+      for (; ts.more(); ts.next()) {
+        // the item's first B tiles are fetched while the MMA drains the previous item
+        if (!a_done && issued == nstage - 1) load_a();
+        mbar_wait_backoff(&empty[stage], phase ^ 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&full[stage], C::B_BYTES);
+          uint8_t* dst = sB + stage * C::B_STRIDE;
+          const int64_t t = ts.t;
+          for (int kb = 0; kb < C::NKB; ++kb)
+            bulk_g2s(dst + kb * kBN * C::RB, b_img + kb * b_region + t * (int64_t)kBN * C::RB,
+                     kBN * C::RB, &full[stage]);
+          bulk_g2s(dst + C::B_EXTRA, b_img + b_extra + t * (int64_t)kBN * kExtraRB,
+                   kBN * kExtraRB, &full[stage]);
+        }
+        __syncwarp();
+        ++issued;
+        if (++stage == nstage) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (!a_done) load_a();
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t IDESC = idesc_f16(kBM, kBN, FMT == 1 ? 0u : 1u);
+    constexpr int NK = C::KSTEPS + 1;
+    const uint32_t a_base = smem_u32(sA);
+    const uint32_t b_base = smem_u32(sB);
+    uint64_t adesc[NK], bdesc[NK];
+#pragma unroll
+    for (int ks = 0; ks < C::KSTEPS; ++ks) {
+      const int kb = (ks * 32) / C::RB;
+      const int koff = (ks * 32) % C::RB;
+      adesc[ks] = smem_desc(a_base + kb * kBM * C::RB + koff, C::SBO, C::LAYOUT);
+      bdesc[ks] = smem_desc(b_base + kb * kBN * C::RB + koff, C::SBO, C::LAYOUT);
+    }
+    adesc[C::KSTEPS] = smem_desc(a_base + C::A_EXTRA, 8 * kExtraRB, 6);
+    bdesc[C::KSTEPS] = smem_desc(b_base + C::B_EXTRA, 8 * kExtraRB, 6);
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, acc_phase = 0, aphase = 0;
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int c = (int)(item / n_qtiles);
+      Seq ts;
+      ts.begin(b_tiles, S, R, c);
+      mbar_wait(a_full, aphase);
+      aphase ^= 1;
+      tc_fence_after();
+      for (; ts.more(); ts.next()) {
+        mbar_wait(&full[stage], phase);
+        mbar_wait(&t_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint64_t bst = (uint64_t)((stage * C::B_STRIDE) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < NK; ++ks)
+            tc_mma_f16(tmem_base + acc * kBN, adesc[ks], bdesc[ks] + bst, IDESC, ks > 0 ? 1u : 0u);
+          tc_commit(&t_full[acc]);
+          tc_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == nstage) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+      if (elect_one()) tc_commit(a_empty);
+      __syncwarp();
+    }
+  } else {
+    // --------------------------------------------------------- filter warps
+    const int f = warp - 2;
+    const int q = warp & 3;           // TMEM lane quarter
+    const int h = f >> 2;             // column half of every tile
+    const int rt = q * 32 + lane;     // row within the query tile
+    constexpr uint32_t SLOT = 32 * 8;
+    const uint32_t pbase = s_pend + (f * kPend * 32 + lane) * 8;
+    uint32_t pa = pbase;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int64_t qtl = item % n_qtiles;
+      const int c = (int)(item / n_qtiles);
+      const int64_t row = (qt0 + qtl) * kBM + rt;
+      const bool valid = row >= q_begin && row < q_end;
+      const int64_t r = valid ? row - q_begin : 0;
+      const int self = self_join ? (int)row : -1;
+      // tiles that may need masking: the one holding this query tile's own
+      // columns (self-join) and the last (padded) one
+      const int t_self = self_join ? (int)(((qt0 + qtl) * kBM) / kBN) : -1;
+      const int t_last = (int)((n_ref - 1) / kBN);
+      float tau = -CUDART_INF_F;  // rows outside the range append nothing
+      if (valid) {
+        tau = CUDART_INF_F;
+        for (int l = 0; l < tau_lists; ++l) tau = fminf(tau, tau_v[r * tau_lists + l]);
+      }
+      int* cnt = mcnt + r * 2 + h;
+      uint2* buf = mbuf + (r * 2 + h) * (int64_t)cap;
+      // move this lane's pending run to its HBM buffer (slots reserved atomically)
+      auto flush = [&]() {
+        const int n = (int)((pa - pbase) / SLOT);
+        if (n > 0) {
+          const int base = atomicAdd(cnt, n);
+          for (int e = 0; e < n; ++e) {
+            const float2 kv = lds_kv(pbase + e * SLOT);
+            if (base + e < cap)
+              buf[base + e] = make_uint2(__float_as_uint(kv.x), (unsigned)__float_as_int(kv.y));
+          }
+        }
+        pa = pbase;
+      };
+      Seq ts;
+      ts.begin(b_tiles, S, R, c);
+      for (; ts.more(); ts.next()) {
+        mbar_wait(&t_full[acc], acc_phase);
+        tc_fence_after();
+        float v[kBH];
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kBN + h * kBH;
+        if (!(DBG & 2)) {
+          tmem_ld64(taddr, *reinterpret_cast<float(*)[64]>(v));
+          tmem_ld64(taddr + 64, *reinterpret_cast<float(*)[64]>(v + 64));
+          tmem_ld_wait();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&t_empty[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        if (DBG & 3) continue;  // profiling: pipeline without the filter work
+        const int t = ts.t;
+        const int j0 = t * kBN + h * kBH;
+        // the self column and padding columns (>= n_ref) are never candidates;
+        // only the query tile's own reference tile and the last tile need masks
+        if (t == t_self || t == t_last) {
+#pragma unroll
+          for (int e = 0; e < kBH; ++e)
+            v[e] = (j0 + e == self || j0 + e >= n_ref) ? CUDART_INF_F : v[e];
+        }
+        // 16 independent min trees first (full ILP), then the appends
+        float m[kBH / 8];
+#pragma unroll
+        for (int g = 0; g < kBH / 8; ++g) m[g] = min8(v + 8 * g);
+        const int gbase = j0 >> 3;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          if (__any_sync(0xffffffffu, pa > pbase + (kPend - 8) * SLOT)) flush();
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            const int gg = hh * 8 + g;
+            if (m[gg] < tau) {
+              sts_kv(pa, m[gg], gbase + gg);
+              pa += SLOT;
+            }
+          }
+        }
+      }
+      flush();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+template <int DPAD, int FMT, int DBG>
+cudaError_t launch3(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
+                    bool self_join, const MainPass& m, int num_sms, cudaStream_t st) {
+  const int nstage = pick_stages3<DPAD>();
+  if (nstage == 0) return cudaErrorInvalidValue;
+  int a, b, c;
+  const int smem = smem3<DPAD>(nstage, &a, &b, &c);
+  auto kern = k_knn_tc3<DPAD, FMT, DBG>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t qt0 = q_begin / kBM;
+  const int64_t qt1 = (q_begin + q_count + kBM - 1) / kBM;
+  const int64_t n_items = (qt1 - qt0) * m.S;
+  const int grid = (int)std::min<int64_t>(num_sms, n_items);
+  if (grid <= 0) return cudaSuccess;
+  kern<<<grid, kThreads, smem, st>>>(
+      reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(), A.extra_offset(),
+      reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
+      B.n_pad / kBN, B.n, qt0, qt1 - qt0, q_begin, q_begin + q_count, self_join ? 1 : 0, m.S,
+      m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int tc3_fits(int dpad) {
+  switch (dpad) {
+    case 16: return pick_stages3<16>() > 0;
+    case 32: return pick_stages3<32>() > 0;
+    case 64: return pick_stages3<64>() > 0;
+  }
+  return 0;
+}
+
+cudaError_t launch_knn_tc3(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
+                           bool self_join, int fmt, const MainPass& m, int num_sms, int dbg,
+                           cudaStream_t st, int* launches) {
+  *launches += 1;
+  // dbg (profiling only): 1 = skip the filter work, 2 = also skip the TMEM loads
+#define TOD_TC3_CASE(D)                                                                        \
+  case D:                                                                                     \
+    if (dbg & 3)                                                                              \
+      return fmt == 1 ? launch3<D, 1, 2>(A, B, q_begin, q_count, self_join, m, num_sms, st)   \
+                      : launch3<D, 2, 2>(A, B, q_begin, q_count, self_join, m, num_sms, st);  \
+    return fmt == 1 ? launch3<D, 1, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st)     \
+                    : launch3<D, 2, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st);
+  switch (A.dpad) {
+    TOD_TC3_CASE(16)
+    TOD_TC3_CASE(32)
+    TOD_TC3_CASE(64)
+  }
+#undef TOD_TC3_CASE
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace tod

@@ -189,7 +189,6 @@ __global__ void __launch_bounds__(kRerankWarps * 32)
 // kept group is re-ranked; columns outside kept groups have w~ >= v (their
 // group's minimum is >= v), so the same certificate applies.
 constexpr int kGrpWarps = 4;
-constexpr int kGrpMaxG = 128;   // lists * K'' group slots per row
 
 // Warp-wide bitonic sort (ascending by (key, id)) of one element per lane.
 __device__ __forceinline__ void warp_sort32(double& key, int& id, int lane) {
@@ -212,22 +211,39 @@ __device__ __forceinline__ void warp_sort32(double& key, int& id, int lane) {
   }
 }
 
-// Group candidates, pruned: the kept groups of all lists are
-// visited in ascending order of their pass-1 minimum; before each batch of 4
-// groups, if the lower bound implied by that minimum (lb2_from_key) already
-// exceeds the current k-th exact distance, every remaining group is provably
-// farther and the scan stops.  Visited groups are expanded to their 8 columns
-// and re-ranked with the oracle formula; a running top-k (by (D64, index)) is
-// merged batch by batch.
+// Group candidates, pruned.  A row's kept groups come from its
+// pass-1 lists (idx/key, -1 = empty slot) and, in the two-pass mode, from the
+// main pass's append buffers.  They are staged unsorted in shared memory and
+// visited in ascending order of their pass-1 minimum by repeated warp-wide
+// selection: before each batch of 4 groups, if the lower bound implied by the
+// smallest remaining minimum (lb2_from_key) already exceeds the current k-th
+// exact distance, every remaining group is provably farther and the scan
+// stops.  Visited groups are expanded to their 8 columns and re-ranked with the
+// oracle formula; a running top-k (by (D64, index)) is merged batch by batch.
+constexpr int kSelMax = 512;    // staged groups per row
+
+__device__ __forceinline__ void warp_argmin(float& key, int& pos) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ok = __shfl_xor_sync(0xffffffffu, key, o);
+    const int op = __shfl_xor_sync(0xffffffffu, pos, o);
+    if (ok < key || (ok == key && op < pos)) {
+      key = ok;
+      pos = op;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kGrpWarps * 32)
     k_rerank_groups(const float* __restrict__ Q, int64_t q_begin, int64_t q_count,
                     const float* __restrict__ X, int64_t n, int d, int k, int self_join,
                     const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_key,
-                    const float* __restrict__ cand_v, int kp, int lists, CertParams cp,
-                    KnnOutDev out, int32_t* __restrict__ fail_rows,
+                    const float* __restrict__ cand_v, int kp, int lists,
+                    const uint2* __restrict__ mbuf, const int* __restrict__ mcnt, int mcap,
+                    CertParams cp, KnnOutDev out, int32_t* __restrict__ fail_rows,
                     int32_t* __restrict__ fail_count, unsigned long long* __restrict__ max_err_bits) {
-  __shared__ float s_gk[kGrpWarps][kGrpMaxG];     // group keys, merged ascending
-  __shared__ int s_gi[kGrpWarps][kGrpMaxG];       // group indices
+  __shared__ float s_gk[kGrpWarps][kSelMax];      // staged group keys (+inf once visited)
+  __shared__ int s_gi[kGrpWarps][kSelMax];        // staged group indices
   __shared__ double s_tk[kGrpWarps][2][kMaxK];    // running top-k (double buffered)
   __shared__ int s_ti[kGrpWarps][2][kMaxK];
   __shared__ double s_bk[kGrpWarps][32];          // sorted batch
@@ -240,49 +256,90 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
   const float* xi = self_join ? X + gi * d : Q + r * d;
   double* xq = s_xq + (size_t)w * d;
   for (int c = lane; c < d; c += 32) xq[c] = (double)xi[c];
-  const int G = lists * kp;
-  // ---- merge the (ascending) lists into one ascending order of group keys
   float* gk = s_gk[w];
   int* gid = s_gi[w];
-  for (int e = lane; e < G; e += 32) {
-    const int a = e / kp, pos = e - a * kp;
-    const float key = cand_key[r * G + e];
-    const int g = cand_idx[r * G + e];
-    int rank = pos;
-    for (int b = 0; b < lists; ++b) {  // rank among the other lists (ties: lower list first)
-      if (b == a) continue;
-      const float* other = cand_key + r * G + b * kp;
-      int lo = 0, hi = kp;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        const float om = other[mid];
-        if (b > a ? (om < key) : (om <= key)) lo = mid + 1;
-        else hi = mid;
-      }
-      rank += lo;
+  // ---- stage every kept group (compacted with ballots)
+  int G = 0;
+  bool overflow = false;
+  const int L = lists * kp;
+  for (int e0 = 0; e0 < L; e0 += 32) {
+    const int e = e0 + lane;
+    const int g = e < L ? cand_idx[r * L + e] : -1;
+    const unsigned live = __ballot_sync(0xffffffffu, g >= 0);
+    const int pos = G + __popc(live & ((1u << lane) - 1u));
+    if (g >= 0 && pos < kSelMax) {
+      gk[pos] = cand_key[r * L + e];
+      gid[pos] = g;
     }
-    gk[rank] = key;
-    gid[rank] = g;
+    G += __popc(live);
   }
+  if (mbuf) {
+    for (int h = 0; h < 2; ++h) {
+      const int c = mcnt[r * 2 + h];
+      overflow |= c > mcap;
+      const int m = c < mcap ? c : mcap;
+      const uint2* src = mbuf + (r * 2 + h) * (int64_t)mcap;
+      for (int e = lane; e < m; e += 32) {
+        const uint2 kv = src[e];
+        if (G + e < kSelMax) {
+          gk[G + e] = __uint_as_float(kv.x);
+          gid[G + e] = (int)kv.y;
+        }
+      }
+      G += m;
+    }
+  }
+  overflow |= G > kSelMax;
+  if (G > kSelMax) G = kSelMax;
   float vmin = CUDART_INF_F;
   for (int c = 0; c < lists; ++c) vmin = fminf(vmin, cand_v[r * lists + c]);
   __syncwarp();
+  // per-lane cached minimum over its strided slice of the staged groups
+  auto slice_min = [&](float& mk, int& mp) {
+    mk = CUDART_INF_F;
+    mp = INT32_MAX;
+    for (int e = lane; e < G; e += 32) {
+      const float kk = gk[e];
+      if (kk < mk) {
+        mk = kk;
+        mp = e;
+      }
+    }
+  };
+  float lk;
+  int lp;
+  slice_min(lk, lp);
   const double gamma64 = gamma_up(cp.d + 2, 1.1102230246251565e-16);
   int cnt = 0;            // entries in the running top-k
   int buf = 0;
   double dk = CUDART_INF;  // current k-th exact distance (valid when cnt == k)
-  double err = 0.0;
-  for (int b = 0; b < G; b += 4) {
-    const int g0 = gid[b];
-    if (g0 < 0) break;  // empty slots sort last (key +inf)
+  int visited = 0;
+  while (visited < G) {
+    // the next 4 groups in ascending key order (ties: staging order)
+    int sel[4];
+    float first = CUDART_INF_F;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      float mk = lk;
+      int mp = lk < CUDART_INF_F ? lp : INT32_MAX;
+      warp_argmin(mk, mp);
+      if (b == 0) first = mk;
+      sel[b] = mp == INT32_MAX ? -1 : gid[mp];
+      if (mp != INT32_MAX && lp == mp && lk < CUDART_INF_F) {  // owner: retire it, rescan its slice
+        gk[mp] = CUDART_INF_F;
+        slice_min(lk, lp);
+      }
+      __syncwarp();
+    }
+    if (sel[0] < 0) break;  // every remaining staged key is +inf
     if (cnt == k) {
       double e2;
-      const double lb2 = lb2_from_key(cp, r, (double)gk[b], &e2);
+      const double lb2 = lb2_from_key(cp, r, (double)first, &e2);
       if (lb2 > 0.0 && dk < lb2 * (1.0 - gamma64)) break;  // all remaining groups are farther
     }
+    visited += 4;
     // expand 4 groups -> 32 columns, one per lane
-    const int gs = b + (lane >> 3);
-    const int g = gs < G ? gid[gs] : -1;
+    const int g = sel[lane >> 3];
     const int64_t j = (int64_t)g * 8 + (lane & 7);
     double key = CUDART_INF;
     int id = INT32_MAX;
@@ -359,9 +416,8 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
     __syncwarp();
     if (cnt == k) dk = s_tk[w][buf][k - 1];
   }
-  double e1 = 0.0;
-  bool cert = cnt == k && row_certified(cp, r, vmin, s_tk[w][buf][k - 1], &e1);
-  err = e1;
+  double err = 0.0;
+  bool cert = !overflow && cnt == k && row_certified(cp, r, vmin, s_tk[w][buf][k - 1], &err);
   if (cp.force_fail) cert = false;
   if (lane == 0 && err > 0.0)
     atomicMax(max_err_bits, (unsigned long long)__double_as_longlong(err));
@@ -512,12 +568,12 @@ __global__ void __launch_bounds__(kFbMaxP)
 }  // namespace
 
 cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, const float* X,
-                          int64_t n, int d, int k, bool self_join, Cands c, CertParams cp,
-                          KnnOutDev out, int32_t* fail_rows, int32_t* fail_count,
+                          int64_t n, int d, int k, bool self_join, Cands c, const MainPass* mp,
+                          CertParams cp, KnnOutDev out, int32_t* fail_rows, int32_t* fail_count,
                           double* max_err, cudaStream_t st, int* launches) {
   if (k > kMaxK) return cudaErrorInvalidValue;
   if (cp.kind == PASS_TC) {  // group candidates
-    if (c.lists * c.kp > kGrpMaxG || !c.key) return cudaErrorInvalidValue;
+    if (c.lists * c.kp > kSelMax || !c.key) return cudaErrorInvalidValue;
     const int64_t gb = (q_count + kGrpWarps - 1) / kGrpWarps;
     if (gb == 0) return cudaSuccess;
     const size_t smem = (size_t)kGrpWarps * d * 8;
@@ -526,8 +582,8 @@ cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, cons
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_rerank_groups<<<(unsigned)gb, kGrpWarps * 32, smem, st>>>(
-        Q, q_begin, q_count, X, n, d, k, self_join ? 1 : 0, c.idx, c.key, c.v, c.kp, c.lists, cp,
-        out, fail_rows, fail_count, reinterpret_cast<unsigned long long*>(max_err));
+        Q, q_begin, q_count, X, n, d, k, self_join ? 1 : 0, c.idx, c.key, c.v, c.kp, c.lists,
+        mp ? mp->buf : nullptr, mp ? mp->cnt : nullptr, mp ? mp->cap : 0, cp, out, fail_rows, fail_count, reinterpret_cast<unsigned long long*>(max_err));
     *launches += 1;
     return cudaGetLastError();
   }

@@ -27,6 +27,7 @@ STATUS = {0: "TOD_OK", -1: "TOD_E_ARG", -2: "TOD_E_NONFINITE", -3: "TOD_E_RANGE"
 FORMATS = {"auto": 0, "fp16": 1, "bf16": 2, "fp32": 3}
 F_NO_CERTIFY = 0x1
 F_TIMING = 0x2
+F_PASS1_V1 = 0x10   # force the single-query-tile tensor-core schedule (knn_tc.cu)
 
 
 class TodError(RuntimeError):

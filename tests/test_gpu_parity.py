@@ -84,13 +84,43 @@ def test_knn_full_parity(pkg, n, d, k, fmt):
 @pytest.mark.parametrize("split", [1, 2, 4])
 @pytest.mark.parametrize("chunks", [1, 3])
 def test_epilogue_variants_parity(pkg, d, fmt, split, chunks):
-    # every epilogue layout (1/2/4 lists per row, pending widths 16/24/32,
-    # tile- and chunk-level reserves) and parked state across chunks
+    # every epilogue layout of the single-query-tile schedule (1/2/4 lists per
+    # row, pending widths 16/24/32, tile- and chunk-level reserves) and parked
+    # state across chunks
     n, k = 2300, 10
     X = datagen.gaussian_mixture(n, d, seed=77 + d)
-    with _ctx(pkg, fmt=fmt, split=split, chunks=chunks) as ctx:
+    with _ctx(pkg, fmt=fmt, split=split, chunks=chunks, flags=pkg.F_PASS1_V1) as ctx:
         res = ctx.knn(torch.from_numpy(X).cuda(), k)
     _check_rows(res, X, k, np.arange(n))
+
+
+@pytest.mark.parametrize("n,d,k,fmt,chunks", [
+    (20_000, 32, 20, "fp16", 0),   # two-pass: sample pass (every 8th tile) + main pass
+    (20_000, 64, 10, "fp16", 0),   # d=64 (SW128 operands)
+    (17_001, 32, 10, "fp16", 4),   # sample pass in 4 chunks, ragged tail
+    (9_000, 16, 6, "fp16", 2),     # smallest two-pass size, SW32 layout
+    (12_345, 64, 10, "bf16", 3),
+    (5_000, 32, 20, "fp16", 3),    # below the two-pass threshold: single pass, 3 chunks
+])
+def test_two_pass_parity(pkg, n, d, k, fmt, chunks):
+    # sample pass (every 8th tile) + append-only main pass (two-pass selection)
+    # full-table parity at sizes that span the sampling and chunk logic
+    X = datagen.gaussian_mixture(n, d, seed=n + 3 * d)
+    with _ctx(pkg, fmt=fmt, chunks=chunks) as ctx:
+        res = ctx.knn(torch.from_numpy(X).cuda(), k)
+    _check_rows(res, X, k, np.arange(n))
+    if fmt == "fp16":
+        assert res.stats["certified"] >= 0.99 * n, res.stats
+
+
+def test_single_and_two_pass_identical(pkg):
+    X = datagen.gaussian_mixture(30_000, 32, seed=31)
+    Xd = torch.from_numpy(X).cuda()
+    outs = []
+    for flags in (0, pkg.F_PASS1_V1):
+        with _ctx(pkg, flags=flags) as ctx:
+            outs.append(ctx.knn(Xd, 20))
+    assert torch.equal(outs[0].idx, outs[1].idx) and torch.equal(outs[0].dist64, outs[1].dist64)
 
 
 def test_forced_fallback_tier(pkg):
