@@ -211,25 +211,88 @@ __device__ __forceinline__ void warp_sort32(double& key, int& id, int lane) {
   }
 }
 
-// Group candidates, pruned.  A row's kept groups come from its
-// pass-1 lists (idx/key, -1 = empty slot) and, in the two-pass mode, from the
-// main pass's append buffers.  They are staged unsorted in shared memory and
-// visited in ascending order of their pass-1 minimum by repeated warp-wide
-// selection: before each batch of 4 groups, if the lower bound implied by the
-// smallest remaining minimum (lb2_from_key) already exceeds the current k-th
-// exact distance, every remaining group is provably farther and the scan
-// stops.  Visited groups are expanded to their 8 columns and re-ranked with the
-// oracle formula; a running top-k (by (D64, index)) is merged batch by batch.
-constexpr int kSelMax = 512;    // staged groups per row
+// Upper bound, in original units, on the exact squared distance D64 of row r to
+// the best column of a group whose pass-1 key is w (the group's minimum w~):
+// that column has w_ij <= w + E_i, so ||xhat_i - xhat_j||^2 <= a_i^2 + w + E_i,
+// and the residuals e_i, e_j <= emax bound the exact distance from above.
+// (Mirror image of lb2_from_key; tensor-core pass only.)
+__device__ double ub2_from_key(const CertParams& cp, int64_t r, double w) {
+  const double u53 = 1.1102230246251565e-16;
+  const double a2i = cp.qa2[r];
+  const double ei = cp.qe[r];
+  const double amax2 = cp.g->amax2;
+  const double emax = cp.g->emax;
+  const double rep = cp.g->repmax;
+  const double ai = sqrt(a2i) * (1.0 + 4 * u53);
+  const double am = sqrt(amax2) * (1.0 + 4 * u53);
+  const double gam = gamma_up(2.0 * (cp.dpad + 16), 2.384185791015625e-07 /*2^-22*/);
+  const double E = (gam * (2.0 * ai * am + 1.002 * amax2) + rep) * (1.0 + 1e-6) + 1e-300;
+  const double slack = (cp.d + 8) * 2.0 * u53 * (fabs(a2i) + fabs(w) + E);
+  double R2 = a2i + w + E + slack;
+  if (!(R2 > 0.0)) R2 = 0.0;
+  const double Rh = sqrt(R2) * (1.0 + 2.0 * u53);
+  const double UB = (Rh + ei + emax) * (1.0 + 8.0 * u53);
+  const double ubo = UB / cp.g->s;  // s = 2^e: exact
+  return ubo * ubo * (1.0 + 8.0 * u53) * (1.0 + gamma_up(cp.d + 2, u53));
+}
 
-__device__ __forceinline__ void warp_argmin(float& key, int& pos) {
+// Group candidates (DESIGN.md §5 "Re-rank").  A row's kept groups come from its
+// pass-1 lists (idx/key, -1 = empty slot) and, in the two-pass mode, from the
+// main pass's append buffers; they are staged unsorted in shared memory.
+//  1. kappa = a key with >= k staged groups at or below it (bisection on the
+//     ordered key bits); each of those groups holds a distinct column with
+//     D64 <= UB := ub2_from_key(kappa), so the k-th exact distance is <= UB.
+//  2. Only groups whose lower bound lb2_from_key(key)(1-gamma) <= UB can hold
+//     a top-k column; they are expanded to their 8 columns and evaluated with
+//     the oracle formula (O1); columns with D64 <= UB are kept.
+//  3. The k smallest by (D64, index) are selected once: a warp bitonic sort
+//     when <= 64 columns survive, else k rounds of warp argmin.
+constexpr int kSelMax = 512;    // staged groups per row
+constexpr int kColMax = 256;    // surviving columns per row
+
+__device__ __forceinline__ uint32_t f2ord(float f) {  // order-preserving float -> uint
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t o) {
+  return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
+}
+
+// Warp bitonic sort of 64 (key, id) pairs, 2 per lane (element p = 2*lane + e),
+// ascending by (key, id); empty slots carry (+inf, INT32_MAX).
+__device__ __forceinline__ void warp_sort64(double (&k)[2], int (&id)[2], int lane) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float ok = __shfl_xor_sync(0xffffffffu, key, o);
-    const int op = __shfl_xor_sync(0xffffffffu, pos, o);
-    if (ok < key || (ok == key && op < pos)) {
-      key = ok;
-      pos = op;
+  for (int kk = 2; kk <= 64; kk <<= 1) {
+#pragma unroll
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j == 1) {
+        const int p = 2 * lane;
+        const bool up = (p & kk) == 0;
+        const bool sw = up ? key_less(k[1], id[1], k[0], id[0]) : key_less(k[0], id[0], k[1], id[1]);
+        if (sw) {
+          const double tk = k[0];
+          const int ti = id[0];
+          k[0] = k[1];
+          id[0] = id[1];
+          k[1] = tk;
+          id[1] = ti;
+        }
+      } else {
+        const int lm = j >> 1;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int p = 2 * lane + e;
+          const double ok = __shfl_xor_sync(0xffffffffu, k[e], lm);
+          const int oi = __shfl_xor_sync(0xffffffffu, id[e], lm);
+          const bool up = (p & kk) == 0;
+          const bool lower = (p & j) == 0;
+          const bool other_less = key_less(ok, oi, k[e], id[e]);
+          if ((lower == up) ? other_less : !other_less) {
+            k[e] = ok;
+            id[e] = oi;
+          }
+        }
+      }
     }
   }
 }
@@ -242,12 +305,12 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
                     const uint2* __restrict__ mbuf, const int* __restrict__ mcnt, int mcap,
                     CertParams cp, KnnOutDev out, int32_t* __restrict__ fail_rows,
                     int32_t* __restrict__ fail_count, unsigned long long* __restrict__ max_err_bits) {
-  __shared__ float s_gk[kGrpWarps][kSelMax];      // staged group keys (+inf once visited)
+  __shared__ float s_gk[kGrpWarps][kSelMax];      // staged group keys
   __shared__ int s_gi[kGrpWarps][kSelMax];        // staged group indices
-  __shared__ double s_tk[kGrpWarps][2][kMaxK];    // running top-k (double buffered)
-  __shared__ int s_ti[kGrpWarps][2][kMaxK];
-  __shared__ double s_bk[kGrpWarps][32];          // sorted batch
-  __shared__ int s_bi[kGrpWarps][32];
+  __shared__ double s_ck[kGrpWarps][kColMax];     // surviving columns: D64
+  __shared__ int s_ci[kGrpWarps][kColMax];        //                    index
+  __shared__ double s_tk[kGrpWarps][kMaxK];       // selected top-k
+  __shared__ int s_ti[kGrpWarps][kMaxK];
   extern __shared__ double s_xq[];                // [warps][d] query row in fp64
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * kGrpWarps + w;
@@ -294,55 +357,61 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
   float vmin = CUDART_INF_F;
   for (int c = 0; c < lists; ++c) vmin = fminf(vmin, cand_v[r * lists + c]);
   __syncwarp();
-  // per-lane cached minimum over its strided slice of the staged groups
-  auto slice_min = [&](float& mk, int& mp) {
-    mk = CUDART_INF_F;
-    mp = INT32_MAX;
-    for (int e = lane; e < G; e += 32) {
-      const float kk = gk[e];
-      if (kk < mk) {
-        mk = kk;
-        mp = e;
-      }
-    }
-  };
-  float lk;
-  int lp;
-  slice_min(lk, lp);
   const double gamma64 = gamma_up(cp.d + 2, 1.1102230246251565e-16);
-  int cnt = 0;            // entries in the running top-k
-  int buf = 0;
-  double dk = CUDART_INF;  // current k-th exact distance (valid when cnt == k)
-  int visited = 0;
-  while (visited < G) {
-    // the next 4 groups in ascending key order (ties: staging order)
-    int sel[4];
-    float first = CUDART_INF_F;
+  // ---- 1. kappa and UB
+  double UB = CUDART_INF;
+  if (G >= k) {
+    uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+    for (int e = lane; e < G; e += 32) {
+      const uint32_t o = f2ord(gk[e]);
+      lo = min(lo, o);
+      hi = max(hi, o);
+    }
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      float mk = lk;
-      int mp = lk < CUDART_INF_F ? lp : INT32_MAX;
-      warp_argmin(mk, mp);
-      if (b == 0) first = mk;
-      sel[b] = mp == INT32_MAX ? -1 : gid[mp];
-      if (mp != INT32_MAX && lp == mp && lk < CUDART_INF_F) {  // owner: retire it, rescan its slice
-        gk[mp] = CUDART_INF_F;
-        slice_min(lk, lp);
-      }
-      __syncwarp();
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     }
-    if (sel[0] < 0) break;  // every remaining staged key is +inf
-    if (cnt == k) {
+    // invariant: count(key <= hi) >= k; shrink hi while keeping it
+    if (lo < hi) --lo;  // count(key <= lo) < k unless lo is the minimum itself
+    for (int it = 0; it < 24 && hi - lo > 1; ++it) {
+      const uint32_t mid = lo + ((hi - lo) >> 1);
+      int c = 0;
+      for (int e = lane; e < G; e += 32) c += f2ord(gk[e]) <= mid;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (c >= k) hi = mid;
+      else lo = mid;
+    }
+    const float kappa = ord2f(hi);
+    if (kappa < CUDART_INF_F) UB = ub2_from_key(cp, r, (double)kappa);
+  }
+  // ---- 2. expand the groups that can hold a top-k column
+  // (compacted in place into gid[0, nv), then 4 groups = 32 columns per step)
+  int nv = 0;
+  for (int e0 = 0; e0 < G; e0 += 32) {
+    const int e = e0 + lane;
+    bool vis = false;
+    int g = -1;
+    if (e < G) {
       double e2;
-      const double lb2 = lb2_from_key(cp, r, (double)first, &e2);
-      if (lb2 > 0.0 && dk < lb2 * (1.0 - gamma64)) break;  // all remaining groups are farther
+      const double lb2 = lb2_from_key(cp, r, (double)gk[e], &e2);
+      vis = !(lb2 > 0.0 && lb2 * (1.0 - gamma64) > UB);
+      g = gid[e];
     }
-    visited += 4;
-    // expand 4 groups -> 32 columns, one per lane
-    const int g = sel[lane >> 3];
+    const unsigned vm = __ballot_sync(0xffffffffu, vis);
+    if (vis) gid[nv + __popc(vm & ((1u << lane) - 1u))] = g;
+    nv += __popc(vm);
+  }
+  __syncwarp();
+  double* ck = s_ck[w];
+  int* ci = s_ci[w];
+  int nc = 0;
+  for (int b0 = 0; b0 < nv; b0 += 4) {
+    const int gs = b0 + (lane >> 3);
+    const int g = gs < nv ? gid[gs] : -1;
     const int64_t j = (int64_t)g * 8 + (lane & 7);
     double key = CUDART_INF;
-    int id = INT32_MAX;
     if (g >= 0 && j < n && !(self_join && j == gi)) {
       const float* xj = X + j * d;
       double acc = 0.0;  // O1, bit-identical to the oracle (no FMA, ascending c)
@@ -366,63 +435,88 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
         }
       }
       key = acc;
-      id = (int)j;
     }
-    // merge the sorted batch into the running top-k (merge path by ranks)
-    warp_sort32(key, id, lane);
-    const double* tk = s_tk[w][buf];
-    const int* ti = s_ti[w][buf];
-    double* nk = s_tk[w][buf ^ 1];
-    int* ni = s_ti[w][buf ^ 1];
-    const unsigned valid = __ballot_sync(0xffffffffu, id != INT32_MAX);
-    const int nb = __popc(valid);  // valid batch entries are the first nb lanes
-    s_bk[w][lane] = key;
-    s_bi[w][lane] = id;
-    __syncwarp();
-    // batch element (lane) position = lane + #(list entries less than it)
-    if (lane < nb) {
-      int lo = 0, hi = cnt;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (key_less(tk[mid], ti[mid], key, id)) lo = mid + 1;
-        else hi = mid;
-      }
-      const int p = lane + lo;
-      if (p < k) {
-        nk[p] = key;
-        ni[p] = id;
-      }
+    const bool keep = key <= UB && key < CUDART_INF;
+    const unsigned km = __ballot_sync(0xffffffffu, keep);
+    const int pos = nc + __popc(km & ((1u << lane) - 1u));
+    if (keep && pos < kColMax) {
+      ck[pos] = key;
+      ci[pos] = (int)j;
     }
-    // list element e position = e + #(batch elements less than it)
-    for (int e = lane; e < cnt; e += 32) {
-      const double ek = tk[e];
-      const int ei = ti[e];
-      int lo = 0, hi = nb;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        const double bk = s_bk[w][mid];
-        const int bi = s_bi[w][mid];
-        if (key_less(bk, bi, ek, ei)) lo = mid + 1;
-        else hi = mid;
-      }
-      const int p = e + lo;
-      if (p < k) {
-        nk[p] = ek;
-        ni[p] = ei;
-      }
-    }
-    cnt = min(k, cnt + nb);
-    buf ^= 1;
-    __syncwarp();
-    if (cnt == k) dk = s_tk[w][buf][k - 1];
+    nc += __popc(km);
   }
+  overflow |= nc > kColMax;
+  if (nc > kColMax) nc = kColMax;
+  __syncwarp();
+  // ---- 3. the k smallest by (D64, index)
+  double* tk = s_tk[w];
+  int* ti = s_ti[w];
+  if (nc <= 64) {
+    double kk[2];
+    int ii[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int p = 2 * lane + e;
+      kk[e] = p < nc ? ck[p] : CUDART_INF;
+      ii[e] = p < nc ? ci[p] : INT32_MAX;
+    }
+    warp_sort64(kk, ii, lane);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int p = 2 * lane + e;
+      if (p < k) {
+        tk[p] = kk[e];
+        ti[p] = ii[e];
+      }
+    }
+  } else {
+    // k rounds of warp argmin; each lane caches the minimum of its slice
+    auto slice_min = [&](double& mk, int& mi, int& mp) {
+      mk = CUDART_INF;
+      mi = INT32_MAX;
+      mp = -1;
+      for (int e = lane; e < nc; e += 32)
+        if (key_less(ck[e], ci[e], mk, mi)) {
+          mk = ck[e];
+          mi = ci[e];
+          mp = e;
+        }
+    };
+    double lk;
+    int li, lp;
+    slice_min(lk, li, lp);
+    for (int m = 0; m < k; ++m) {
+      double bk = lk;
+      int bi = li;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (key_less(ok, oi, bk, bi)) {
+          bk = ok;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        tk[m] = bk;
+        ti[m] = bi;
+      }
+      if (lp >= 0 && li == bi && bi != INT32_MAX) {  // owner retires it
+        ck[lp] = CUDART_INF;
+        ci[lp] = INT32_MAX;
+        slice_min(lk, li, lp);
+      }
+    }
+  }
+  __syncwarp();
   double err = 0.0;
-  bool cert = !overflow && cnt == k && row_certified(cp, r, vmin, s_tk[w][buf][k - 1], &err);
+  const bool have = nc >= k;
+  bool cert = !overflow && have && row_certified(cp, r, vmin, tk[k - 1], &err);
   if (cp.force_fail) cert = false;
   if (lane == 0 && err > 0.0)
     atomicMax(max_err_bits, (unsigned long long)__double_as_longlong(err));
   if (cert) {
-    write_row(out, r, k, s_tk[w][buf], s_ti[w][buf], lane, 32);
+    write_row(out, r, k, tk, ti, lane, 32);
   } else if (lane == 0) {
     const int slot = atomicAdd(fail_count, 1);
     fail_rows[slot] = (int32_t)r;
