@@ -32,7 +32,7 @@ struct Buf {
 };
 
 struct Workspace {
-  Buf bufs[32];
+  Buf bufs[48];
   void release() {
     for (auto& b : bufs) {
       if (b.p) cudaFree(b.p);
@@ -44,8 +44,9 @@ struct Workspace {
 enum BufId {
   B_X = 0, B_Q, B_IMG_B, B_A2_B, B_E_B, B_IMG_A, B_A2_A, B_E_A, B_MU, B_PART,
   B_G, B_CIDX, B_CV, B_FAIL, B_SMALL, B_IDX, B_DIST, B_DIST64, B_KTH, B_MEAN, B_KD64,
-  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT, B_NBUF
+  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT, B_FAILUB, B_NBUF
 };
+static_assert(B_NBUF <= 48, "Workspace::bufs too small");
 
 }  // namespace
 
@@ -310,6 +311,8 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
   }
   TOD_TRY(ensure(ctx, B_FAIL, (size_t)std::max<int64_t>(q_count, 1) * 4, &p));
   int32_t* fail_rows = static_cast<int32_t*>(p);
+  TOD_TRY(ensure(ctx, B_FAILUB, (size_t)std::max<int64_t>(q_count, 1) * 8, &p));
+  double* fail_ub = static_cast<double*>(p);
 
   CertParams cp{};
   cp.kind = plan.kind;
@@ -416,7 +419,7 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     return TOD_OK;
   }
   TOD_CUDA(launch_rerank(dQ, q_begin, q_count, dX, n, d, k, self, cands, plan.two ? &mp : nullptr,
-                         cp, out, fail_rows,
+                         cp, out, fail_rows, fail_ub,
                          &small->fail_count, &small->max_err, st, launches));
   tm.mark();  // 4: fallback start
   SmallDev h{};
@@ -425,7 +428,7 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
   if (h.g.nonfinite) return fail(ctx, TOD_E_NONFINITE, "X (or Q) contains NaN or Inf");
   if (h.fail_count > 0) {
     TOD_TRY(ensure(ctx, B_FBPART, fallback_workspace(h.fail_count, k, n, ctx->num_sms), &p));
-    TOD_CUDA(launch_fallback(dQ, q_begin, dX, n, d, k, self, fail_rows, h.fail_count, out, p,
+    TOD_CUDA(launch_fallback(dQ, q_begin, dX, n, d, k, self, fail_rows, fail_ub, h.fail_count, out, p,
                              ctx->num_sms, st, launches));
   }
   tm.mark();  // 5: end of kNN

@@ -122,12 +122,13 @@ struct KnnOutDev {
 cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, const float* X,
                           int64_t n, int d, int k, bool self_join, Cands c, const MainPass* mp,
                           CertParams cp,
-                          KnnOutDev out, int32_t* fail_rows, int32_t* fail_count,
+                          KnnOutDev out, int32_t* fail_rows, double* fail_ub, int32_t* fail_count,
                           double* max_err, cudaStream_t st, int* launches);
 int fallback_slices(int nfail, int64_t n, int num_sms);
 size_t fallback_workspace(int nfail, int k, int64_t n, int num_sms);
 cudaError_t launch_fallback(const float* Q, int64_t q_begin, const float* X, int64_t n, int d,
-                            int k, bool self_join, const int32_t* fail_rows, int nfail,
+                            int k, bool self_join, const int32_t* fail_rows,
+                            const double* fail_ub, int nfail,
                             KnnOutDev out, void* ws, int num_sms, cudaStream_t st, int* launches);
 
 // ---- lof.cu

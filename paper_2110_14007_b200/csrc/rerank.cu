@@ -127,7 +127,8 @@ __global__ void __launch_bounds__(kRerankWarps * 32)
              const float* __restrict__ X, int64_t n, int d, int k, int self_join,
              const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_v, int kp, int S,
              CertParams cp, KnnOutDev out, int32_t* __restrict__ fail_rows,
-             int32_t* __restrict__ fail_count, unsigned long long* __restrict__ max_err_bits) {
+             double* __restrict__ fail_ub, int32_t* __restrict__ fail_count,
+             unsigned long long* __restrict__ max_err_bits) {
   __shared__ double s_key[kRerankWarps][kMaxCands];
   __shared__ int s_id[kRerankWarps][kMaxCands];
   __shared__ double s_sk[kRerankWarps][kMaxK];
@@ -179,6 +180,8 @@ __global__ void __launch_bounds__(kRerankWarps * 32)
   } else if (lane == 0) {
     const int slot = atomicAdd(fail_count, 1);
     fail_rows[slot] = (int32_t)r;
+    // the k-th exact distance among kept columns bounds the true k-th from above
+    fail_ub[slot] = nv_local >= k ? s_sk[w][k - 1] : CUDART_INF;
   }
 }
 
@@ -304,7 +307,8 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
                     const float* __restrict__ cand_v, int kp, int lists,
                     const uint2* __restrict__ mbuf, const int* __restrict__ mcnt, int mcap,
                     CertParams cp, KnnOutDev out, int32_t* __restrict__ fail_rows,
-                    int32_t* __restrict__ fail_count, unsigned long long* __restrict__ max_err_bits) {
+                    double* __restrict__ fail_ub, int32_t* __restrict__ fail_count,
+                    unsigned long long* __restrict__ max_err_bits) {
   __shared__ float s_gk[kGrpWarps][kSelMax];      // staged group keys
   __shared__ int s_gi[kGrpWarps][kSelMax];        // staged group indices
   __shared__ double s_ck[kGrpWarps][kColMax];     // surviving columns: D64
@@ -520,6 +524,9 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
   } else if (lane == 0) {
     const int slot = atomicAdd(fail_count, 1);
     fail_rows[slot] = (int32_t)r;
+    // both UB and the k-th exact distance among kept columns bound the true
+    // k-th distance from above (the fallback only collects columns below it)
+    fail_ub[slot] = fmin(UB, have ? tk[k - 1] : CUDART_INF);
   }
 }
 
@@ -532,12 +539,161 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
 // row over P SMs makes a handful of failures cost one pass over X, not one
 // SM's bandwidth.
 constexpr int kFbThreads = 256;
+constexpr int kFbCap = 1024;   // collected columns per failing row (threshold tier)
+constexpr int kFbQB = 4;       // failing rows per block of the collect kernel
+
+// Threshold tier of the fallback: every column whose D64 (oracle formula O1)
+// is <= ub_f -- an upper bound on row f's k-th distance handed over by the
+// re-rank -- is collected; the k smallest of them are the row's answer.  Each
+// block scans one reference slice for kFbQB failing rows, so X is read once per
+// row group; appends are warp-aggregated.
+__global__ void __launch_bounds__(kFbThreads)
+    k_fb_collect(const float* __restrict__ Q, int64_t q_begin, const float* __restrict__ X,
+                 int64_t n, int d, int self_join, const int32_t* __restrict__ fail_rows,
+                 const double* __restrict__ fail_ub, int nfail, int P,
+                 double* __restrict__ ck, int* __restrict__ ci, int* __restrict__ ccnt) {
+  extern __shared__ double s_q[];  // [kFbQB][d]
+  const int t = threadIdx.x, lane = t & 31;
+  const int p = blockIdx.x, f0 = blockIdx.y * kFbQB;
+  const int nq = min(kFbQB, nfail - f0);
+  int64_t gq[kFbQB];
+  double ub[kFbQB];
+#pragma unroll
+  for (int q = 0; q < kFbQB; ++q) {
+    const int f = f0 + (q < nq ? q : 0);
+    const int64_t r = fail_rows[f];
+    gq[q] = q_begin + r;
+    ub[q] = q < nq ? fail_ub[f] : -1.0;
+    const float* xi = self_join ? X + gq[q] * d : Q + r * d;
+    for (int c = t; c < d; c += kFbThreads) s_q[q * d + c] = (double)xi[c];
+  }
+  __syncthreads();
+  const int64_t j_lo = n * p / P, j_hi = n * (p + 1) / P;
+  for (int64_t jb = j_lo; jb < j_hi; jb += kFbThreads) {
+    const int64_t j = jb + t;
+    double acc[kFbQB];
+#pragma unroll
+    for (int q = 0; q < kFbQB; ++q) acc[q] = 0.0;
+    if (j < j_hi) {
+      const float* xj = X + j * d;
+      for (int c = 0; c < d; ++c) {  // O1 per row: ascending c, no FMA
+        const double xv = (double)__ldg(xj + c);
+#pragma unroll
+        for (int q = 0; q < kFbQB; ++q) {
+          const double tt = __dsub_rn(s_q[q * d + c], xv);
+          acc[q] = __dadd_rn(acc[q], __dmul_rn(tt, tt));
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kFbQB; ++q) {
+      const bool keep = j < j_hi && !(self_join && j == gq[q]) && acc[q] <= ub[q];
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (m) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(ccnt + f0 + q, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const int pos = base + __popc(m & ((1u << lane) - 1u));
+        if (keep && pos < kFbCap) {
+          ck[(int64_t)(f0 + q) * kFbCap + pos] = acc[q];
+          ci[(int64_t)(f0 + q) * kFbCap + pos] = (int)j;
+        }
+      }
+    }
+  }
+}
+
+// One warp per failing row: the k smallest collected columns by (D64, index).
+// Rows whose collection is unusable (fewer than k, or more than kFbCap) are
+// left to the block brute-force tier (done = 0).
+__global__ void __launch_bounds__(128)
+    k_fb_select(int k, const int32_t* __restrict__ fail_rows, int nfail,
+                double* __restrict__ ck, int* __restrict__ ci, const int* __restrict__ ccnt,
+                int* __restrict__ done, KnnOutDev out) {
+  __shared__ double s_tk[4][kMaxK];
+  __shared__ int s_ti[4][kMaxK];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int f = blockIdx.x * 4 + w;
+  if (f >= nfail) return;
+  const int c = ccnt[f];
+  if (c < k || c > kFbCap) {
+    if (lane == 0) done[f] = 0;
+    return;
+  }
+  double* bk = ck + (int64_t)f * kFbCap;
+  int* bi = ci + (int64_t)f * kFbCap;
+  double* tk = s_tk[w];
+  int* ti = s_ti[w];
+  if (c <= 64) {
+    double kk[2];
+    int ii[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int p = 2 * lane + e;
+      kk[e] = p < c ? bk[p] : CUDART_INF;
+      ii[e] = p < c ? bi[p] : INT32_MAX;
+    }
+    warp_sort64(kk, ii, lane);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int p = 2 * lane + e;
+      if (p < k) {
+        tk[p] = kk[e];
+        ti[p] = ii[e];
+      }
+    }
+  } else {
+    auto slice_min = [&](double& mk, int& mi, int& mp) {
+      mk = CUDART_INF;
+      mi = INT32_MAX;
+      mp = -1;
+      for (int e = lane; e < c; e += 32)
+        if (key_less(bk[e], bi[e], mk, mi)) {
+          mk = bk[e];
+          mi = bi[e];
+          mp = e;
+        }
+    };
+    double lk;
+    int li, lp;
+    slice_min(lk, li, lp);
+    for (int m = 0; m < k; ++m) {
+      double b = lk;
+      int b2 = li;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ok = __shfl_xor_sync(0xffffffffu, b, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, b2, o);
+        if (key_less(ok, oi, b, b2)) {
+          b = ok;
+          b2 = oi;
+        }
+      }
+      if (lane == 0) {
+        tk[m] = b;
+        ti[m] = b2;
+      }
+      if (lp >= 0 && li == b2 && b2 != INT32_MAX) {
+        bk[lp] = CUDART_INF;
+        bi[lp] = INT32_MAX;
+        slice_min(lk, li, lp);
+      }
+    }
+  }
+  __syncwarp();
+  write_row(out, fail_rows[f], k, tk, ti, lane, 32);
+  if (lane == 0) done[f] = 1;
+}
+
+
 
 template <int KMAX>
 __global__ void __launch_bounds__(kFbThreads)
     k_fallback_part(const float* __restrict__ Q, int64_t q_begin, const float* __restrict__ X,
                     int64_t n, int d, int k, int self_join, const int32_t* __restrict__ fail_rows,
-                    int P, double* __restrict__ part_key, int* __restrict__ part_id) {
+                    int P, const int* __restrict__ done, double* __restrict__ part_key,
+                    int* __restrict__ part_id) {
+  if (done[blockIdx.y]) return;  // answered by the threshold tier
   __shared__ double s_hk[kFbThreads / 32];
   __shared__ int s_hi[kFbThreads / 32];
   __shared__ int s_ht[kFbThreads / 32];
@@ -610,8 +766,9 @@ constexpr int kFbMaxP = 64;
 
 __global__ void __launch_bounds__(kFbMaxP)
     k_fallback_merge(int k, const int32_t* __restrict__ fail_rows, int P,
-                     const double* __restrict__ part_key, const int* __restrict__ part_id,
-                     KnnOutDev out) {
+                     const int* __restrict__ done, const double* __restrict__ part_key,
+                     const int* __restrict__ part_id, KnnOutDev out) {
+  if (done[blockIdx.x]) return;
   __shared__ double s_key[kMaxK];
   __shared__ int s_id[kMaxK];
   __shared__ double s_hk[kFbMaxP / 32];
@@ -663,8 +820,8 @@ __global__ void __launch_bounds__(kFbMaxP)
 
 cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, const float* X,
                           int64_t n, int d, int k, bool self_join, Cands c, const MainPass* mp,
-                          CertParams cp, KnnOutDev out, int32_t* fail_rows, int32_t* fail_count,
-                          double* max_err, cudaStream_t st, int* launches) {
+                          CertParams cp, KnnOutDev out, int32_t* fail_rows, double* fail_ub,
+                          int32_t* fail_count, double* max_err, cudaStream_t st, int* launches) {
   if (k > kMaxK) return cudaErrorInvalidValue;
   if (cp.kind == PASS_TC) {  // group candidates
     if (c.lists * c.kp > kSelMax || !c.key) return cudaErrorInvalidValue;
@@ -677,7 +834,8 @@ cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, cons
     if (e != cudaSuccess) return e;
     k_rerank_groups<<<(unsigned)gb, kGrpWarps * 32, smem, st>>>(
         Q, q_begin, q_count, X, n, d, k, self_join ? 1 : 0, c.idx, c.key, c.v, c.kp, c.lists,
-        mp ? mp->buf : nullptr, mp ? mp->cnt : nullptr, mp ? mp->cap : 0, cp, out, fail_rows, fail_count, reinterpret_cast<unsigned long long*>(max_err));
+        mp ? mp->buf : nullptr, mp ? mp->cnt : nullptr, mp ? mp->cap : 0, cp, out, fail_rows,
+        fail_ub, fail_count, reinterpret_cast<unsigned long long*>(max_err));
     *launches += 1;
     return cudaGetLastError();
   }
@@ -686,14 +844,17 @@ cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, cons
   if (blocks == 0) return cudaSuccess;
   k_rerank<<<(unsigned)blocks, kRerankWarps * 32, 0, st>>>(
       Q, q_begin, q_count, X, n, d, k, self_join ? 1 : 0, c.idx, c.v, c.kp, c.lists, cp, out,
-      fail_rows, fail_count, reinterpret_cast<unsigned long long*>(max_err));
+      fail_rows, fail_ub, fail_count, reinterpret_cast<unsigned long long*>(max_err));
   *launches += 1;
   return cudaGetLastError();
 }
 
+constexpr int kFbThrMaxRows = 65536;  // larger failure sets skip the threshold tier
+
 size_t fallback_workspace(int nfail, int k, int64_t n, int num_sms) {
   const int P = fallback_slices(nfail, n, num_sms);
-  return (size_t)nfail * P * k * (sizeof(double) + sizeof(int));
+  const size_t thr = nfail <= kFbThrMaxRows ? (size_t)nfail * kFbCap * 12 : 0;
+  return (size_t)nfail * P * k * (sizeof(double) + sizeof(int)) + thr + (size_t)nfail * 8 + 64;
 }
 
 int fallback_slices(int nfail, int64_t n, int num_sms) {
@@ -704,24 +865,48 @@ int fallback_slices(int nfail, int64_t n, int num_sms) {
 }
 
 cudaError_t launch_fallback(const float* Q, int64_t q_begin, const float* X, int64_t n, int d,
-                            int k, bool self_join, const int32_t* fail_rows, int nfail,
-                            KnnOutDev out, void* ws, int num_sms, cudaStream_t st, int* launches) {
+                            int k, bool self_join, const int32_t* fail_rows,
+                            const double* fail_ub, int nfail, KnnOutDev out, void* ws,
+                            int num_sms, cudaStream_t st, int* launches) {
   if (nfail <= 0) return cudaSuccess;
   if (k > kMaxK) return cudaErrorInvalidValue;
   const int P = fallback_slices(nfail, n, num_sms);
-  double* pk = static_cast<double*>(ws);
+  const bool thr = nfail <= kFbThrMaxRows && (size_t)kFbQB * d * 8 <= 96 * 1024;
+  // workspace: [ck nfail*cap f64][pk nfail*P*k f64][pi nfail*P*k i32][ci nfail*cap i32][done][ccnt]
+  double* ck = static_cast<double*>(ws);
+  double* pk = ck + (thr ? (size_t)nfail * kFbCap : 0);
   int* pi = reinterpret_cast<int*>(pk + (size_t)nfail * P * k);
+  int* ci = pi + (size_t)nfail * P * k;
+  int* done = ci + (thr ? (size_t)nfail * kFbCap : 0);
+  int* ccnt = done + nfail;
+  cudaError_t e = cudaMemsetAsync(done, 0, (size_t)nfail * 8, st);  // done and ccnt
+  if (e != cudaSuccess) return e;
+  if (thr) {
+    const int qb = (nfail + kFbQB - 1) / kFbQB;
+    int Pt = (2 * num_sms + qb - 1) / qb;
+    while (Pt > 1 && n / Pt < 1024) --Pt;
+    if (Pt < 1) Pt = 1;
+    const size_t smem = (size_t)kFbQB * d * 8;
+    e = cudaFuncSetAttribute(k_fb_collect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_fb_collect<<<dim3(Pt, qb), kFbThreads, smem, st>>>(Q, q_begin, X, n, d, self_join ? 1 : 0,
+                                                          fail_rows, fail_ub, nfail, Pt, ck, ci,
+                                                          ccnt);
+    k_fb_select<<<(nfail + 3) / 4, 128, 0, st>>>(k, fail_rows, nfail, ck, ci, ccnt, done, out);
+    *launches += 2;
+  }
   const dim3 grid(P, nfail);
   if (k <= 32)
     k_fallback_part<32><<<grid, kFbThreads, 0, st>>>(Q, q_begin, X, n, d, k, self_join ? 1 : 0,
-                                                     fail_rows, P, pk, pi);
+                                                     fail_rows, P, done, pk, pi);
   else if (k <= 64)
     k_fallback_part<64><<<grid, kFbThreads, 0, st>>>(Q, q_begin, X, n, d, k, self_join ? 1 : 0,
-                                                     fail_rows, P, pk, pi);
+                                                     fail_rows, P, done, pk, pi);
   else
     k_fallback_part<kMaxK><<<grid, kFbThreads, 0, st>>>(Q, q_begin, X, n, d, k,
-                                                        self_join ? 1 : 0, fail_rows, P, pk, pi);
-  k_fallback_merge<<<nfail, kFbMaxP, 0, st>>>(k, fail_rows, P, pk, pi, out);
+                                                        self_join ? 1 : 0, fail_rows, P, done, pk,
+                                                        pi);
+  k_fallback_merge<<<nfail, kFbMaxP, 0, st>>>(k, fail_rows, P, done, pk, pi, out);
   *launches += 2;
   return cudaGetLastError();
 }
