@@ -99,6 +99,9 @@ typedef struct {
   double max_abs_err;      /* largest per-row pass-1 error term (E_i + quantization), scaled units */
   float ms_stage, ms_prep, ms_main, ms_certify, ms_fallback, ms_lof, ms_total;  /* with TOD_F_TIMING */
   int64_t kernel_launches; /* kernels launched by this call */
+  int64_t cand_groups;     /* 8-column candidate groups kept by pass 1, summed over rows (tensor-core pass) */
+  int64_t visited_groups;  /* groups the re-rank expanded to exact fp64 distances, summed over rows */
+  int64_t cand_columns;    /* exact distances at or below the per-row bound kept for the final selection */
 } tod_stats;
 
 /* Per-neighbour and per-row outputs of the kNN functional operator (P:270,

@@ -175,6 +175,10 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
     // groups; kps = 2K'/R leaves a wide margin for the sample's variance.
     p->two = 1;
     p->R = 8;
+    if (const char* e = getenv("TOD_SAMPLE_R")) {  // experiment knob (power of two >= 2)
+      const int v = atoi(e);
+      if (v >= 2 && v <= 64 && (v & (v - 1)) == 0) p->R = v;
+    }
     const int kps = std::min(64, std::max(8, roundup((2 * kp + p->R - 1) / p->R, 4)));
     const double img_bytes = (double)bt256 * 256 * (p->dpad + 16) * 2;
     p->main_S = std::max(1, (int)std::ceil(img_bytes / (48.0 * 1024 * 1024)));
@@ -263,6 +267,7 @@ struct SmallDev {
   int32_t fail_count;
   int32_t pad;
   double max_err;
+  unsigned long long counters[3];  // re-rank telemetry: staged groups, visited groups, kept columns
 };
 
 // Core: all pointers device.  Q == nullptr => self-join over X, rows
@@ -376,12 +381,13 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
       mp.R = plan.R;
       mp.tau_v = cands.v;
       mp.tau_lists = cands.lists;
-      mp.cap = plan.cap;
-      TOD_TRY(ensure(ctx, B_MBUF, (size_t)std::max<int64_t>(q_count, 1) * 2 * plan.cap * 8, &p));
+      mp.parts = tc3_parts(plan.dpad);
+      mp.cap = plan.cap * 2 / mp.parts;  // plan.cap is per column half
+      TOD_TRY(ensure(ctx, B_MBUF, (size_t)std::max<int64_t>(q_count, 1) * mp.parts * mp.cap * 8, &p));
       mp.buf = static_cast<uint2*>(p);
-      TOD_TRY(ensure(ctx, B_MCNT, (size_t)std::max<int64_t>(q_count, 1) * 2 * 4, &p));
+      TOD_TRY(ensure(ctx, B_MCNT, (size_t)std::max<int64_t>(q_count, 1) * mp.parts * 4, &p));
       mp.cnt = static_cast<int*>(p);
-      TOD_CUDA(cudaMemsetAsync(mp.cnt, 0, (size_t)std::max<int64_t>(q_count, 1) * 2 * 4, st));
+      TOD_CUDA(cudaMemsetAsync(mp.cnt, 0, (size_t)std::max<int64_t>(q_count, 1) * mp.parts * 4, st));
       TOD_CUDA(launch_knn_tc3(A, B, self ? q_begin : 0, q_count, self, plan.fmt, mp,
                               ctx->num_sms, cands.dbg, st, launches));
     }
@@ -420,7 +426,7 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
   }
   TOD_CUDA(launch_rerank(dQ, q_begin, q_count, dX, n, d, k, self, cands, plan.two ? &mp : nullptr,
                          cp, out, fail_rows, fail_ub,
-                         &small->fail_count, &small->max_err, st, launches));
+                         &small->fail_count, &small->max_err, small->counters, st, launches));
   tm.mark();  // 4: fallback start
   SmallDev h{};
   TOD_CUDA(cudaMemcpyAsync(&h, small, sizeof(SmallDev), cudaMemcpyDeviceToHost, st));
@@ -442,6 +448,9 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     stats->dpad = plan.dpad;
     stats->scale = plan.kind == PASS_TC ? h.g.s : 1.0;
     stats->max_abs_err = h.max_err;
+    stats->cand_groups = (int64_t)h.counters[0];
+    stats->visited_groups = (int64_t)h.counters[1];
+    stats->cand_columns = (int64_t)h.counters[2];
   }
   return TOD_OK;
 }

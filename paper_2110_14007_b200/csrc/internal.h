@@ -87,11 +87,13 @@ struct MainPass {
   int R = 0;                  // sample stride: tiles t % R == 0 are skipped (0 = none)
   const float* tau_v = nullptr;  // [q_count][tau_lists] sample-list thresholds
   int tau_lists = 1;
-  uint2* buf = nullptr;       // [q_count][2][cap] (key bits, group index)
-  int* cnt = nullptr;         // [q_count][2] appended counts (may exceed cap = overflow)
+  uint2* buf = nullptr;       // [q_count][parts][cap] (key bits, group index)
+  int* cnt = nullptr;         // [q_count][parts] appended counts (may exceed cap = overflow)
   int cap = 0;
+  int parts = 2;              // column parts per tile (one buffer per (row, part))
 };
 int tc3_fits(int dpad);
+int tc3_parts(int dpad);      // column parts (= filter warps / 4) the main pass uses
 cudaError_t launch_knn_tc3(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                            bool self_join, int fmt, const MainPass& m, int num_sms, int dbg,
                            cudaStream_t st, int* launches);
@@ -123,7 +125,8 @@ cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, cons
                           int64_t n, int d, int k, bool self_join, Cands c, const MainPass* mp,
                           CertParams cp,
                           KnnOutDev out, int32_t* fail_rows, double* fail_ub, int32_t* fail_count,
-                          double* max_err, cudaStream_t st, int* launches);
+                          double* max_err, unsigned long long* counters, cudaStream_t st,
+                          int* launches);
 int fallback_slices(int nfail, int64_t n, int num_sms);
 size_t fallback_workspace(int nfail, int k, int64_t n, int num_sms);
 cudaError_t launch_fallback(const float* Q, int64_t q_begin, const float* X, int64_t n, int d,

@@ -40,10 +40,7 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBN = 256;
-constexpr int kBH = 128;        // columns per filter warp per tile
 constexpr int kExtraRB = 32;
-constexpr int kFW = 8;
-constexpr int kThreads = 64 + 32 * kFW;
 constexpr int kSmemMax = 232448;
 constexpr int kMaxStage = 4;
 constexpr int kPend = 16;       // pending slots per row (checks every 8 groups)
@@ -65,24 +62,25 @@ struct Cfg3 {
   static constexpr int B_EXTRA = kBN * NKB * RB;
 };
 
-template <int DPAD>
+// FW filter warps: 4 lane quarters x FW/4 column parts of every 256-column tile.
+template <int DPAD, int FW>
 __host__ __device__ constexpr int smem3(int nstage, int* off_b, int* off_p, int* off_bar) {
   using C = Cfg3<DPAD>;
   int o = C::A_STRIDE;
   *off_b = o;
   o += nstage * C::B_STRIDE;
   *off_p = o;
-  o += kFW * kPend * 32 * 8;
+  o += FW * kPend * 32 * 8;
   *off_bar = o;
   o += 8 * (2 * kMaxStage + 2 + 4) + 16;
   return o + 1024;
 }
 
-template <int DPAD>
+template <int DPAD, int FW>
 int pick_stages3() {
   int a, b, c;
   for (int ns = kMaxStage; ns >= 2; --ns)
-    if (smem3<DPAD>(ns, &a, &b, &c) <= kSmemMax) return ns;
+    if (smem3<DPAD, FW>(ns, &a, &b, &c) <= kSmemMax) return ns;
   return 0;
 }
 
@@ -114,8 +112,8 @@ __device__ __forceinline__ float min8(const float* v) {
                fminf(fminf(v[3], v[4]), fminf(fminf(v[5], v[6]), v[7])));
 }
 
-template <int DPAD, int FMT, int DBG>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int DPAD, int FMT, int DBG, int FW>
+__global__ void __launch_bounds__(64 + 32 * FW, 1)
     k_knn_tc3(const uint8_t* __restrict__ a_img, size_t a_region, size_t a_extra,
               const uint8_t* __restrict__ b_img, size_t b_region, size_t b_extra, int64_t b_tiles,
               int64_t n_ref, int64_t qt0, int64_t n_qtiles, int64_t q_begin, int64_t q_end,
@@ -123,10 +121,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float* __restrict__ tau_v, int tau_lists,
               uint2* __restrict__ mbuf, int* __restrict__ mcnt, int cap) {
   using C = Cfg3<DPAD>;
+  constexpr int H = FW / 4;        // column parts per tile
+  constexpr int BH = kBN / H;      // columns per filter warp per tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   int off_b, off_p, off_bar;
-  smem3<DPAD>(nstage, &off_b, &off_p, &off_bar);
+  smem3<DPAD, FW>(nstage, &off_b, &off_p, &off_bar);
   uint8_t* sA = smem;
   uint8_t* sB = smem + off_b;
   const uint32_t s_pend = smem_u32(smem + off_p);
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(a_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&t_full[i], 1);
-      mbar_init(&t_empty[i], kFW);
+      mbar_init(&t_empty[i], FW);
     }
     fence_mbar_init();
   }
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // --------------------------------------------------------- filter warps
     const int f = warp - 2;
     const int q = warp & 3;           // TMEM lane quarter
-    const int h = f >> 2;             // column half of every tile
+    const int h = f >> 2;             // column part of every tile
     const int rt = q * 32 + lane;     // row within the query tile
     constexpr uint32_t SLOT = 32 * 8;
     const uint32_t pbase = s_pend + (f * kPend * 32 + lane) * 8;
@@ -287,8 +287,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tau = CUDART_INF_F;
         for (int l = 0; l < tau_lists; ++l) tau = fminf(tau, tau_v[r * tau_lists + l]);
       }
-      int* cnt = mcnt + r * 2 + h;
-      uint2* buf = mbuf + (r * 2 + h) * (int64_t)cap;
+      int* cnt = mcnt + r * H + h;
+      uint2* buf = mbuf + (r * H + h) * (int64_t)cap;
       // move this lane's pending run to its HBM buffer (slots reserved atomically)
       auto flush = [&]() {
         const int n = (int)((pa - pbase) / SLOT);
@@ -307,11 +307,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (; ts.more(); ts.next()) {
         mbar_wait(&t_full[acc], acc_phase);
         tc_fence_after();
-        float v[kBH];
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kBN + h * kBH;
+        float v[BH];
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kBN + h * BH;
         if (!(DBG & 2)) {
-          tmem_ld64(taddr, *reinterpret_cast<float(*)[64]>(v));
-          tmem_ld64(taddr + 64, *reinterpret_cast<float(*)[64]>(v + 64));
+#pragma unroll
+          for (int u = 0; u < BH / 64; ++u)
+            tmem_ld64(taddr + 64 * u, *reinterpret_cast<float(*)[64]>(v + 64 * u));
           tmem_ld_wait();
         }
         tc_fence_before();
@@ -323,21 +324,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (DBG & 3) continue;  // profiling: pipeline without the filter work
         const int t = ts.t;
-        const int j0 = t * kBN + h * kBH;
+        const int j0 = t * kBN + h * BH;
         // the self column and padding columns (>= n_ref) are never candidates;
         // only the query tile's own reference tile and the last tile need masks
         if (t == t_self || t == t_last) {
 #pragma unroll
-          for (int e = 0; e < kBH; ++e)
+          for (int e = 0; e < BH; ++e)
             v[e] = (j0 + e == self || j0 + e >= n_ref) ? CUDART_INF_F : v[e];
         }
-        // 16 independent min trees first (full ILP), then the appends
-        float m[kBH / 8];
+        // independent min trees first (full ILP), then the appends
+        float m[BH / 8];
 #pragma unroll
-        for (int g = 0; g < kBH / 8; ++g) m[g] = min8(v + 8 * g);
+        for (int g = 0; g < BH / 8; ++g) m[g] = min8(v + 8 * g);
         const int gbase = j0 >> 3;
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
+        for (int hh = 0; hh < BH / 64; ++hh) {
           if (__any_sync(0xffffffffu, pa > pbase + (kPend - 8) * SLOT)) flush();
 #pragma unroll
           for (int g = 0; g < 8; ++g) {
@@ -360,14 +361,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int DPAD, int FMT, int DBG>
+template <int DPAD, int FMT, int DBG, int FW>
 cudaError_t launch3(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                     bool self_join, const MainPass& m, int num_sms, cudaStream_t st) {
-  const int nstage = pick_stages3<DPAD>();
+  const int nstage = pick_stages3<DPAD, FW>();
   if (nstage == 0) return cudaErrorInvalidValue;
+  if (m.parts != FW / 4) return cudaErrorInvalidValue;
   int a, b, c;
-  const int smem = smem3<DPAD>(nstage, &a, &b, &c);
-  auto kern = k_knn_tc3<DPAD, FMT, DBG>;
+  const int smem = smem3<DPAD, FW>(nstage, &a, &b, &c);
+  auto kern = k_knn_tc3<DPAD, FMT, DBG, FW>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t qt0 = q_begin / kBM;
@@ -375,7 +377,7 @@ cudaError_t launch3(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
   const int64_t n_items = (qt1 - qt0) * m.S;
   const int grid = (int)std::min<int64_t>(num_sms, n_items);
   if (grid <= 0) return cudaSuccess;
-  kern<<<grid, kThreads, smem, st>>>(
+  kern<<<grid, 64 + 32 * FW, smem, st>>>(
       reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(), A.extra_offset(),
       reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
       B.n_pad / kBN, B.n, qt0, qt1 - qt0, q_begin, q_begin + q_count, self_join ? 1 : 0, m.S,
@@ -385,33 +387,49 @@ cudaError_t launch3(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
 
 }  // namespace
 
-int tc3_fits(int dpad) {
+// Filter warps per CTA: 16 (4 per SM sub-partition, 64 columns each) when 3+
+// operand stages still fit in shared memory, else 8.
+template <int DPAD>
+int tc3_fw() {
+  return pick_stages3<DPAD, 16>() >= 3 ? 16 : (pick_stages3<DPAD, 8>() > 0 ? 8 : 0);
+}
+
+int tc3_parts(int dpad) {
   switch (dpad) {
-    case 16: return pick_stages3<16>() > 0;
-    case 32: return pick_stages3<32>() > 0;
-    case 64: return pick_stages3<64>() > 0;
+    case 16: return tc3_fw<16>() / 4;
+    case 32: return tc3_fw<32>() / 4;
+    case 64: return tc3_fw<64>() / 4;
   }
   return 0;
 }
+
+int tc3_fits(int dpad) { return tc3_parts(dpad) > 0; }
 
 cudaError_t launch_knn_tc3(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                            bool self_join, int fmt, const MainPass& m, int num_sms, int dbg,
                            cudaStream_t st, int* launches) {
   *launches += 1;
   // dbg (profiling only): 1 = skip the filter work, 2 = also skip the TMEM loads
-#define TOD_TC3_CASE(D)                                                                        \
-  case D:                                                                                     \
-    if (dbg & 3)                                                                              \
-      return fmt == 1 ? launch3<D, 1, 2>(A, B, q_begin, q_count, self_join, m, num_sms, st)   \
-                      : launch3<D, 2, 2>(A, B, q_begin, q_count, self_join, m, num_sms, st);  \
-    return fmt == 1 ? launch3<D, 1, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st)     \
-                    : launch3<D, 2, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st);
+#define TOD_TC3_FW(D, FW)                                                                       \
+  if (dbg & 3)                                                                                 \
+    return fmt == 1 ? launch3<D, 1, 2, FW>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
+                    : launch3<D, 2, 2, FW>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+  return fmt == 1 ? launch3<D, 1, 0, FW>(A, B, q_begin, q_count, self_join, m, num_sms, st)    \
+                  : launch3<D, 2, 0, FW>(A, B, q_begin, q_count, self_join, m, num_sms, st);
+#define TOD_TC3_CASE(D)          \
+  case D:                        \
+    if (tc3_fw<D>() == 16) {     \
+      TOD_TC3_FW(D, 16)          \
+    } else {                     \
+      TOD_TC3_FW(D, 8)           \
+    }
   switch (A.dpad) {
     TOD_TC3_CASE(16)
     TOD_TC3_CASE(32)
     TOD_TC3_CASE(64)
   }
 #undef TOD_TC3_CASE
+#undef TOD_TC3_FW
   return cudaErrorInvalidValue;
 }
 

@@ -143,11 +143,10 @@ struct Pieces {
 // [xhat | norm pieces]; side 1 = query image A: [-2 xhat | constants].
 // Padding rows are zero (the epilogue masks padding columns).
 template <int FMT>
-__global__ void k_quant(const float* __restrict__ X, int64_t n, int d,
-                        const double* __restrict__ mu, PrepGlobals* g, Image img, int side) {
-  const int lane = threadIdx.x & 31;
-  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (r >= img.n_pad) return;
+__device__ __forceinline__ void quant_row(const float* __restrict__ X, int64_t n, int d,
+                                          const double* __restrict__ mu, PrepGlobals* g,
+                                          const Image& img, int side, int64_t r, int lane,
+                                          unsigned long long* s_max) {
   const double s = g->s;
   const int epr = img.rb / 2;  // elements per row per main region
   const unsigned M = img.layout == 2 ? 7u : (img.layout == 4 ? 3u : 1u);
@@ -229,9 +228,30 @@ __global__ void k_quant(const float* __restrict__ X, int64_t n, int d,
                    (1.0 + 8.0 * eps);
   img.e[r] = e;
   if (side == 0) {
-    atomic_max_nonneg(reinterpret_cast<unsigned long long*>(&g->amax2), a2);
-    atomic_max_nonneg(reinterpret_cast<unsigned long long*>(&g->emax), e);
-    atomic_max_nonneg(reinterpret_cast<unsigned long long*>(&g->repmax), rep);
+    atomic_max_nonneg(&s_max[0], a2);
+    atomic_max_nonneg(&s_max[1], e);
+    atomic_max_nonneg(&s_max[2], rep);
+  }
+}
+
+
+template <int FMT>
+__global__ void k_quant(const float* __restrict__ X, int64_t n, int d,
+                        const double* __restrict__ mu, PrepGlobals* g, Image img, int side) {
+  // per-block maxima (one global atomic per block and quantity, not per row:
+  // same-address atomics from every row serialise in L2)
+  __shared__ unsigned long long s_max[3];
+  if (threadIdx.x < 3) s_max[threadIdx.x] = 0ull;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r < img.n_pad) quant_row<FMT>(X, n, d, mu, g, img, side, r, lane, s_max);
+  __syncthreads();
+  if (side == 0 && threadIdx.x < 3 && s_max[threadIdx.x] != 0ull) {
+    unsigned long long* dst = threadIdx.x == 0 ? reinterpret_cast<unsigned long long*>(&g->amax2)
+                            : threadIdx.x == 1 ? reinterpret_cast<unsigned long long*>(&g->emax)
+                                               : reinterpret_cast<unsigned long long*>(&g->repmax);
+    atomicMax(dst, s_max[threadIdx.x]);
   }
 }
 

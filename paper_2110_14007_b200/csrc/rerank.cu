@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kRerankWarps * 32)
   double err = 0.0;
   bool cert = nv_local >= k && row_certified(cp, r, vmin, s_sk[w][k - 1], &err);
   if (cp.force_fail) cert = false;
-  if (lane == 0 && err > 0.0)
+  if (lane == 0 && err > 0.0 && (r & 31) == 0)  // sampled: same-address atomics serialise
     atomicMax(max_err_bits, (unsigned long long)__double_as_longlong(err));
   if (cert) {
     write_row(out, r, k, s_sk[w], s_si[w], lane, 32);
@@ -192,27 +192,6 @@ __global__ void __launch_bounds__(kRerankWarps * 32)
 // kept group is re-ranked; columns outside kept groups have w~ >= v (their
 // group's minimum is >= v), so the same certificate applies.
 constexpr int kGrpWarps = 4;
-
-// Warp-wide bitonic sort (ascending by (key, id)) of one element per lane.
-__device__ __forceinline__ void warp_sort32(double& key, int& id, int lane) {
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const double ok = __shfl_xor_sync(0xffffffffu, key, j);
-      const int oi = __shfl_xor_sync(0xffffffffu, id, j);
-      const bool up = (lane & k) == 0;
-      const bool lower = (lane & j) == 0;
-      // keep the smaller in the lower lane of an ascending pair
-      const bool other_less = key_less(ok, oi, key, id);
-      const bool take = (lower == up) ? other_less : !other_less;
-      if (take) {
-        key = ok;
-        id = oi;
-      }
-    }
-  }
-}
 
 // Upper bound, in original units, on the exact squared distance D64 of row r to
 // the best column of a group whose pass-1 key is w (the group's minimum w~):
@@ -237,6 +216,32 @@ __device__ double ub2_from_key(const CertParams& cp, int64_t r, double w) {
   const double UB = (Rh + ei + emax) * (1.0 + 8.0 * u53);
   const double ubo = UB / cp.g->s;  // s = 2^e: exact
   return ubo * ubo * (1.0 + 8.0 * u53) * (1.0 + gamma_up(cp.d + 2, u53));
+}
+
+// Largest pass-1 key w (rounded up to fp32) for which lb2_from_key(w)(1-gamma)
+// could still be <= UB: lb2_from_key is increasing in w, so inverting it with
+// every rounding pushed upward gives a cutoff above which a group provably holds
+// no column at distance <= UB.  (A larger cutoff only visits more groups.)
+__device__ float key_cut_from_ub(const CertParams& cp, int64_t r, double UB) {
+  if (!(UB < CUDART_INF)) return CUDART_INF_F;
+  const double u53 = 1.1102230246251565e-16;
+  const double a2i = cp.qa2[r];
+  const double ei = cp.qe[r];
+  const double amax2 = cp.g->amax2;
+  const double emax = cp.g->emax;
+  const double rep = cp.g->repmax;
+  const double ai = sqrt(a2i) * (1.0 + 4 * u53);
+  const double am = sqrt(amax2) * (1.0 + 4 * u53);
+  const double gam = gamma_up(2.0 * (cp.dpad + 16), 2.384185791015625e-07 /*2^-22*/);
+  const double E = (gam * (2.0 * ai * am + 1.002 * amax2) + rep) * (1.0 + 1e-6) + 1e-300;
+  const double g64 = gamma_up(cp.d + 2, u53);
+  const double T = sqrt(UB / ((1.0 - 8.0 * u53) * (1.0 - g64))) * (1.0 + 4 * u53);
+  const double Z = (T * cp.g->s / (1.0 - 8.0 * u53) + ei + emax) * (1.0 + 4 * u53);
+  const double Zr = Z / (1.0 - 2.0 * u53) * (1.0 + 4 * u53);
+  const double w0 = Zr * Zr - a2i + E;
+  const double slack = (cp.d + 8) * 2.0 * u53 * (fabs(a2i) + fabs(w0) + E);
+  const double w = w0 + 2.0 * slack + 1e-9 * (fabs(a2i) + fabs(w0) + E);
+  return __double2float_ru(w);
 }
 
 // Group candidates (DESIGN.md §5 "Re-rank").  A row's kept groups come from its
@@ -300,15 +305,43 @@ __device__ __forceinline__ void warp_sort64(double (&k)[2], int (&id)[2], int la
   }
 }
 
-__global__ void __launch_bounds__(kGrpWarps * 32)
-    k_rerank_groups(const float* __restrict__ Q, int64_t q_begin, int64_t q_count,
-                    const float* __restrict__ X, int64_t n, int d, int k, int self_join,
-                    const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_key,
-                    const float* __restrict__ cand_v, int kp, int lists,
-                    const uint2* __restrict__ mbuf, const int* __restrict__ mcnt, int mcap,
-                    CertParams cp, KnnOutDev out, int32_t* __restrict__ fail_rows,
-                    double* __restrict__ fail_ub, int32_t* __restrict__ fail_count,
-                    unsigned long long* __restrict__ max_err_bits) {
+// 256-bit read-only global load (sm_100: LDG.E.ENL2.256); p must be 32-byte aligned.
+__device__ __forceinline__ void ldg8(const float* p, float* v) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]),
+                 "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+
+// O1 for a compile-time d (multiple of 8): the whole reference row in flight as
+// 32-byte loads (full sectors), the query row read as 16-byte pairs of doubles
+// (shared-memory broadcast); the sum stays sequential in c, no FMA.
+template <int DT>
+__device__ __forceinline__ double d64_fixed(const double* __restrict__ xq, const float* xj) {
+  float v[DT];
+#pragma unroll
+  for (int u = 0; u < DT / 8; ++u) ldg8(xj + 8 * u, v + 8 * u);
+  double acc = 0.0;
+#pragma unroll
+  for (int c = 0; c < DT; c += 2) {
+    const double2 q2 = *reinterpret_cast<const double2*>(xq + c);
+    double t = __dsub_rn(q2.x, (double)v[c]);
+    acc = __dadd_rn(acc, __dmul_rn(t, t));
+    t = __dsub_rn(q2.y, (double)v[c + 1]);
+    acc = __dadd_rn(acc, __dmul_rn(t, t));
+  }
+  return acc;
+}
+
+template <int DT>
+__device__ __forceinline__ void rerank_groups_row(
+    const float* __restrict__ Q, int64_t q_begin, int64_t q_count, const float* __restrict__ X,
+    int64_t n, int d, int k, int self_join, const int32_t* __restrict__ cand_idx,
+    const float* __restrict__ cand_key, const float* __restrict__ cand_v, int kp, int lists,
+    const uint2* __restrict__ mbuf, const int* __restrict__ mcnt, int mcap, int mparts,
+    const CertParams& cp,
+    const KnnOutDev& out, int32_t* __restrict__ fail_rows, double* __restrict__ fail_ub,
+    int32_t* __restrict__ fail_count, unsigned long long* s_red) {
   __shared__ float s_gk[kGrpWarps][kSelMax];      // staged group keys
   __shared__ int s_gi[kGrpWarps][kSelMax];        // staged group indices
   __shared__ double s_ck[kGrpWarps][kColMax];     // surviving columns: D64
@@ -341,11 +374,11 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
     G += __popc(live);
   }
   if (mbuf) {
-    for (int h = 0; h < 2; ++h) {
-      const int c = mcnt[r * 2 + h];
+    for (int h = 0; h < mparts; ++h) {
+      const int c = mcnt[r * mparts + h];
       overflow |= c > mcap;
       const int m = c < mcap ? c : mcap;
-      const uint2* src = mbuf + (r * 2 + h) * (int64_t)mcap;
+      const uint2* src = mbuf + (r * mparts + h) * (int64_t)mcap;
       for (int e = lane; e < m; e += 32) {
         const uint2 kv = src[e];
         if (G + e < kSelMax) {
@@ -361,7 +394,6 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
   float vmin = CUDART_INF_F;
   for (int c = 0; c < lists; ++c) vmin = fminf(vmin, cand_v[r * lists + c]);
   __syncwarp();
-  const double gamma64 = gamma_up(cp.d + 2, 1.1102230246251565e-16);
   // ---- 1. kappa and UB
   double UB = CUDART_INF;
   if (G >= k) {
@@ -376,16 +408,22 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
       lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
       hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     }
-    // invariant: count(key <= hi) >= k; shrink hi while keeping it
+    // invariant: count(key <= hi) >= k; shrink hi while keeping it (stop once
+    // at most k + 8 groups remain at or below it: kappa need not be tight)
     if (lo < hi) --lo;  // count(key <= lo) < k unless lo is the minimum itself
-    for (int it = 0; it < 24 && hi - lo > 1; ++it) {
+    int chi = G;
+    for (int it = 0; it < 20 && hi - lo > 1 && chi > k + 8; ++it) {
       const uint32_t mid = lo + ((hi - lo) >> 1);
       int c = 0;
       for (int e = lane; e < G; e += 32) c += f2ord(gk[e]) <= mid;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-      if (c >= k) hi = mid;
-      else lo = mid;
+      if (c >= k) {
+        hi = mid;
+        chi = c;
+      } else {
+        lo = mid;
+      }
     }
     const float kappa = ord2f(hi);
     if (kappa < CUDART_INF_F) UB = ub2_from_key(cp, r, (double)kappa);
@@ -393,14 +431,13 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
   // ---- 2. expand the groups that can hold a top-k column
   // (compacted in place into gid[0, nv), then 4 groups = 32 columns per step)
   int nv = 0;
+  const float kcut = key_cut_from_ub(cp, r, UB);
   for (int e0 = 0; e0 < G; e0 += 32) {
     const int e = e0 + lane;
     bool vis = false;
     int g = -1;
     if (e < G) {
-      double e2;
-      const double lb2 = lb2_from_key(cp, r, (double)gk[e], &e2);
-      vis = !(lb2 > 0.0 && lb2 * (1.0 - gamma64) > UB);
+      vis = gk[e] <= kcut;
       g = gid[e];
     }
     const unsigned vm = __ballot_sync(0xffffffffu, vis);
@@ -419,7 +456,29 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
     if (g >= 0 && j < n && !(self_join && j == gi)) {
       const float* xj = X + j * d;
       double acc = 0.0;  // O1, bit-identical to the oracle (no FMA, ascending c)
-      if ((d & 3) == 0) {
+      if constexpr (DT > 0) {
+        acc = d64_fixed<DT>(xq, xj);
+      } else if ((d & 15) == 0) {
+        // 4 independent 16-byte loads in flight, then the 16 terms in order
+        const float4* x4 = reinterpret_cast<const float4*>(xj);
+        for (int c16 = 0; c16 < (d >> 4); ++c16) {
+          float4 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] = __ldg(x4 + 4 * c16 + u);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double* xc = xq + 16 * c16 + 4 * u;
+            double t = __dsub_rn(xc[0], (double)v[u].x);
+            acc = __dadd_rn(acc, __dmul_rn(t, t));
+            t = __dsub_rn(xc[1], (double)v[u].y);
+            acc = __dadd_rn(acc, __dmul_rn(t, t));
+            t = __dsub_rn(xc[2], (double)v[u].z);
+            acc = __dadd_rn(acc, __dmul_rn(t, t));
+            t = __dsub_rn(xc[3], (double)v[u].w);
+            acc = __dadd_rn(acc, __dmul_rn(t, t));
+          }
+        }
+      } else if ((d & 3) == 0) {
         const float4* x4 = reinterpret_cast<const float4*>(xj);
         for (int c4 = 0; c4 < (d >> 2); ++c4) {
           const float4 v = __ldg(x4 + c4);
@@ -517,8 +576,12 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
   const bool have = nc >= k;
   bool cert = !overflow && have && row_certified(cp, r, vmin, tk[k - 1], &err);
   if (cp.force_fail) cert = false;
-  if (lane == 0 && err > 0.0)
-    atomicMax(max_err_bits, (unsigned long long)__double_as_longlong(err));
+  if (lane == 0) {
+    if (err > 0.0) atomicMax(&s_red[0], (unsigned long long)__double_as_longlong(err));
+    atomicAdd(&s_red[1], (unsigned long long)G);
+    atomicAdd(&s_red[2], (unsigned long long)nv);
+    atomicAdd(&s_red[3], (unsigned long long)nc);
+  }
   if (cert) {
     write_row(out, r, k, tk, ti, lane, 32);
   } else if (lane == 0) {
@@ -529,6 +592,30 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
     fail_ub[slot] = fmin(UB, have ? tk[k - 1] : CUDART_INF);
   }
 }
+
+template <int DT>
+__global__ void __launch_bounds__(kGrpWarps * 32)
+    k_rerank_groups(const float* __restrict__ Q, int64_t q_begin, int64_t q_count,
+                    const float* __restrict__ X, int64_t n, int d, int k, int self_join,
+                    const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_key,
+                    const float* __restrict__ cand_v, int kp, int lists,
+                    const uint2* __restrict__ mbuf, const int* __restrict__ mcnt, int mcap,
+                    int mparts,
+                    CertParams cp, KnnOutDev out, int32_t* __restrict__ fail_rows,
+                    double* __restrict__ fail_ub, int32_t* __restrict__ fail_count,
+                    unsigned long long* __restrict__ max_err_bits,
+                    unsigned long long* __restrict__ counters) {
+  __shared__ unsigned long long s_red[4];         // block reductions: max err, G, nv, nc
+  if (threadIdx.x < 4) s_red[threadIdx.x] = 0ull;
+  __syncthreads();
+  rerank_groups_row<DT>(Q, q_begin, q_count, X, n, d, k, self_join, cand_idx, cand_key, cand_v, kp,
+                    lists, mbuf, mcnt, mcap, mparts, cp, out, fail_rows, fail_ub, fail_count, s_red);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_red[0]) atomicMax(max_err_bits, s_red[0]);
+  if (threadIdx.x >= 1 && threadIdx.x < 4 && s_red[threadIdx.x])
+    atomicAdd(counters + threadIdx.x - 1, s_red[threadIdx.x]);
+}
+
 
 // ---------------------------------------------------------------- fallback
 // Brute-force fp64 tier for rows the certificate could not prove ("recalculate
@@ -821,7 +908,8 @@ __global__ void __launch_bounds__(kFbMaxP)
 cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, const float* X,
                           int64_t n, int d, int k, bool self_join, Cands c, const MainPass* mp,
                           CertParams cp, KnnOutDev out, int32_t* fail_rows, double* fail_ub,
-                          int32_t* fail_count, double* max_err, cudaStream_t st, int* launches) {
+                          int32_t* fail_count, double* max_err, unsigned long long* counters,
+                          cudaStream_t st, int* launches) {
   if (k > kMaxK) return cudaErrorInvalidValue;
   if (cp.kind == PASS_TC) {  // group candidates
     if (c.lists * c.kp > kSelMax || !c.key) return cudaErrorInvalidValue;
@@ -829,13 +917,18 @@ cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, cons
     if (gb == 0) return cudaSuccess;
     const size_t smem = (size_t)kGrpWarps * d * 8;
     if (smem > 160 * 1024) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(k_rerank_groups,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // compile-time d for the common widths (32-byte aligned rows), else generic
+    const bool al = ((reinterpret_cast<uintptr_t>(X) & 31) == 0);
+    auto kern = (al && d == 16) ? k_rerank_groups<16>
+              : (al && d == 32) ? k_rerank_groups<32>
+              : (al && d == 64) ? k_rerank_groups<64> : k_rerank_groups<0>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_rerank_groups<<<(unsigned)gb, kGrpWarps * 32, smem, st>>>(
+    kern<<<(unsigned)gb, kGrpWarps * 32, smem, st>>>(
         Q, q_begin, q_count, X, n, d, k, self_join ? 1 : 0, c.idx, c.key, c.v, c.kp, c.lists,
-        mp ? mp->buf : nullptr, mp ? mp->cnt : nullptr, mp ? mp->cap : 0, cp, out, fail_rows,
-        fail_ub, fail_count, reinterpret_cast<unsigned long long*>(max_err));
+        mp ? mp->buf : nullptr, mp ? mp->cnt : nullptr, mp ? mp->cap : 0, mp ? mp->parts : 0, cp,
+        out, fail_rows,
+        fail_ub, fail_count, reinterpret_cast<unsigned long long*>(max_err), counters);
     *launches += 1;
     return cudaGetLastError();
   }

@@ -50,7 +50,9 @@ class Stats(ctypes.Structure):
                 ("ms_stage", ctypes.c_float), ("ms_prep", ctypes.c_float),
                 ("ms_main", ctypes.c_float), ("ms_certify", ctypes.c_float),
                 ("ms_fallback", ctypes.c_float), ("ms_lof", ctypes.c_float),
-                ("ms_total", ctypes.c_float), ("kernel_launches", ctypes.c_int64)]
+                ("ms_total", ctypes.c_float), ("kernel_launches", ctypes.c_int64),
+                ("cand_groups", ctypes.c_int64), ("visited_groups", ctypes.c_int64),
+                ("cand_columns", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -1,4 +1,4 @@
-"""Profiling driver: one tod_knn call on a seeded mixture (for ncu)."""
+"""Profiling driver: tod_knn calls on a seeded mixture (for ncu / phase timings)."""
 import argparse
 import os
 import sys
@@ -25,5 +25,8 @@ with tod.Context(fmt=a.fmt, chunks=a.chunks, kprime=a.kprime, flags=tod.F_TIMING
     for _ in range(a.reps):
         r = ctx.knn(X, a.k, want=("idx", "score_kth"))
         torch.cuda.synchronize()
-        print({k: r.stats[k] for k in ("certified", "fallback_rows", "kprime", "chunks", "ms_prep",
-                                        "ms_main", "ms_certify", "ms_fallback")})
+        st = r.stats
+        print("cert %d fb %d kp %d S %d | prep %.3f main %.3f cert %.3f fb %.3f ms | per row: groups %.1f visited %.1f cols %.1f"
+              % (st["certified"], st["fallback_rows"], st["kprime"], st["chunks"], st["ms_prep"],
+                 st["ms_main"], st["ms_certify"], st["ms_fallback"], st["cand_groups"] / a.n,
+                 st["visited_groups"] / a.n, st["cand_columns"] / a.n))
