@@ -73,6 +73,7 @@ typedef enum {
 #define TOD_F_NO_CERTIFY   0x1u  /* testing: treat every row as uncertified -> fp64 brute-force tier */
 #define TOD_F_TIMING       0x2u  /* record per-phase CUDA-event times in tod_stats */
 #define TOD_F_DEBUG_NULL_EPILOGUE 0x100u  /* profiling only: pass 1 skips its epilogue (results invalid) */
+#define TOD_F_MAIN_1SM     0x20u  /* testing: run the main pass on single SMs (knn_tc3.cu) instead of CTA pairs */
 #define TOD_F_PASS1_V1     0x10u   /* testing: force the single-query-tile tensor-core schedule (knn_tc.cu) */
 #define TOD_F_DEBUG_TRACE  0x800u  /* profiling only: per-tile clock64 stamps of CTA 0 written to $TOD_TRACE_FILE */
 

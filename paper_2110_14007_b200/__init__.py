@@ -6,7 +6,7 @@ processes (dist.py).  It never imports the CPU oracle (oracle/), and it has no
 CPU fallback.
 """
 from .tod import (Context, KnnResult, TodError, load_library, header_symbols, LIB_PATH,  # noqa: F401
-                  F_NO_CERTIFY, F_TIMING, F_PASS1_V1, FORMATS)
+                  F_NO_CERTIFY, F_TIMING, F_PASS1_V1, F_MAIN_1SM, FORMATS)
 
 __all__ = ["Context", "KnnResult", "TodError", "load_library", "header_symbols", "LIB_PATH",
-           "F_NO_CERTIFY", "F_TIMING", "F_PASS1_V1", "FORMATS"]
+           "F_NO_CERTIFY", "F_TIMING", "F_PASS1_V1", "F_MAIN_1SM", "FORMATS"]

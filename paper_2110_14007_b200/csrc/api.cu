@@ -388,8 +388,14 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
       TOD_TRY(ensure(ctx, B_MCNT, (size_t)std::max<int64_t>(q_count, 1) * mp.parts * 4, &p));
       mp.cnt = static_cast<int*>(p);
       TOD_CUDA(cudaMemsetAsync(mp.cnt, 0, (size_t)std::max<int64_t>(q_count, 1) * mp.parts * 4, st));
-      TOD_CUDA(launch_knn_tc3(A, B, self ? q_begin : 0, q_count, self, plan.fmt, mp,
-                              ctx->num_sms, cands.dbg, st, launches));
+      const char* pe = getenv("TOD_MAIN_PAIR");  // experiment knob: 1 = force pairs, 0 = never
+      const bool pair = pe ? atoi(pe) != 0 : tc4_preferred(plan.dpad) != 0;
+      if (pair && !(ctx->cfg.flags & TOD_F_MAIN_1SM) && tc4_fits(plan.dpad, mp.parts))
+        TOD_CUDA(launch_knn_tc4(A, B, self ? q_begin : 0, q_count, self, plan.fmt, mp,
+                                ctx->num_sms, cands.dbg, st, launches));
+      else
+        TOD_CUDA(launch_knn_tc3(A, B, self ? q_begin : 0, q_count, self, plan.fmt, mp,
+                                ctx->num_sms, cands.dbg, st, launches));
     }
   } else {
     TOD_CUDA(launch_finite_check(dX, n, d, g, st, launches));

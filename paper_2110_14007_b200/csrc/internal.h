@@ -94,6 +94,12 @@ struct MainPass {
 };
 int tc3_fits(int dpad);
 int tc3_parts(int dpad);      // column parts (= filter warps / 4) the main pass uses
+// ---- knn_tc4.cu  (the same main pass on CTA pairs: tcgen05 cta_group::2, M = 256)
+int tc4_fits(int dpad, int parts);
+int tc4_preferred(int dpad);   // shapes where the pair beats the single-SM main pass
+cudaError_t launch_knn_tc4(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
+                           bool self_join, int fmt, const MainPass& m, int num_sms, int dbg,
+                           cudaStream_t st, int* launches);
 cudaError_t launch_knn_tc3(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                            bool self_join, int fmt, const MainPass& m, int num_sms, int dbg,
                            cudaStream_t st, int* launches);

@@ -1,0 +1,459 @@
+// knn_tc4.cu — K2 main pass on CTA PAIRS (tcgen05 cta_group::2), dpad <= 64.
+//
+// Same computation as knn_tc3.cu (the append-only threshold filter of the
+// two-pass candidate selection; arithmetic of Eq. (3)'s right-hand
+// side, fused with topk), scheduled for the measured
+// bottleneck of the single-SM version: shared-memory bandwidth.  A 128x256
+// single-SM MMA step reads its whole A and B tiles from one SM's shared memory
+// and the B tile is also written there by the copy engine (~1.9 bytes per
+// distance at d = 32 against 128 B/clk).  Here two SMs of a cluster issue one
+// M = 256 MMA (leader CTA only): each SM stages its own 128 query rows (A) and
+// HALF of every 256-column reference tile (B), and receives its 128 x 256
+// slice of the product in its own TMEM.  Per-SM operand traffic per distance
+// falls by ~40 % (B is written and read once per pair, not once per SM).
+//
+// Synchronisation across the pair (barriers live at the same shared offset in
+// both CTAs):
+//   full[s], a_full     CTA 0: arrival count 2 = its own expect_tx arrival +
+//                       a forwarded arrival from CTA 1 once CTA 1's copy landed
+//                       (CTA 1's warp 1 forwards; CTA 1's own barriers count 1).
+//   empty[s], a_empty,  multicast tcgen05.commit from the leader's MMA thread
+//   t_full[acc]         to both CTAs.
+//   t_empty[acc]        CTA 0 only: all 32 filter warps of the pair arrive
+//                       (CTA 1's remotely) before the accumulator is reused.
+#include <math_constants.h>
+
+#include <algorithm>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace tod {
+
+namespace {
+
+constexpr int kBM = 128;        // query rows per CTA (= TMEM lanes)
+constexpr int kBN = 256;        // reference columns per tile (MMA N)
+constexpr int kBNH = 128;       // reference rows of each tile staged per CTA
+constexpr int kExtraRB = 32;
+constexpr int kSmemMax = 232448;
+constexpr int kMaxStage = 6;
+constexpr int kPend = 16;
+
+__host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
+
+template <int DPAD>
+struct Cfg4 {
+  static constexpr int RB = DPAD * 2 < 128 ? DPAD * 2 : 128;
+  static constexpr int NKB = DPAD * 2 / RB;
+  static constexpr int LAYOUT = RB == 128 ? 2 : (RB == 64 ? 4 : 6);
+  static constexpr int SBO = 8 * RB;
+  static constexpr int KSTEPS = DPAD / 16;
+  static constexpr int A_ONE = kBM * (DPAD + 16) * 2;
+  static constexpr int A_STRIDE = align_up(A_ONE, 1024);
+  static constexpr int A_EXTRA = kBM * NKB * RB;
+  static constexpr int B_BYTES = kBNH * (DPAD + 16) * 2;   // this CTA's half tile
+  static constexpr int B_STRIDE = align_up(B_BYTES, 1024);
+  static constexpr int B_EXTRA = kBNH * NKB * RB;
+};
+
+template <int DPAD, int FW>
+__host__ __device__ constexpr int smem4(int nstage, int* off_b, int* off_p, int* off_bar) {
+  using C = Cfg4<DPAD>;
+  int o = C::A_STRIDE;
+  *off_b = o;
+  o += nstage * C::B_STRIDE;
+  *off_p = o;
+  o += FW * kPend * 32 * 8;
+  *off_bar = o;
+  o += 8 * (2 * kMaxStage + 2 + 4) + 16;
+  return o + 1024;
+}
+
+template <int DPAD, int FW>
+int pick_stages4() {
+  int a, b, c;
+  for (int ns = kMaxStage; ns >= 2; --ns)
+    if (smem4<DPAD, FW>(ns, &a, &b, &c) <= kSmemMax) return ns;
+  return 0;
+}
+
+struct Seq {
+  int t, end;
+  int mask;
+  bool on;
+  __device__ __forceinline__ void begin(int64_t bt, int S, int R, int c) {
+    on = R > 0;
+    mask = R - 1;
+    t = (int)(bt * c / S);
+    end = (int)(bt * (c + 1) / S);
+    skip();
+  }
+  __device__ __forceinline__ void skip() {
+    if (on && (t & mask) == 0) ++t;
+  }
+  __device__ __forceinline__ bool more() const { return t < end; }
+  __device__ __forceinline__ void next() {
+    ++t;
+    skip();
+  }
+};
+
+__device__ __forceinline__ float min8(const float* v) {
+  return fminf(fminf(fminf(v[0], v[1]), v[2]),
+               fminf(fminf(v[3], v[4]), fminf(fminf(v[5], v[6]), v[7])));
+}
+
+template <int DPAD, int FMT, int DBG, int FW>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
+    k_knn_tc4(const uint8_t* __restrict__ a_img, size_t a_region, size_t a_extra,
+              const uint8_t* __restrict__ b_img, size_t b_region, size_t b_extra, int64_t b_tiles,
+              int64_t n_ref, int64_t qt0, int64_t n_qpairs, int64_t q_begin, int64_t q_end,
+              int self_join, int S, int R, int nstage,
+              const float* __restrict__ tau_v, int tau_lists,
+              uint2* __restrict__ mbuf, int* __restrict__ mcnt, int cap) {
+  using C = Cfg4<DPAD>;
+  constexpr int H = FW / 4;
+  constexpr int BH = kBN / H;
+  extern __shared__ uint8_t smem_raw[];
+  // identical layout in both CTAs: every offset below is valid in the peer too
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  int off_b, off_p, off_bar;
+  smem4<DPAD, FW>(nstage, &off_b, &off_p, &off_bar);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + off_b;
+  const uint32_t s_pend = smem_u32(smem + off_p);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + off_bar);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kMaxStage;
+  uint64_t* a_full = bars + 2 * kMaxStage;
+  uint64_t* a_empty = a_full + 1;
+  uint64_t* t_full = a_empty + 1;   // [2]
+  uint64_t* t_empty = t_full + 2;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nstage; ++i) {
+      mbar_init(&full[i], leader ? 2 : 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(a_full, leader ? 2 : 1);
+    mbar_init(a_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&t_full[i], 1);
+      mbar_init(&t_empty[i], 2 * FW);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc2(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int64_t n_items = n_qpairs * S;
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0) {
+    // -------------------------------------------------------------- producer
+    // (both CTAs: own query tile, own half of each reference tile)
+    int stage = 0;
+    uint32_t phase = 0, aphase = 0;
+    for (int64_t item = cid; item < n_items; item += ncl) {
+      const int64_t qtl = (item % n_qpairs) * 2 + rank;
+      const int c = (int)(item / n_qpairs);
+      Seq ts;
+      ts.begin(b_tiles, S, R, c);
+      int issued = 0;
+      bool a_done = false;
+      auto load_a = [&]() {
+        mbar_wait_cl_backoff(a_empty, aphase ^ 1);
+        aphase ^= 1;
+        if (elect_one()) {
+          mbar_arrive_expect_tx(a_full, C::A_ONE);
+          for (int kb = 0; kb < C::NKB; ++kb)
+            bulk_g2s(sA + kb * kBM * C::RB, a_img + kb * a_region + qtl * (int64_t)kBM * C::RB,
+                     kBM * C::RB, a_full);
+          bulk_g2s(sA + C::A_EXTRA, a_img + a_extra + qtl * (int64_t)kBM * kExtraRB,
+                   kBM * kExtraRB, a_full);
+        }
+        __syncwarp();
+        a_done = true;
+      };
+      for (; ts.more(); ts.next()) {
+        if (!a_done && issued == nstage - 1) load_a();
+        mbar_wait_cl_backoff(&empty[stage], phase ^ 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&full[stage], C::B_BYTES);
+          uint8_t* dst = sB + stage * C::B_STRIDE;
+          const int64_t row0 = (int64_t)ts.t * kBN + rank * kBNH;
+          for (int kb = 0; kb < C::NKB; ++kb)
+            bulk_g2s(dst + kb * kBNH * C::RB, b_img + kb * b_region + row0 * C::RB,
+                     kBNH * C::RB, &full[stage]);
+          bulk_g2s(dst + C::B_EXTRA, b_img + b_extra + row0 * kExtraRB, kBNH * kExtraRB,
+                   &full[stage]);
+        }
+        __syncwarp();
+        ++issued;
+        if (++stage == nstage) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (!a_done) load_a();
+    }
+  } else if (warp == 1 && leader) {
+    // --------------------------------------------- MMA issuer (leader CTA)
+    constexpr uint32_t IDESC = idesc_f16(2 * kBM, kBN, FMT == 1 ? 0u : 1u);
+    constexpr int NK = C::KSTEPS + 1;
+    const uint32_t a_base = smem_u32(sA);
+    const uint32_t b_base = smem_u32(sB);
+    uint64_t adesc[NK], bdesc[NK];
+#pragma unroll
+    for (int ks = 0; ks < C::KSTEPS; ++ks) {
+      const int kb = (ks * 32) / C::RB;
+      const int koff = (ks * 32) % C::RB;
+      adesc[ks] = smem_desc(a_base + kb * kBM * C::RB + koff, C::SBO, C::LAYOUT);
+      bdesc[ks] = smem_desc(b_base + kb * kBNH * C::RB + koff, C::SBO, C::LAYOUT);
+    }
+    adesc[C::KSTEPS] = smem_desc(a_base + C::A_EXTRA, 8 * kExtraRB, 6);
+    bdesc[C::KSTEPS] = smem_desc(b_base + C::B_EXTRA, 8 * kExtraRB, 6);
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, acc_phase = 0, aphase = 0;
+    for (int64_t item = cid; item < n_items; item += ncl) {
+      const int c = (int)(item / n_qpairs);
+      Seq ts;
+      ts.begin(b_tiles, S, R, c);
+      mbar_wait_cl(a_full, aphase);
+      aphase ^= 1;
+      tc_fence_after();
+      for (; ts.more(); ts.next()) {
+        mbar_wait_cl(&full[stage], phase);
+        mbar_wait_cl(&t_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint64_t bst = (uint64_t)((stage * C::B_STRIDE) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < NK; ++ks)
+            tc_mma_f16_2cta(tmem_base + acc * kBN, adesc[ks], bdesc[ks] + bst, IDESC,
+                            ks > 0 ? 1u : 0u);
+          tc_commit_mc(&t_full[acc], 0x3);
+          tc_commit_mc(&empty[stage], 0x3);
+        }
+        __syncwarp();
+        if (++stage == nstage) {
+          stage = 0;
+          phase ^= 1;
+        }
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+      if (elect_one()) tc_commit_mc(a_empty, 0x3);
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    // ---------------------------------- forwarder (CTA 1): copies landed here
+    const uint32_t r_full = mapa_shared(smem_u32(full), 0);
+    const uint32_t r_afull = mapa_shared(smem_u32(a_full), 0);
+    int stage = 0;
+    uint32_t phase = 0, aphase = 0;
+    for (int64_t item = cid; item < n_items; item += ncl) {
+      const int c = (int)(item / n_qpairs);
+      Seq ts;
+      ts.begin(b_tiles, S, R, c);
+      // the producer may issue up to nstage-1 B tiles before the A tile: the
+      // forwarder must not block on A first (the leader needs those B tiles
+      // to finish the previous item, which releases A)
+      int fwd = 0;
+      bool a_fwd = false;
+      for (; ts.more(); ts.next()) {
+        if (!a_fwd && fwd == nstage - 1) {
+          mbar_wait_cl(a_full, aphase);
+          aphase ^= 1;
+          if (lane == 0) mbar_arrive_cluster(r_afull);
+          a_fwd = true;
+        }
+        mbar_wait_cl(&full[stage], phase);
+        if (lane == 0) mbar_arrive_cluster(r_full + stage * 8);
+        __syncwarp();
+        ++fwd;
+        if (++stage == nstage) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (!a_fwd) {
+        mbar_wait_cl(a_full, aphase);
+        aphase ^= 1;
+        if (lane == 0) mbar_arrive_cluster(r_afull);
+      }
+      __syncwarp();
+    }
+  } else {
+    // --------------------------------------------------------- filter warps
+    const int f = warp - 2;
+    const int q = warp & 3;
+    const int h = f >> 2;
+    const int rt = q * 32 + lane;
+    constexpr uint32_t SLOT = 32 * 8;
+    const uint32_t pbase = s_pend + (f * kPend * 32 + lane) * 8;
+    uint32_t pa = pbase;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const uint32_t r_tempty = mapa_shared(smem_u32(t_empty), 0);
+    for (int64_t item = cid; item < n_items; item += ncl) {
+      const int64_t qtl = (item % n_qpairs) * 2 + rank;
+      const int c = (int)(item / n_qpairs);
+      const int64_t row = (qt0 + qtl) * kBM + rt;
+      const bool valid = row >= q_begin && row < q_end;
+      const int64_t r = valid ? row - q_begin : 0;
+      const int self = self_join ? (int)row : -1;
+      const int t_self = self_join ? (int)(((qt0 + qtl) * kBM) / kBN) : -1;
+      const int t_last = (int)((n_ref - 1) / kBN);
+      float tau = -CUDART_INF_F;
+      if (valid) {
+        tau = CUDART_INF_F;
+        for (int l = 0; l < tau_lists; ++l) tau = fminf(tau, tau_v[r * tau_lists + l]);
+      }
+      int* cnt = mcnt + r * H + h;
+      uint2* buf = mbuf + (r * H + h) * (int64_t)cap;
+      auto flush = [&]() {
+        const int n = (int)((pa - pbase) / SLOT);
+        if (n > 0) {
+          const int base = atomicAdd(cnt, n);
+          for (int e = 0; e < n; ++e) {
+            const float2 kv = lds_kv(pbase + e * SLOT);
+            if (base + e < cap)
+              buf[base + e] = make_uint2(__float_as_uint(kv.x), (unsigned)__float_as_int(kv.y));
+          }
+        }
+        pa = pbase;
+      };
+      Seq ts;
+      ts.begin(b_tiles, S, R, c);
+      for (; ts.more(); ts.next()) {
+        mbar_wait_cl(&t_full[acc], acc_phase);
+        tc_fence_after();
+        float v[BH];
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kBN + h * BH;
+        if (!(DBG & 2)) {
+#pragma unroll
+          for (int u = 0; u < BH / 64; ++u)
+            tmem_ld64(taddr + 64 * u, *reinterpret_cast<float(*)[64]>(v + 64 * u));
+          tmem_ld_wait();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(&t_empty[acc]);
+          else mbar_arrive_cluster(r_tempty + acc * 8);
+        }
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        if (DBG & 3) continue;
+        const int t = ts.t;
+        const int j0 = t * kBN + h * BH;
+        if (t == t_self || t == t_last) {
+#pragma unroll
+          for (int e = 0; e < BH; ++e)
+            v[e] = (j0 + e == self || j0 + e >= n_ref) ? CUDART_INF_F : v[e];
+        }
+        float m[BH / 8];
+#pragma unroll
+        for (int g = 0; g < BH / 8; ++g) m[g] = min8(v + 8 * g);
+        const int gbase = j0 >> 3;
+#pragma unroll
+        for (int hh = 0; hh < BH / 64; ++hh) {
+          if (__any_sync(0xffffffffu, pa > pbase + (kPend - 8) * SLOT)) flush();
+#pragma unroll
+          for (int g = 0; g < 8; ++g) {
+            const int gg = hh * 8 + g;
+            if (m[gg] < tau) {
+              sts_kv(pa, m[gg], gbase + gg);
+              pa += SLOT;
+            }
+          }
+        }
+      }
+      flush();
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc2(tmem_base, 512);
+  }
+}
+
+template <int DPAD, int FMT, int DBG, int FW>
+cudaError_t launch4(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
+                    bool self_join, const MainPass& m, int num_sms, cudaStream_t st) {
+  const int nstage = pick_stages4<DPAD, FW>();
+  if (nstage < 3) return cudaErrorInvalidValue;
+  if (m.parts != FW / 4) return cudaErrorInvalidValue;
+  int a, b, c;
+  const int smem = smem4<DPAD, FW>(nstage, &a, &b, &c);
+  auto kern = k_knn_tc4<DPAD, FMT, DBG, FW>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t qt0 = q_begin / kBM;
+  const int64_t qt1 = (q_begin + q_count + kBM - 1) / kBM;
+  const int64_t n_qpairs = (qt1 - qt0 + 1) / 2;
+  const int64_t n_items = n_qpairs * m.S;
+  const int64_t pairs = std::min<int64_t>(num_sms / 2, n_items);
+  if (pairs <= 0) return cudaSuccess;
+  kern<<<(unsigned)(2 * pairs), 64 + 32 * FW, smem, st>>>(
+      reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(), A.extra_offset(),
+      reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
+      B.n_pad / kBN, B.n, qt0, n_qpairs, q_begin, q_begin + q_count, self_join ? 1 : 0, m.S,
+      m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// Measured on B200 (C2 d=32 / C3 d=64 shapes): the pair wins where the MMA is
+// long enough to cover the cross-SM release latency of the accumulators (d=64:
+// pass 1 130 vs 136 ms); at d <= 32 the single-SM kernel is faster (1.05 vs
+// 1.18 ms), so the pair is the default for dpad = 64 only.
+int tc4_fits(int dpad, int parts) {
+  if (parts != 4) return 0;
+  switch (dpad) {
+    case 16: return pick_stages4<16, 16>() >= 3;
+    case 32: return pick_stages4<32, 16>() >= 3;
+    case 64: return pick_stages4<64, 16>() >= 3;
+  }
+  return 0;
+}
+int tc4_preferred(int dpad) { return dpad == 64; }
+
+cudaError_t launch_knn_tc4(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
+                           bool self_join, int fmt, const MainPass& m, int num_sms, int dbg,
+                           cudaStream_t st, int* launches) {
+  *launches += 1;
+#define TOD_TC4_CASE(D)                                                                          \
+  case D:                                                                                       \
+    if (dbg & 3)                                                                                \
+      return fmt == 1 ? launch4<D, 1, 2, 16>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
+                      : launch4<D, 2, 2, 16>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+    return fmt == 1 ? launch4<D, 1, 0, 16>(A, B, q_begin, q_count, self_join, m, num_sms, st)   \
+                    : launch4<D, 2, 0, 16>(A, B, q_begin, q_count, self_join, m, num_sms, st);
+  switch (A.dpad) {
+    TOD_TC4_CASE(16)
+    TOD_TC4_CASE(32)
+    TOD_TC4_CASE(64)
+  }
+#undef TOD_TC4_CASE
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace tod

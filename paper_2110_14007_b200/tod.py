@@ -28,6 +28,7 @@ FORMATS = {"auto": 0, "fp16": 1, "bf16": 2, "fp32": 3}
 F_NO_CERTIFY = 0x1
 F_TIMING = 0x2
 F_PASS1_V1 = 0x10   # force the single-query-tile tensor-core schedule (knn_tc.cu)
+F_MAIN_1SM = 0x20   # run the two-pass main pass on single SMs (knn_tc3.cu), not CTA pairs
 
 
 class TodError(RuntimeError):

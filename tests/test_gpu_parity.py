@@ -4,6 +4,8 @@ contract"): neighbour indices bit-exact (order included); fp32 scores within
 1e-5 relative (they are in fact bit-identical because the re-rank evaluates the
 oracle's own fp64 formula, so the tests demand exact equality and report the
 relative error on failure)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -102,12 +104,19 @@ def test_epilogue_variants_parity(pkg, d, fmt, split, chunks):
     (12_345, 64, 10, "bf16", 3),
     (5_000, 32, 20, "fp16", 3),    # below the two-pass threshold: single pass, 3 chunks
 ])
-def test_two_pass_parity(pkg, n, d, k, fmt, chunks):
-    # sample pass (every 8th tile) + append-only main pass (two-pass selection)
-    # full-table parity at sizes that span the sampling and chunk logic
+@pytest.mark.parametrize("pair", [True, False])
+def test_two_pass_parity(pkg, n, d, k, fmt, chunks, pair):
+    # sample pass (every 8th tile) + append-only main pass (two-pass selection),
+    # main pass on CTA pairs (cta_group::2) or single SMs; full-table parity at
+    # sizes that span the sampling and chunk logic
     X = datagen.gaussian_mixture(n, d, seed=n + 3 * d)
-    with _ctx(pkg, fmt=fmt, chunks=chunks) as ctx:
-        res = ctx.knn(torch.from_numpy(X).cuda(), k)
+    flags = 0 if pair else pkg.F_MAIN_1SM
+    os.environ["TOD_MAIN_PAIR"] = "1" if pair else "0"
+    try:
+        with _ctx(pkg, fmt=fmt, chunks=chunks, flags=flags) as ctx:
+            res = ctx.knn(torch.from_numpy(X).cuda(), k)
+    finally:
+        os.environ.pop("TOD_MAIN_PAIR", None)
     _check_rows(res, X, k, np.arange(n))
     if fmt == "fp16":
         assert res.stats["certified"] >= 0.99 * n, res.stats
