@@ -214,7 +214,7 @@ def run_gpu(args):
     ctx = tod.Context(device=dev, fmt=fmt, flags=tod.F_TIMING, stream=stream.cuda_stream)
     stages = tdist.CudaStages(ctx)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    main_ms, launches, last_stats = [], [], {}
+    main_ms, kern_ms, launches, last_stats = [], [], [], {}
 
     def step():
         if lof:
@@ -255,6 +255,7 @@ def run_gpu(args):
         step()
         evs[i][1].record(stream)
         main_ms.append(last_stats.get("ms_main", 0.0))
+        kern_ms.append(last_stats.get("ms_main_kernel", 0.0))
         launches.append(last_stats.get("kernel_launches", 0) + (2 if lof else 0))
     torch.cuda.synchronize()
     t1 = time.time()
@@ -264,10 +265,11 @@ def run_gpu(args):
     step_ms = np.array([a.elapsed_time(b) for a, b in evs])
     ms = float(step_ms.mean())
     main = float(np.mean(main_ms))
+    kmain = float(np.mean(kern_ms))
     if world > 1:
-        t = torch.tensor([ms, main], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms, main, kmain], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, main = float(t[0]), float(t[1])
+        ms, main, kmain = float(t[0]), float(t[1]), float(t[2])
 
     # ---- e2e: the same step through the C ABI with HOST buffers (pinned),
     # H2D of X and D2H of the scores inside the timed region (rank-local shard).
@@ -309,8 +311,28 @@ def run_gpu(args):
 
     if rank == 0:
         peak_b, peak_s, hbm, peak_src = _peaks()
-        flops = 2.0 * n * n * d / world           # algorithmic contraction flops per launch (per GPU)
-        achieved = flops / (main * 1e-3) / 1e12
+        # Dominant kernel: the tensor-core main pass (k_knn_tc3 single-SM or
+        # k_knn_tc4 CTA pairs), timed with CUDA events around its launch on the
+        # launching stream.  Algorithmic work per (query, reference) pair = 2d
+        # flops of the -2XY^T contraction; the main pass covers
+        # every reference column outside the sample tiles (every 8th
+        # 256-column tile), for the rows of this rank.
+        rows = tdist.shard_rows(n, world, rank)[1]
+        mk = last_stats.get("main_kernel", 0)
+        if mk:
+            bt = (n + 255) // 256
+            samp_cols = sum(min(256, n - 256 * t) for t in range(0, bt, 8))
+            pairs_main = rows * (n - samp_cols)
+            kname = {3: "k_knn_tc3 (single-SM tcgen05 main pass)",
+                     4: "k_knn_tc4 (CTA-pair tcgen05 cta_group::2 main pass)"}[mk]
+            kms = kmain
+        else:
+            pairs_main = rows * n
+            kname = "k_knn_tc (tcgen05 fused distance + top-K')"
+            kms = main
+        flops = 2.0 * pairs_main * d          # algorithmic contraction flops per launch (per GPU)
+        achieved = flops / (kms * 1e-3) / 1e12
+        pass1_tf = 2.0 * rows * n * d / (main * 1e-3) / 1e12
         qps = n / (ms * 1e-3)
         line = {
             "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": world,
@@ -328,11 +350,18 @@ def run_gpu(args):
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_b,
                          "unit": "TFLOP/s", "frac": achieved / peak_b,
                          "traffic": _traffic(args.config),
-                         "kernel": "k_knn_tc (tcgen05 fused distance + top-K')",
-                         "kernel_ms": main, "flops_per_launch": flops,
+                         "kernel": kname, "kernel_ms": kms, "flops_per_launch": flops,
+                         "pass1": {"kernels": "sample k_knn_tc + main" if mk else "k_knn_tc",
+                                   "ms": main, "achieved_tflops": pass1_tf,
+                                   "frac": pass1_tf / peak_b},
                          "peak_source": "%s bf16_tflops (fp16 dense rate = bf16 on B200)" % peak_src},
             "phase_ms": {kk: last_stats.get(kk) for kk in
-                         ("ms_prep", "ms_main", "ms_certify", "ms_fallback", "ms_lof")},
+                         ("ms_prep", "ms_main", "ms_main_kernel", "ms_certify", "ms_fallback",
+                          "ms_lof")},
+            "candidates_per_row": {
+                "staged_groups": last_stats.get("cand_groups", 0) / max(1, rows),
+                "visited_groups": last_stats.get("visited_groups", 0) / max(1, rows),
+                "kept_columns": last_stats.get("cand_columns", 0) / max(1, rows)},
             "certified_rows": last_stats.get("certified"),
             "fallback_rows": last_stats.get("fallback_rows"),
             "e2e": {"value": n / (e2e * 1e-3),

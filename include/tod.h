@@ -103,6 +103,8 @@ typedef struct {
   int64_t cand_groups;     /* 8-column candidate groups kept by pass 1, summed over rows (tensor-core pass) */
   int64_t visited_groups;  /* groups the re-rank expanded to exact fp64 distances, summed over rows */
   int64_t cand_columns;    /* exact distances at or below the per-row bound kept for the final selection */
+  float ms_main_kernel;    /* two-pass mode, TOD_F_TIMING: the main-pass kernel alone (ms_main also has the sample pass) */
+  int32_t main_kernel;     /* main-pass kernel used: 0 = none (single pass), 3 = single-SM, 4 = CTA pairs */
 } tod_stats;
 
 /* Per-neighbour and per-row outputs of the kNN functional operator (P:270,

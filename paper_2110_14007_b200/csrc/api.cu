@@ -59,6 +59,7 @@ struct tod_ctx {
   std::string msg;
   Workspace ws;
   cudaEvent_t ev[8] = {};
+  cudaEvent_t evk[2] = {};  // around the main-pass kernel (two-pass mode)
 };
 
 namespace {
@@ -276,6 +277,8 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
                    int64_t q_count, int d, int k, KnnOutDev out, tod_stats* stats, Timer& tm,
                    int* launches) {
   const bool self = dQ == nullptr;
+  bool main_timed = false;
+  int main_kernel = 0;
   Plan plan;
   TOD_TRY(make_plan(ctx, n, q_count, d, k, &plan));
   cudaStream_t st = ctx->stream;
@@ -390,12 +393,16 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
       TOD_CUDA(cudaMemsetAsync(mp.cnt, 0, (size_t)std::max<int64_t>(q_count, 1) * mp.parts * 4, st));
       const char* pe = getenv("TOD_MAIN_PAIR");  // experiment knob: 1 = force pairs, 0 = never
       const bool pair = pe ? atoi(pe) != 0 : tc4_preferred(plan.dpad) != 0;
+      if (tm.on) cudaEventRecord(ctx->evk[0], st);
+      main_timed = tm.on;
       if (pair && !(ctx->cfg.flags & TOD_F_MAIN_1SM) && tc4_fits(plan.dpad, mp.parts))
         TOD_CUDA(launch_knn_tc4(A, B, self ? q_begin : 0, q_count, self, plan.fmt, mp,
                                 ctx->num_sms, cands.dbg, st, launches));
       else
         TOD_CUDA(launch_knn_tc3(A, B, self ? q_begin : 0, q_count, self, plan.fmt, mp,
                                 ctx->num_sms, cands.dbg, st, launches));
+      main_kernel = (pair && !(ctx->cfg.flags & TOD_F_MAIN_1SM) && tc4_fits(plan.dpad, mp.parts)) ? 4 : 3;
+      if (tm.on) cudaEventRecord(ctx->evk[1], st);
     }
   } else {
     TOD_CUDA(launch_finite_check(dX, n, d, g, st, launches));
@@ -454,6 +461,9 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     stats->dpad = plan.dpad;
     stats->scale = plan.kind == PASS_TC ? h.g.s : 1.0;
     stats->max_abs_err = h.max_err;
+    stats->main_kernel = main_kernel;
+    stats->ms_main_kernel = 0.f;
+    if (main_timed) cudaEventElapsedTime(&stats->ms_main_kernel, ctx->evk[0], ctx->evk[1]);
     stats->cand_groups = (int64_t)h.counters[0];
     stats->visited_groups = (int64_t)h.counters[1];
     stats->cand_columns = (int64_t)h.counters[2];
@@ -603,6 +613,7 @@ tod_status tod_create(const tod_config* cfg, tod_ctx** out) {
     ctx->own_stream = true;
   }
   for (auto& ev : ctx->ev) cudaEventCreate(&ev);
+  for (auto& ev : ctx->evk) cudaEventCreate(&ev);
   *out = ctx;
   return TOD_OK;
 }
@@ -613,6 +624,8 @@ tod_status tod_destroy(tod_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   ctx->ws.release();
   for (auto& ev : ctx->ev)
+    if (ev) cudaEventDestroy(ev);
+  for (auto ev : ctx->evk)
     if (ev) cudaEventDestroy(ev);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
