@@ -18,6 +18,8 @@ Definitions:
      LOF_p = (sum_m lrd_{o_m} sequential) / (k * lrd_p), LOF_p = 1 when
      lrd_p = +inf (reading A6); all fp64, rounded to fp32 at the end.
      Neighbourhoods are the k-exact sets of O2 (reading A5).
+  O5 NWR: {j != i : D64(i,j) <= phi}, phi on the squared distance
+     of Eq. (3), neighbours ascending by j (CSR).
 
 Every function here is pinned by tests/test_oracle.py against hand-derived
 values, exact integer brute force, scipy/sklearn library routines and
@@ -69,6 +71,11 @@ def _load():
         lib.oracle_knn_query.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                          ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]
+        lib.oracle_nwr_rows.restype = ctypes.c_int
+        lib.oracle_nwr_rows.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                        ctypes.c_double, ctypes.c_void_p, ctypes.c_int64,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_int32]
         lib.oracle_num_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -143,6 +150,32 @@ def knn_query(Q, X, k: int, threads: int = 0):
     if rc != 0:
         raise RuntimeError("oracle_knn_query failed")
     return idx, dd
+
+
+def nwr(X, phi: float, rows=None, threads: int = 0):
+    """O5 NWR (§5.3): for each query row i (default: all),
+    the rows j != i with D64(i, j) <= phi, phi a threshold on the SQUARED
+    distance of Eq. (3).  Returns (counts int64 [r], row_ptr int64 [r+1],
+    cols int64 [total]) in CSR form, neighbours ascending by j."""
+    X = _f32(X)
+    n, d = X.shape
+    if rows is None:
+        rows = np.arange(n, dtype=np.int64)
+    rows = np.ascontiguousarray(rows, dtype=np.int64).ravel()
+    counts = np.empty(rows.size, np.int64)
+    lib = _load()
+    if lib.oracle_nwr_rows(X.ctypes.data, n, d, float(phi), rows.ctypes.data, rows.size,
+                           counts.ctypes.data, None, None, int(threads)) != 0:
+        raise RuntimeError("oracle_nwr_rows failed")
+    row_ptr = np.zeros(rows.size + 1, np.int64)
+    np.cumsum(counts, out=row_ptr[1:])
+    cols = np.empty(int(row_ptr[-1]), np.int64)
+    c2 = np.empty_like(counts)
+    if lib.oracle_nwr_rows(X.ctypes.data, n, d, float(phi), rows.ctypes.data, rows.size,
+                           c2.ctypes.data, row_ptr.ctypes.data, cols.ctypes.data,
+                           int(threads)) != 0:
+        raise RuntimeError("oracle_nwr_rows failed")
+    return counts, row_ptr, cols
 
 
 def euclid(d64_sorted) -> np.ndarray:

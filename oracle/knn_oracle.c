@@ -165,3 +165,44 @@ int oracle_knn_query(const float* Q, int64_t nq, const float* X, int64_t n, int3
     }
     return failed ? -1 : 0;
 }
+
+/*
+ * NWR -- neighbours within range (§5.3): "each pairwise
+ * distance in D is compared with phi, and NWR outputs the indices of samples
+ * where D_ij <= phi", D_ij the SQUARED Euclidean distance of Eq. (3), here its
+ * exact definition O1 (oracle_d64).  Self excluded (reading A3).
+ * Pass 1 (cols == NULL): counts_out[r] = |{j != rows[r] : D64 <= phi}|.
+ * Pass 2: the neighbours of each row, ascending j, written at cols + offs[r].
+ */
+int oracle_nwr_rows(const float* X, int64_t n, int32_t d, double phi, const int64_t* rows,
+                    int64_t nrows, int64_t* counts_out, const int64_t* offs, int64_t* cols,
+                    int32_t nthreads) {
+    if (!X || !rows || !counts_out || n < 1 || d < 1 || nrows < 0) return -1;
+    if (cols && !offs) return -1;
+    int failed = 0;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1)
+#endif
+    for (int64_t r = 0; r < nrows; ++r) {
+        const int64_t i = rows[r];
+        if (i < 0 || i >= n) {
+#ifdef _OPENMP
+#pragma omp atomic write
+#endif
+            failed = 1;
+            continue;
+        }
+        const float* xi = X + (size_t)i * d;
+        int64_t c = 0;
+        for (int64_t j = 0; j < n; ++j) {
+            if (j == i) continue;
+            if (oracle_d64(xi, X + (size_t)j * d, d) <= phi) {
+                if (cols) cols[offs[r] + c] = j;
+                ++c;
+            }
+        }
+        counts_out[r] = c;
+    }
+    return failed ? -1 : 0;
+}

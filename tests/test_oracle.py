@@ -255,3 +255,65 @@ def test_c1_oracle_under_one_second():
     oracle.scores(dd)
     oracle.lof_from_knn(idx, dd)
     assert time.perf_counter() - t < 1.0
+
+
+# ------------------------------------------------------------------- O5 NWR
+def _nwr_lists(X, phi, rows=None):
+    counts, ptr, cols = oracle.nwr(X, phi, rows=rows)
+    return [cols[ptr[r]:ptr[r + 1]].tolist() for r in range(counts.size)]
+
+
+def test_nwr_golden_boundary_inclusive(golden_dir):
+    g = _load(golden_dir, "nwr_line.json")
+    X = np.array(g["X"], np.float32)
+    for case in g["cases"]:
+        assert _nwr_lists(X, case["phi"]) == case["neighbours"], case["phi"]
+
+
+def test_nwr_symmetric_and_monotone_in_phi():
+    X = datagen.gaussian_mixture(300, 6, seed=21)
+    D = oracle.cdist64(X[:60])
+    phi = float(np.median(D))
+    lists = _nwr_lists(X[:60], phi)
+    A = np.zeros((60, 60), bool)
+    for i, l in enumerate(lists):
+        A[i, l] = True
+    assert np.array_equal(A, A.T)                  # D64 is bitwise symmetric
+    assert not A.diagonal().any()                  # self excluded
+    small = _nwr_lists(X[:60], phi / 2)
+    assert all(set(s) <= set(b) for s, b in zip(small, lists))
+
+
+def test_nwr_exact_integers_vs_python_ints():
+    X = datagen.lattice(400, 5, seed=7, extent=3)  # massive exact ties
+    Xi = X.astype(np.int64)
+    phi = 6.0
+    want = []
+    for i in range(400):
+        d2 = ((Xi - Xi[i]) ** 2).sum(1)            # exact integers
+        want.append([j for j in range(400) if j != i and d2[j] <= 6])
+    assert _nwr_lists(X, phi) == want
+
+
+def test_nwr_contains_knn_at_kth_distance():
+    X = datagen.gaussian_mixture(500, 8, seed=5)
+    k = 7
+    idx, dd = oracle.knn(X, k)
+    for i in (0, 17, 250, 499):
+        got = _nwr_lists(X, float(dd[i, k - 1]), rows=[i])[0]
+        assert set(idx[i].tolist()) <= set(got) and len(got) >= k
+        below = _nwr_lists(X, float(np.nextafter(dd[i, k - 1], -np.inf)), rows=[i])[0]
+        assert len(below) < k
+
+
+def test_nwr_vs_scipy_away_from_boundary():
+    from scipy.spatial.distance import cdist
+    X = datagen.gaussian_mixture(400, 12, seed=9)
+    D = cdist(X.astype(np.float64), X.astype(np.float64), "sqeuclidean")
+    phi = float(np.quantile(D, 0.05))
+    lists = _nwr_lists(X, phi)
+    for i in range(0, 400, 7):
+        near = np.abs(D[i] - phi) <= 1e-9 * phi     # library rounding differs only here
+        want = set(np.nonzero((D[i] <= phi) & ~near)[0].tolist()) - {i}
+        got = set(lists[i])
+        assert want <= got and got - want <= set(np.nonzero(near)[0].tolist())
