@@ -38,7 +38,12 @@ CONFIGS = {
     "c2": (100_000, 32, 20, True, "auto", "C2: kNN+LOF n=100000 d=32 k=20"),
     "c3": (1_000_000, 64, 10, False, "bf16", "C3: kNN n=1000000 d=64 k=10 bf16 PQ path"),
     "c3f16": (1_000_000, 64, 10, False, "fp16", "C3 shape, fp16 PQ path"),
+    # NEXT-2: NWR on the C2-shaped data; phi = 12 on the squared
+    # distance (86 % of rows have no neighbour, mean 39, max ~1900: the paper's
+    # "preset distance threshold (usually a small number)")
+    "nwr": (100_000, 32, 0, False, "fp16", "NWR (neighbours within range) n=100000 d=32 phi=12"),
 }
+NWR_PHI = 12.0
 METRIC = "kNN/LOF queries/sec & dist-evals/sec at 1/2/4/8 B200; % of distance roofline"
 
 
@@ -190,6 +195,80 @@ def _traffic(cfg_name):
         with open(p) as f:
             return json.load(f).get(cfg_name)
     return None
+
+
+def run_gpu_nwr(args):
+    """NWR leg (tod_nwr): one step = counts + CSR neighbour lists of all rows."""
+    import torch
+    import datagen
+    import paper_2110_14007_b200 as tod
+    n, d, _, _, fmt, desc = CONFIGS[args.config]
+    X = datagen.gaussian_mixture(n, d, seed=0)
+    Xd = torch.from_numpy(X).cuda()
+    stream = torch.cuda.current_stream()
+    ctx = tod.Context(device=torch.cuda.current_device(), fmt=fmt, flags=tod.F_TIMING,
+                      stream=stream.cuda_stream)
+    c, p, _, st = ctx.nwr(Xd, NWR_PHI, lists=False)
+    cap = int(int(p[-1]) * 1.1) + 1024
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    for _ in range(args.warmup):
+        ctx.nwr(Xd, NWR_PHI, capacity=cap)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(torch.cuda.current_device())
+    sampler.start()
+    time.sleep(0.15)
+    times, kms, stats = [], [], {}
+    t0 = time.time()
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        counts, ptr, cols, stats = ctx.nwr(Xd, NWR_PHI, capacity=cap)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+        kms.append(stats["ms_main_kernel"])
+    t1 = time.time()
+    clocks = sampler.stop(t0, t1)
+    ms, km = float(np.mean(times)), float(np.mean(kms))
+    # e2e: host buffers through the C ABI (H2D of X, D2H of counts/row_ptr/cols)
+    Xh = torch.from_numpy(X).pin_memory()
+    e2e = []
+    for i in range(min(args.steps, 10)):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ch, ph, lh, _ = ctx.nwr(Xh, NWR_PHI, capacity=cap)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e.append(e0.elapsed_time(e1))
+    total = int(ptr[-1])
+    peak_b, _, _, peak_src = _peaks()
+    flops = 2.0 * n * n * d
+    ach = flops / (km * 1e-3) / 1e12
+    line = {"metric": "NWR queries/sec (neighbours within range, exact)", "value": n / (ms * 1e-3),
+            "unit": "queries/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f16 operands/f32 accumulate (main pass), f64 verification",
+            "data": "synthetic (Gaussian mixture + uniform outliers, seed 0)",
+            "config": {"workload": desc, "n": n, "d": d, "phi": NWR_PHI, "pairs": total,
+                       "l2": "flushed between steps (256 MiB write)"},
+            "dist_evals_per_s": n * n / (ms * 1e-3),
+            "roofline": {"bound": "tensor", "achieved": ach, "peak": peak_b, "unit": "TFLOP/s",
+                         "frac": ach / peak_b, "traffic": None,
+                         "kernel": {3: "k_knn_tc3", 4: "k_knn_tc4"}.get(stats.get("main_kernel"), "?"),
+                         "kernel_ms": km, "flops_per_launch": flops,
+                         "peak_source": "%s bf16_tflops" % peak_src},
+            "fallback_rows": stats.get("fallback_rows"),
+            "e2e": {"value": n / (float(np.mean(e2e)) * 1e-3), "unit": "queries/s",
+                    "h2d_bytes_per_step": n * d * 4,
+                    "d2h_bytes_per_step": n * 8 + (n + 1) * 8 + total * 4},
+            "gpu_launches": int(stats.get("kernel_launches", 0)) * args.steps,
+            "clocks": clocks}
+    print(json.dumps(line), flush=True)
+    ctx.close()
+    return 0
 
 
 def run_gpu(args):
@@ -395,6 +474,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "nwr":
+        return run_gpu_nwr(args)
     return run_gpu(args)
 
 

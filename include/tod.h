@@ -196,6 +196,32 @@ tod_status tod_lof_finish(tod_ctx* ctx, int64_t n, int32_t k, int64_t q_begin, i
  * X [n x d], nothing excluded, 1 <= k <= n.  Same ordering and outputs as
  * tod_knn (indices refer to rows of X).
  */
+/*
+ * tod_nwr — neighbours within range (NWR, a functional operator of the paper's
+ * programming model; §5.3, the paper's provable-quantization
+ * case study).  For every query row i in [q_begin, q_begin + q_count) of X
+ * (self-join), the rows j != i with  D_ij <= phi, where D_ij is the SQUARED
+ * Euclidean distance of Eq. (3) evaluated exactly as the oracle's O1
+ * (sequential fp64, no FMA) -- the output equals the fp64 brute force exactly.
+ * Method (§5.1): fp16 tensor-core evaluation (the append-only main
+ * pass) with a per-row rigorous bound selects candidate 8-column groups; every
+ * candidate pair is decided in fp64; rows whose candidate buffers overflow are
+ * recomputed by fp64 brute force ("recalculate on the subset").
+ *   phi        finite threshold on the squared distance (phi < 0 => no pairs).
+ *   counts     [q_count] int64 neighbour counts (nullable).
+ *   row_ptr    [q_count + 1] int64 CSR offsets, row_ptr[0] = 0 (nullable).
+ *   cols       [capacity] int32 neighbour indices, ascending within each row
+ *              (nullable: call once without to size it, then again).
+ *   total      (required) total number of pairs.
+ * Pointers may be host or device (host buffers are staged).  Errors: as
+ * tod_knn; TOD_E_RANGE if cols != NULL and capacity < *total (counts, row_ptr
+ * and *total are still written); TOD_E_UNSUPPORTED for d > 64 or the FP32
+ * format.
+ */
+tod_status tod_nwr(tod_ctx* ctx, const float* X, int64_t n, int32_t d, double phi,
+                   int64_t q_begin, int64_t q_count, int64_t* counts, int64_t* row_ptr,
+                   int32_t* cols, int64_t capacity, int64_t* total, tod_stats* stats);
+
 tod_status tod_knn_query(tod_ctx* ctx, const float* Q, int64_t nq, const float* X, int64_t n,
                          int32_t d, int32_t k, const tod_knn_out* out, tod_stats* stats);
 

@@ -44,7 +44,7 @@ struct Workspace {
 enum BufId {
   B_X = 0, B_Q, B_IMG_B, B_A2_B, B_E_B, B_IMG_A, B_A2_A, B_E_A, B_MU, B_PART,
   B_G, B_CIDX, B_CV, B_FAIL, B_SMALL, B_IDX, B_DIST, B_DIST64, B_KTH, B_MEAN, B_KD64,
-  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT, B_FAILUB, B_NBUF
+  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT, B_FAILUB, B_NWRTAU, B_NWRCNT, B_NWRPTR, B_NWRCOLS, B_SCAN, B_NBUF
 };
 static_assert(B_NBUF <= 48, "Workspace::bufs too small");
 
@@ -271,6 +271,63 @@ struct SmallDev {
   unsigned long long counters[3];  // re-rank telemetry: staged groups, visited groups, kept columns
 };
 
+// Input quantization (a1) for the tensor-core passes: column mean, power-of-two
+// scale, reference image B over all n rows and query image A over the 128-row
+// query tiles covering [q_begin, q_begin+q_count) (self-join) or over Q.
+tod_status prep_tc(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, int64_t q_begin,
+                   int64_t q_count, int d, int fmt, int dpad, PrepGlobals* g, Image* Aout,
+                   Image* Bout, CertParams* cp, int* launches) {
+  cudaStream_t st = ctx->stream;
+  const bool self = dQ == nullptr;
+  void* p;
+  const int64_t n_pad = (n + 255) / 256 * 256;
+  // query image rows: the 128-row query tiles covering [q_begin, q_begin+q_count)
+  const int64_t a_row0 = self ? (q_begin / 128) * 128 : 0;
+  const int64_t a_rows = self ? std::min<int64_t>(n, (q_begin + q_count + 127) / 128 * 128) - a_row0
+                              : q_count;
+  const int64_t a_pad = (a_rows + 255) / 256 * 256;
+  const int rb = std::min(128, dpad * 2);
+  auto make_img = [&](int id_img, int id_a2, int id_e, int64_t rows, int64_t rows_pad,
+                      Image* img) -> tod_status {
+    void* q;
+    img->n = rows;
+    img->n_pad = rows_pad;
+    img->dpad = dpad;
+    img->rb = rb;
+    img->nkb = dpad * 2 / rb;
+    img->layout = rb == 128 ? 2 : (rb == 64 ? 4 : 6);
+    TOD_TRY(ensure(ctx, id_img, img->total_bytes(), &q));
+    img->data = static_cast<uint16_t*>(q);
+    TOD_TRY(ensure(ctx, id_a2, (size_t)std::max<int64_t>(rows, 1) * 8, &q));
+    img->a2 = static_cast<double*>(q);
+    TOD_TRY(ensure(ctx, id_e, (size_t)std::max<int64_t>(rows, 1) * 8, &q));
+    img->e = static_cast<double*>(q);
+    return TOD_OK;
+  };
+  Image& B = *Bout;
+  Image& A = *Aout;
+  TOD_TRY(make_img(B_IMG_B, B_A2_B, B_E_B, n, n_pad, &B));
+  TOD_TRY(make_img(B_IMG_A, B_A2_A, B_E_A, a_rows, a_pad, &A));
+  const int stat_blocks = (int)((n + 1023) / 1024);
+  TOD_TRY(ensure(ctx, B_MU, (size_t)d * 8, &p));
+  double* mu = static_cast<double*>(p);
+  TOD_TRY(ensure(ctx, B_PART, (size_t)stat_blocks * d * 8, &p));
+  double* part = static_cast<double*>(p);
+  TOD_CUDA(launch_prep_stats(dX, n, d, mu, part, stat_blocks, g, st, launches));
+  TOD_CUDA(launch_prep_absmax(dX, n, d, mu, g, st, launches));
+  if (!self) {
+    TOD_CUDA(launch_finite_check(dQ, q_count, d, g, st, launches));
+    TOD_CUDA(launch_prep_absmax(dQ, q_count, d, mu, g, st, launches));
+  }
+  TOD_CUDA(launch_prep_scale(g, fmt, dpad, st, launches));
+  TOD_CUDA(launch_prep_quant(dX, n, d, mu, g, fmt, B, 0, st, launches));
+  const float* qsrc = self ? dX + a_row0 * d : dQ;
+  TOD_CUDA(launch_prep_quant(qsrc, a_rows, d, mu, g, fmt, A, 1, st, launches));
+  cp->qa2 = A.a2 + (self ? q_begin - a_row0 : 0);
+  cp->qe = A.e + (self ? q_begin - a_row0 : 0);
+  return TOD_OK;
+}
+
 // Core: all pointers device.  Q == nullptr => self-join over X, rows
 // [q_begin, q_begin+q_count).  Else queries Q[0..q_count) against X.
 tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, int64_t q_begin,
@@ -332,50 +389,9 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
 
   tm.mark();  // 1: prep start
   if (plan.kind == PASS_TC) {
-    const int64_t n_pad = (n + 255) / 256 * 256;
-    // query image rows: the 128-row query tiles covering [q_begin, q_begin+q_count)
-    const int64_t a_row0 = self ? (q_begin / 128) * 128 : 0;
-    const int64_t a_rows = self ? std::min<int64_t>(n, (q_begin + q_count + 127) / 128 * 128) - a_row0
-                                : q_count;
-    const int64_t a_pad = (a_rows + 255) / 256 * 256;
-    const int rb = std::min(128, plan.dpad * 2);
-    auto make_img = [&](int id_img, int id_a2, int id_e, int64_t rows, int64_t rows_pad,
-                        Image* img) -> tod_status {
-      void* q;
-      img->n = rows;
-      img->n_pad = rows_pad;
-      img->dpad = plan.dpad;
-      img->rb = rb;
-      img->nkb = plan.dpad * 2 / rb;
-      img->layout = rb == 128 ? 2 : (rb == 64 ? 4 : 6);
-      TOD_TRY(ensure(ctx, id_img, img->total_bytes(), &q));
-      img->data = static_cast<uint16_t*>(q);
-      TOD_TRY(ensure(ctx, id_a2, (size_t)std::max<int64_t>(rows, 1) * 8, &q));
-      img->a2 = static_cast<double*>(q);
-      TOD_TRY(ensure(ctx, id_e, (size_t)std::max<int64_t>(rows, 1) * 8, &q));
-      img->e = static_cast<double*>(q);
-      return TOD_OK;
-    };
     Image B, A;
-    TOD_TRY(make_img(B_IMG_B, B_A2_B, B_E_B, n, n_pad, &B));
-    TOD_TRY(make_img(B_IMG_A, B_A2_A, B_E_A, a_rows, a_pad, &A));
-    const int stat_blocks = (int)((n + 1023) / 1024);
-    TOD_TRY(ensure(ctx, B_MU, (size_t)d * 8, &p));
-    double* mu = static_cast<double*>(p);
-    TOD_TRY(ensure(ctx, B_PART, (size_t)stat_blocks * d * 8, &p));
-    double* part = static_cast<double*>(p);
-    TOD_CUDA(launch_prep_stats(dX, n, d, mu, part, stat_blocks, g, st, launches));
-    TOD_CUDA(launch_prep_absmax(dX, n, d, mu, g, st, launches));
-    if (!self) {
-      TOD_CUDA(launch_finite_check(dQ, q_count, d, g, st, launches));
-      TOD_CUDA(launch_prep_absmax(dQ, q_count, d, mu, g, st, launches));
-    }
-    TOD_CUDA(launch_prep_scale(g, plan.fmt, plan.dpad, st, launches));
-    TOD_CUDA(launch_prep_quant(dX, n, d, mu, g, plan.fmt, B, 0, st, launches));
-    const float* qsrc = self ? dX + a_row0 * d : dQ;
-    TOD_CUDA(launch_prep_quant(qsrc, a_rows, d, mu, g, plan.fmt, A, 1, st, launches));
-    cp.qa2 = A.a2 + (self ? q_begin - a_row0 : 0);
-    cp.qe = A.e + (self ? q_begin - a_row0 : 0);
+    TOD_TRY(prep_tc(ctx, dX, n, dQ, q_begin, q_count, d, plan.fmt, plan.dpad, g, &A, &B, &cp,
+                    launches));
     tm.mark();  // 2: main start
     TOD_CUDA(launch_knn_tc(A, B, self ? q_begin : 0, q_count, self, plan.fmt, cands,
                            ctx->num_sms, st, launches));
@@ -467,6 +483,100 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     stats->cand_groups = (int64_t)h.counters[0];
     stats->visited_groups = (int64_t)h.counters[1];
     stats->cand_columns = (int64_t)h.counters[2];
+  }
+  return TOD_OK;
+}
+
+// NWR core (all pointers device): counts, then (cols != nullptr) the CSR
+// neighbour lists.  Returns the total pair count in *total.
+tod_status run_nwr(tod_ctx* ctx, const float* dX, int64_t n, int d, double phi, int64_t q_begin,
+                   int64_t q_count, int64_t* dcounts, int64_t* drow_ptr, int32_t* dcols,
+                   int64_t capacity, int64_t* total, tod_stats* stats, Timer& tm,
+                   int* launches) {
+  cudaStream_t st = ctx->stream;
+  int fmt = ctx->cfg.format;
+  if (fmt == TOD_FMT_AUTO) fmt = TOD_FMT_FP16;
+  if (fmt != TOD_FMT_FP16 && fmt != TOD_FMT_BF16)
+    return fail(ctx, TOD_E_UNSUPPORTED, "NWR runs on the tensor-core pass (fp16/bf16 format)");
+  if (d > 64) return fail(ctx, TOD_E_UNSUPPORTED, "NWR supports d <= 64 in this build (d=%d)", d);
+  const int dpad = d <= 16 ? 16 : d <= 32 ? 32 : 64;
+  void* p;
+  TOD_TRY(ensure(ctx, B_SMALL, sizeof(SmallDev), &p));
+  SmallDev* small = static_cast<SmallDev*>(p);
+  TOD_CUDA(cudaMemsetAsync(small, 0, sizeof(SmallDev), st));
+  CertParams cp{};
+  cp.kind = PASS_TC;
+  cp.d = d;
+  cp.dpad = dpad;
+  cp.s = 1.0;
+  cp.g = &small->g;
+  tm.mark();  // 1: prep
+  Image A, B;
+  TOD_TRY(prep_tc(ctx, dX, n, nullptr, q_begin, q_count, d, fmt, dpad, &small->g, &A, &B, &cp,
+                  launches));
+  TOD_TRY(ensure(ctx, B_NWRTAU, (size_t)std::max<int64_t>(q_count, 1) * 4, &p));
+  float* tau = static_cast<float*>(p);
+  TOD_CUDA(launch_nwr_tau(q_count, phi, cp, tau, st, launches));
+  tm.mark();  // 2: main pass
+  MainPass mp;
+  const double img_bytes = (double)B.n_pad * (dpad + 16) * 2;
+  mp.S = std::max(1, (int)std::ceil(img_bytes / (48.0 * 1024 * 1024)));
+  mp.R = 0;
+  mp.tau_v = tau;
+  mp.tau_lists = 1;
+  mp.parts = tc3_parts(dpad);
+  // candidate slots per (row, part): as many as a 4 GB budget allows, 128..1024
+  // (rows beyond it are answered by the fp64 brute-force tier)
+  mp.cap = 1024;
+  while (mp.cap > 128 && (double)q_count * mp.parts * mp.cap * 8 > 4.0e9) mp.cap >>= 1;
+  TOD_TRY(ensure(ctx, B_MBUF, (size_t)std::max<int64_t>(q_count, 1) * mp.parts * mp.cap * 8, &p));
+  mp.buf = static_cast<uint2*>(p);
+  TOD_TRY(ensure(ctx, B_MCNT, (size_t)std::max<int64_t>(q_count, 1) * mp.parts * 4, &p));
+  mp.cnt = static_cast<int*>(p);
+  TOD_CUDA(cudaMemsetAsync(mp.cnt, 0, (size_t)std::max<int64_t>(q_count, 1) * mp.parts * 4, st));
+  const bool pair = tc4_preferred(dpad) && !(ctx->cfg.flags & TOD_F_MAIN_1SM) &&
+                    tc4_fits(dpad, mp.parts);
+  if (tm.on) cudaEventRecord(ctx->evk[0], st);
+  if (pair)
+    TOD_CUDA(launch_knn_tc4(A, B, q_begin, q_count, true, fmt, mp, ctx->num_sms, 0, st, launches));
+  else
+    TOD_CUDA(launch_knn_tc3(A, B, q_begin, q_count, true, fmt, mp, ctx->num_sms, 0, st, launches));
+  if (tm.on) cudaEventRecord(ctx->evk[1], st);
+  tm.mark();  // 3: verification
+  TOD_TRY(ensure(ctx, B_FAIL, (size_t)std::max<int64_t>(q_count, 1) * 4, &p));
+  int32_t* ovf_rows = static_cast<int32_t*>(p);
+  TOD_CUDA(launch_nwr_verify(nullptr, q_begin, q_count, dX, n, d, true, phi, mp, 0, dcounts,
+                             nullptr, nullptr, ovf_rows, &small->fail_count, st, launches));
+  SmallDev h{};
+  TOD_CUDA(cudaMemcpyAsync(&h, small, sizeof(SmallDev), cudaMemcpyDeviceToHost, st));
+  TOD_CUDA(cudaStreamSynchronize(st));
+  if (h.g.nonfinite) return fail(ctx, TOD_E_NONFINITE, "X contains NaN or Inf");
+  const int novf = h.fail_count;
+  TOD_CUDA(launch_nwr_brute(nullptr, q_begin, dX, n, d, true, phi, ovf_rows, novf, 0, dcounts,
+                            nullptr, nullptr, st, launches));
+  TOD_TRY(ensure(ctx, B_SCAN, scan_workspace(q_count), &p));
+  int64_t* part = static_cast<int64_t*>(p);
+  TOD_CUDA(launch_scan(dcounts, q_count, drow_ptr, part, st, launches));
+  TOD_CUDA(cudaMemcpyAsync(total, drow_ptr + q_count, 8, cudaMemcpyDeviceToHost, st));
+  TOD_CUDA(cudaStreamSynchronize(st));
+  tm.mark();  // 4: lists
+  if (dcols && *total <= capacity) {
+    TOD_CUDA(launch_nwr_verify(nullptr, q_begin, q_count, dX, n, d, true, phi, mp, 1, dcounts,
+                               drow_ptr, dcols, ovf_rows, &small->fail_count, st, launches));
+    TOD_CUDA(launch_nwr_brute(nullptr, q_begin, dX, n, d, true, phi, ovf_rows, novf, 1, dcounts,
+                              drow_ptr, dcols, st, launches));
+  }
+  tm.mark();  // 5
+  if (stats) {
+    stats->rows = q_count;
+    stats->certified = q_count - novf;
+    stats->fallback_rows = novf;
+    stats->format = fmt;
+    stats->dpad = dpad;
+    stats->scale = h.g.s;
+    stats->main_kernel = pair ? 4 : 3;
+    stats->chunks = mp.S;
+    if (tm.on) cudaEventElapsedTime(&stats->ms_main_kernel, ctx->evk[0], ctx->evk[1]);
   }
   return TOD_OK;
 }
@@ -677,6 +787,63 @@ tod_status tod_knn_query(tod_ctx* ctx, const float* Q, int64_t nq, const float* 
   tm.mark();
   TOD_CUDA(cudaStreamSynchronize(ctx->stream));
   finish_stats(stats, tm, launches, 0);
+  ctx->msg.clear();
+  return TOD_OK;
+}
+
+tod_status tod_nwr(tod_ctx* ctx, const float* X, int64_t n, int32_t d, double phi,
+                   int64_t q_begin, int64_t q_count, int64_t* counts, int64_t* row_ptr,
+                   int32_t* cols, int64_t capacity, int64_t* total, tod_stats* stats) {
+  TOD_TRY(validate_common(ctx, n, d, 1));
+  if (!(phi == phi) || phi == INFINITY) return fail(ctx, TOD_E_ARG, "phi must be finite");
+  if (q_begin < 0 || q_count < 0 || q_begin + q_count > n)
+    return fail(ctx, TOD_E_RANGE, "query rows [%lld, %lld) outside [0, %lld)", (long long)q_begin,
+                (long long)(q_begin + q_count), (long long)n);
+  if (!total) return fail(ctx, TOD_E_ARG, "total must not be NULL");
+  if (cols && capacity < 0) return fail(ctx, TOD_E_ARG, "negative capacity");
+  TOD_CUDA(cudaSetDevice(ctx->device));
+  if (stats) memset(stats, 0, sizeof *stats);
+  *total = 0;
+  Timer tm{ctx, (ctx->cfg.flags & TOD_F_TIMING) != 0};
+  int launches = 0;
+  tm.mark();  // 0
+  const float* dX;
+  TOD_TRY(stage_input(ctx, X, (size_t)n * d, B_X, &dX));
+  int64_t *dcounts, *dptr;
+  int32_t* dcols;
+  bool st_c, st_p, st_l;
+  // counts and row_ptr are always computed (device temporaries when not requested)
+  void* p;
+  TOD_TRY(dev_view(ctx, counts, (size_t)q_count, B_NWRCNT, &dcounts, &st_c));
+  if (!dcounts) {
+    TOD_TRY(ensure(ctx, B_NWRCNT, (size_t)std::max<int64_t>(q_count, 1) * 8, &p));
+    dcounts = static_cast<int64_t*>(p);
+  }
+  TOD_TRY(dev_view(ctx, row_ptr, (size_t)q_count + 1, B_NWRPTR, &dptr, &st_p));
+  if (!dptr) {
+    TOD_TRY(ensure(ctx, B_NWRPTR, (size_t)(q_count + 1) * 8, &p));
+    dptr = static_cast<int64_t*>(p);
+  }
+  TOD_TRY(dev_view(ctx, cols, (size_t)std::max<int64_t>(capacity, 1), B_NWRCOLS, &dcols, &st_l));
+  if (q_count > 0) {
+    TOD_TRY(run_nwr(ctx, dX, n, d, phi, q_begin, q_count, dcounts, dptr, dcols, capacity, total,
+                    stats, tm, &launches));
+  } else {
+    TOD_CUDA(cudaMemsetAsync(dptr, 0, 8, ctx->stream));
+  }
+  cudaStream_t st = ctx->stream;
+  if (st_c) TOD_CUDA(cudaMemcpyAsync(counts, dcounts, (size_t)q_count * 8, cudaMemcpyDeviceToHost, st));
+  if (st_p)
+    TOD_CUDA(cudaMemcpyAsync(row_ptr, dptr, (size_t)(q_count + 1) * 8, cudaMemcpyDeviceToHost, st));
+  const bool fits = *total <= capacity;
+  if (st_l && fits && *total > 0)
+    TOD_CUDA(cudaMemcpyAsync(cols, dcols, (size_t)*total * 4, cudaMemcpyDeviceToHost, st));
+  tm.mark();
+  TOD_CUDA(cudaStreamSynchronize(st));
+  finish_stats(stats, tm, launches, 0);
+  if (cols && !fits)
+    return fail(ctx, TOD_E_RANGE, "cols capacity %lld < %lld neighbour pairs (counts, row_ptr and "
+                "total are valid)", (long long)capacity, (long long)*total);
   ctx->msg.clear();
   return TOD_OK;
 }

@@ -140,6 +140,22 @@ cudaError_t launch_fallback(const float* Q, int64_t q_begin, const float* X, int
                             const double* fail_ub, int nfail,
                             KnnOutDev out, void* ws, int num_sms, cudaStream_t st, int* launches);
 
+// ---- rerank.cu: NWR (neighbours within range, §5.3)
+cudaError_t launch_nwr_tau(int64_t q_count, double phi, CertParams cp, float* tau,
+                           cudaStream_t st, int* launches);
+cudaError_t launch_nwr_verify(const float* Q, int64_t q_begin, int64_t q_count, const float* X,
+                              int64_t n, int d, bool self_join, double phi, const MainPass& mp,
+                              int mode, int64_t* counts, const int64_t* row_ptr, int32_t* cols,
+                              int32_t* ovf_rows, int32_t* ovf_count, cudaStream_t st,
+                              int* launches);
+cudaError_t launch_nwr_brute(const float* Q, int64_t q_begin, const float* X, int64_t n, int d,
+                             bool self_join, double phi, const int32_t* rows, int nrows, int mode,
+                             int64_t* counts, const int64_t* row_ptr, int32_t* cols,
+                             cudaStream_t st, int* launches);
+size_t scan_workspace(int64_t q);
+cudaError_t launch_scan(const int64_t* counts, int64_t q, int64_t* row_ptr, void* ws,
+                        cudaStream_t st, int* launches);
+
 // ---- lof.cu
 cudaError_t launch_lof_lrd(int64_t q_count, int k, const int64_t* idx, const double* dist64,
                            const double* kdist64_all, double* lrd64_out, cudaStream_t st,

@@ -617,6 +617,206 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
 }
 
 
+// ===================================================================== NWR
+// Neighbours within range (§5.3): {j != i : D_ij <= phi},
+// D_ij the squared distance of Eq. (3) evaluated as the oracle's O1.  Provable
+// quantization applied as the paper prescribes: the fp16
+// tensor-core main pass decides every pair it can, the rest is verified in fp64.
+//  * tau_i = key_cut_from_ub(phi): every column with D64 <= phi has its pass-1
+//    key w~ <= tau_i (lower-bound inversion, all roundings upward), so the
+//    append-only main pass with threshold tau_i keeps a superset of row i's
+//    neighbours (a group is kept when its minimum is below tau_i).
+//  * verify: the kept groups, sorted by index, expanded and decided with O1
+//    (exactly the oracle's comparison), neighbours written ascending by j.
+//  * rows whose candidate buffers overflowed are answered by fp64 brute force.
+
+__global__ void k_nwr_tau(int64_t q_count, double phi, CertParams cp, float* __restrict__ tau) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= q_count) return;
+  const float cut = key_cut_from_ub(cp, r, phi);
+  tau[r] = nextafterf(cut, CUDART_INF_F);  // the filter keeps groups with min < tau
+}
+
+constexpr int kNwrWarps = 4;
+constexpr int kNwrMaxG = 4096;   // staged groups per row (4 parts x up to 1024)
+
+// mode 0: counts[r] (or -1 if the row's buffers overflowed: brute-force later);
+// mode 1: neighbours written at cols + row_ptr[r], ascending.
+template <int DT>
+__global__ void __launch_bounds__(kNwrWarps * 32)
+    k_nwr_verify(const float* __restrict__ Q, int64_t q_begin, int64_t q_count,
+                 const float* __restrict__ X, int64_t n, int d, int self_join, double phi,
+                 const uint2* __restrict__ mbuf, const int* __restrict__ mcnt, int mcap,
+                 int mparts, int mode, int64_t* __restrict__ counts,
+                 const int64_t* __restrict__ row_ptr, int32_t* __restrict__ cols,
+                 int32_t* __restrict__ ovf_rows, int32_t* __restrict__ ovf_count) {
+  extern __shared__ double s_xq[];  // [warps][d] query rows, then [warps][maxg] groups
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * kNwrWarps + w;
+  if (r >= q_count) return;
+  const int64_t gi = q_begin + r;
+  const float* xi = self_join ? X + gi * d : Q + r * d;
+  double* xq = s_xq + (size_t)w * d;
+  for (int c = lane; c < d; c += 32) xq[c] = (double)xi[c];
+  const int maxg = mparts * mcap;
+  int* g = reinterpret_cast<int*>(s_xq + (size_t)kNwrWarps * d) + (size_t)w * maxg;
+  int G = 0;
+  bool over = false;
+  for (int h = 0; h < mparts; ++h) {
+    const int c = mcnt[r * mparts + h];
+    over |= c > mcap;
+    const int m = c < mcap ? c : mcap;
+    const uint2* src = mbuf + (r * mparts + h) * (int64_t)mcap;
+    for (int e = lane; e < m; e += 32) g[G + e] = (int)src[e].y;
+    G += m;
+  }
+  if (over) {
+    if (mode == 0 && lane == 0) {
+      counts[r] = -1;
+      ovf_rows[atomicAdd(ovf_count, 1)] = (int32_t)r;
+    }
+    return;
+  }
+  // mode 1: sort the group indices ascending (bitonic over the next power of
+  // two) so the neighbours come out ascending; counting needs no order
+  int P = 1;
+  while (mode == 1 && P < G) P <<= 1;
+  for (int e = G + lane; e < P; e += 32) g[e] = INT32_MAX;
+  __syncwarp();
+  for (int kk = 2; mode == 1 && kk <= P; kk <<= 1)
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int e = lane; e < P; e += 32) {
+        const int l = e ^ j;
+        if (l > e) {
+          const int a = g[e], b = g[l];
+          const bool up = (e & kk) == 0;
+          if (up ? a > b : a < b) {
+            g[e] = b;
+            g[l] = a;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  int64_t cnt = 0;
+  int64_t base = mode == 1 ? row_ptr[r] : 0;
+  for (int b0 = 0; b0 < G; b0 += 4) {
+    const int gs = b0 + (lane >> 3);
+    const int grp = gs < G ? g[gs] : -1;
+    const int64_t j = (int64_t)grp * 8 + (lane & 7);
+    bool keep = false;
+    if (grp >= 0 && j < n && !(self_join && j == gi)) {
+      const float* xj = X + j * d;
+      double acc;
+      if constexpr (DT > 0) {
+        acc = d64_fixed<DT>(xq, xj);
+      } else {
+        acc = 0.0;  // O1: ascending c, no FMA
+        for (int c = 0; c < d; ++c) {
+          const double t = __dsub_rn(xq[c], (double)__ldg(xj + c));
+          acc = __dadd_rn(acc, __dmul_rn(t, t));
+        }
+      }
+      keep = acc <= phi;
+    }
+    const unsigned km = __ballot_sync(0xffffffffu, keep);
+    if (mode == 1 && keep) cols[base + cnt + __popc(km & ((1u << lane) - 1u))] = (int32_t)j;
+    cnt += __popc(km);
+  }
+  if (mode == 0 && lane == 0) counts[r] = cnt;
+}
+
+// fp64 brute force for rows whose candidate buffers overflowed; one block per
+// row, columns in ascending order (block prefix sums keep the order in mode 1).
+__global__ void __launch_bounds__(256)
+    k_nwr_brute(const float* __restrict__ Q, int64_t q_begin, const float* __restrict__ X,
+                int64_t n, int d, int self_join, double phi, const int32_t* __restrict__ rows,
+                int mode, int64_t* __restrict__ counts, const int64_t* __restrict__ row_ptr,
+                int32_t* __restrict__ cols) {
+  __shared__ int s_w[8];
+  __shared__ int64_t s_base;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t r = rows[blockIdx.x];
+  const int64_t gi = q_begin + r;
+  const float* xi = self_join ? X + gi * d : Q + r * d;
+  if (t == 0) s_base = mode == 1 ? row_ptr[r] : 0;
+  __syncthreads();
+  for (int64_t j0 = 0; j0 < n; j0 += 256) {
+    const int64_t j = j0 + t;
+    bool keep = false;
+    if (j < n && !(self_join && j == gi)) {
+      const float* xj = X + j * d;
+      double acc = 0.0;
+      for (int c = 0; c < d; ++c) {
+        const double tt = __dsub_rn((double)xi[c], (double)__ldg(xj + c));
+        acc = __dadd_rn(acc, __dmul_rn(tt, tt));
+      }
+      keep = acc <= phi;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) s_w[w] = __popc(m);
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int q = 0; q < 8; ++q) {
+      before += q < w ? s_w[q] : 0;
+      tot += s_w[q];
+    }
+    if (mode == 1 && keep) cols[s_base + before + __popc(m & ((1u << lane) - 1u))] = (int32_t)j;
+    __syncthreads();
+    if (t == 0) s_base += tot;
+    __syncthreads();
+  }
+  if (mode == 0 && t == 0) counts[r] = s_base;
+}
+
+// Exclusive scan of q int64 counts into row_ptr[0..q] (3 phases, 1024 per block).
+__global__ void k_scan_part(const int64_t* __restrict__ c, int64_t q, int64_t* __restrict__ part) {
+  __shared__ int64_t s[32];
+  int64_t v = 0;
+  for (int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x; i < min(q, (int64_t)(blockIdx.x + 1) * 1024);
+       i += blockDim.x)
+    v += c[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    part[blockIdx.x] = t;
+  }
+}
+__global__ void k_scan_parts(int64_t* __restrict__ part, int nb, int64_t* __restrict__ total) {
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int b = 0; b < nb; ++b) {
+      const int64_t v = part[b];
+      part[b] = acc;
+      acc += v;
+    }
+    *total = acc;
+  }
+}
+__global__ void k_scan_final(const int64_t* __restrict__ c, int64_t q, const int64_t* __restrict__ part,
+                             const int64_t* __restrict__ total, int64_t* __restrict__ row_ptr) {
+  __shared__ int64_t s[1024];
+  const int64_t i0 = (int64_t)blockIdx.x * 1024;
+  for (int e = threadIdx.x; e < 1024; e += blockDim.x) s[e] = (i0 + e < q) ? c[i0 + e] : 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {  // 1024 sequential adds per block: cheap next to the passes
+    int64_t acc = part[blockIdx.x];
+    for (int e = 0; e < 1024; ++e) {
+      const int64_t v = s[e];
+      s[e] = acc;
+      acc += v;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 1024; e += blockDim.x)
+    if (i0 + e < q) row_ptr[i0 + e] = s[e];
+  if (blockIdx.x == 0 && threadIdx.x == 0) row_ptr[q] = *total;
+}
+
 // ---------------------------------------------------------------- fallback
 // Brute-force fp64 tier for rows the certificate could not prove ("recalculate
 // on the subset").  Phase 1: grid (P slices x failing rows); block
@@ -904,6 +1104,64 @@ __global__ void __launch_bounds__(kFbMaxP)
 }
 
 }  // namespace
+
+cudaError_t launch_nwr_tau(int64_t q_count, double phi, CertParams cp, float* tau,
+                           cudaStream_t st, int* launches) {
+  if (q_count <= 0) return cudaSuccess;
+  k_nwr_tau<<<(unsigned)((q_count + 255) / 256), 256, 0, st>>>(q_count, phi, cp, tau);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_nwr_verify(const float* Q, int64_t q_begin, int64_t q_count, const float* X,
+                              int64_t n, int d, bool self_join, double phi, const MainPass& mp,
+                              int mode, int64_t* counts, const int64_t* row_ptr, int32_t* cols,
+                              int32_t* ovf_rows, int32_t* ovf_count, cudaStream_t st,
+                              int* launches) {
+  if (q_count <= 0) return cudaSuccess;
+  if (mp.parts * mp.cap > kNwrMaxG) return cudaErrorInvalidValue;
+  int maxg = 1;
+  while (maxg < mp.parts * mp.cap) maxg <<= 1;  // room for the bitonic padding
+  const size_t smem = (size_t)kNwrWarps * d * 8 + (size_t)kNwrWarps * maxg * 4;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  const bool al = ((reinterpret_cast<uintptr_t>(X) & 31) == 0);
+  auto kern = (al && d == 16) ? k_nwr_verify<16>
+            : (al && d == 32) ? k_nwr_verify<32>
+            : (al && d == 64) ? k_nwr_verify<64> : k_nwr_verify<0>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)((q_count + kNwrWarps - 1) / kNwrWarps), kNwrWarps * 32, smem, st>>>(
+      Q, q_begin, q_count, X, n, d, self_join ? 1 : 0, phi, mp.buf, mp.cnt, mp.cap, mp.parts, mode,
+      counts, row_ptr, cols, ovf_rows, ovf_count);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_nwr_brute(const float* Q, int64_t q_begin, const float* X, int64_t n, int d,
+                             bool self_join, double phi, const int32_t* rows, int nrows, int mode,
+                             int64_t* counts, const int64_t* row_ptr, int32_t* cols,
+                             cudaStream_t st, int* launches) {
+  if (nrows <= 0) return cudaSuccess;
+  k_nwr_brute<<<nrows, 256, 0, st>>>(Q, q_begin, X, n, d, self_join ? 1 : 0, phi, rows, mode,
+                                     counts, row_ptr, cols);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+size_t scan_workspace(int64_t q) { return (size_t)((q + 1023) / 1024 + 2) * 8; }
+
+cudaError_t launch_scan(const int64_t* counts, int64_t q, int64_t* row_ptr, void* ws,
+                        cudaStream_t st, int* launches) {
+  const int nb = (int)((q + 1023) / 1024);
+  int64_t* part = static_cast<int64_t*>(ws);
+  int64_t* total = part + nb + 1;
+  if (nb == 0) return cudaMemsetAsync(row_ptr, 0, 8, st);
+  k_scan_part<<<nb, 256, 0, st>>>(counts, q, part);
+  k_scan_parts<<<1, 32, 0, st>>>(part, nb, total);
+  k_scan_final<<<nb, 256, 0, st>>>(counts, q, part, total, row_ptr);
+  *launches += 3;
+  return cudaGetLastError();
+}
 
 cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, const float* X,
                           int64_t n, int d, int k, bool self_join, Cands c, const MainPass* mp,

@@ -92,6 +92,8 @@ def load_library(path: str = LIB_PATH):
         "tod_lof": ([P, P, I64, I32, I32, P, P, ctypes.POINTER(KnnOut), ctypes.POINTER(Stats)],
                     ctypes.c_int),
         "tod_lof_lrd": ([P, I64, I32, I64, P, P, P, P], ctypes.c_int),
+        "tod_nwr": ([P, P, I64, I32, ctypes.c_double, I64, I64, P, P, P, I64,
+                     ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(Stats)], ctypes.c_int),
         "tod_lof_finish": ([P, I64, I32, I64, I64, P, P, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
@@ -137,7 +139,8 @@ def _as_f32_2d(x):
 def _empty_like_host_or_dev(ref, shape, dtype_np):
     if _is_torch(ref):
         import torch
-        tmap = {np.int64: torch.int64, np.float32: torch.float32, np.float64: torch.float64}
+        tmap = {np.int64: torch.int64, np.int32: torch.int32, np.float32: torch.float32,
+                np.float64: torch.float64}
         return torch.empty(shape, dtype=tmap[dtype_np], device=ref.device)
     return np.empty(shape, dtype=dtype_np)
 
@@ -226,6 +229,36 @@ class Context:
         self._check(self.lib.tod_knn_query(self.h, _ptr(Q), Q.shape[0], _ptr(X), X.shape[0],
                                            X.shape[1], k, ctypes.byref(ko), ctypes.byref(s)))
         return KnnResult(**o, stats=s.as_dict())
+
+    def nwr(self, X, phi: float, q_begin: int = 0, q_count=None, lists: bool = True,
+            capacity: int = 0):
+        """tod_nwr: neighbours within range (D_ij <= phi, squared distance) of rows
+        [q_begin, q_begin+q_count).  Returns (counts int64[q], row_ptr int64[q+1],
+        cols int32[total] | None, stats).  With lists=True and no capacity given the
+        call sizes cols from a counting call first (two library calls)."""
+        X = _as_f32_2d(X)
+        n, d = X.shape
+        if q_count is None:
+            q_count = n - q_begin
+        counts = _empty_like_host_or_dev(X, (q_count,), np.int64)
+        row_ptr = _empty_like_host_or_dev(X, (q_count + 1,), np.int64)
+        total = ctypes.c_int64(0)
+        s = Stats()
+        if lists and capacity <= 0:
+            self._check(self.lib.tod_nwr(self.h, _ptr(X), n, d, float(phi), q_begin, q_count,
+                                         _ptr(counts), _ptr(row_ptr), None, 0,
+                                         ctypes.byref(total), ctypes.byref(s)))
+            capacity = max(1, int(total.value))
+        cols = None
+        if lists:
+            cols = _empty_like_host_or_dev(X, (capacity,), np.int32)
+        self._check(self.lib.tod_nwr(self.h, _ptr(X), n, d, float(phi), q_begin, q_count,
+                                     _ptr(counts), _ptr(row_ptr), _ptr(cols),
+                                     capacity if lists else 0, ctypes.byref(total),
+                                     ctypes.byref(s)))
+        if cols is not None:
+            cols = cols[: int(total.value)]
+        return counts, row_ptr, cols, s.as_dict()
 
     def lof(self, X, k: int, want_knn=()):
         """tod_lof: returns (lof fp32[n], lrd fp32[n], KnnResult|None, stats)."""

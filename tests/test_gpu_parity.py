@@ -259,3 +259,62 @@ def test_c3_full_size_sampled_bf16(pkg):
         res = ctx.knn(torch.from_numpy(X).cuda(), k)
     rows = _sample_rows(1_000_000, lab, 16, seed=2)
     _check_rows(res, X, k, rows)
+
+
+# ------------------------------------------------------------ NWR (NEXT-2)
+def _nwr_check(got, X, phi, rows):
+    counts, ptr, cols, st = got
+    rc, rp, rl = oracle.nwr(X, phi, rows=rows)
+    assert np.array_equal(_np(counts), rc)
+    assert np.array_equal(_np(ptr), rp)
+    assert np.array_equal(_np(cols).astype(np.int64), rl)
+    return st
+
+
+@pytest.mark.parametrize("n,d,q", [(3000, 32, 8.0), (2999, 64, 12.0), (1000, 16, 5.0),
+                                   (20_000, 32, 4.0), (777, 10, 6.0)])
+def test_nwr_full_parity(pkg, n, d, q):
+    # phi = the q-th percentile of squared k-NN-scale distances: a few to ~100
+    # neighbours per row; bit-exact CSR against the fp64 brute force
+    X = datagen.gaussian_mixture(n, d, seed=n + 11 * d)
+    _, dd = oracle.knn(X, 10, rows=np.arange(0, n, max(1, n // 200)))
+    phi = float(np.percentile(dd[:, -1], 50)) * (q / 8.0)
+    with _ctx(pkg) as ctx:
+        got = ctx.nwr(torch.from_numpy(X).cuda(), phi)
+    st = _nwr_check(got, X, phi, np.arange(n))
+    assert st["rows"] == n
+
+
+def test_nwr_boundary_and_ties_lattice(pkg):
+    # integer lattice + duplicates: many pairs exactly on phi (boundary inclusive)
+    X = datagen.with_duplicates(datagen.lattice(3000, 16, seed=3, extent=2), frac=0.05, seed=4)
+    for phi in (0.0, 2.0, 5.0):
+        with _ctx(pkg) as ctx:
+            got = ctx.nwr(torch.from_numpy(X).cuda(), phi)
+        _nwr_check(got, X, phi, np.arange(3000))
+
+
+def test_nwr_overflow_rows_brute_force_and_query_range(pkg):
+    # a phi so large that every row overflows its candidate buffers (-> fp64
+    # brute force), on a query-row subrange, host buffers
+    X = datagen.gaussian_mixture(40_000, 32, seed=77)   # 5000 groups > 4 x 1024 slots
+    phi = 1e9
+    with _ctx(pkg) as ctx:
+        got = ctx.nwr(X, phi, q_begin=100, q_count=50)
+    st = _nwr_check(got, X, phi, np.arange(100, 150))
+    assert st["fallback_rows"] == 50
+    # small phi on the same range: no overflow
+    with _ctx(pkg) as ctx:
+        got = ctx.nwr(X, 1.0, q_begin=4000, q_count=3000)
+    assert _nwr_check(got, X, 1.0, np.arange(4000, 7000))["fallback_rows"] == 0
+
+
+def test_nwr_capacity_error_reports_total(pkg):
+    X = datagen.gaussian_mixture(2000, 16, seed=5)
+    phi = 50.0
+    with _ctx(pkg) as ctx:
+        c, p, _, _ = ctx.nwr(torch.from_numpy(X).cuda(), phi, lists=False)
+        total = int(p[-1])
+        with pytest.raises(pkg.TodError) as e:
+            ctx.nwr(torch.from_numpy(X).cuda(), phi, capacity=max(1, total - 1))
+    assert e.value.status == -3 and total > 1
