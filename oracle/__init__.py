@@ -18,6 +18,8 @@ Definitions:
      LOF_p = (sum_m lrd_{o_m} sequential) / (k * lrd_p), LOF_p = 1 when
      lrd_p = +inf (reading A6); all fp64, rounded to fp32 at the end.
      Neighbourhoods are the k-exact sets of O2 (reading A5).
+  O6 ABOD: -variance of the neighbour-pair cosines (reading A20).
+  O7 kNN classifier (Appendix B): majority vote, nearest-first ties.
   O5 NWR: {j != i : D64(i,j) <= phi}, phi on the squared distance
      of Eq. (3), neighbours ascending by j (CSR).
 
@@ -176,6 +178,68 @@ def nwr(X, phi: float, rows=None, threads: int = 0):
                            int(threads)) != 0:
         raise RuntimeError("oracle_nwr_rows failed")
     return counts, row_ptr, cols
+
+
+def abod_from_knn(X, idx):
+    """O6 ABOD (PAPER.md P:269-270, Fig. 3(a): kNN FO then cosine similarity FO;
+    reading A20): for row i with neighbours o_1..o_k (O2 order), v_m = x_{o_m} - x_i
+    (fp64 of the fp32 inputs), |v_m| = sqrt(sum_c v_mc^2, sequential); for each
+    pair (a < b), lexicographic, with |v_a|, |v_b| > 0:
+        cos_ab = (sum_c v_ac * v_bc, sequential) / (|v_a| * |v_b|);
+    mean = (sum cos, pair order) / P;  var = (sum (cos - mean)^2, pair order) / P;
+    score_i = fp32(-var)  (0 when P = 0).  Higher = more outlying.
+    Plain Python loops in fp64 (each op IEEE RN, no FMA)."""
+    X = _f32(X).astype(np.float64)
+    idx = np.asarray(idx)
+    n, k = idx.shape
+    out = np.empty(n, np.float32)
+    d = X.shape[1]
+    for i in range(n):
+        V = [X[int(o)] - X[i] for o in idx[i]]
+        nrm = []
+        for v in V:
+            acc = 0.0
+            for c in range(d):
+                acc = acc + float(v[c]) * float(v[c])
+            nrm.append(acc ** 0.5)
+        cos = []
+        for a in range(k):
+            for b in range(a + 1, k):
+                if nrm[a] > 0.0 and nrm[b] > 0.0:
+                    dot = 0.0
+                    for c in range(d):
+                        dot = dot + float(V[a][c]) * float(V[b][c])
+                    cos.append(dot / (nrm[a] * nrm[b]))
+        if not cos:
+            out[i] = 0.0
+            continue
+        s = 0.0
+        for c_ in cos:
+            s = s + c_
+        mean = s / len(cos)
+        s2 = 0.0
+        for c_ in cos:
+            t = c_ - mean
+            s2 = s2 + t * t
+        out[i] = np.float32(-(s2 / len(cos)))
+    return out
+
+
+def knn_classify(idx, labels):
+    """O7 kNN classifier (Appendix B: cdist -> topk ->
+    majority vote): majority label among the k neighbours (O2 order); ties go to
+    the tied class whose first neighbour is nearest (reading A21)."""
+    idx = np.asarray(idx)
+    labels = np.asarray(labels)
+    out = np.empty(idx.shape[0], np.int32)
+    for i in range(idx.shape[0]):
+        ls = [int(labels[int(o)]) for o in idx[i]]
+        cnt = {}
+        for l in ls:
+            cnt[l] = cnt.get(l, 0) + 1
+        best = max(cnt.values())
+        out[i] = next(l for l in ls if cnt[l] == best)
+    return out
 
 
 def euclid(d64_sorted) -> np.ndarray:

@@ -317,3 +317,53 @@ def test_nwr_vs_scipy_away_from_boundary():
         want = set(np.nonzero((D[i] <= phi) & ~near)[0].tolist()) - {i}
         got = set(lists[i])
         assert want <= got and got - want <= set(np.nonzero(near)[0].tolist())
+
+
+# ---------------------------------------------------------- O6 ABOD, O7 kNN_CLF
+def test_abod_golden_row0(golden_dir):
+    g = _load(golden_dir, "abod_clf_examples.json")
+    X = np.array(g["abod_X"], np.float32)
+    idx, _ = oracle.knn(X, g["abod_k"])
+    assert idx[0].tolist() == [1, 2, 3]
+    s = oracle.abod_from_knn(X, idx)
+    assert s[0] == np.float32(g["abod_row0"])
+
+
+def test_abod_k2_is_zero_and_duplicates_skipped():
+    X = datagen.gaussian_mixture(50, 4, seed=3)
+    idx, _ = oracle.knn(X, 2)
+    assert (oracle.abod_from_knn(X, idx) == 0).all()          # single pair: variance 0
+    Xd = np.vstack([X[:1], X[:1], X[:1], X[:1]])                # all coincident: no pairs
+    idx, _ = oracle.knn(Xd, 3)
+    assert (oracle.abod_from_knn(Xd, idx) == 0).all()
+
+
+def test_abod_vs_numpy_formula_and_outlier_argmax():
+    X = datagen.gaussian_mixture(300, 5, seed=8)
+    X = np.vstack([X, X.mean(0, keepdims=True) + 60.0]).astype(np.float32)  # far isolated point
+    k = 8
+    idx, _ = oracle.knn(X, k)
+    s = oracle.abod_from_knn(X, idx)
+    # independent vectorised formula (library float64 ops; tolerance for summation order)
+    for i in (0, 37, 300):
+        V = X[idx[i]].astype(np.float64) - X[i].astype(np.float64)
+        Vn = V / np.linalg.norm(V, axis=1, keepdims=True)
+        C = Vn @ Vn.T
+        cos = C[np.triu_indices(k, 1)]
+        assert abs(float(s[i]) - (-np.var(cos))) <= 1e-6 * max(1e-12, np.var(cos)) + 1e-12
+    assert int(np.argmax(s)) == 300
+
+
+def test_knn_classify_golden_and_vs_sklearn():
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "abod_clf_examples.json")))
+    for labs, want in zip(g["clf_labels_of_neighbours"], g["clf_pred"]):
+        idx = np.arange(len(labs))[None, :]
+        assert int(oracle.knn_classify(idx, np.array(labs))[0]) == want
+    from sklearn.neighbors import KNeighborsClassifier
+    rng = np.random.default_rng(0)
+    Xtr = np.vstack([rng.normal(0, 1, (200, 3)), rng.normal(3, 1, (200, 3))]).astype(np.float32)
+    ytr = np.repeat([0, 1], 200)
+    Xte = rng.normal(1.5, 1.5, (100, 3)).astype(np.float32)
+    idx, _ = oracle.knn_query(Xte, Xtr, 5)       # odd k, 2 classes: no vote ties
+    ref = KNeighborsClassifier(5, algorithm="brute").fit(Xtr, ytr).predict(Xte)
+    assert np.array_equal(oracle.knn_classify(idx, ytr), ref)
