@@ -222,6 +222,32 @@ tod_status tod_nwr(tod_ctx* ctx, const float* X, int64_t n, int32_t d, double ph
                    int64_t q_begin, int64_t q_count, int64_t* counts, int64_t* row_ptr,
                    int32_t* cols, int64_t capacity, int64_t* total, tod_stats* stats);
 
+/*
+ * tod_abod — angle-based outlier scores (§4.2, Fig. 3(a):
+ * the kNN functional operator followed by cosine similarity; Kriegel 2008,
+ * cited P:182).  For each query row i in [q_begin, q_begin+q_count) of X
+ * (self-join, exact neighbours as tod_knn): score_i = -Var over neighbour
+ * pairs (a < b) of cos(x_a - x_i, x_b - x_i), pairs with a coincident
+ * neighbour skipped, 0 if none remain (reading A20; higher = more outlying).
+ * fp64 with the oracle's operation order; fp32 out.
+ *   score    [q_count] fp32 (required).  knn_out: optional neighbour outputs.
+ * Errors: as tod_knn; TOD_E_UNSUPPORTED for k > 48.
+ */
+tod_status tod_abod(tod_ctx* ctx, const float* X, int64_t n, int32_t d, int32_t k,
+                    int64_t q_begin, int64_t q_count, float* score, const tod_knn_out* knn_out,
+                    tod_stats* stats);
+
+/*
+ * tod_knn_classify — kNN classifier (Appendix B: cdist ->
+ * topk -> majority vote).  For each row of Q (nq x d) the k nearest rows of X
+ * (exact, as tod_knn_query) vote with labels[] (int32 per row of X); ties go to
+ * the tied class whose first neighbour is nearest (reading A21).
+ *   pred     [nq] int32 (required).
+ */
+tod_status tod_knn_classify(tod_ctx* ctx, const float* Q, int64_t nq, const float* X, int64_t n,
+                            int32_t d, int32_t k, const int32_t* labels, int32_t* pred,
+                            tod_stats* stats);
+
 tod_status tod_knn_query(tod_ctx* ctx, const float* Q, int64_t nq, const float* X, int64_t n,
                          int32_t d, int32_t k, const tod_knn_out* out, tod_stats* stats);
 

@@ -30,6 +30,7 @@ invariants.  Nothing here is "parity unpinned".
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 import threading
@@ -180,7 +181,7 @@ def nwr(X, phi: float, rows=None, threads: int = 0):
     return counts, row_ptr, cols
 
 
-def abod_from_knn(X, idx):
+def abod_from_knn(X, idx, rows=None):
     """O6 ABOD (PAPER.md P:269-270, Fig. 3(a): kNN FO then cosine similarity FO;
     reading A20): for row i with neighbours o_1..o_k (O2 order), v_m = x_{o_m} - x_i
     (fp64 of the fp32 inputs), |v_m| = sqrt(sum_c v_mc^2, sequential); for each
@@ -192,16 +193,18 @@ def abod_from_knn(X, idx):
     X = _f32(X).astype(np.float64)
     idx = np.asarray(idx)
     n, k = idx.shape
+    rows = np.arange(n) if rows is None else np.asarray(rows)   # query row of idx[t]
     out = np.empty(n, np.float32)
     d = X.shape[1]
-    for i in range(n):
-        V = [X[int(o)] - X[i] for o in idx[i]]
+    for t in range(n):
+        i = int(rows[t])
+        V = [X[int(o)] - X[i] for o in idx[t]]
         nrm = []
         for v in V:
             acc = 0.0
             for c in range(d):
                 acc = acc + float(v[c]) * float(v[c])
-            nrm.append(acc ** 0.5)
+            nrm.append(math.sqrt(acc))   # IEEE correctly rounded
         cos = []
         for a in range(k):
             for b in range(a + 1, k):
@@ -211,7 +214,7 @@ def abod_from_knn(X, idx):
                         dot = dot + float(V[a][c]) * float(V[b][c])
                     cos.append(dot / (nrm[a] * nrm[b]))
         if not cos:
-            out[i] = 0.0
+            out[t] = 0.0
             continue
         s = 0.0
         for c_ in cos:
@@ -219,9 +222,9 @@ def abod_from_knn(X, idx):
         mean = s / len(cos)
         s2 = 0.0
         for c_ in cos:
-            t = c_ - mean
-            s2 = s2 + t * t
-        out[i] = np.float32(-(s2 / len(cos)))
+            u = c_ - mean
+            s2 = s2 + u * u
+        out[t] = np.float32(-(s2 / len(cos)))
     return out
 
 

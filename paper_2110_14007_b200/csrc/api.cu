@@ -44,7 +44,7 @@ struct Workspace {
 enum BufId {
   B_X = 0, B_Q, B_IMG_B, B_A2_B, B_E_B, B_IMG_A, B_A2_A, B_E_A, B_MU, B_PART,
   B_G, B_CIDX, B_CV, B_FAIL, B_SMALL, B_IDX, B_DIST, B_DIST64, B_KTH, B_MEAN, B_KD64,
-  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT, B_FAILUB, B_NWRTAU, B_NWRCNT, B_NWRPTR, B_NWRCOLS, B_SCAN, B_NBUF
+  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT, B_FAILUB, B_NWRTAU, B_NWRCNT, B_NWRPTR, B_NWRCOLS, B_SCAN, B_ABOD, B_LABELS, B_PRED, B_NBUF
 };
 static_assert(B_NBUF <= 48, "Workspace::bufs too small");
 
@@ -844,6 +844,88 @@ tod_status tod_nwr(tod_ctx* ctx, const float* X, int64_t n, int32_t d, double ph
   if (cols && !fits)
     return fail(ctx, TOD_E_RANGE, "cols capacity %lld < %lld neighbour pairs (counts, row_ptr and "
                 "total are valid)", (long long)capacity, (long long)*total);
+  ctx->msg.clear();
+  return TOD_OK;
+}
+
+tod_status tod_abod(tod_ctx* ctx, const float* X, int64_t n, int32_t d, int32_t k,
+                    int64_t q_begin, int64_t q_count, float* score, const tod_knn_out* knn_out,
+                    tod_stats* stats) {
+  TOD_TRY(validate_common(ctx, n, d, k));
+  if (n < 2 || k > n - 1) return fail(ctx, TOD_E_RANGE, "need 1 <= k <= n-1 (n=%lld k=%d)", (long long)n, k);
+  if (k > abod_max_k()) return fail(ctx, TOD_E_UNSUPPORTED, "ABOD supports k <= %d", abod_max_k());
+  if (q_begin < 0 || q_count < 0 || q_begin + q_count > n)
+    return fail(ctx, TOD_E_RANGE, "query rows outside [0, n)");
+  if (!score) return fail(ctx, TOD_E_ARG, "score must not be NULL");
+  TOD_CUDA(cudaSetDevice(ctx->device));
+  if (stats) memset(stats, 0, sizeof *stats);
+  Timer tm{ctx, (ctx->cfg.flags & TOD_F_TIMING) != 0};
+  int launches = 0;
+  tm.mark();
+  const float* dX;
+  TOD_TRY(stage_input(ctx, X, (size_t)n * d, B_X, &dX));
+  OutStage os;
+  TOD_TRY(stage_outputs(ctx, knn_out, q_count, k, &os));
+  void* p;
+  if (!os.dev.idx) {  // ABOD needs the neighbour indices on the device
+    TOD_TRY(ensure(ctx, B_IDX, (size_t)std::max<int64_t>(q_count, 1) * k * 8, &p));
+    os.dev.idx = static_cast<int64_t*>(p);
+  }
+  float* dscore;
+  bool st_s;
+  TOD_TRY(dev_view(ctx, score, (size_t)q_count, B_ABOD, &dscore, &st_s));
+  if (q_count > 0) {
+    TOD_TRY(run_knn(ctx, dX, n, nullptr, q_begin, q_count, d, k, os.dev, stats, tm, &launches));
+    TOD_CUDA(launch_abod(dX, q_begin, q_count, d, k, os.dev.idx, dscore, ctx->stream, &launches));
+  }
+  TOD_TRY(unstage_outputs(ctx, knn_out, q_count, k, os));
+  if (st_s) TOD_CUDA(cudaMemcpyAsync(score, dscore, (size_t)q_count * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  tm.mark();
+  TOD_CUDA(cudaStreamSynchronize(ctx->stream));
+  finish_stats(stats, tm, launches, 0);
+  ctx->msg.clear();
+  return TOD_OK;
+}
+
+tod_status tod_knn_classify(tod_ctx* ctx, const float* Q, int64_t nq, const float* X, int64_t n,
+                            int32_t d, int32_t k, const int32_t* labels, int32_t* pred,
+                            tod_stats* stats) {
+  TOD_TRY(validate_common(ctx, n, d, k));
+  if (k > n) return fail(ctx, TOD_E_RANGE, "need 1 <= k <= n (n=%lld k=%d)", (long long)n, k);
+  if (nq < 0 || nq > INT32_MAX) return fail(ctx, TOD_E_RANGE, "nq out of range");
+  if (!labels || !pred) return fail(ctx, TOD_E_ARG, "labels and pred must not be NULL");
+  TOD_CUDA(cudaSetDevice(ctx->device));
+  if (stats) memset(stats, 0, sizeof *stats);
+  Timer tm{ctx, (ctx->cfg.flags & TOD_F_TIMING) != 0};
+  int launches = 0;
+  tm.mark();
+  const float *dX, *dQ = nullptr;
+  TOD_TRY(stage_input(ctx, X, (size_t)n * d, B_X, &dX));
+  if (nq > 0) TOD_TRY(stage_input(ctx, Q, (size_t)nq * d, B_Q, &dQ));
+  void* p;
+  const int32_t* dlab;
+  if (is_device_ptr(labels, ctx->device)) {
+    dlab = labels;
+  } else {
+    TOD_TRY(ensure(ctx, B_LABELS, (size_t)n * 4, &p));
+    TOD_CUDA(cudaMemcpyAsync(p, labels, (size_t)n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    dlab = static_cast<const int32_t*>(p);
+  }
+  int32_t* dpred;
+  bool st_p;
+  TOD_TRY(dev_view(ctx, pred, (size_t)std::max<int64_t>(nq, 1), B_PRED, &dpred, &st_p));
+  KnnOutDev kd{};
+  TOD_TRY(ensure(ctx, B_IDX, (size_t)std::max<int64_t>(nq, 1) * k * 8, &p));
+  kd.idx = static_cast<int64_t*>(p);
+  if (nq > 0) {
+    TOD_TRY(run_knn(ctx, dX, n, dQ, 0, nq, d, k, kd, stats, tm, &launches));
+    TOD_CUDA(launch_knn_classify(nq, k, kd.idx, dlab, dpred, ctx->stream, &launches));
+  }
+  if (st_p && nq > 0)
+    TOD_CUDA(cudaMemcpyAsync(pred, dpred, (size_t)nq * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  tm.mark();
+  TOD_CUDA(cudaStreamSynchronize(ctx->stream));
+  finish_stats(stats, tm, launches, 0);
   ctx->msg.clear();
   return TOD_OK;
 }

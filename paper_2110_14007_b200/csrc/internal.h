@@ -156,6 +156,13 @@ size_t scan_workspace(int64_t q);
 cudaError_t launch_scan(const int64_t* counts, int64_t q, int64_t* row_ptr, void* ws,
                         cudaStream_t st, int* launches);
 
+// ---- consumers.cu (ABOD, kNN classifier on the exact neighbour lists)
+cudaError_t launch_abod(const float* X, int64_t q_begin, int64_t q_count, int d, int k,
+                        const int64_t* idx, float* score, cudaStream_t st, int* launches);
+int abod_max_k();
+cudaError_t launch_knn_classify(int64_t nq, int k, const int64_t* idx, const int32_t* labels,
+                                int32_t* pred, cudaStream_t st, int* launches);
+
 // ---- lof.cu
 cudaError_t launch_lof_lrd(int64_t q_count, int k, const int64_t* idx, const double* dist64,
                            const double* kdist64_all, double* lrd64_out, cudaStream_t st,

@@ -92,6 +92,10 @@ def load_library(path: str = LIB_PATH):
         "tod_lof": ([P, P, I64, I32, I32, P, P, ctypes.POINTER(KnnOut), ctypes.POINTER(Stats)],
                     ctypes.c_int),
         "tod_lof_lrd": ([P, I64, I32, I64, P, P, P, P], ctypes.c_int),
+        "tod_abod": ([P, P, I64, I32, I32, I64, I64, P, ctypes.POINTER(KnnOut),
+                      ctypes.POINTER(Stats)], ctypes.c_int),
+        "tod_knn_classify": ([P, P, I64, P, I64, I32, I32, P, P, ctypes.POINTER(Stats)],
+                             ctypes.c_int),
         "tod_nwr": ([P, P, I64, I32, ctypes.c_double, I64, I64, P, P, P, I64,
                      ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(Stats)], ctypes.c_int),
         "tod_lof_finish": ([P, I64, I32, I64, I64, P, P, P, P], ctypes.c_int),
@@ -259,6 +263,36 @@ class Context:
         if cols is not None:
             cols = cols[: int(total.value)]
         return counts, row_ptr, cols, s.as_dict()
+
+    def abod(self, X, k: int, q_begin: int = 0, q_count=None, want_knn=()):
+        """tod_abod: -variance of neighbour-pair cosines per row; (score fp32[q], KnnResult|None, stats)."""
+        X = _as_f32_2d(X)
+        n, d = X.shape
+        if q_count is None:
+            q_count = n - q_begin
+        score = _empty_like_host_or_dev(X, (q_count,), np.float32)
+        o, ko = self._alloc_knn(X, q_count, k, want_knn)
+        s = Stats()
+        self._check(self.lib.tod_abod(self.h, _ptr(X), n, d, k, q_begin, q_count, _ptr(score),
+                                      ctypes.byref(ko) if want_knn else None, ctypes.byref(s)))
+        res = KnnResult(**o, stats=s.as_dict()) if want_knn else None
+        return score, res, s.as_dict()
+
+    def knn_classify(self, Q, X, labels, k: int):
+        """tod_knn_classify: majority vote of the k nearest rows of X; int32[nq]."""
+        Q = _as_f32_2d(Q)
+        X = _as_f32_2d(X)
+        if _is_torch(X):
+            import torch
+            labels = torch.as_tensor(labels, dtype=torch.int32, device=X.device).contiguous()
+        else:
+            labels = np.ascontiguousarray(labels, dtype=np.int32)
+        pred = _empty_like_host_or_dev(Q, (Q.shape[0],), np.int32)
+        s = Stats()
+        self._check(self.lib.tod_knn_classify(self.h, _ptr(Q), Q.shape[0], _ptr(X), X.shape[0],
+                                              X.shape[1], k, _ptr(labels), _ptr(pred),
+                                              ctypes.byref(s)))
+        return pred
 
     def lof(self, X, k: int, want_knn=()):
         """tod_lof: returns (lof fp32[n], lrd fp32[n], KnnResult|None, stats)."""

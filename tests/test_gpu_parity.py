@@ -318,3 +318,38 @@ def test_nwr_capacity_error_reports_total(pkg):
         with pytest.raises(pkg.TodError) as e:
             ctx.nwr(torch.from_numpy(X).cuda(), phi, capacity=max(1, total - 1))
     assert e.value.status == -3 and total > 1
+
+
+# ------------------------------------------------ ABOD, kNN classifier (NEXT-3)
+@pytest.mark.parametrize("n,d,k", [(1500, 16, 10), (900, 32, 5), (700, 10, 2)])
+def test_abod_bitexact(pkg, n, d, k):
+    X = datagen.gaussian_mixture(n, d, seed=n + k)
+    X = datagen.with_duplicates(X, frac=0.02, seed=1)     # coincident neighbours: skipped pairs
+    ri, _ = oracle.knn(X, k)
+    ref = oracle.abod_from_knn(X, ri)
+    with _ctx(pkg) as ctx:
+        s, res, st = ctx.abod(torch.from_numpy(X).cuda(), k, want_knn=("idx",))
+    assert np.array_equal(_np(res.idx), ri)
+    assert np.array_equal(_np(s), ref)
+
+
+def test_abod_query_range_host_buffers(pkg):
+    X = datagen.gaussian_mixture(12_000, 32, seed=4)       # two-pass kNN path
+    rows = np.arange(3000, 3400)
+    ri, _ = oracle.knn(X, 8, rows=rows)
+    with _ctx(pkg) as ctx:
+        s, _, _ = ctx.abod(X, 8, q_begin=3000, q_count=400)
+    assert np.array_equal(s, oracle.abod_from_knn(X, ri, rows=rows))
+
+
+def test_knn_classify_parity(pkg):
+    rng = np.random.default_rng(3)
+    Xtr = datagen.gaussian_mixture(5000, 24, seed=11)
+    ytr = rng.integers(0, 4, 5000).astype(np.int32)
+    Xte = datagen.gaussian_mixture(700, 24, seed=12)
+    for k in (1, 6, 15):
+        ri, _ = oracle.knn_query(Xte, Xtr, k)
+        ref = oracle.knn_classify(ri, ytr)
+        with _ctx(pkg) as ctx:
+            pred = ctx.knn_classify(torch.from_numpy(Xte).cuda(), torch.from_numpy(Xtr).cuda(), ytr, k)
+        assert np.array_equal(_np(pred), ref), k
