@@ -18,7 +18,8 @@ Definitions:
      LOF_p = (sum_m lrd_{o_m} sequential) / (k * lrd_p), LOF_p = 1 when
      lrd_p = +inf (reading A6); all fp64, rounded to fp32 at the end.
      Neighbourhoods are the k-exact sets of O2 (reading A5).
-  O6 ABOD: -variance of the neighbour-pair cosines (reading A20).
+  O6 ABOD: -variance of the distance-weighted neighbour-pair
+     angle factor <a,b>/(|a|^2 |b|^2) (Kriegel 2008; reading A20).
   O7 kNN classifier (Appendix B): majority vote, nearest-first ties.
   O5 NWR: {j != i : D64(i,j) <= phi}, phi on the squared distance
      of Eq. (3), neighbours ascending by j (CSR).
@@ -182,12 +183,13 @@ def nwr(X, phi: float, rows=None, threads: int = 0):
 
 
 def abod_from_knn(X, idx, rows=None):
-    """O6 ABOD (PAPER.md P:269-270, Fig. 3(a): kNN FO then cosine similarity FO;
-    reading A20): for row i with neighbours o_1..o_k (O2 order), v_m = x_{o_m} - x_i
-    (fp64 of the fp32 inputs), |v_m| = sqrt(sum_c v_mc^2, sequential); for each
-    pair (a < b), lexicographic, with |v_a|, |v_b| > 0:
-        cos_ab = (sum_c v_ac * v_bc, sequential) / (|v_a| * |v_b|);
-    mean = (sum cos, pair order) / P;  var = (sum (cos - mean)^2, pair order) / P;
+    """O6 ABOD: the angle-based outlier factor of Kriegel et al. 2008 (cited
+    PAPER.md P:182; built as kNN FO + angle FO; reading A20) over the
+    k-exact neighbours, as in PyOD's fast ABOD: for row i with neighbours
+    o_1..o_k (O2 order), v_m = x_{o_m} - x_i (fp64 of the fp32 inputs),
+    q_m = sum_c v_mc^2 (sequential); for each pair (a < b), lexicographic, with
+    q_a, q_b > 0:   w_ab = (sum_c v_ac * v_bc, sequential) / (q_a * q_b);
+    mean = (sum w, pair order) / P;  var = (sum (w - mean)^2, pair order) / P;
     score_i = fp32(-var)  (0 when P = 0).  Higher = more outlying.
     Plain Python loops in fp64 (each op IEEE RN, no FMA)."""
     X = _f32(X).astype(np.float64)
@@ -199,32 +201,32 @@ def abod_from_knn(X, idx, rows=None):
     for t in range(n):
         i = int(rows[t])
         V = [X[int(o)] - X[i] for o in idx[t]]
-        nrm = []
+        q = []
         for v in V:
             acc = 0.0
             for c in range(d):
                 acc = acc + float(v[c]) * float(v[c])
-            nrm.append(math.sqrt(acc))   # IEEE correctly rounded
-        cos = []
+            q.append(acc)
+        w = []
         for a in range(k):
             for b in range(a + 1, k):
-                if nrm[a] > 0.0 and nrm[b] > 0.0:
+                if q[a] > 0.0 and q[b] > 0.0:
                     dot = 0.0
                     for c in range(d):
                         dot = dot + float(V[a][c]) * float(V[b][c])
-                    cos.append(dot / (nrm[a] * nrm[b]))
-        if not cos:
+                    w.append(dot / (q[a] * q[b]))
+        if not w:
             out[t] = 0.0
             continue
         s = 0.0
-        for c_ in cos:
-            s = s + c_
-        mean = s / len(cos)
+        for x in w:
+            s = s + x
+        mean = s / len(w)
         s2 = 0.0
-        for c_ in cos:
-            u = c_ - mean
+        for x in w:
+            u = x - mean
             s2 = s2 + u * u
-        out[t] = np.float32(-(s2 / len(cos)))
+        out[t] = np.float32(-(s2 / len(w)))
     return out
 
 

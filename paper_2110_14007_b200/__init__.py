@@ -8,5 +8,7 @@ CPU fallback.
 from .tod import (Context, KnnResult, TodError, load_library, header_symbols, LIB_PATH,  # noqa: F401
                   F_NO_CERTIFY, F_TIMING, F_PASS1_V1, F_MAIN_1SM, FORMATS)
 
-__all__ = ["Context", "KnnResult", "TodError", "load_library", "header_symbols", "LIB_PATH",
+from . import detectors  # noqa: F401,E402  (PyOD-style fit/decision_scores_/labels_)
+
+__all__ = ["detectors", "Context", "KnnResult", "TodError", "load_library", "header_symbols", "LIB_PATH",
            "F_NO_CERTIFY", "F_TIMING", "F_PASS1_V1", "F_MAIN_1SM", "FORMATS"]

@@ -2,11 +2,12 @@
 // (§4.2 Fig. 3(a): "kNN FO ... then cosine similarity FO";
 // Appendix B: kNN classifier = cdist -> topk -> vote).
 //
-// ABOD (reading A20): for query row i with neighbours o_1..o_k
-// (ascending (D64, index), the exact kNN of tod_knn), v_m = x_{o_m} - x_i in
-// fp64, |v_m| = sqrt(sum_c v_mc^2) sequential, and for each neighbour pair
-// (a < b) with nonzero vectors cos_ab = (sum_c v_ac v_bc) / (|v_a| |v_b|);
-// score = -(population variance of the cosines), two-pass in pair order,
+// ABOD (Kriegel 2008, cited P:182; reading A20): for query row i
+// with neighbours o_1..o_k (ascending (D64, index), the exact kNN of tod_knn),
+// v_m = x_{o_m} - x_i in fp64, q_m = sum_c v_mc^2 sequential, and for each
+// neighbour pair (a < b) with nonzero vectors w_ab = (sum_c v_ac v_bc) / (q_a q_b)
+// (the distance-weighted angle factor); score = -(population variance of the
+// w_ab), two-pass in pair order,
 // every operation explicit RN fp64 (no FMA): the oracle's O6 op for op, so
 // the fp32 scores are bit-identical.  One warp per row: lanes compute pairs,
 // lane 0 folds the sums in pair order.
@@ -45,7 +46,7 @@ __global__ void __launch_bounds__(kAbodWarps * 32)
   for (int m = lane; m < k; m += 32) {
     double acc = 0.0;
     for (int c = 0; c < d; ++c) acc = __dadd_rn(acc, __dmul_rn(V[m * d + c], V[m * d + c]));
-    s_nrm[w][m] = __dsqrt_rn(acc);
+    s_nrm[w][m] = acc;  // squared norm
   }
   __syncwarp();
   const int npairs = k * (k - 1) / 2;
@@ -59,6 +60,7 @@ __global__ void __launch_bounds__(kAbodWarps * 32)
     const int b = a + 1 + rem;
     const double na = s_nrm[w][a], nb = s_nrm[w][b];
     double c = CUDART_NAN;  // NaN marks a skipped pair (coincident neighbour)
+    // na, nb: squared norms q_a, q_b
     if (na > 0.0 && nb > 0.0) {
       double dot = 0.0;
       for (int t = 0; t < d; ++t) dot = __dadd_rn(dot, __dmul_rn(V[a * d + t], V[b * d + t]));

@@ -353,3 +353,38 @@ def test_knn_classify_parity(pkg):
         with _ctx(pkg) as ctx:
             pred = ctx.knn_classify(torch.from_numpy(Xte).cuda(), torch.from_numpy(Xtr).cuda(), ytr, k)
         assert np.array_equal(_np(pred), ref), k
+
+
+# ------------------------------------------------ detector wrapper (NEXT-4)
+def test_detectors_fit_labels_auc(pkg):
+    from sklearn.metrics import roc_auc_score
+    from paper_2110_14007_b200 import detectors
+    X, lab = datagen.gaussian_mixture(6000, 16, seed=2, return_labels=True)
+    k = 10
+    ri, rd = oracle.knn(X, k)
+    kth, mean = oracle.scores(rd)
+    _, lof_ref = oracle.lof_from_knn(ri, rd)
+    for det, ref in ((detectors.KNN(k, contamination=0.05), kth),
+                     (detectors.KNN(k, method="mean", contamination=0.05), mean),
+                     (detectors.LOF(k, contamination=0.05), lof_ref.astype(np.float32))):
+        det.fit(torch.from_numpy(X).cuda())
+        assert np.array_equal(det.decision_scores_.astype(np.float32), ref)
+        assert abs(det.labels_.mean() - 0.05) < 0.01
+        assert roc_auc_score(lab, det.decision_scores_) == roc_auc_score(lab, ref)
+        assert roc_auc_score(lab, det.decision_scores_) > 0.9
+        det.close()
+    abod = detectors.ABOD(k, contamination=0.05).fit(torch.from_numpy(X).cuda())
+    assert np.array_equal(abod.decision_scores_.astype(np.float32), oracle.abod_from_knn(X, ri))
+    assert roc_auc_score(lab, abod.decision_scores_) > 0.8
+
+
+def test_detector_decision_function_matches_query_oracle(pkg):
+    from paper_2110_14007_b200 import detectors
+    X = datagen.gaussian_mixture(4000, 24, seed=5)
+    Xt = datagen.gaussian_mixture(300, 24, seed=6)
+    det = detectors.KNN(7).fit(torch.from_numpy(X).cuda())
+    s = det.decision_function(torch.from_numpy(Xt).cuda())
+    ri, rd = oracle.knn_query(Xt, X, 7)
+    assert np.array_equal(s.astype(np.float32), oracle.scores(rd)[0])
+    assert np.array_equal(det.predict(torch.from_numpy(Xt).cuda()), (s > det.threshold_).astype(np.int64))
+    det.close()

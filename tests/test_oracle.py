@@ -347,11 +347,18 @@ def test_abod_vs_numpy_formula_and_outlier_argmax():
     # independent vectorised formula (library float64 ops; tolerance for summation order)
     for i in (0, 37, 300):
         V = X[idx[i]].astype(np.float64) - X[i].astype(np.float64)
-        Vn = V / np.linalg.norm(V, axis=1, keepdims=True)
-        C = Vn @ Vn.T
-        cos = C[np.triu_indices(k, 1)]
-        assert abs(float(s[i]) - (-np.var(cos))) <= 1e-6 * max(1e-12, np.var(cos)) + 1e-12
+        q = (V * V).sum(1)
+        W = (V @ V.T) / np.outer(q, q)
+        w = W[np.triu_indices(k, 1)]
+        assert abs(float(s[i]) - (-np.var(w))) <= 1e-6 * max(1e-30, np.var(w)) + 1e-30
     assert int(np.argmax(s)) == 300
+
+
+def test_abod_detects_uniform_outliers():
+    from sklearn.metrics import roc_auc_score
+    X, lab = datagen.gaussian_mixture(3000, 16, seed=2, return_labels=True)
+    idx, _ = oracle.knn(X, 10)
+    assert roc_auc_score(lab, oracle.abod_from_knn(X, idx)) > 0.9
 
 
 def test_knn_classify_golden_and_vs_sklearn():
