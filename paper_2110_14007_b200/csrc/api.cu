@@ -197,7 +197,12 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
     // Two-pass: the sample pass keeps ~2K'/R groups per row in total, split over
     // the lists (its threshold is the minimum of the lists' thresholds).
     auto khalf = [&](int sp) {
-      if (p->two) return std::max(4, roundup((2 * kp + p->R * sp - 1) / (p->R * sp), 4));
+      if (p->two) {
+        // per-list size from the reference stride 8 (TOD_SAMPLE_KR overrides, experiment knob)
+        int kr = 8;
+        if (const char* e = getenv("TOD_SAMPLE_KR")) kr = std::max(1, atoi(e));
+        return std::max(4, roundup((2 * kp + kr * sp - 1) / (kr * sp), 4));
+      }
       return sp == 1 ? kp : (sp == 2 ? roundup(kp / 2 + 8, 4) : roundup(kp / 4 + 4, 4));
     };
     int sp = ctx->cfg.epilogue_split;
@@ -308,7 +313,7 @@ tod_status prep_tc(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
   Image& A = *Aout;
   TOD_TRY(make_img(B_IMG_B, B_A2_B, B_E_B, n, n_pad, &B));
   TOD_TRY(make_img(B_IMG_A, B_A2_A, B_E_A, a_rows, a_pad, &A));
-  const int stat_blocks = (int)((n + 1023) / 1024);
+  const int stat_blocks = (int)((n + 127) / 128);  // prep.cu kRowsPerStatBlock
   TOD_TRY(ensure(ctx, B_MU, (size_t)d * 8, &p));
   double* mu = static_cast<double*>(p);
   TOD_TRY(ensure(ctx, B_PART, (size_t)stat_blocks * d * 8, &p));

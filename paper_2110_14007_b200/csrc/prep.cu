@@ -17,7 +17,7 @@ namespace tod {
 namespace {
 
 constexpr int kStatThreads = 256;
-constexpr int kRowsPerStatBlock = 1024;
+constexpr int kRowsPerStatBlock = 128;  // short fp64 add chains, many blocks
 
 __device__ __forceinline__ void atomic_max_nonneg(unsigned long long* addr, double v) {
   // Non-negative doubles order like their bit patterns.
@@ -68,13 +68,21 @@ __global__ void k_colsum_partial(const float* __restrict__ X, int64_t n, int d,
   if (t == 0 && bad) atomicOr(&g->nonfinite, 1);
 }
 
+// One block (256 threads) per column: thread t sums partials t, t+256, ... in
+// order, then a fixed-shape tree -- deterministic for a given (n, d).
 __global__ void k_colmean(const double* __restrict__ partial, int blocks, int64_t n, int d,
                           double* __restrict__ mu) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= d) return;
+  __shared__ double red[256];
+  const int c = blockIdx.x;
   double acc = 0.0;
-  for (int b = 0; b < blocks; ++b) acc += partial[(int64_t)b * d + c];
-  mu[c] = acc / (double)n;
+  for (int b = threadIdx.x; b < blocks; b += 256) acc += partial[(int64_t)b * d + c];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) mu[c] = red[0] / (double)n;
 }
 
 __global__ void k_finite(const float* __restrict__ X, int64_t total, PrepGlobals* g) {
@@ -90,12 +98,17 @@ __global__ void k_absmax(const float* __restrict__ X, int64_t n, int d,
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  __shared__ unsigned long long s_m;
+  if (threadIdx.x == 0) s_m = 0ull;
+  __syncthreads();
   double m = 0.0;
   for (int64_t r = warp; r < n; r += nwarps)
     for (int c = lane; c < d; c += 32) m = fmax(m, fabs((double)X[r * d + c] - mu[c]));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if (lane == 0) atomic_max_nonneg(&g->absmax_bits, m);
+  if (lane == 0) atomic_max_nonneg(&s_m, m);   // block-local first: one global atomic per block
+  __syncthreads();
+  if (threadIdx.x == 0 && s_m) atomicMax(&g->absmax_bits, s_m);
 }
 
 // s = 2^e with max|s*(x-mu)| in [2^(E-1), 2^E), E = floor((30 - log2 dpad)/2),
@@ -262,7 +275,7 @@ cudaError_t launch_prep_stats(const float* X, int64_t n, int d, double* mu, doub
   const int blocks = (int)((n + kRowsPerStatBlock - 1) / kRowsPerStatBlock);
   if (blocks > partial_blocks) return cudaErrorInvalidValue;
   k_colsum_partial<<<blocks, kStatThreads, 0, st>>>(X, n, d, partial, g);
-  k_colmean<<<(d + 127) / 128, 128, 0, st>>>(partial, blocks, n, d, mu);
+  k_colmean<<<d, 256, 0, st>>>(partial, blocks, n, d, mu);
   *launches += 2;
   return cudaGetLastError();
 }

@@ -841,7 +841,7 @@ __global__ void __launch_bounds__(kFbThreads)
                  double* __restrict__ ck, int* __restrict__ ci, int* __restrict__ ccnt) {
   extern __shared__ double s_q[];  // [kFbQB][d]
   const int t = threadIdx.x, lane = t & 31;
-  const int p = blockIdx.x, f0 = blockIdx.y * kFbQB;
+  const int p = blockIdx.y, f0 = blockIdx.x * kFbQB;  // x: row groups (large), y: slices
   const int nq = min(kFbQB, nfail - f0);
   int64_t gq[kFbQB];
   double ub[kFbQB];
@@ -980,13 +980,13 @@ __global__ void __launch_bounds__(kFbThreads)
                     int64_t n, int d, int k, int self_join, const int32_t* __restrict__ fail_rows,
                     int P, const int* __restrict__ done, double* __restrict__ part_key,
                     int* __restrict__ part_id) {
-  if (done[blockIdx.y]) return;  // answered by the threshold tier
+  if (done[blockIdx.x]) return;  // answered by the threshold tier
   __shared__ double s_hk[kFbThreads / 32];
   __shared__ int s_hi[kFbThreads / 32];
   __shared__ int s_ht[kFbThreads / 32];
   __shared__ int s_win;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int p = blockIdx.x, f = blockIdx.y;
+  const int p = blockIdx.y, f = blockIdx.x;  // x: failing rows (large), y: slices
   const int64_t r = fail_rows[f];
   const int64_t gi = q_begin + r;
   const float* xi = self_join ? X + gi * d : Q + r * d;
@@ -1240,13 +1240,13 @@ cudaError_t launch_fallback(const float* Q, int64_t q_begin, const float* X, int
     const size_t smem = (size_t)kFbQB * d * 8;
     e = cudaFuncSetAttribute(k_fb_collect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_fb_collect<<<dim3(Pt, qb), kFbThreads, smem, st>>>(Q, q_begin, X, n, d, self_join ? 1 : 0,
+    k_fb_collect<<<dim3(qb, Pt), kFbThreads, smem, st>>>(Q, q_begin, X, n, d, self_join ? 1 : 0,
                                                           fail_rows, fail_ub, nfail, Pt, ck, ci,
                                                           ccnt);
     k_fb_select<<<(nfail + 3) / 4, 128, 0, st>>>(k, fail_rows, nfail, ck, ci, ccnt, done, out);
     *launches += 2;
   }
-  const dim3 grid(P, nfail);
+  const dim3 grid(nfail, P);
   if (k <= 32)
     k_fallback_part<32><<<grid, kFbThreads, 0, st>>>(Q, q_begin, X, n, d, k, self_join ? 1 : 0,
                                                      fail_rows, P, done, pk, pi);

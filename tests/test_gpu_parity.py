@@ -388,3 +388,14 @@ def test_detector_decision_function_matches_query_oracle(pkg):
     assert np.array_equal(s.astype(np.float32), oracle.scores(rd)[0])
     assert np.array_equal(det.predict(torch.from_numpy(Xt).cuda()), (s > det.threshold_).astype(np.int64))
     det.close()
+
+
+def test_forced_fallback_more_rows_than_grid_y(pkg):
+    # > 65535 failing rows: the fallback grids put rows on x (gridDim.y <= 65535)
+    n, k = 70_000, 5
+    X = datagen.gaussian_mixture(n, 16, seed=17)
+    with _ctx(pkg, flags=pkg.F_NO_CERTIFY) as ctx:
+        res = ctx.knn(torch.from_numpy(X).cuda(), k)
+    assert res.stats["fallback_rows"] == n
+    rows = np.random.default_rng(0).choice(n, 64, replace=False)
+    _check_rows(res, X, k, rows)
