@@ -16,7 +16,9 @@
 // the same formula, per-thread sorted top-k lists, block k-way merge.
 #include <math_constants.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -333,6 +335,35 @@ __device__ __forceinline__ double d64_fixed(const double* __restrict__ xq, const
   return acc;
 }
 
+// Per-warp telemetry (one global atomic per warp at exit, not per row).
+struct RowTel {
+  unsigned long long G = 0, nv = 0, nc = 0;
+  double maxerr = 0.0;
+};
+
+// fp32 screen distance (difference form, FMA, 4 independent partial sums): all
+// terms are >= 0, so |D32 - rho^2| <= gamma_{d+2}(2^-24) rho^2 whatever the order.
+template <int DT>
+__device__ __forceinline__ float d32_fixed(const float* __restrict__ xqf, const float* xj) {
+  float v[DT];
+#pragma unroll
+  for (int u = 0; u < DT / 8; ++u) ldg8(xj + 8 * u, v + 8 * u);
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int c = 0; c < DT; c += 4) {
+    const float4 q = *reinterpret_cast<const float4*>(xqf + c);
+    float t = q.x - v[c];
+    a[0] = fmaf(t, t, a[0]);
+    t = q.y - v[c + 1];
+    a[1] = fmaf(t, t, a[1]);
+    t = q.z - v[c + 2];
+    a[2] = fmaf(t, t, a[2]);
+    t = q.w - v[c + 3];
+    a[3] = fmaf(t, t, a[3]);
+  }
+  return (a[0] + a[1]) + (a[2] + a[3]);
+}
+
 template <int DT>
 __device__ __forceinline__ void rerank_groups_row(
     const float* __restrict__ Q, int64_t q_begin, int64_t q_count, const float* __restrict__ X,
@@ -341,21 +372,21 @@ __device__ __forceinline__ void rerank_groups_row(
     const uint2* __restrict__ mbuf, const int* __restrict__ mcnt, int mcap, int mparts,
     const CertParams& cp,
     const KnnOutDev& out, int32_t* __restrict__ fail_rows, double* __restrict__ fail_ub,
-    int32_t* __restrict__ fail_count, unsigned long long* s_red) {
+    int32_t* __restrict__ fail_count, int64_t r, RowTel& tel) {
   __shared__ float s_gk[kGrpWarps][kSelMax];      // staged group keys
   __shared__ int s_gi[kGrpWarps][kSelMax];        // staged group indices
   __shared__ double s_ck[kGrpWarps][kColMax];     // surviving columns: D64
   __shared__ int s_ci[kGrpWarps][kColMax];        //                    index
   __shared__ double s_tk[kGrpWarps][kMaxK];       // selected top-k
   __shared__ int s_ti[kGrpWarps][kMaxK];
+  __shared__ __align__(16) float s_xqf[kGrpWarps][64];  // fp32 query row (screen, DT > 0)
   extern __shared__ double s_xq[];                // [warps][d] query row in fp64
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t r = (int64_t)blockIdx.x * kGrpWarps + w;
-  if (r >= q_count) return;
   const int64_t gi = q_begin + r;
   const float* xi = self_join ? X + gi * d : Q + r * d;
   double* xq = s_xq + (size_t)w * d;
   for (int c = lane; c < d; c += 32) xq[c] = (double)xi[c];
+
   float* gk = s_gk[w];
   int* gid = s_gi[w];
   // ---- stage every kept group (compacted with ballots)
@@ -374,20 +405,41 @@ __device__ __forceinline__ void rerank_groups_row(
     G += __popc(live);
   }
   if (mbuf) {
-    for (int h = 0; h < mparts; ++h) {
-      const int c = mcnt[r * mparts + h];
-      overflow |= c > mcap;
-      const int m = c < mcap ? c : mcap;
-      const uint2* src = mbuf + (r * mparts + h) * (int64_t)mcap;
-      for (int e = lane; e < m; e += 32) {
-        const uint2 kv = src[e];
-        if (G + e < kSelMax) {
-          gk[G + e] = __uint_as_float(kv.x);
-          gid[G + e] = (int)kv.y;
+    // all part counts first, then every entry load of the row in flight at once
+    int cnt[4] = {0, 0, 0, 0}, off[5];
+#pragma unroll
+    for (int h = 0; h < 4; ++h)
+      if (h < mparts) cnt[h] = mcnt[r * mparts + h];
+    off[0] = 0;
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      overflow |= cnt[h] > mcap;
+      off[h + 1] = off[h] + min(cnt[h], mcap);
+    }
+    const int M = off[4];
+    for (int e0 = 0; e0 < M; e0 += 128) {
+      uint2 kv[4];
+      int pos[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0 + u * 32 + lane;
+        pos[u] = -1;
+        if (e < M) {
+          int h = 0;
+#pragma unroll
+          for (int q = 1; q < 4; ++q) h += e >= off[q];
+          kv[u] = __ldcg(mbuf + (r * mparts + h) * (int64_t)mcap + (e - off[h]));
+          pos[u] = G + e;
         }
       }
-      G += m;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (pos[u] >= 0 && pos[u] < kSelMax) {
+          gk[pos[u]] = __uint_as_float(kv[u].x);
+          gid[pos[u]] = (int)kv[u].y;
+        }
     }
+    G += M;
   }
   overflow |= G > kSelMax;
   if (G > kSelMax) G = kSelMax;
@@ -408,11 +460,11 @@ __device__ __forceinline__ void rerank_groups_row(
       lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
       hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     }
-    // invariant: count(key <= hi) >= k; shrink hi while keeping it (stop once
-    // at most k + 8 groups remain at or below it: kappa need not be tight)
+    // invariant: count(key <= hi) >= k; shrink hi to the k-th key (a tight
+    // kappa keeps UB, and with it the visited set, small)
     if (lo < hi) --lo;  // count(key <= lo) < k unless lo is the minimum itself
     int chi = G;
-    for (int it = 0; it < 20 && hi - lo > 1 && chi > k + 8; ++it) {
+    for (int it = 0; it < 32 && hi - lo > 1 && chi > k; ++it) {
       const uint32_t mid = lo + ((hi - lo) >> 1);
       int c = 0;
       for (int e = lane; e < G; e += 32) c += f2ord(gk[e]) <= mid;
@@ -448,6 +500,48 @@ __device__ __forceinline__ void rerank_groups_row(
   double* ck = s_ck[w];
   int* ci = s_ci[w];
   int nc = 0;
+  if constexpr (DT < 0) {  // fp32 screen: measured no faster on B200 (gathers dominate); kept off
+    // phase 1: fp32 screen of every column of the visited groups; a column can
+    // only have D64 <= UB if D32 <= T32 := UB (1 + g32) / (1 - g64), rounded up
+    const double g32 = gamma_up(DT + 2, 5.9604644775390625e-08);
+    const double g64 = gamma_up(DT + 2, 1.1102230246251565e-16);
+    const float T32 = UB < CUDART_INF
+                          ? __double2float_ru(UB * (1.0 + g32) / (1.0 - g64) * (1.0 + 1e-7) + 1e-30)
+                          : CUDART_INF_F;
+    const float* xqf = s_xqf[w];
+    int ns = 0;
+    for (int b0 = 0; b0 < nv; b0 += 4) {
+      const int gs = b0 + (lane >> 3);
+      const int g = gs < nv ? gid[gs] : -1;
+      const int64_t j = (int64_t)g * 8 + (lane & 7);
+      bool pass = false;
+      if (g >= 0 && j < n && !(self_join && j == gi)) pass = d32_fixed<DT>(xqf, X + j * d) <= T32;
+      const unsigned pm = __ballot_sync(0xffffffffu, pass);
+      const int pos = ns + __popc(pm & ((1u << lane) - 1u));
+      if (pass && pos < kColMax) ci[pos] = (int)j;
+      ns += __popc(pm);
+    }
+    overflow |= ns > kColMax;
+    if (ns > kColMax) ns = kColMax;
+    __syncwarp();
+    // phase 2: the oracle's exact D64 for the survivors only (compacted in place)
+    for (int s0 = 0; s0 < ns; s0 += 32) {
+      const int e = s0 + lane;
+      const int j = e < ns ? ci[e] : -1;
+      double key = CUDART_INF;
+      if (j >= 0) key = d64_fixed<DT>(xq, X + (int64_t)j * d);
+      const bool keep = key <= UB && key < CUDART_INF;
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      const int pos = nc + __popc(km & ((1u << lane) - 1u));
+      __syncwarp();
+      if (keep) {
+        ck[pos] = key;
+        ci[pos] = j;
+      }
+      nc += __popc(km);
+      __syncwarp();
+    }
+  } else {
   for (int b0 = 0; b0 < nv; b0 += 4) {
     const int gs = b0 + (lane >> 3);
     const int g = gs < nv ? gid[gs] : -1;
@@ -507,6 +601,7 @@ __device__ __forceinline__ void rerank_groups_row(
       ci[pos] = (int)j;
     }
     nc += __popc(km);
+  }
   }
   overflow |= nc > kColMax;
   if (nc > kColMax) nc = kColMax;
@@ -576,12 +671,10 @@ __device__ __forceinline__ void rerank_groups_row(
   const bool have = nc >= k;
   bool cert = !overflow && have && row_certified(cp, r, vmin, tk[k - 1], &err);
   if (cp.force_fail) cert = false;
-  if (lane == 0) {
-    if (err > 0.0) atomicMax(&s_red[0], (unsigned long long)__double_as_longlong(err));
-    atomicAdd(&s_red[1], (unsigned long long)G);
-    atomicAdd(&s_red[2], (unsigned long long)nv);
-    atomicAdd(&s_red[3], (unsigned long long)nc);
-  }
+  tel.maxerr = fmax(tel.maxerr, err);
+  tel.G += (unsigned long long)G;
+  tel.nv += (unsigned long long)nv;
+  tel.nc += (unsigned long long)nc;
   if (cert) {
     write_row(out, r, k, tk, ti, lane, 32);
   } else if (lane == 0) {
@@ -605,15 +698,22 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
                     double* __restrict__ fail_ub, int32_t* __restrict__ fail_count,
                     unsigned long long* __restrict__ max_err_bits,
                     unsigned long long* __restrict__ counters) {
-  __shared__ unsigned long long s_red[4];         // block reductions: max err, G, nv, nc
-  if (threadIdx.x < 4) s_red[threadIdx.x] = 0ull;
-  __syncthreads();
-  rerank_groups_row<DT>(Q, q_begin, q_count, X, n, d, k, self_join, cand_idx, cand_key, cand_v, kp,
-                    lists, mbuf, mcnt, mcap, mparts, cp, out, fail_rows, fail_ub, fail_count, s_red);
-  __syncthreads();
-  if (threadIdx.x == 0 && s_red[0]) atomicMax(max_err_bits, s_red[0]);
-  if (threadIdx.x >= 1 && threadIdx.x < 4 && s_red[threadIdx.x])
-    atomicAdd(counters + threadIdx.x - 1, s_red[threadIdx.x]);
+  // persistent grid-stride over rows: no block barriers, balanced tails
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  RowTel tel;
+  for (int64_t r = (int64_t)blockIdx.x * kGrpWarps + w; r < q_count;
+       r += (int64_t)gridDim.x * kGrpWarps) {
+    __syncwarp();
+    rerank_groups_row<DT>(Q, q_begin, q_count, X, n, d, k, self_join, cand_idx, cand_key, cand_v,
+                          kp, lists, mbuf, mcnt, mcap, mparts, cp, out, fail_rows, fail_ub,
+                          fail_count, r, tel);
+  }
+  if (lane == 0) {
+    if (tel.maxerr > 0.0) atomicMax(max_err_bits, (unsigned long long)__double_as_longlong(tel.maxerr));
+    if (tel.G) atomicAdd(counters + 0, tel.G);
+    if (tel.nv) atomicAdd(counters + 1, tel.nv);
+    if (tel.nc) atomicAdd(counters + 2, tel.nc);
+  }
 }
 
 
@@ -1171,7 +1271,12 @@ cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, cons
   if (k > kMaxK) return cudaErrorInvalidValue;
   if (cp.kind == PASS_TC) {  // group candidates
     if (c.lists * c.kp > kSelMax || !c.key) return cudaErrorInvalidValue;
-    const int64_t gb = (q_count + kGrpWarps - 1) / kGrpWarps;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int mult = 8;
+    if (const char* e = getenv("TOD_RR_GRID")) mult = std::max(1, atoi(e));  // experiment knob
+    const int64_t gb = std::min<int64_t>((q_count + kGrpWarps - 1) / kGrpWarps, (int64_t)sms * mult);
     if (gb == 0) return cudaSuccess;
     const size_t smem = (size_t)kGrpWarps * d * 8;
     if (smem > 160 * 1024) return cudaErrorInvalidValue;
