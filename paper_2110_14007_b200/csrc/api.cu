@@ -44,7 +44,7 @@ struct Workspace {
 enum BufId {
   B_X = 0, B_Q, B_IMG_B, B_A2_B, B_E_B, B_IMG_A, B_A2_A, B_E_A, B_MU, B_PART,
   B_G, B_CIDX, B_CV, B_FAIL, B_SMALL, B_IDX, B_DIST, B_DIST64, B_KTH, B_MEAN, B_KD64,
-  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT, B_FAILUB, B_NWRTAU, B_NWRCNT, B_NWRPTR, B_NWRCOLS, B_SCAN, B_ABOD, B_LABELS, B_PRED, B_NBUF
+  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT, B_FAILUB, B_NWRTAU, B_NWRCNT, B_NWRPTR, B_NWRCOLS, B_SCAN, B_ABOD, B_LABELS, B_PRED, B_SAMP, B_NBUF
 };
 static_assert(B_NBUF <= 48, "Workspace::bufs too small");
 
@@ -131,6 +131,7 @@ struct Plan {
   int two;       // TC: two-pass candidate selection (sample pass + append-only main pass)
   int R;         // two-pass: sample stride over 256-column reference tiles
   int main_S;    // two-pass: main-pass reference chunks
+  int kp_target; // two-pass: K' (target count of kept groups)
   int cap;       // two-pass: main-pass buffer slots per (row, column half)
 };
 
@@ -175,6 +176,7 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
     // which appends ~R*kps groups per row.  K' is the target count of kept
     // groups; kps = 2K'/R leaves a wide margin for the sample's variance.
     p->two = 1;
+    p->kp_target = kp;
     p->R = 8;
     if (const char* e = getenv("TOD_SAMPLE_R")) {  // experiment knob (power of two >= 2)
       const int v = atoi(e);
@@ -206,7 +208,7 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
       return sp == 1 ? kp : (sp == 2 ? roundup(kp / 2 + 8, 4) : roundup(kp / 4 + 4, 4));
     };
     int sp = ctx->cfg.epilogue_split;
-    if (p->two && sp == 4) sp = 2;
+    if (p->two && sp == 4) sp = 2;  // measured: 4 lists of K''=4 certify < 98 %
     if (sp != 1 && sp != 2 && sp != 4) {
       sp = 1;
       for (int cand : {4, 2}) {
@@ -398,11 +400,35 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     TOD_TRY(prep_tc(ctx, dX, n, dQ, q_begin, q_count, d, plan.fmt, plan.dpad, g, &A, &B, &cp,
                     launches));
     tm.mark();  // 2: main start
-    TOD_CUDA(launch_knn_tc(A, B, self ? q_begin : 0, q_count, self, plan.fmt, cands,
-                           ctx->num_sms, st, launches));
+    // Two-pass sample: key-only register top-4 per (row, column part) over the
+    // sample tiles (knn_tc3 sample mode), tau = the j-th smallest of those; the
+    // main pass then covers every tile.  TOD_SAMPLE_V1=1 (experiment knob)
+    // keeps the list-based sample pass of knn_tc.cu instead.
+    // Measured on B200: key-only sample wins at d <= 32 (C2 pass 1 1.44 -> 1.35 ms), the
+    // list-based sample at d = 64 (C3 132 vs 137 ms: there the main pass would also
+    // have to cover the sample tiles on the CTA-pair kernel).
+    const char* sv = getenv("TOD_SAMPLE_V1");
+    const bool samp_v1 = plan.two && (sv ? atoi(sv) != 0 : plan.dpad > 32);
+    if (plan.two && !samp_v1) {
+      MainPass sm;
+      sm.S = 1;
+      sm.R = plan.R;
+      sm.parts = tc3_parts(plan.dpad);
+      TOD_TRY(ensure(ctx, B_SAMP, (size_t)std::max<int64_t>(q_count, 1) * sm.parts * 4 * 4, &p));
+      sm.samp = static_cast<float*>(p);
+      TOD_CUDA(launch_knn_tc3(A, B, self ? q_begin : 0, q_count, self, plan.fmt, sm, ctx->num_sms,
+                              0, st, launches));
+      const int j = std::min(4 * sm.parts, std::max(4, (2 * plan.kp_target + plan.R - 1) / plan.R));
+      TOD_CUDA(launch_tau_combine(q_count, sm.parts, j, sm.samp, cands.v, st, launches));
+      cands.lists = 1;
+      cands.kp = 0;
+    } else {
+      TOD_CUDA(launch_knn_tc(A, B, self ? q_begin : 0, q_count, self, plan.fmt, cands,
+                             ctx->num_sms, st, launches));
+    }
     if (plan.two) {
       mp.S = plan.main_S;
-      mp.R = plan.R;
+      mp.R = samp_v1 ? plan.R : 0;
       mp.tau_v = cands.v;
       mp.tau_lists = cands.lists;
       mp.parts = tc3_parts(plan.dpad);
@@ -476,9 +502,9 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     stats->rows = q_count;
     stats->certified = q_count - h.fail_count;
     stats->fallback_rows = h.fail_count;
-    stats->kprime = plan.kp;
+    stats->kprime = plan.two ? plan.kp_target : plan.kp;
     stats->format = plan.fmt;
-    stats->chunks = plan.S;
+    stats->chunks = plan.two ? plan.main_S : plan.S;
     stats->dpad = plan.dpad;
     stats->scale = plan.kind == PASS_TC ? h.g.s : 1.0;
     stats->max_abs_err = h.max_err;

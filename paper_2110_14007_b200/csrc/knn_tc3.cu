@@ -86,11 +86,22 @@ int pick_stages3() {
 
 // Tiles of chunk c: [bt*c/S, bt*(c+1)/S) minus the sample tiles (t % R == 0;
 // R is a power of two, 0 = no sample pass).
+// SMP (sample pass): chunk c covers sample tiles t = si*R, si in [bs*c/S, bs*(c+1)/S).
+template <int SMP>
 struct Seq {
   int t, end;
   int mask;
+  int R;
   bool on;
-  __device__ __forceinline__ void begin(int64_t bt, int S, int R, int c) {
+  __device__ __forceinline__ void begin(int64_t bt, int S, int R_, int c) {
+    R = R_;
+    if constexpr (SMP) {
+      const int64_t bs = (bt + R - 1) / R;
+      t = (int)(bs * c / S) * R;
+      end = (int)(bs * (c + 1) / S) * R;
+      if (end > bt) end = (int)bt;
+      return;
+    }
     on = R > 0;
     mask = R - 1;
     t = (int)(bt * c / S);
@@ -102,6 +113,10 @@ struct Seq {
   }
   __device__ __forceinline__ bool more() const { return t < end; }
   __device__ __forceinline__ void next() {
+    if constexpr (SMP) {
+      t += R;
+      return;
+    }
     ++t;
     skip();
   }
@@ -112,14 +127,15 @@ __device__ __forceinline__ float min8(const float* v) {
                fminf(fminf(v[3], v[4]), fminf(fminf(v[5], v[6]), v[7])));
 }
 
-template <int DPAD, int FMT, int DBG, int FW>
+template <int DPAD, int FMT, int DBG, int FW, int SMP>
 __global__ void __launch_bounds__(64 + 32 * FW, 1)
     k_knn_tc3(const uint8_t* __restrict__ a_img, size_t a_region, size_t a_extra,
               const uint8_t* __restrict__ b_img, size_t b_region, size_t b_extra, int64_t b_tiles,
               int64_t n_ref, int64_t qt0, int64_t n_qtiles, int64_t q_begin, int64_t q_end,
               int self_join, int S, int R, int nstage,
               const float* __restrict__ tau_v, int tau_lists,
-              uint2* __restrict__ mbuf, int* __restrict__ mcnt, int cap) {
+              uint2* __restrict__ mbuf, int* __restrict__ mcnt, int cap,
+              float* __restrict__ samp) {
   using C = Cfg3<DPAD>;
   constexpr int H = FW / 4;        // column parts per tile
   constexpr int BH = kBN / H;      // columns per filter warp per tile
@@ -169,7 +185,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t qtl = item % n_qtiles;
       const int c = (int)(item / n_qtiles);
-      Seq ts;
+      Seq<SMP> ts;
       ts.begin(b_tiles, S, R, c);
       int issued = 0;
       bool a_done = false;
@@ -230,7 +246,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
     uint32_t phase = 0, acc_phase = 0, aphase = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int c = (int)(item / n_qtiles);
-      Seq ts;
+      Seq<SMP> ts;
       ts.begin(b_tiles, S, R, c);
       mbar_wait(a_full, aphase);
       aphase ^= 1;
@@ -302,7 +318,8 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
         }
         pa = pbase;
       };
-      Seq ts;
+      float top[4] = {CUDART_INF_F, CUDART_INF_F, CUDART_INF_F, CUDART_INF_F};  // SMP
+      Seq<SMP> ts;
       ts.begin(b_tiles, S, R, c);
       for (; ts.more(); ts.next()) {
         mbar_wait(&t_full[acc], acc_phase);
@@ -336,6 +353,19 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
         float m[BH / 8];
 #pragma unroll
         for (int g = 0; g < BH / 8; ++g) m[g] = min8(v + 8 * g);
+        if constexpr (SMP) {
+          // sample pass: the 4 smallest group minima of this (row, part), keys
+          // only, by a branch-free insertion network (new_i = min(r_i, max(r_i-1, x)))
+#pragma unroll
+          for (int g = 0; g < BH / 8; ++g) {
+            const float x = m[g];
+            top[3] = fminf(top[3], fmaxf(top[2], x));
+            top[2] = fminf(top[2], fmaxf(top[1], x));
+            top[1] = fminf(top[1], fmaxf(top[0], x));
+            top[0] = fminf(top[0], x);
+          }
+          continue;
+        }
         const int gbase = j0 >> 3;
 #pragma unroll
         for (int hh = 0; hh < BH / 64; ++hh) {
@@ -350,7 +380,14 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
           }
         }
       }
-      flush();
+      if constexpr (SMP) {
+        if (valid) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) samp[(r * H + h) * 4 + i] = top[i];
+        }
+      } else {
+        flush();
+      }
     }
   }
   tc_fence_before();
@@ -361,7 +398,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
   }
 }
 
-template <int DPAD, int FMT, int DBG, int FW>
+template <int DPAD, int FMT, int DBG, int FW, int SMP>
 cudaError_t launch3(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                     bool self_join, const MainPass& m, int num_sms, cudaStream_t st) {
   const int nstage = pick_stages3<DPAD, FW>();
@@ -369,7 +406,7 @@ cudaError_t launch3(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
   if (m.parts != FW / 4) return cudaErrorInvalidValue;
   int a, b, c;
   const int smem = smem3<DPAD, FW>(nstage, &a, &b, &c);
-  auto kern = k_knn_tc3<DPAD, FMT, DBG, FW>;
+  auto kern = k_knn_tc3<DPAD, FMT, DBG, FW, SMP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t qt0 = q_begin / kBM;
@@ -381,11 +418,44 @@ cudaError_t launch3(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
       reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(), A.extra_offset(),
       reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
       B.n_pad / kBN, B.n, qt0, qt1 - qt0, q_begin, q_begin + q_count, self_join ? 1 : 0, m.S,
-      m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap);
+      m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap, m.samp);
   return cudaGetLastError();
 }
 
+// tau_i = the j-th smallest of the row's sample minima (parts x 4 values;
+// +inf when fewer than j are finite, i.e. tiny inputs: keep everything).
+__global__ void k_tau_combine(int64_t q, int parts, int j, const float* __restrict__ samp,
+                              float* __restrict__ tau) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= q) return;
+  float v[16];
+  const int nv = parts * 4;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) v[e] = e < nv ? samp[r * nv + e] : CUDART_INF_F;
+#pragma unroll
+  for (int a = 1; a < 16; ++a)
+#pragma unroll
+    for (int b = a; b > 0; --b) {
+      const float lo = fminf(v[b - 1], v[b]), hi = fmaxf(v[b - 1], v[b]);
+      v[b - 1] = lo;
+      v[b] = hi;
+    }
+  float t = CUDART_INF_F;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) t = (e == j - 1) ? v[e] : t;
+  tau[r] = t;
+}
+
 }  // namespace
+
+cudaError_t launch_tau_combine(int64_t q, int parts, int j, const float* samp, float* tau,
+                               cudaStream_t st, int* launches) {
+  if (q <= 0) return cudaSuccess;
+  if (parts * 4 > 16 || j < 1 || j > parts * 4) return cudaErrorInvalidValue;
+  k_tau_combine<<<(unsigned)((q + 255) / 256), 256, 0, st>>>(q, parts, j, samp, tau);
+  *launches += 1;
+  return cudaGetLastError();
+}
 
 // Filter warps per CTA: 16 (4 per SM sub-partition, 64 columns each) when 3+
 // operand stages still fit in shared memory, else 8.
@@ -410,12 +480,15 @@ cudaError_t launch_knn_tc3(const Image& A, const Image& B, int64_t q_begin, int6
                            cudaStream_t st, int* launches) {
   *launches += 1;
   // dbg (profiling only): 1 = skip the filter work, 2 = also skip the TMEM loads
-#define TOD_TC3_FW(D, FW)                                                                       \
-  if (dbg & 3)                                                                                 \
-    return fmt == 1 ? launch3<D, 1, 2, FW>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
-                    : launch3<D, 2, 2, FW>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
-  return fmt == 1 ? launch3<D, 1, 0, FW>(A, B, q_begin, q_count, self_join, m, num_sms, st)    \
-                  : launch3<D, 2, 0, FW>(A, B, q_begin, q_count, self_join, m, num_sms, st);
+#define TOD_TC3_FW(D, FW)                                                                          \
+  if (m.samp)                                                                                     \
+    return fmt == 1 ? launch3<D, 1, 0, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
+                    : launch3<D, 2, 0, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+  if (dbg & 3)                                                                                    \
+    return fmt == 1 ? launch3<D, 1, 2, FW, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
+                    : launch3<D, 2, 2, FW, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+  return fmt == 1 ? launch3<D, 1, 0, FW, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st)    \
+                  : launch3<D, 2, 0, FW, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st);
 #define TOD_TC3_CASE(D)          \
   case D:                        \
     if (tc3_fw<D>() == 16) {     \

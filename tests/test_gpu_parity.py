@@ -122,6 +122,23 @@ def test_two_pass_parity(pkg, n, d, k, fmt, chunks, pair):
         assert res.stats["certified"] >= 0.99 * n, res.stats
 
 
+@pytest.mark.parametrize("v1", ["0", "1"])
+@pytest.mark.parametrize("d", [32, 64])
+def test_sample_pass_variants_parity(pkg, v1, d):
+    # key-only register sample (knn_tc3 sample mode) and the list-based sample
+    # (knn_tc.cu) at both widths
+    n, k = 15_000, 12
+    X = datagen.gaussian_mixture(n, d, seed=d + 5)
+    os.environ["TOD_SAMPLE_V1"] = v1
+    try:
+        with _ctx(pkg) as ctx:
+            res = ctx.knn(torch.from_numpy(X).cuda(), k)
+    finally:
+        os.environ.pop("TOD_SAMPLE_V1", None)
+    _check_rows(res, X, k, np.arange(n))
+    assert res.stats["certified"] >= 0.99 * n
+
+
 def test_single_and_two_pass_identical(pkg):
     X = datagen.gaussian_mixture(30_000, 32, seed=31)
     Xd = torch.from_numpy(X).cuda()
