@@ -394,13 +394,15 @@ def run_gpu(args):
         # k_knn_tc4 CTA pairs), timed with CUDA events around its launch on the
         # launching stream.  Algorithmic work per (query, reference) pair = 2d
         # flops of the -2XY^T contraction; the main pass covers
-        # every reference column outside the sample tiles (every 8th
-        # 256-column tile), for the rows of this rank.
+        # every reference column (key-only sample, d <= 32) or every column
+        # outside the sample tiles (list sample, d = 64), for this rank's rows.
         rows = tdist.shard_rows(n, world, rank)[1]
         mk = last_stats.get("main_kernel", 0)
         if mk:
             bt = (n + 255) // 256
             samp_cols = sum(min(256, n - 256 * t) for t in range(0, bt, 8))
+            if last_stats.get("sample_pass") == 2:   # key-only sample: main covers every tile
+                samp_cols = 0
             pairs_main = rows * (n - samp_cols)
             kname = {3: "k_knn_tc3 (single-SM tcgen05 main pass)",
                      4: "k_knn_tc4 (CTA-pair tcgen05 cta_group::2 main pass)"}[mk]

@@ -105,6 +105,9 @@ typedef struct {
   int64_t cand_columns;    /* exact distances at or below the per-row bound kept for the final selection */
   float ms_main_kernel;    /* two-pass mode, TOD_F_TIMING: the main-pass kernel alone (ms_main also has the sample pass) */
   int32_t main_kernel;     /* main-pass kernel used: 0 = none (single pass), 3 = single-SM, 4 = CTA pairs */
+  int32_t sample_pass;     /* two-pass sample: 0 = none, 1 = list-based (main pass skips the sample
+                              tiles), 2 = key-only (main pass covers every tile) */
+  int32_t reserved_;
 } tod_stats;
 
 /* Per-neighbour and per-row outputs of the kNN functional operator (P:270,

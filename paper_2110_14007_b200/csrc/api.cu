@@ -343,6 +343,7 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
   const bool self = dQ == nullptr;
   bool main_timed = false;
   int main_kernel = 0;
+  int sample_pass = 0;
   Plan plan;
   TOD_TRY(make_plan(ctx, n, q_count, d, k, &plan));
   cudaStream_t st = ctx->stream;
@@ -409,6 +410,7 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     // have to cover the sample tiles on the CTA-pair kernel).
     const char* sv = getenv("TOD_SAMPLE_V1");
     const bool samp_v1 = plan.two && (sv ? atoi(sv) != 0 : plan.dpad > 32);
+    if (plan.two) sample_pass = samp_v1 ? 1 : 2;
     if (plan.two && !samp_v1) {
       MainPass sm;
       sm.S = 1;
@@ -509,6 +511,7 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     stats->scale = plan.kind == PASS_TC ? h.g.s : 1.0;
     stats->max_abs_err = h.max_err;
     stats->main_kernel = main_kernel;
+    stats->sample_pass = sample_pass;
     stats->ms_main_kernel = 0.f;
     if (main_timed) cudaEventElapsedTime(&stats->ms_main_kernel, ctx->evk[0], ctx->evk[1]);
     stats->cand_groups = (int64_t)h.counters[0];

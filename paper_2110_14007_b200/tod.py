@@ -54,7 +54,8 @@ class Stats(ctypes.Structure):
                 ("ms_total", ctypes.c_float), ("kernel_launches", ctypes.c_int64),
                 ("cand_groups", ctypes.c_int64), ("visited_groups", ctypes.c_int64),
                 ("cand_columns", ctypes.c_int64), ("ms_main_kernel", ctypes.c_float),
-                ("main_kernel", ctypes.c_int32)]
+                ("main_kernel", ctypes.c_int32), ("sample_pass", ctypes.c_int32),
+                ("reserved_", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
