@@ -38,6 +38,8 @@ CONFIGS = {
     "c2": (100_000, 32, 20, True, "auto", "C2: kNN+LOF n=100000 d=32 k=20"),
     "c3": (1_000_000, 64, 10, False, "bf16", "C3: kNN n=1000000 d=64 k=10 bf16 PQ path"),
     "c3f16": (1_000_000, 64, 10, False, "fp16", "C3 shape, fp16 PQ path"),
+    "c5": (2_000_000, 512, 50, False, "fp16", "C5: kNN n=2000000 d=512 k=50 (tensor-bound regime)"),
+    "c5s": (500_000, 512, 50, False, "fp16", "C5 shape at n=500000 (1-GPU sample of C5)"),
     # NEXT-2: NWR on the C2-shaped data; phi = 12 on the squared
     # distance (86 % of rows have no neighbour, mean 39, max ~1900: the paper's
     # "preset distance threshold (usually a small number)")

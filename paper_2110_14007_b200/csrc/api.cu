@@ -142,9 +142,9 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
   p->fmt = fmt;
   p->kind = fmt == TOD_FMT_FP32 ? PASS_SIMT : PASS_TC;
   if (p->kind == PASS_TC) {
-    if (d > 128)
-      return fail(ctx, TOD_E_UNSUPPORTED, "tensor-core pass supports d <= 128 in this build (d=%d)", d);
-    p->dpad = d <= 16 ? 16 : d <= 32 ? 32 : d <= 64 ? 64 : 128;
+    if (d > 512)
+      return fail(ctx, TOD_E_UNSUPPORTED, "tensor-core pass supports d <= 512 in this build (d=%d)", d);
+    p->dpad = d <= 16 ? 16 : d <= 32 ? 32 : d <= 64 ? 64 : d <= 128 ? 128 : d <= 256 ? 256 : 512;
   } else {
     if (d > 64) return fail(ctx, TOD_E_UNSUPPORTED, "fp32 SIMT pass supports d <= 64 (d=%d)", d);
     p->dpad = d;
@@ -169,8 +169,8 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
   p->cap = 0;
   const int64_t bt256 = (n_ref + 255) / 256;
   int64_t bt_v1 = 0;  // reference tiles seen by the v1 kernel (the sample pass: every R-th)
-  if (p->kind == PASS_TC && !(ctx->cfg.flags & TOD_F_PASS1_V1) && p->dpad <= 64 &&
-      tc3_fits(p->dpad) && bt256 >= 32) {
+  if (p->kind == PASS_TC && !(ctx->cfg.flags & TOD_F_PASS1_V1) && tc3_fits(p->dpad) &&
+      (bt256 >= 32 || p->dpad > 128)) {
     // Two-pass candidate selection: the sample pass keeps kps
     // groups per row over every R-th tile; its threshold filters the main pass,
     // which appends ~R*kps groups per row.  K' is the target count of kept
@@ -188,6 +188,8 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
     p->cap = roundup(std::max(64, 2 * (p->R - 1) * kps), 32);
     bt_v1 = (bt256 + p->R - 1) / p->R;
   }
+  if (p->kind == PASS_TC && !p->two && p->dpad > 128)
+    return fail(ctx, TOD_E_UNSUPPORTED, "d=%d needs the two-pass tensor-core path", d);
   if (p->kind == PASS_TC && !p->two && p->dpad <= 64) bt_v1 = bt256;
   if (p->kind == PASS_TC) {
     // Reference chunks: each chunk's operand image should stay L2-resident
@@ -409,7 +411,7 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     // list-based sample at d = 64 (C3 132 vs 137 ms: there the main pass would also
     // have to cover the sample tiles on the CTA-pair kernel).
     const char* sv = getenv("TOD_SAMPLE_V1");
-    const bool samp_v1 = plan.two && (sv ? atoi(sv) != 0 : plan.dpad > 32);
+    const bool samp_v1 = plan.two && plan.dpad <= 128 && (sv ? atoi(sv) != 0 : plan.dpad == 64);
     if (plan.two) sample_pass = samp_v1 ? 1 : 2;
     if (plan.two && !samp_v1) {
       MainPass sm;

@@ -60,15 +60,21 @@ struct Cfg3 {
   static constexpr int B_BYTES = kBN * (DPAD + 16) * 2;
   static constexpr int B_STRIDE = align_up(B_BYTES, 1024);
   static constexpr int B_EXTRA = kBN * NKB * RB;
+  // K-pipelined mode (dpad > 64): A and B both streamed, one 64-element K
+  // region (or the 16-wide extra block) per ring stage.
+  static constexpr bool KP = DPAD > 64;
+  static constexpr int KS_A = kBM * 128;                 // A slice of a region (SW128)
+  static constexpr int KS_BYTES = kBM * 128 + kBN * 128; // 48 KB
+  static constexpr int KX_BYTES = kBM * 32 + kBN * 32;   // extra-block stage
 };
 
 // FW filter warps: 4 lane quarters x FW/4 column parts of every 256-column tile.
 template <int DPAD, int FW>
 __host__ __device__ constexpr int smem3(int nstage, int* off_b, int* off_p, int* off_bar) {
   using C = Cfg3<DPAD>;
-  int o = C::A_STRIDE;
+  int o = C::KP ? 0 : C::A_STRIDE;
   *off_b = o;
-  o += nstage * C::B_STRIDE;
+  o += nstage * (C::KP ? C::KS_BYTES : C::B_STRIDE);
   *off_p = o;
   o += FW * kPend * 32 * 8;
   *off_bar = o;
@@ -178,7 +184,85 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
   const uint32_t tmem_base = *tmem_slot;
   const int64_t n_items = n_qtiles * S;
 
-  if (warp == 0) {
+  if (warp == 0 && C::KP) {
+    // ---------------------------------------- producer, K-pipelined (dpad > 64)
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int64_t qtl = item % n_qtiles;
+      const int c = (int)(item / n_qtiles);
+      Seq<SMP> ts;
+      ts.begin(b_tiles, S, R, c);
+      for (; ts.more(); ts.next()) {
+        const int64_t t = ts.t;
+        for (int kb = 0; kb <= C::NKB; ++kb) {
+          mbar_wait_backoff(&empty[stage], phase ^ 1);
+          if (elect_one()) {
+            uint8_t* dst = sB + stage * C::KS_BYTES;
+            if (kb < C::NKB) {
+              mbar_arrive_expect_tx(&full[stage], C::KS_BYTES);
+              bulk_g2s(dst, a_img + kb * a_region + qtl * (int64_t)kBM * 128, kBM * 128, &full[stage]);
+              bulk_g2s(dst + C::KS_A, b_img + kb * b_region + t * (int64_t)kBN * 128, kBN * 128,
+                       &full[stage]);
+            } else {
+              mbar_arrive_expect_tx(&full[stage], C::KX_BYTES);
+              bulk_g2s(dst, a_img + a_extra + qtl * (int64_t)kBM * kExtraRB, kBM * kExtraRB,
+                       &full[stage]);
+              bulk_g2s(dst + kBM * kExtraRB, b_img + b_extra + t * (int64_t)kBN * kExtraRB,
+                       kBN * kExtraRB, &full[stage]);
+            }
+          }
+          __syncwarp();
+          if (++stage == nstage) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1 && C::KP) {
+    // ------------------------------------------- MMA issuer, K-pipelined
+    constexpr uint32_t IDESC = idesc_f16(kBM, kBN, FMT == 1 ? 0u : 1u);
+    const uint32_t s_base = smem_u32(sB);
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int c = (int)(item / n_qtiles);
+      Seq<SMP> ts;
+      ts.begin(b_tiles, S, R, c);
+      for (; ts.more(); ts.next()) {
+        mbar_wait(&t_empty[acc], acc_phase ^ 1);
+        for (int kb = 0; kb <= C::NKB; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = s_base + stage * C::KS_BYTES;
+          if (elect_one()) {
+            if (kb < C::NKB) {
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks)
+                tc_mma_f16(tmem_base + acc * kBN, smem_desc(a0 + ks * 32, 8 * 128, 2),
+                           smem_desc(a0 + C::KS_A + ks * 32, 8 * 128, 2), IDESC,
+                           (kb > 0 || ks > 0) ? 1u : 0u);
+            } else {
+              tc_mma_f16(tmem_base + acc * kBN, smem_desc(a0, 8 * kExtraRB, 6),
+                         smem_desc(a0 + kBM * kExtraRB, 8 * kExtraRB, 6), IDESC, 1u);
+              tc_commit(&t_full[acc]);
+            }
+            tc_commit(&empty[stage]);
+          }
+          __syncwarp();
+          if (++stage == nstage) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 0) {
     // -------------------------------------------------------------- producer
     int stage = 0;
     uint32_t phase = 0, aphase = 0;
@@ -469,6 +553,9 @@ int tc3_parts(int dpad) {
     case 16: return tc3_fw<16>() / 4;
     case 32: return tc3_fw<32>() / 4;
     case 64: return tc3_fw<64>() / 4;
+    case 128: return tc3_fw<128>() / 4;
+    case 256: return tc3_fw<256>() / 4;
+    case 512: return tc3_fw<512>() / 4;
   }
   return 0;
 }
@@ -500,6 +587,9 @@ cudaError_t launch_knn_tc3(const Image& A, const Image& B, int64_t q_begin, int6
     TOD_TC3_CASE(16)
     TOD_TC3_CASE(32)
     TOD_TC3_CASE(64)
+    TOD_TC3_CASE(128)
+    TOD_TC3_CASE(256)
+    TOD_TC3_CASE(512)
   }
 #undef TOD_TC3_CASE
 #undef TOD_TC3_FW

@@ -122,6 +122,21 @@ def test_two_pass_parity(pkg, n, d, k, fmt, chunks, pair):
         assert res.stats["certified"] >= 0.99 * n, res.stats
 
 
+@pytest.mark.parametrize("n,d,k", [
+    (3000, 200, 10),     # dpad 256, small n: two-pass forced (K-pipelined main pass)
+    (12_000, 100, 12),   # dpad 128, K-pipelined two-pass
+    (9000, 512, 20),     # dpad 512 (C5 width)
+    (2000, 300, 50),     # C5's k
+])
+def test_high_dimensional_parity(pkg, n, d, k):
+    X = datagen.gaussian_mixture(n, d, seed=n + d)
+    with _ctx(pkg) as ctx:
+        res = ctx.knn(torch.from_numpy(X).cuda(), k)
+    rows = np.arange(n) if n <= 3000 else np.random.default_rng(0).choice(n, 400, replace=False)
+    _check_rows(res, X, k, np.sort(rows))
+    assert res.stats["certified"] >= 0.95 * n, res.stats
+
+
 @pytest.mark.parametrize("v1", ["0", "1"])
 @pytest.mark.parametrize("d", [32, 64])
 def test_sample_pass_variants_parity(pkg, v1, d):
@@ -416,3 +431,30 @@ def test_forced_fallback_more_rows_than_grid_y(pkg):
     assert res.stats["fallback_rows"] == n
     rows = np.random.default_rng(0).choice(n, 64, replace=False)
     _check_rows(res, X, k, rows)
+
+
+@pytest.mark.parametrize("dt", ["float16", "bfloat16"])
+def test_tensor_core_accumulation_model(pkg, dt):
+    # Reading A9: the certificate bounds the fp32 tensor-core accumulation error
+    # by gamma_m(2^-23) sum|A B| with m = 5 ceil(K/16) + 2.  Guard it on this
+    # device: the measured worst error (cancellation-heavy and wide-range
+    # operands, fp16/bf16 -> fp32 tcgen05 GEMMs) must stay below half the model.
+    dtype = getattr(torch, dt)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    for K in (48, 80, 144, 528):
+        m = 5 * ((K + 15) // 16) + 2
+        model = m * 2.0            # gamma_m(2^-23) in units of 2^-24 (first order)
+        worst = 0.0
+        for trial in range(3):
+            A = torch.randn(1024, K, generator=g, device="cuda")
+            B = torch.randn(1024, K, generator=g, device="cuda")
+            if trial == 1:
+                A, B = A + 30, -(B + 30)
+            if trial == 2:
+                A = A * torch.exp2(torch.randint(-8, 8, A.shape, generator=g, device="cuda").float())
+            A, B = A.to(dtype), B.to(dtype)
+            C = torch.mm(A, B.t(), out_dtype=torch.float32).double()
+            Ad, Bd = A.double(), B.double()
+            err = (C - Ad @ Bd.t()).abs() / (Ad.abs() @ Bd.abs().t() * 2.0 ** -24)
+            worst = max(worst, err.max().item())
+        assert worst < model / 2, (K, worst, model)
