@@ -151,10 +151,12 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
   }
   int kp = ctx->cfg.kprime;
   const int kmax_list = p->kind == PASS_TC ? 64 : 128;
+  int kp_policy = kp;  // uncapped (the two-pass main pass has no list capacity)
   if (kp <= 0) {
     if (fmt == TOD_FMT_FP16) kp = roundup(k + 24, 8);
     else if (fmt == TOD_FMT_BF16) kp = roundup(std::max(6 * k, k + 40), 16);
     else kp = roundup(std::max(k + 8, 16), 8);
+    kp_policy = kp;
     kp = std::min(kp, kmax_list);
   }
   if (kp < k) kp = k;  // never fewer candidates than outputs
@@ -176,7 +178,7 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
     // which appends ~R*kps groups per row.  K' is the target count of kept
     // groups; kps = 2K'/R leaves a wide margin for the sample's variance.
     p->two = 1;
-    p->kp_target = kp;
+    p->kp_target = std::max(kp, kp_policy);
     p->R = 8;
     if (const char* e = getenv("TOD_SAMPLE_R")) {  // experiment knob (power of two >= 2)
       const int v = atoi(e);
@@ -418,12 +420,17 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
       sm.S = 1;
       sm.R = plan.R;
       sm.parts = tc3_parts(plan.dpad);
-      TOD_TRY(ensure(ctx, B_SAMP, (size_t)std::max<int64_t>(q_count, 1) * sm.parts * 4 * 4, &p));
+      // tau = the j-th smallest sample minimum, j ~ 2K'/R; 8 per (row, part) when
+      // 4 per part cannot supply j (large k)
+      const int jw = std::max(4, (2 * plan.kp_target + plan.R - 1) / plan.R);
+      sm.samp_t = jw > 3 * sm.parts ? 8 : 4;
+      const int nv = sm.parts * sm.samp_t;
+      TOD_TRY(ensure(ctx, B_SAMP, (size_t)std::max<int64_t>(q_count, 1) * nv * 4, &p));
       sm.samp = static_cast<float*>(p);
       TOD_CUDA(launch_knn_tc3(A, B, self ? q_begin : 0, q_count, self, plan.fmt, sm, ctx->num_sms,
                               0, st, launches));
-      const int j = std::min(4 * sm.parts, std::max(4, (2 * plan.kp_target + plan.R - 1) / plan.R));
-      TOD_CUDA(launch_tau_combine(q_count, sm.parts, j, sm.samp, cands.v, st, launches));
+      const int j = std::min(nv, jw);
+      TOD_CUDA(launch_tau_combine(q_count, nv, j, sm.samp, cands.v, st, launches));
       cands.lists = 1;
       cands.kp = 0;
     } else {

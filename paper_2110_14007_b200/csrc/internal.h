@@ -91,10 +91,11 @@ struct MainPass {
   int* cnt = nullptr;         // [q_count][parts] appended counts (may exceed cap = overflow)
   int cap = 0;
   int parts = 2;              // column parts per tile (one buffer per (row, part))
-  float* samp = nullptr;      // sample mode (knn_tc3 only): [q_count][parts][4] smallest group
-                              // minima over the sample tiles t = 0, R, 2R, ... (no appends)
+  float* samp = nullptr;      // sample mode (knn_tc3 only): [q_count][parts][samp_t] smallest
+                              // group minima over the sample tiles t = 0, R, 2R, ... (no appends)
+  int samp_t = 4;             // 4 or 8
 };
-cudaError_t launch_tau_combine(int64_t q, int parts, int j, const float* samp, float* tau,
+cudaError_t launch_tau_combine(int64_t q, int nv, int j, const float* samp, float* tau,
                                cudaStream_t st, int* launches);
 int tc3_fits(int dpad);
 int tc3_parts(int dpad);      // column parts (= filter warps / 4) the main pass uses

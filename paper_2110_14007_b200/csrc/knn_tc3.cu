@@ -402,7 +402,10 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
         }
         pa = pbase;
       };
-      float top[4] = {CUDART_INF_F, CUDART_INF_F, CUDART_INF_F, CUDART_INF_F};  // SMP
+      constexpr int T = SMP > 0 ? SMP : 1;  // sample pass: T smallest minima per (row, part)
+      float top[T];
+#pragma unroll
+      for (int i = 0; i < T; ++i) top[i] = CUDART_INF_F;
       Seq<SMP> ts;
       ts.begin(b_tiles, S, R, c);
       for (; ts.more(); ts.next()) {
@@ -438,14 +441,13 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
 #pragma unroll
         for (int g = 0; g < BH / 8; ++g) m[g] = min8(v + 8 * g);
         if constexpr (SMP) {
-          // sample pass: the 4 smallest group minima of this (row, part), keys
+          // sample pass: the T smallest group minima of this (row, part), keys
           // only, by a branch-free insertion network (new_i = min(r_i, max(r_i-1, x)))
 #pragma unroll
           for (int g = 0; g < BH / 8; ++g) {
             const float x = m[g];
-            top[3] = fminf(top[3], fmaxf(top[2], x));
-            top[2] = fminf(top[2], fmaxf(top[1], x));
-            top[1] = fminf(top[1], fmaxf(top[0], x));
+#pragma unroll
+            for (int i = T - 1; i > 0; --i) top[i] = fminf(top[i], fmaxf(top[i - 1], x));
             top[0] = fminf(top[0], x);
           }
           continue;
@@ -467,7 +469,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
       if constexpr (SMP) {
         if (valid) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) samp[(r * H + h) * 4 + i] = top[i];
+          for (int i = 0; i < T; ++i) samp[(r * H + h) * T + i] = top[i];
         }
       } else {
         flush();
@@ -508,16 +510,15 @@ cudaError_t launch3(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
 
 // tau_i = the j-th smallest of the row's sample minima (parts x 4 values;
 // +inf when fewer than j are finite, i.e. tiny inputs: keep everything).
-__global__ void k_tau_combine(int64_t q, int parts, int j, const float* __restrict__ samp,
+__global__ void k_tau_combine(int64_t q, int nv, int j, const float* __restrict__ samp,
                               float* __restrict__ tau) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= q) return;
-  float v[16];
-  const int nv = parts * 4;
+  float v[32];
 #pragma unroll
-  for (int e = 0; e < 16; ++e) v[e] = e < nv ? samp[r * nv + e] : CUDART_INF_F;
+  for (int e = 0; e < 32; ++e) v[e] = e < nv ? samp[r * nv + e] : CUDART_INF_F;
 #pragma unroll
-  for (int a = 1; a < 16; ++a)
+  for (int a = 1; a < 32; ++a)
 #pragma unroll
     for (int b = a; b > 0; --b) {
       const float lo = fminf(v[b - 1], v[b]), hi = fmaxf(v[b - 1], v[b]);
@@ -526,17 +527,17 @@ __global__ void k_tau_combine(int64_t q, int parts, int j, const float* __restri
     }
   float t = CUDART_INF_F;
 #pragma unroll
-  for (int e = 0; e < 16; ++e) t = (e == j - 1) ? v[e] : t;
+  for (int e = 0; e < 32; ++e) t = (e == j - 1) ? v[e] : t;
   tau[r] = t;
 }
 
 }  // namespace
 
-cudaError_t launch_tau_combine(int64_t q, int parts, int j, const float* samp, float* tau,
+cudaError_t launch_tau_combine(int64_t q, int nv, int j, const float* samp, float* tau,
                                cudaStream_t st, int* launches) {
   if (q <= 0) return cudaSuccess;
-  if (parts * 4 > 16 || j < 1 || j > parts * 4) return cudaErrorInvalidValue;
-  k_tau_combine<<<(unsigned)((q + 255) / 256), 256, 0, st>>>(q, parts, j, samp, tau);
+  if (nv > 32 || j < 1 || j > nv) return cudaErrorInvalidValue;
+  k_tau_combine<<<(unsigned)((q + 255) / 256), 256, 0, st>>>(q, nv, j, samp, tau);
   *launches += 1;
   return cudaGetLastError();
 }
@@ -568,9 +569,12 @@ cudaError_t launch_knn_tc3(const Image& A, const Image& B, int64_t q_begin, int6
   *launches += 1;
   // dbg (profiling only): 1 = skip the filter work, 2 = also skip the TMEM loads
 #define TOD_TC3_FW(D, FW)                                                                          \
+  if (m.samp && m.samp_t == 8)                                                                    \
+    return fmt == 1 ? launch3<D, 1, 0, FW, 8>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
+                    : launch3<D, 2, 0, FW, 8>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
   if (m.samp)                                                                                     \
-    return fmt == 1 ? launch3<D, 1, 0, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
-                    : launch3<D, 2, 0, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+    return fmt == 1 ? launch3<D, 1, 0, FW, 4>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
+                    : launch3<D, 2, 0, FW, 4>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
   if (dbg & 3)                                                                                    \
     return fmt == 1 ? launch3<D, 1, 2, FW, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
                     : launch3<D, 2, 2, FW, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st); \

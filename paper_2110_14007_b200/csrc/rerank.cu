@@ -333,17 +333,21 @@ __device__ __forceinline__ void ldg8(const float* p, float* v) {
 // (shared-memory broadcast); the sum stays sequential in c, no FMA.
 template <int DT>
 __device__ __forceinline__ double d64_fixed(const double* __restrict__ xq, const float* xj) {
-  float v[DT];
-#pragma unroll
-  for (int u = 0; u < DT / 8; ++u) ldg8(xj + 8 * u, v + 8 * u);
+  constexpr int CH = DT < 64 ? DT : 64;  // dims per chunk held in registers
   double acc = 0.0;
+#pragma unroll 1
+  for (int cb = 0; cb < DT; cb += CH) {
+    float v[CH];
 #pragma unroll
-  for (int c = 0; c < DT; c += 2) {
-    const double2 q2 = *reinterpret_cast<const double2*>(xq + c);
-    double t = __dsub_rn(q2.x, (double)v[c]);
-    acc = __dadd_rn(acc, __dmul_rn(t, t));
-    t = __dsub_rn(q2.y, (double)v[c + 1]);
-    acc = __dadd_rn(acc, __dmul_rn(t, t));
+    for (int u = 0; u < CH / 8; ++u) ldg8(xj + cb + 8 * u, v + 8 * u);
+#pragma unroll
+    for (int c = 0; c < CH; c += 2) {
+      const double2 q2 = *reinterpret_cast<const double2*>(xq + cb + c);
+      double t = __dsub_rn(q2.x, (double)v[c]);
+      acc = __dadd_rn(acc, __dmul_rn(t, t));
+      t = __dsub_rn(q2.y, (double)v[c + 1]);
+      acc = __dadd_rn(acc, __dmul_rn(t, t));
+    }
   }
   return acc;
 }
@@ -969,6 +973,7 @@ __global__ void __launch_bounds__(kFbThreads)
   }
   __syncthreads();
   const int64_t j_lo = n * p / P, j_hi = n * (p + 1) / P;
+  const bool vec8 = (d & 7) == 0 && (reinterpret_cast<uintptr_t>(X) & 31) == 0;
   for (int64_t jb = j_lo; jb < j_hi; jb += kFbThreads) {
     const int64_t j = jb + t;
     double acc[kFbQB];
@@ -976,12 +981,28 @@ __global__ void __launch_bounds__(kFbThreads)
     for (int q = 0; q < kFbQB; ++q) acc[q] = 0.0;
     if (j < j_hi) {
       const float* xj = X + j * d;
-      for (int c = 0; c < d; ++c) {  // O1 per row: ascending c, no FMA
-        const double xv = (double)__ldg(xj + c);
+      if (vec8) {  // 32-byte loads, 8 dims at a time, same per-row order
+        for (int c8 = 0; c8 < d; c8 += 8) {
+          float v[8];
+          ldg8(xj + c8, v);
 #pragma unroll
-        for (int q = 0; q < kFbQB; ++q) {
-          const double tt = __dsub_rn(s_q[q * d + c], xv);
-          acc[q] = __dadd_rn(acc[q], __dmul_rn(tt, tt));
+          for (int u = 0; u < 8; ++u) {
+            const double xv = (double)v[u];
+#pragma unroll
+            for (int q = 0; q < kFbQB; ++q) {
+              const double tt = __dsub_rn(s_q[q * d + c8 + u], xv);
+              acc[q] = __dadd_rn(acc[q], __dmul_rn(tt, tt));
+            }
+          }
+        }
+      } else {
+        for (int c = 0; c < d; ++c) {  // O1 per row: ascending c, no FMA
+          const double xv = (double)__ldg(xj + c);
+#pragma unroll
+          for (int q = 0; q < kFbQB; ++q) {
+            const double tt = __dsub_rn(s_q[q * d + c], xv);
+            acc[q] = __dadd_rn(acc[q], __dmul_rn(tt, tt));
+          }
         }
       }
     }
@@ -1297,7 +1318,10 @@ cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, cons
     const bool al = ((reinterpret_cast<uintptr_t>(X) & 31) == 0);
     auto kern = (al && d == 16) ? k_rerank_groups<16>
               : (al && d == 32) ? k_rerank_groups<32>
-              : (al && d == 64) ? k_rerank_groups<64> : k_rerank_groups<0>;
+              : (al && d == 64) ? k_rerank_groups<64>
+              : (al && d == 128) ? k_rerank_groups<128>
+              : (al && d == 256) ? k_rerank_groups<256>
+              : (al && d == 512) ? k_rerank_groups<512> : k_rerank_groups<0>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<(unsigned)gb, kGrpWarps * 32, smem, st>>>(
