@@ -67,22 +67,30 @@ __device__ __forceinline__ double acc_gamma(int dpad) {
 // squared distances).  Lane-parallel over m; lane 0 does the sequential sums.
 __device__ void write_row(const KnnOutDev& out, int64_t r, int k, const double* keys,
                           const int* ids, int lane, int nlanes) {
-  for (int m = lane; m < k; m += nlanes) {
-    const double dd = __dsqrt_rn(keys[m]);
-    if (out.idx) out.idx[r * k + m] = ids[m];
-    if (out.dist64) out.dist64[r * k + m] = dd;
-    if (out.dist) out.dist[r * k + m] = __double2float_rn(dd);
-  }
-  if (lane == 0) {
-    const double kth = __dsqrt_rn(keys[k - 1]);
-    if (out.kdist64) out.kdist64[r] = kth;
-    if (out.score_kth) out.score_kth[r] = __double2float_rn(kth);
+  // Called by one full warp (nlanes == 32).  Each square root is taken once,
+  // by the lane that owns the rank; the mean is summed in rank order through
+  // shuffles (the oracle's sequential order, O3).
+  (void)nlanes;
+  double acc = 0.0;
+  for (int m0 = 0; m0 < k; m0 += 32) {
+    const int m = m0 + lane;
+    double dd = 0.0;
+    if (m < k) {
+      dd = __dsqrt_rn(keys[m]);
+      if (out.idx) out.idx[r * k + m] = ids[m];
+      if (out.dist64) out.dist64[r * k + m] = dd;
+      if (out.dist) out.dist[r * k + m] = __double2float_rn(dd);
+      if (m == k - 1) {
+        if (out.kdist64) out.kdist64[r] = dd;
+        if (out.score_kth) out.score_kth[r] = __double2float_rn(dd);
+      }
+    }
     if (out.score_mean) {
-      double acc = 0.0;
-      for (int m = 0; m < k; ++m) acc = __dadd_rn(acc, __dsqrt_rn(keys[m]));
-      out.score_mean[r] = __double2float_rn(__ddiv_rn(acc, (double)k));
+      const int cnt = k - m0 < 32 ? k - m0 : 32;
+      for (int t = 0; t < cnt; ++t) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, dd, t));
     }
   }
+  if (lane == 0 && out.score_mean) out.score_mean[r] = __double2float_rn(__ddiv_rn(acc, (double)k));
 }
 
 // Lower bound, in original units, on the exact squared distance rho^2 of row r
@@ -281,6 +289,25 @@ __device__ __forceinline__ float ord2f(uint32_t o) {
   return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
 }
 
+// Warp bitonic sort of 32 (key, id) pairs, one per lane, ascending by (key, id).
+__device__ __forceinline__ void warp_sort32(double& key, int& id, int lane) {
+#pragma unroll
+  for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      const double ok = __shfl_xor_sync(0xffffffffu, key, j);
+      const int oi = __shfl_xor_sync(0xffffffffu, id, j);
+      const bool up = (lane & kk) == 0;
+      const bool lower = (lane & j) == 0;
+      const bool other_less = key_less(ok, oi, key, id);
+      if ((lower == up) ? other_less : !other_less) {
+        key = ok;
+        id = oi;
+      }
+    }
+  }
+}
+
 // Warp bitonic sort of 64 (key, id) pairs, 2 per lane (element p = 2*lane + e),
 // ascending by (key, id); empty slots carry (+inf, INT32_MAX).
 __device__ __forceinline__ void warp_sort64(double (&k)[2], int (&id)[2], int lane) {
@@ -467,7 +494,17 @@ __device__ __forceinline__ void rerank_groups_row(
   double UB = CUDART_INF;
   if (G >= k) {
     uint32_t lo = 0xFFFFFFFFu, hi = 0u;
-    for (int e = lane; e < G; e += 32) {
+    uint32_t ok[8];  // this lane's ordered keys (G <= 256), 0xFFFFFFFF = none
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = lane + 32 * u;
+      ok[u] = (e < G) ? f2ord(gk[e]) : 0xFFFFFFFFu;
+      if (e < G) {
+        lo = min(lo, ok[u]);
+        hi = max(hi, ok[u]);
+      }
+    }
+    for (int e = lane + 256; e < G; e += 32) {
       const uint32_t o = f2ord(gk[e]);
       lo = min(lo, o);
       hi = max(hi, o);
@@ -484,7 +521,9 @@ __device__ __forceinline__ void rerank_groups_row(
     for (int it = 0; it < 32 && hi - lo > 1 && chi > k; ++it) {
       const uint32_t mid = lo + ((hi - lo) >> 1);
       int c = 0;
-      for (int e = lane; e < G; e += 32) c += f2ord(gk[e]) <= mid;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) c += ok[u] <= mid;
+      for (int e = lane + 256; e < G; e += 32) c += f2ord(gk[e]) <= mid;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
       if (c >= k) {
@@ -626,7 +665,15 @@ __device__ __forceinline__ void rerank_groups_row(
   // ---- 3. the k smallest by (D64, index)
   double* tk = s_tk[w];
   int* ti = s_ti[w];
-  if (nc <= 64) {
+  if (nc <= 32) {
+    double kk1 = lane < nc ? ck[lane] : CUDART_INF;
+    int ii1 = lane < nc ? ci[lane] : INT32_MAX;
+    warp_sort32(kk1, ii1, lane);
+    if (lane < k) {
+      tk[lane] = kk1;
+      ti[lane] = ii1;
+    }
+  } else if (nc <= 64) {
     double kk[2];
     int ii[2];
 #pragma unroll
