@@ -40,6 +40,7 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBN = 256;
+static_assert(kBN == 256, "filter addresses accumulators as acc << 8");
 constexpr int kExtraRB = 32;
 constexpr int kSmemMax = 232448;
 constexpr int kMaxStage = 4;
@@ -93,7 +94,7 @@ int pick_stages3() {
 // Tiles of chunk c: [bt*c/S, bt*(c+1)/S) minus the sample tiles (t % R == 0;
 // R is a power of two, 0 = no sample pass).
 // SMP (sample pass): chunk c covers sample tiles t = si*R, si in [bs*c/S, bs*(c+1)/S).
-template <int SMP>
+template <int SMP, int SKIP = 1>
 struct Seq {
   int t, end;
   int mask;
@@ -115,7 +116,8 @@ struct Seq {
     skip();
   }
   __device__ __forceinline__ void skip() {
-    if (on && (t & mask) == 0) ++t;
+    if constexpr (SKIP)
+      if (on && (t & mask) == 0) ++t;
   }
   __device__ __forceinline__ bool more() const { return t < end; }
   __device__ __forceinline__ void next() {
@@ -133,7 +135,9 @@ __device__ __forceinline__ float min8(const float* v) {
                fminf(fminf(v[3], v[4]), fminf(fminf(v[5], v[6]), v[7])));
 }
 
-template <int DPAD, int FMT, int DBG, int FW, int SMP>
+// MODE: 0 = main pass over every tile, 1 = main pass skipping the sample tiles
+// (t % R == 0), 4 / 8 = sample pass keeping that many minima per (row, part).
+template <int DPAD, int FMT, int DBG, int FW, int MODE>
 __global__ void __launch_bounds__(64 + 32 * FW, 1)
     k_knn_tc3(const uint8_t* __restrict__ a_img, size_t a_region, size_t a_extra,
               const uint8_t* __restrict__ b_img, size_t b_region, size_t b_extra, int64_t b_tiles,
@@ -143,6 +147,8 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
               uint2* __restrict__ mbuf, int* __restrict__ mcnt, int cap,
               float* __restrict__ samp) {
   using C = Cfg3<DPAD>;
+  constexpr int SMP = MODE >= 4 ? MODE : 0;
+  constexpr int SKIP = MODE == 1 ? 1 : 0;
   constexpr int H = FW / 4;        // column parts per tile
   constexpr int BH = kBN / H;      // columns per filter warp per tile
   extern __shared__ uint8_t smem_raw[];
@@ -191,7 +197,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t qtl = item % n_qtiles;
       const int c = (int)(item / n_qtiles);
-      Seq<SMP> ts;
+      Seq<SMP, SKIP> ts;
       ts.begin(b_tiles, S, R, c);
       for (; ts.more(); ts.next()) {
         const int64_t t = ts.t;
@@ -228,7 +234,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
     uint32_t phase = 0, acc_phase = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int c = (int)(item / n_qtiles);
-      Seq<SMP> ts;
+      Seq<SMP, SKIP> ts;
       ts.begin(b_tiles, S, R, c);
       for (; ts.more(); ts.next()) {
         mbar_wait(&t_empty[acc], acc_phase ^ 1);
@@ -269,7 +275,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t qtl = item % n_qtiles;
       const int c = (int)(item / n_qtiles);
-      Seq<SMP> ts;
+      Seq<SMP, SKIP> ts;
       ts.begin(b_tiles, S, R, c);
       int issued = 0;
       bool a_done = false;
@@ -330,7 +336,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
     uint32_t phase = 0, acc_phase = 0, aphase = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int c = (int)(item / n_qtiles);
-      Seq<SMP> ts;
+      Seq<SMP, SKIP> ts;
       ts.begin(b_tiles, S, R, c);
       mbar_wait(a_full, aphase);
       aphase ^= 1;
@@ -369,8 +375,8 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
     constexpr uint32_t SLOT = 32 * 8;
     const uint32_t pbase = s_pend + (f * kPend * 32 + lane) * 8;
     uint32_t pa = pbase;
-    int acc = 0;
-    uint32_t acc_phase = 0;
+    uint32_t tcount = 0;  // tiles consumed: accumulator = tcount & 1, phase = (tcount >> 1) & 1
+    const uint32_t taddr0 = tmem_base + ((uint32_t)(q * 32) << 16) + h * BH;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t qtl = item % n_qtiles;
       const int c = (int)(item / n_qtiles);
@@ -406,13 +412,14 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
       float top[T];
 #pragma unroll
       for (int i = 0; i < T; ++i) top[i] = CUDART_INF_F;
-      Seq<SMP> ts;
+      Seq<SMP, SKIP> ts;
       ts.begin(b_tiles, S, R, c);
       for (; ts.more(); ts.next()) {
-        mbar_wait(&t_full[acc], acc_phase);
+        const uint32_t acc = tcount & 1u;
+        mbar_wait(&t_full[acc], (tcount >> 1) & 1u);
         tc_fence_after();
         float v[BH];
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kBN + h * BH;
+        const uint32_t taddr = taddr0 + (acc << 8);  // acc * kBN
         if (!(DBG & 2)) {
 #pragma unroll
           for (int u = 0; u < BH / 64; ++u)
@@ -422,10 +429,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&t_empty[acc]);
-        if (++acc == 2) {
-          acc = 0;
-          acc_phase ^= 1;
-        }
+        ++tcount;
         if (DBG & 3) continue;  // profiling: pipeline without the filter work
         const int t = ts.t;
         const int j0 = t * kBN + h * BH;
@@ -484,7 +488,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
   }
 }
 
-template <int DPAD, int FMT, int DBG, int FW, int SMP>
+template <int DPAD, int FMT, int DBG, int FW, int MODE>
 cudaError_t launch3(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                     bool self_join, const MainPass& m, int num_sms, cudaStream_t st) {
   const int nstage = pick_stages3<DPAD, FW>();
@@ -492,7 +496,7 @@ cudaError_t launch3(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
   if (m.parts != FW / 4) return cudaErrorInvalidValue;
   int a, b, c;
   const int smem = smem3<DPAD, FW>(nstage, &a, &b, &c);
-  auto kern = k_knn_tc3<DPAD, FMT, DBG, FW, SMP>;
+  auto kern = k_knn_tc3<DPAD, FMT, DBG, FW, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t qt0 = q_begin / kBM;
@@ -576,8 +580,11 @@ cudaError_t launch_knn_tc3(const Image& A, const Image& B, int64_t q_begin, int6
     return fmt == 1 ? launch3<D, 1, 0, FW, 4>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
                     : launch3<D, 2, 0, FW, 4>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
   if (dbg & 3)                                                                                    \
-    return fmt == 1 ? launch3<D, 1, 2, FW, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
-                    : launch3<D, 2, 2, FW, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+    return fmt == 1 ? launch3<D, 1, 2, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
+                    : launch3<D, 2, 2, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+  if (m.R > 0)                                                                                    \
+    return fmt == 1 ? launch3<D, 1, 0, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
+                    : launch3<D, 2, 0, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
   return fmt == 1 ? launch3<D, 1, 0, FW, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st)    \
                   : launch3<D, 2, 0, FW, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st);
 #define TOD_TC3_CASE(D)          \
