@@ -34,6 +34,7 @@ namespace {
 
 constexpr int kBM = 128;        // query rows per CTA (= TMEM lanes)
 constexpr int kBN = 256;        // reference columns per tile (MMA N)
+static_assert(kBN == 256, "filter addresses accumulators as acc << 8");
 constexpr int kBNH = 128;       // reference rows of each tile staged per CTA
 constexpr int kExtraRB = 32;
 constexpr int kSmemMax = 232448;
@@ -304,8 +305,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
     constexpr uint32_t SLOT = 32 * 8;
     const uint32_t pbase = s_pend + (f * kPend * 32 + lane) * 8;
     uint32_t pa = pbase;
-    int acc = 0;
-    uint32_t acc_phase = 0;
+    uint32_t tcount = 0;  // tiles consumed: accumulator = tcount & 1, phase = (tcount >> 1) & 1
+    const uint32_t taddr0 = tmem_base + ((uint32_t)(q * 32) << 16) + h * BH;
     const uint32_t r_tempty = mapa_shared(smem_u32(t_empty), 0);
     for (int64_t item = cid; item < n_items; item += ncl) {
       const int64_t qtl = (item % n_qpairs) * 2 + rank;
@@ -338,10 +339,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
       Seq ts;
       ts.begin(b_tiles, S, R, c);
       for (; ts.more(); ts.next()) {
-        mbar_wait_cl(&t_full[acc], acc_phase);
+        const uint32_t acc = tcount & 1u;
+        mbar_wait_cl(&t_full[acc], (tcount >> 1) & 1u);
         tc_fence_after();
         float v[BH];
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * kBN + h * BH;
+        const uint32_t taddr = taddr0 + (acc << 8);  // acc * kBN
         if (!(DBG & 2)) {
 #pragma unroll
           for (int u = 0; u < BH / 64; ++u)
@@ -354,10 +356,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
           if (leader) mbar_arrive(&t_empty[acc]);
           else mbar_arrive_cluster(r_tempty + acc * 8);
         }
-        if (++acc == 2) {
-          acc = 0;
-          acc_phase ^= 1;
-        }
+        ++tcount;
         if (DBG & 3) continue;
         const int t = ts.t;
         const int j0 = t * kBN + h * BH;
