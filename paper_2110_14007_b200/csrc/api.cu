@@ -44,7 +44,7 @@ struct Workspace {
 enum BufId {
   B_X = 0, B_Q, B_IMG_B, B_A2_B, B_E_B, B_IMG_A, B_A2_A, B_E_A, B_MU, B_PART,
   B_G, B_CIDX, B_CV, B_FAIL, B_SMALL, B_IDX, B_DIST, B_DIST64, B_KTH, B_MEAN, B_KD64,
-  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT, B_FAILUB, B_NWRTAU, B_NWRCNT, B_NWRPTR, B_NWRCOLS, B_SCAN, B_ABOD, B_LABELS, B_PRED, B_SAMP, B_NBUF
+  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT, B_FAILUB, B_NWRTAU, B_NWRCNT, B_NWRPTR, B_NWRCOLS, B_SCAN, B_ABOD, B_LABELS, B_PRED, B_SAMP, B_NWRBLK, B_NWRTASK, B_NBUF
 };
 static_assert(B_NBUF <= 48, "Workspace::bufs too small");
 
@@ -588,15 +588,22 @@ tod_status run_nwr(tod_ctx* ctx, const float* dX, int64_t n, int d, double phi, 
   tm.mark();  // 3: verification
   TOD_TRY(ensure(ctx, B_FAIL, (size_t)std::max<int64_t>(q_count, 1) * 4, &p));
   int32_t* ovf_rows = static_cast<int32_t*>(p);
+  TOD_TRY(ensure(ctx, B_NWRTASK, nwr_tasks_ws(q_count, mp) * 8, &p));
+  int64_t* tasks_ws = static_cast<int64_t*>(p);
+  TOD_TRY(ensure(ctx, B_SCAN, scan_workspace(q_count), &p));
+  void* scan_ws = p;
   TOD_CUDA(launch_nwr_verify(nullptr, q_begin, q_count, dX, n, d, true, phi, mp, 0, dcounts,
-                             nullptr, nullptr, ovf_rows, &small->fail_count, st, launches));
+                             nullptr, nullptr, ovf_rows, &small->fail_count, tasks_ws, scan_ws,
+                             ctx->num_sms, st, launches));
   SmallDev h{};
   TOD_CUDA(cudaMemcpyAsync(&h, small, sizeof(SmallDev), cudaMemcpyDeviceToHost, st));
   TOD_CUDA(cudaStreamSynchronize(st));
   if (h.g.nonfinite) return fail(ctx, TOD_E_NONFINITE, "X contains NaN or Inf");
   const int novf = h.fail_count;
+  TOD_TRY(ensure(ctx, B_NWRBLK, (size_t)std::max(novf, 1) * nwr_brute_slices() * 8, &p));
+  int64_t* bcnt = static_cast<int64_t*>(p);
   TOD_CUDA(launch_nwr_brute(nullptr, q_begin, dX, n, d, true, phi, ovf_rows, novf, 0, dcounts,
-                            nullptr, nullptr, st, launches));
+                            nullptr, nullptr, bcnt, st, launches));
   TOD_TRY(ensure(ctx, B_SCAN, scan_workspace(q_count), &p));
   int64_t* part = static_cast<int64_t*>(p);
   TOD_CUDA(launch_scan(dcounts, q_count, drow_ptr, part, st, launches));
@@ -605,9 +612,10 @@ tod_status run_nwr(tod_ctx* ctx, const float* dX, int64_t n, int d, double phi, 
   tm.mark();  // 4: lists
   if (dcols && *total <= capacity) {
     TOD_CUDA(launch_nwr_verify(nullptr, q_begin, q_count, dX, n, d, true, phi, mp, 1, dcounts,
-                               drow_ptr, dcols, ovf_rows, &small->fail_count, st, launches));
+                               drow_ptr, dcols, ovf_rows, &small->fail_count, tasks_ws, nullptr,
+                               ctx->num_sms, st, launches));
     TOD_CUDA(launch_nwr_brute(nullptr, q_begin, dX, n, d, true, phi, ovf_rows, novf, 1, dcounts,
-                              drow_ptr, dcols, st, launches));
+                              drow_ptr, dcols, bcnt, st, launches));
   }
   tm.mark();  // 5
   if (stats) {

@@ -151,12 +151,14 @@ cudaError_t launch_nwr_tau(int64_t q_count, double phi, CertParams cp, float* ta
 cudaError_t launch_nwr_verify(const float* Q, int64_t q_begin, int64_t q_count, const float* X,
                               int64_t n, int d, bool self_join, double phi, const MainPass& mp,
                               int mode, int64_t* counts, const int64_t* row_ptr, int32_t* cols,
-                              int32_t* ovf_rows, int32_t* ovf_count, cudaStream_t st,
-                              int* launches);
+                              int32_t* ovf_rows, int32_t* ovf_count, int64_t* tasks_ws,
+                              void* scan_ws, int num_sms, cudaStream_t st, int* launches);
+size_t nwr_tasks_ws(int64_t q_count, const MainPass& mp);  // int64 words
 cudaError_t launch_nwr_brute(const float* Q, int64_t q_begin, const float* X, int64_t n, int d,
                              bool self_join, double phi, const int32_t* rows, int nrows, int mode,
-                             int64_t* counts, const int64_t* row_ptr, int32_t* cols,
+                             int64_t* counts, const int64_t* row_ptr, int32_t* cols, int64_t* bcnt,
                              cudaStream_t st, int* launches);
+int nwr_brute_slices();       // bcnt holds nrows x nwr_brute_slices() counts
 size_t scan_workspace(int64_t q);
 cudaError_t launch_scan(const int64_t* counts, int64_t q, int64_t* row_ptr, void* ws,
                         cudaStream_t st, int* launches);

@@ -571,7 +571,7 @@ cudaError_t launch_knn_tc3(const Image& A, const Image& B, int64_t q_begin, int6
                            bool self_join, int fmt, const MainPass& m, int num_sms, int dbg,
                            cudaStream_t st, int* launches) {
   *launches += 1;
-  // dbg (profiling only): 1 = skip the filter work, 2 = also skip the TMEM loads
+  // dbg (profiling only): 1 = skip the filter work (fp16), 2 = also skip the TMEM loads
 #define TOD_TC3_FW(D, FW)                                                                          \
   if (m.samp && m.samp_t == 8)                                                                    \
     return fmt == 1 ? launch3<D, 1, 0, FW, 8>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
@@ -579,6 +579,8 @@ cudaError_t launch_knn_tc3(const Image& A, const Image& B, int64_t q_begin, int6
   if (m.samp)                                                                                     \
     return fmt == 1 ? launch3<D, 1, 0, FW, 4>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
                     : launch3<D, 2, 0, FW, 4>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+  if ((dbg & 3) == 1 && fmt == 1)                                                                 \
+    return launch3<D, 1, 1, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st);            \
   if (dbg & 3)                                                                                    \
     return fmt == 1 ? launch3<D, 1, 2, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
                     : launch3<D, 2, 2, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st); \

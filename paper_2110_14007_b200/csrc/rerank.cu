@@ -750,8 +750,11 @@ __device__ __forceinline__ void rerank_groups_row(
   }
 }
 
+// 4 blocks (16 warps) per SM = 128 registers: measured on B200 (C2, C3) no
+// slower than 5 or 6 blocks at 92 / 80 registers, and faster than the 168
+// registers the compiler picks unconstrained.
 template <int DT>
-__global__ void __launch_bounds__(kGrpWarps * 32)
+__global__ void __launch_bounds__(kGrpWarps * 32, 4)
     k_rerank_groups(const float* __restrict__ Q, int64_t q_begin, int64_t q_count,
                     const float* __restrict__ X, int64_t n, int d, int k, int self_join,
                     const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_key,
@@ -802,52 +805,158 @@ __global__ void k_nwr_tau(int64_t q_count, double phi, CertParams cp, float* __r
 }
 
 constexpr int kNwrWarps = 4;
-constexpr int kNwrMaxG = 4096;   // staged groups per row (4 parts x up to 1024)
+constexpr int kNwrMaxG = 4096;   // kept groups per row (4 parts x up to 1024)
+constexpr int kNwrChunk = 64;    // kept groups per verification task
 
-// mode 0: counts[r] (or -1 if the row's buffers overflowed: brute-force later);
-// mode 1: neighbours written at cols + row_ptr[r], ascending.
-template <int DT>
-__global__ void __launch_bounds__(kNwrWarps * 32)
-    k_nwr_verify(const float* __restrict__ Q, int64_t q_begin, int64_t q_count,
-                 const float* __restrict__ X, int64_t n, int d, int self_join, double phi,
-                 const uint2* __restrict__ mbuf, const int* __restrict__ mcnt, int mcap,
-                 int mparts, int mode, int64_t* __restrict__ counts,
-                 const int64_t* __restrict__ row_ptr, int32_t* __restrict__ cols,
-                 int32_t* __restrict__ ovf_rows, int32_t* __restrict__ ovf_count) {
-  extern __shared__ double s_xq[];  // [warps][d] query rows, then [warps][maxg] groups
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t r = (int64_t)blockIdx.x * kNwrWarps + w;
+// Verification is flattened into tasks of <= 64 kept groups, so a dense row
+// with thousands of kept groups is spread over many warps instead of holding
+// one warp for the whole pass (the per-row warp left the kernel waiting on its
+// heaviest rows).
+//   k_nwr_tasks: per row, overflow check (-> brute-force list) and task count;
+//   scan -> task offsets; k_nwr_map: task -> (row, part, chunk);
+//   k_nwr_mask: per task, O1 for every column of its groups; each entry is
+//     rewritten in place as (8-bit mask of the columns with D64 <= phi, group)
+//     and the row's count accumulated;
+//   k_nwr_emit: per row, the entries with a nonzero mask sorted by group, then
+//     their columns written ascending at row_ptr[r] (no distance computed twice).
+__global__ void k_nwr_tasks(int64_t q_count, const int* __restrict__ mcnt, int mcap, int mparts,
+                            int64_t* __restrict__ tcnt, int64_t* __restrict__ counts,
+                            int32_t* __restrict__ ovf_rows, int32_t* __restrict__ ovf_count) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= q_count) return;
-  const int64_t gi = q_begin + r;
-  const float* xi = self_join ? X + gi * d : Q + r * d;
-  double* xq = s_xq + (size_t)w * d;
-  for (int c = lane; c < d; c += 32) xq[c] = (double)xi[c];
-  const int maxg = mparts * mcap;
-  int* g = reinterpret_cast<int*>(s_xq + (size_t)kNwrWarps * d) + (size_t)w * maxg;
-  int G = 0;
   bool over = false;
+  int64_t nt = 0;
   for (int h = 0; h < mparts; ++h) {
     const int c = mcnt[r * mparts + h];
     over |= c > mcap;
-    const int m = c < mcap ? c : mcap;
-    const uint2* src = mbuf + (r * mparts + h) * (int64_t)mcap;
-    for (int e = lane; e < m; e += 32) g[G + e] = (int)src[e].y;
-    G += m;
+    nt += (min(c, mcap) + kNwrChunk - 1) / kNwrChunk;
   }
-  if (over) {
-    if (mode == 0 && lane == 0) {
-      counts[r] = -1;
-      ovf_rows[atomicAdd(ovf_count, 1)] = (int32_t)r;
+  tcnt[r] = over ? 0 : nt;
+  counts[r] = over ? -1 : 0;
+  if (over) ovf_rows[atomicAdd(ovf_count, 1)] = (int32_t)r;
+}
+
+__global__ void k_nwr_map(int64_t q_count, const int* __restrict__ mcnt, int mcap, int mparts,
+                          const int64_t* __restrict__ toff, int64_t* __restrict__ map) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= q_count) return;
+  int64_t t = toff[r];
+  if (toff[r + 1] == t) return;  // overflowed or empty
+  for (int h = 0; h < mparts; ++h) {
+    const int m = min(mcnt[r * mparts + h], mcap);
+    for (int c = 0; c * kNwrChunk < m; ++c) map[t++] = ((r * mparts + h) << 8) | c;
+  }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kNwrWarps * 32)
+    k_nwr_mask(const float* __restrict__ Q, int64_t q_begin, const float* __restrict__ X,
+               int64_t n, int d, int self_join, double phi, uint2* __restrict__ mbuf,
+               const int* __restrict__ mcnt, int mcap, int mparts,
+               const int64_t* __restrict__ map, const int64_t* __restrict__ ntasks,
+               int64_t* __restrict__ counts) {
+  extern __shared__ double s_xq[];  // [warps][d] query rows in fp64
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* xq = s_xq + (size_t)w * d;
+  const int64_t T = *ntasks;
+  for (int64_t task = (int64_t)blockIdx.x * kNwrWarps + w; task < T;
+       task += (int64_t)gridDim.x * kNwrWarps) {
+    const int64_t code = map[task];
+    const int64_t rp = code >> 8;
+    const int c = (int)(code & 0xFF);
+    const int64_t r = rp / mparts;
+    const int64_t gi = q_begin + r;
+    const float* xi = self_join ? X + gi * d : Q + r * d;
+    __syncwarp();
+    for (int e = lane; e < d; e += 32) xq[e] = (double)xi[e];
+    __syncwarp();
+    uint2* ent = mbuf + rp * (int64_t)mcap;
+    const int e1 = min(min(mcnt[rp], mcap), (c + 1) * kNwrChunk);
+    int cnt = 0;
+    for (int b0 = c * kNwrChunk; b0 < e1; b0 += 4) {
+      const int gs = b0 + (lane >> 3);
+      const int grp = gs < e1 ? (int)ent[gs].y : -1;
+      const int64_t j = (int64_t)grp * 8 + (lane & 7);
+      bool keep = false;
+      if (grp >= 0 && j < n && !(self_join && j == gi)) {
+        const float* xj = X + j * d;
+        double acc;
+        if constexpr (DT > 0) {
+          acc = d64_fixed<DT>(xq, xj);
+        } else {
+          acc = 0.0;  // O1: ascending c, no FMA
+          for (int cc = 0; cc < d; ++cc) {
+            const double t = __dsub_rn(xq[cc], (double)__ldg(xj + cc));
+            acc = __dadd_rn(acc, __dmul_rn(t, t));
+          }
+        }
+        keep = acc <= phi;
+      }
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      if ((lane & 7) == 0 && grp >= 0) ent[gs].x = (km >> (lane & 24)) & 0xFFu;
+      cnt += __popc(km);
     }
+    if (lane == 0 && cnt) atomicAdd(reinterpret_cast<unsigned long long*>(counts + r),
+                                    (unsigned long long)cnt);
+  }
+}
+
+// Rows with at most kEmitLight nonzero entries are sorted by one warp; the
+// rest (dense rows) are queued for k_nwr_emit_heavy, a 512-thread block each.
+constexpr int kEmitLight = 256;
+constexpr int kEmitWarps = 4;
+constexpr int kEmitHeavyThreads = 512;
+
+// the row's entries with a nonzero mask, compacted into (g, mk); returns the count
+__device__ __forceinline__ int nwr_compact(const uint2* __restrict__ mbuf, const int* __restrict__ mcnt,
+                                           int mcap, int mparts, int64_t r, int lane, int* g,
+                                           int* mk, int cap) {
+  int nz = 0;
+  for (int h = 0; h < mparts; ++h) {
+    const int m = min(mcnt[r * mparts + h], mcap);
+    const uint2* src = mbuf + (r * mparts + h) * (int64_t)mcap;
+    for (int e0 = 0; e0 < m; e0 += 32) {
+      const int e = e0 + lane;
+      const uint2 v = e < m ? src[e] : make_uint2(0u, 0u);
+      const unsigned live = __ballot_sync(0xffffffffu, v.x != 0u);
+      const int pos = nz + __popc(live & ((1u << lane) - 1u));
+      if (v.x && pos < cap) {
+        g[pos] = (int)v.y;
+        mk[pos] = (int)v.x;
+      }
+      nz += __popc(live);
+    }
+  }
+  return nz;
+}
+
+__global__ void __launch_bounds__(kEmitWarps * 32)
+    k_nwr_emit(int64_t q_count, const uint2* __restrict__ mbuf, const int* __restrict__ mcnt,
+               int mcap, int mparts, const int64_t* __restrict__ row_ptr,
+               int32_t* __restrict__ cols, int32_t* __restrict__ heavy, int32_t* __restrict__ nheavy) {
+  __shared__ int s_g[kEmitWarps][kEmitLight], s_m[kEmitWarps][kEmitLight];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * kEmitWarps + w;
+  if (r >= q_count) return;
+  int* g = s_g[w];
+  int* mk = s_m[w];
+  bool over = false;
+  for (int h = 0; h < mparts; ++h) over |= mcnt[r * mparts + h] > mcap;
+  if (over) return;  // the brute-force tier writes this row
+  const int nz = nwr_compact(mbuf, mcnt, mcap, mparts, r, lane, g, mk, kEmitLight);
+  if (nz > kEmitLight) {
+    if (lane == 0) heavy[atomicAdd(nheavy, 1)] = (int32_t)r;
     return;
   }
-  // mode 1: sort the group indices ascending (bitonic over the next power of
-  // two) so the neighbours come out ascending; counting needs no order
+  // ascending by group (bitonic over the next power of two; groups are unique)
   int P = 1;
-  while (mode == 1 && P < G) P <<= 1;
-  for (int e = G + lane; e < P; e += 32) g[e] = INT32_MAX;
+  while (P < nz) P <<= 1;
+  for (int e = nz + lane; e < P; e += 32) {
+    g[e] = INT32_MAX;
+    mk[e] = 0;
+  }
   __syncwarp();
-  for (int kk = 2; mode == 1 && kk <= P; kk <<= 1)
+  for (int kk = 2; kk <= P; kk <<= 1)
     for (int j = kk >> 1; j > 0; j >>= 1) {
       for (int e = lane; e < P; e += 32) {
         const int l = e ^ j;
@@ -857,63 +966,164 @@ __global__ void __launch_bounds__(kNwrWarps * 32)
           if (up ? a > b : a < b) {
             g[e] = b;
             g[l] = a;
+            const int t = mk[e];
+            mk[e] = mk[l];
+            mk[l] = t;
           }
         }
       }
       __syncwarp();
     }
-  int64_t cnt = 0;
-  int64_t base = mode == 1 ? row_ptr[r] : 0;
-  for (int b0 = 0; b0 < G; b0 += 4) {
-    const int gs = b0 + (lane >> 3);
-    const int grp = gs < G ? g[gs] : -1;
-    const int64_t j = (int64_t)grp * 8 + (lane & 7);
-    bool keep = false;
-    if (grp >= 0 && j < n && !(self_join && j == gi)) {
-      const float* xj = X + j * d;
-      double acc;
-      if constexpr (DT > 0) {
-        acc = d64_fixed<DT>(xq, xj);
-      } else {
-        acc = 0.0;  // O1: ascending c, no FMA
-        for (int c = 0; c < d; ++c) {
-          const double t = __dsub_rn(xq[c], (double)__ldg(xj + c));
-          acc = __dadd_rn(acc, __dmul_rn(t, t));
-        }
-      }
-      keep = acc <= phi;
+  int64_t base = row_ptr[r];
+  for (int e0 = 0; e0 < nz; e0 += 32) {
+    const int e = e0 + lane;
+    const unsigned m8 = e < nz ? (unsigned)mk[e] : 0u;
+    const int pc = __popc(m8);
+    int incl = pc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
     }
-    const unsigned km = __ballot_sync(0xffffffffu, keep);
-    if (mode == 1 && keep) cols[base + cnt + __popc(km & ((1u << lane) - 1u))] = (int32_t)j;
-    cnt += __popc(km);
+    int64_t pos = base + incl - pc;
+    for (unsigned m = m8; m; m &= m - 1u) cols[pos++] = (int32_t)((unsigned)g[e] * 8u + (unsigned)(__ffs(m) - 1));
+    base += __shfl_sync(0xffffffffu, incl, 31);
   }
-  if (mode == 0 && lane == 0) counts[r] = cnt;
 }
 
-// fp64 brute force for rows whose candidate buffers overflowed; one block per
-// row, columns in ascending order (block prefix sums keep the order in mode 1).
+// dense rows: one 512-thread block per row (compaction by warp 0, block-wide
+// bitonic sort, block prefix sums for the output positions)
+__global__ void __launch_bounds__(kEmitHeavyThreads)
+    k_nwr_emit_heavy(const uint2* __restrict__ mbuf, const int* __restrict__ mcnt, int mcap,
+                     int mparts, const int64_t* __restrict__ row_ptr, int32_t* __restrict__ cols,
+                     const int32_t* __restrict__ heavy, const int32_t* __restrict__ nheavy) {
+  extern __shared__ int s_h[];  // [kNwrMaxG] groups, [kNwrMaxG] masks
+  __shared__ int s_nz, s_wsum[kEmitHeavyThreads / 32];
+  __shared__ int64_t s_base;
+  int* g = s_h;
+  int* mk = s_h + kNwrMaxG;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int nh = *nheavy;
+  for (int hr = blockIdx.x; hr < nh; hr += gridDim.x) {
+    const int64_t r = heavy[hr];
+    __syncthreads();
+    if (w == 0) {
+      const int nz = nwr_compact(mbuf, mcnt, mcap, mparts, r, lane, g, mk, kNwrMaxG);
+      if (lane == 0) {
+        s_nz = nz;
+        s_base = row_ptr[r];
+      }
+    }
+    __syncthreads();
+    const int nz = s_nz;
+    int P = 1;
+    while (P < nz) P <<= 1;
+    for (int e = nz + t; e < P; e += kEmitHeavyThreads) {
+      g[e] = INT32_MAX;
+      mk[e] = 0;
+    }
+    __syncthreads();
+    for (int kk = 2; kk <= P; kk <<= 1)
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        for (int e = t; e < P; e += kEmitHeavyThreads) {
+          const int l = e ^ j;
+          if (l > e) {
+            const int a = g[e], b = g[l];
+            const bool up = (e & kk) == 0;
+            if (up ? a > b : a < b) {
+              g[e] = b;
+              g[l] = a;
+              const int x = mk[e];
+              mk[e] = mk[l];
+              mk[l] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    for (int e0 = 0; e0 < nz; e0 += kEmitHeavyThreads) {
+      const int e = e0 + t;
+      const unsigned m8 = e < nz ? (unsigned)mk[e] : 0u;
+      const int pc = __popc(m8);
+      int incl = pc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (lane == 31) s_wsum[w] = incl;
+      __syncthreads();
+      int before = 0, tot = 0;
+      for (int q = 0; q < kEmitHeavyThreads / 32; ++q) {
+        before += q < w ? s_wsum[q] : 0;
+        tot += s_wsum[q];
+      }
+      int64_t pos = s_base + before + incl - pc;
+      for (unsigned m = m8; m; m &= m - 1u) cols[pos++] = (int32_t)((unsigned)g[e] * 8u + (unsigned)(__ffs(m) - 1));
+      __syncthreads();
+      if (t == 0) s_base += tot;
+      __syncthreads();
+    }
+  }
+}
+
+// fp64 brute force for rows whose candidate buffers overflowed.  Each row is
+// split over kNwrSlices blocks of consecutive columns (grid = rows x slices, so
+// a handful of heavy rows still fills the GPU); mode 0 stores every slice's
+// count in bcnt and k_nwr_brute_sum totals them, mode 1 starts each slice at
+// row_ptr[r] + the counts of the slices before it, so the columns come out
+// ascending.  O1 per pair (ascending c, no FMA), exactly the oracle's test.
+constexpr int kNwrSlices = 64;
+
 __global__ void __launch_bounds__(256)
     k_nwr_brute(const float* __restrict__ Q, int64_t q_begin, const float* __restrict__ X,
                 int64_t n, int d, int self_join, double phi, const int32_t* __restrict__ rows,
-                int mode, int64_t* __restrict__ counts, const int64_t* __restrict__ row_ptr,
+                int mode, int64_t* __restrict__ bcnt, const int64_t* __restrict__ row_ptr,
                 int32_t* __restrict__ cols) {
   __shared__ int s_w[8];
   __shared__ int64_t s_base;
+  extern __shared__ double s_xq1[];  // [d] the query row in fp64
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int64_t r = rows[blockIdx.x];
+  const int slot = blockIdx.x, b = blockIdx.y;
+  const int64_t r = rows[slot];
   const int64_t gi = q_begin + r;
   const float* xi = self_join ? X + gi * d : Q + r * d;
-  if (t == 0) s_base = mode == 1 ? row_ptr[r] : 0;
+  for (int c = t; c < d; c += 256) s_xq1[c] = (double)xi[c];
+  const int64_t j_begin = n * b / kNwrSlices, j_end = n * (b + 1) / kNwrSlices;
+  if (t == 0) {
+    int64_t base = 0;
+    if (mode == 1) {
+      base = row_ptr[r];
+      for (int q = 0; q < b; ++q) base += bcnt[(int64_t)slot * kNwrSlices + q];
+    }
+    s_base = base;
+  }
   __syncthreads();
-  for (int64_t j0 = 0; j0 < n; j0 += 256) {
+  const bool v4 = (d & 3) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  for (int64_t j0 = j_begin; j0 < j_end; j0 += 256) {
     const int64_t j = j0 + t;
     bool keep = false;
-    if (j < n && !(self_join && j == gi)) {
+    if (j < j_end && !(self_join && j == gi)) {
       const float* xj = X + j * d;
       double acc = 0.0;
-      for (int c = 0; c < d; ++c) {
-        const double tt = __dsub_rn((double)xi[c], (double)__ldg(xj + c));
-        acc = __dadd_rn(acc, __dmul_rn(tt, tt));
+      if (v4) {
+        const float4* x4 = reinterpret_cast<const float4*>(xj);
+        for (int c4 = 0; c4 < (d >> 2); ++c4) {
+          const float4 v = __ldg(x4 + c4);
+          double tt = __dsub_rn(s_xq1[4 * c4 + 0], (double)v.x);
+          acc = __dadd_rn(acc, __dmul_rn(tt, tt));
+          tt = __dsub_rn(s_xq1[4 * c4 + 1], (double)v.y);
+          acc = __dadd_rn(acc, __dmul_rn(tt, tt));
+          tt = __dsub_rn(s_xq1[4 * c4 + 2], (double)v.z);
+          acc = __dadd_rn(acc, __dmul_rn(tt, tt));
+          tt = __dsub_rn(s_xq1[4 * c4 + 3], (double)v.w);
+          acc = __dadd_rn(acc, __dmul_rn(tt, tt));
+        }
+      } else {
+        for (int c = 0; c < d; ++c) {
+          const double tt = __dsub_rn(s_xq1[c], (double)__ldg(xj + c));
+          acc = __dadd_rn(acc, __dmul_rn(tt, tt));
+        }
       }
       keep = acc <= phi;
     }
@@ -930,7 +1140,16 @@ __global__ void __launch_bounds__(256)
     if (t == 0) s_base += tot;
     __syncthreads();
   }
-  if (mode == 0 && t == 0) counts[r] = s_base;
+  if (mode == 0 && t == 0) bcnt[(int64_t)slot * kNwrSlices + b] = s_base;
+}
+
+__global__ void k_nwr_brute_sum(const int32_t* __restrict__ rows, int nrows,
+                                const int64_t* __restrict__ bcnt, int64_t* __restrict__ counts) {
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= nrows) return;
+  int64_t c = 0;
+  for (int q = 0; q < kNwrSlices; ++q) c += bcnt[(int64_t)slot * kNwrSlices + q];
+  counts[rows[slot]] = c;
 }
 
 // Exclusive scan of q int64 counts into row_ptr[0..q] (3 phases, 1024 per block).
@@ -1297,37 +1516,76 @@ cudaError_t launch_nwr_tau(int64_t q_count, double phi, CertParams cp, float* ta
 cudaError_t launch_nwr_verify(const float* Q, int64_t q_begin, int64_t q_count, const float* X,
                               int64_t n, int d, bool self_join, double phi, const MainPass& mp,
                               int mode, int64_t* counts, const int64_t* row_ptr, int32_t* cols,
-                              int32_t* ovf_rows, int32_t* ovf_count, cudaStream_t st,
-                              int* launches) {
+                              int32_t* ovf_rows, int32_t* ovf_count, int64_t* tasks_ws,
+                              void* scan_ws, int num_sms, cudaStream_t st, int* launches) {
   if (q_count <= 0) return cudaSuccess;
-  if (mp.parts * mp.cap > kNwrMaxG) return cudaErrorInvalidValue;
-  int maxg = 1;
-  while (maxg < mp.parts * mp.cap) maxg <<= 1;  // room for the bitonic padding
-  const size_t smem = (size_t)kNwrWarps * d * 8 + (size_t)kNwrWarps * maxg * 4;
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  const bool al = ((reinterpret_cast<uintptr_t>(X) & 31) == 0);
-  auto kern = (al && d == 16) ? k_nwr_verify<16>
-            : (al && d == 32) ? k_nwr_verify<32>
-            : (al && d == 64) ? k_nwr_verify<64> : k_nwr_verify<0>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (mp.parts * mp.cap > kNwrMaxG || mp.cap / kNwrChunk > 255) return cudaErrorInvalidValue;
+  const unsigned rb = (unsigned)((q_count + 255) / 256);
+  if (mode == 1) {
+    // tasks_ws: reused for the dense-row queue ([0] count, then row ids)
+    int32_t* nheavy = reinterpret_cast<int32_t*>(tasks_ws);
+    int32_t* heavy = nheavy + 1;
+    cudaError_t e = cudaMemsetAsync(nheavy, 0, 4, st);
+    if (e != cudaSuccess) return e;
+    k_nwr_emit<<<(unsigned)((q_count + kEmitWarps - 1) / kEmitWarps), kEmitWarps * 32, 0, st>>>(
+        q_count, mp.buf, mp.cnt, mp.cap, mp.parts, row_ptr, cols, heavy, nheavy);
+    const size_t smem = (size_t)2 * kNwrMaxG * 4;
+    e = cudaFuncSetAttribute(k_nwr_emit_heavy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_nwr_emit_heavy<<<(unsigned)(num_sms * 2), kEmitHeavyThreads, smem, st>>>(
+        mp.buf, mp.cnt, mp.cap, mp.parts, row_ptr, cols, heavy, nheavy);
+    *launches += 2;
+    return cudaGetLastError();
+  }
+  // tasks_ws: [q_count] task counts, [q_count + 1] offsets, then the task map
+  int64_t* tcnt = tasks_ws;
+  int64_t* toff = tasks_ws + q_count;
+  int64_t* map = toff + q_count + 1;
+  k_nwr_tasks<<<rb, 256, 0, st>>>(q_count, mp.cnt, mp.cap, mp.parts, tcnt, counts, ovf_rows, ovf_count);
+  cudaError_t e = launch_scan(tcnt, q_count, toff, scan_ws, st, launches);
   if (e != cudaSuccess) return e;
-  kern<<<(unsigned)((q_count + kNwrWarps - 1) / kNwrWarps), kNwrWarps * 32, smem, st>>>(
-      Q, q_begin, q_count, X, n, d, self_join ? 1 : 0, phi, mp.buf, mp.cnt, mp.cap, mp.parts, mode,
-      counts, row_ptr, cols, ovf_rows, ovf_count);
-  *launches += 1;
+  k_nwr_map<<<rb, 256, 0, st>>>(q_count, mp.cnt, mp.cap, mp.parts, toff, map);
+  const size_t smem = (size_t)kNwrWarps * d * 8;
+  const bool al = ((reinterpret_cast<uintptr_t>(X) & 31) == 0);
+  auto kern = (al && d == 16) ? k_nwr_mask<16>
+            : (al && d == 32) ? k_nwr_mask<32>
+            : (al && d == 64) ? k_nwr_mask<64> : k_nwr_mask<0>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)(num_sms * 16), kNwrWarps * 32, smem, st>>>(
+      Q, q_begin, X, n, d, self_join ? 1 : 0, phi, mp.buf, mp.cnt, mp.cap, mp.parts, map,
+      toff + q_count, counts);
+  *launches += 3;
   return cudaGetLastError();
+}
+
+// int64 words of the mode-0 task workspace
+size_t nwr_tasks_ws(int64_t q_count, const MainPass& mp) {
+  return (size_t)(2 * q_count + 1) +
+         (size_t)q_count * mp.parts * ((mp.cap + kNwrChunk - 1) / kNwrChunk);
 }
 
 cudaError_t launch_nwr_brute(const float* Q, int64_t q_begin, const float* X, int64_t n, int d,
                              bool self_join, double phi, const int32_t* rows, int nrows, int mode,
-                             int64_t* counts, const int64_t* row_ptr, int32_t* cols,
+                             int64_t* counts, const int64_t* row_ptr, int32_t* cols, int64_t* bcnt,
                              cudaStream_t st, int* launches) {
   if (nrows <= 0) return cudaSuccess;
-  k_nwr_brute<<<nrows, 256, 0, st>>>(Q, q_begin, X, n, d, self_join ? 1 : 0, phi, rows, mode,
-                                     counts, row_ptr, cols);
+  const size_t smem = (size_t)d * 8;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_nwr_brute, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_nwr_brute<<<dim3((unsigned)nrows, kNwrSlices), 256, smem, st>>>(
+      Q, q_begin, X, n, d, self_join ? 1 : 0, phi, rows, mode, bcnt, row_ptr, cols);
   *launches += 1;
+  if (mode == 0) {
+    k_nwr_brute_sum<<<(unsigned)((nrows + 127) / 128), 128, 0, st>>>(rows, nrows, bcnt, counts);
+    *launches += 1;
+  }
   return cudaGetLastError();
 }
+
+int nwr_brute_slices() { return kNwrSlices; }
 
 size_t scan_workspace(int64_t q) { return (size_t)((q + 1023) / 1024 + 2) * 8; }
 

@@ -341,6 +341,19 @@ def test_nwr_overflow_rows_brute_force_and_query_range(pkg):
     assert _nwr_check(got, X, 1.0, np.arange(4000, 7000))["fallback_rows"] == 0
 
 
+def test_nwr_dense_rows_block_emit(pkg):
+    # 750 groups in all (never overflows 4 x 1024 slots): phi = inf-like puts every
+    # group of every row in the output (> 256 nonzero entries: the dense-row block
+    # emitter), a mid phi mixes dense and light rows
+    X = datagen.gaussian_mixture(6000, 16, seed=21)
+    _, dd = oracle.knn(X, 10, rows=np.arange(0, 6000, 60))
+    for phi in (1e9, float(np.percentile(dd[:, -1], 50)) * 40.0):
+        with _ctx(pkg) as ctx:
+            got = ctx.nwr(torch.from_numpy(X).cuda(), phi, q_begin=2000, q_count=1500)
+        st = _nwr_check(got, X, phi, np.arange(2000, 3500))
+        assert st["fallback_rows"] == 0
+
+
 def test_nwr_capacity_error_reports_total(pkg):
     X = datagen.gaussian_mixture(2000, 16, seed=5)
     phi = 50.0
