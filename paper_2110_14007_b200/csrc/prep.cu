@@ -152,10 +152,11 @@ struct Pieces {
   }
 };
 
-// One warp per row (rows [0, n_pad)).  side 0 = reference image B:
+// W lanes per row (W = 32, or 16 / 8 when dpad/2 <= 16 / 8 element pairs, so
+// narrow rows share a warp; rows [0, n_pad)).  side 0 = reference image B:
 // [xhat | norm pieces]; side 1 = query image A: [-2 xhat | constants].
 // Padding rows are zero (the epilogue masks padding columns).
-template <int FMT>
+template <int FMT, int W>
 __device__ __forceinline__ void quant_row(const float* __restrict__ X, int64_t n, int d,
                                           const double* __restrict__ mu, PrepGlobals* g,
                                           const Image& img, int side, int64_t r, int lane,
@@ -166,7 +167,7 @@ __device__ __forceinline__ void quant_row(const float* __restrict__ X, int64_t n
   uint8_t* base = reinterpret_cast<uint8_t*>(img.data);
   double a2 = 0.0, r2 = 0.0, tt = 0.0;
   const bool real = r < n;
-  for (int p = lane; p < img.dpad / 2; p += 32) {
+  for (int p = lane; p < img.dpad / 2; p += W) {
     const int c0 = 2 * p, c1 = 2 * p + 1;
     double t0 = 0.0, t1 = 0.0;
     if (real && c0 < d) t0 = ((double)X[r * d + c0] - mu[c0]) * s;
@@ -188,7 +189,7 @@ __device__ __forceinline__ void quant_row(const float* __restrict__ X, int64_t n
         (uint32_t)w0 | ((uint32_t)w1 << 16);
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+  for (int o = W / 2; o > 0; o >>= 1) {  // within the row's W-lane segment
     a2 += __shfl_xor_sync(0xffffffffu, a2, o);
     r2 += __shfl_xor_sync(0xffffffffu, r2, o);
     tt += __shfl_xor_sync(0xffffffffu, tt, o);
@@ -248,7 +249,7 @@ __device__ __forceinline__ void quant_row(const float* __restrict__ X, int64_t n
 }
 
 
-template <int FMT>
+template <int FMT, int W>
 __global__ void k_quant(const float* __restrict__ X, int64_t n, int d,
                         const double* __restrict__ mu, PrepGlobals* g, Image img, int side) {
   // per-block maxima (one global atomic per block and quantity, not per row:
@@ -256,9 +257,11 @@ __global__ void k_quant(const float* __restrict__ X, int64_t n, int d,
   __shared__ unsigned long long s_max[3];
   if (threadIdx.x < 3) s_max[threadIdx.x] = 0ull;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (r < img.n_pad) quant_row<FMT>(X, n, d, mu, g, img, side, r, lane, s_max);
+  const int lane = threadIdx.x & (W - 1);
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / W;
+  // (n_pad is a multiple of 256 rows, so every warp's segments are all in range
+  // or all out of it: the segment shuffles never mix live and exited lanes)
+  if (r < img.n_pad) quant_row<FMT, W>(X, n, d, mu, g, img, side, r, lane, s_max);
   __syncthreads();
   if (side == 0 && threadIdx.x < 3 && s_max[threadIdx.x] != 0ull) {
     unsigned long long* dst = threadIdx.x == 0 ? reinterpret_cast<unsigned long long*>(&g->amax2)
@@ -308,12 +311,16 @@ cudaError_t launch_prep_scale(PrepGlobals* g, int fmt, int dpad, cudaStream_t st
 
 cudaError_t launch_prep_quant(const float* X, int64_t n, int d, const double* mu, PrepGlobals* g,
                               int fmt, Image img, int side, cudaStream_t st, int* launches) {
-  const int64_t threads = img.n_pad * 32;
+  const int W = img.dpad / 2 <= 8 ? 8 : (img.dpad / 2 <= 16 ? 16 : 32);  // lanes per row
+  const int64_t threads = img.n_pad * W;
   const int blocks = (int)((threads + 255) / 256);
-  if (fmt == 1)
-    k_quant<1><<<blocks, 256, 0, st>>>(X, n, d, mu, g, img, side);
-  else
-    k_quant<2><<<blocks, 256, 0, st>>>(X, n, d, mu, g, img, side);
+#define TOD_QUANT(F, WW) k_quant<F, WW><<<blocks, 256, 0, st>>>(X, n, d, mu, g, img, side)
+  if (fmt == 1) {
+    if (W == 8) TOD_QUANT(1, 8); else if (W == 16) TOD_QUANT(1, 16); else TOD_QUANT(1, 32);
+  } else {
+    if (W == 8) TOD_QUANT(2, 8); else if (W == 16) TOD_QUANT(2, 16); else TOD_QUANT(2, 32);
+  }
+#undef TOD_QUANT
   *launches += 1;
   return cudaGetLastError();
 }

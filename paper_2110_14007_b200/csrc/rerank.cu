@@ -514,11 +514,13 @@ __device__ __forceinline__ void rerank_groups_row(
       lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
       hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
     }
-    // invariant: count(key <= hi) >= k; shrink hi to the k-th key (a tight
-    // kappa keeps UB, and with it the visited set, small)
+    // invariant: count(key <= hi) >= k; shrink hi towards the k-th key (a tight
+    // kappa keeps UB, and with it the visited set, small).  Stopping within
+    // 64 ulps of it (relative 2^-17, far below the bound's own slack) saves the
+    // last halvings; any hi with count >= k gives a valid UB.
     if (lo < hi) --lo;  // count(key <= lo) < k unless lo is the minimum itself
     int chi = G;
-    for (int it = 0; it < 32 && hi - lo > 1 && chi > k; ++it) {
+    for (int it = 0; it < 32 && hi - lo > 64 && chi > k; ++it) {
       const uint32_t mid = lo + ((hi - lo) >> 1);
       int c = 0;
 #pragma unroll
