@@ -213,12 +213,13 @@ def run_gpu_nwr(args):
     c, p, _, st = ctx.nwr(Xd, NWR_PHI, lists=False)
     cap = int(int(p[-1]) * 1.1) + 1024
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    # the clock sampler starts before the warm-up (it keeps only the samples inside
+    # the timed window), so the GPU never idles between warm-up and timing
+    sampler = ClockSampler(torch.cuda.current_device())
+    sampler.start()
     for _ in range(args.warmup):
         ctx.nwr(Xd, NWR_PHI, capacity=cap)
     torch.cuda.synchronize()
-    sampler = ClockSampler(torch.cuda.current_device())
-    sampler.start()
-    time.sleep(0.15)
     times, kms, stats = [], [], {}
     t0 = time.time()
     for i in range(args.steps):
@@ -316,14 +317,15 @@ def run_gpu(args):
 
     stages.knn = knn_capture
 
+    # the clock sampler starts before the warm-up (it keeps only the samples inside
+    # the timed window), so the GPU never idles between warm-up and timing
+    sampler = ClockSampler(dev)
+    sampler.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    sampler = ClockSampler(dev)
-    sampler.start()
-    time.sleep(0.15)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     torch.cuda.synchronize()
