@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define TOD_ABI_VERSION 1
+#define TOD_ABI_VERSION 2
 
 typedef enum {
   TOD_OK = 0,
@@ -86,6 +86,13 @@ typedef struct {
   int32_t chunks;          /* reference chunks S per query tile (load balance); 0 = auto */
   int32_t epilogue_split;  /* tensor-core pass: epilogue warps per TMEM lane quarter (1 or 2; 2 splits each
                               tile's columns into two per-row lists of K'/2+8); 0 = auto */
+  size_t workspace_bytes;  /* automatic batching ("store as many samples as possible"):
+                              budget for the query-dependent device workspace of tod_knn /
+                              tod_knn_query / tod_lof (candidate buffers and lists, per-row bounds,
+                              the query image); when one call's estimate exceeds it, the query rows
+                              are processed in chunks of 128-row multiples (>= 128 rows), with
+                              results bit-identical to one unchunked call.  0 = no limit.  The
+                              reference-side buffers (X, its quantized image) are not covered. */
 } tod_config;
 
 typedef struct {
@@ -107,7 +114,7 @@ typedef struct {
   int32_t main_kernel;     /* main-pass kernel used: 0 = none (single pass), 3 = single-SM, 4 = CTA pairs */
   int32_t sample_pass;     /* two-pass sample: 0 = none, 1 = list-based (main pass skips the sample
                               tiles), 2 = key-only (main pass covers every tile) */
-  int32_t reserved_;
+  int32_t query_chunks;    /* query-row chunks the call was split into (workspace_bytes); 1 = none */
 } tod_stats;
 
 /* Per-neighbour and per-row outputs of the kNN functional operator (P:270,

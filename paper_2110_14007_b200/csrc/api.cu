@@ -704,6 +704,71 @@ tod_status stage_input(tod_ctx* ctx, const float* user, size_t count, int id, co
   return TOD_OK;
 }
 
+// Automatic batching (SURVEY 8(a) level 3): the query-dependent
+// device workspace of one run_knn call, per query row, from the plan.
+size_t knn_bytes_per_row(const Plan& p, int k) {
+  size_t b = (size_t)p.lists * p.kp * 12 + (size_t)p.lists * 4;  // pass-1 lists + thresholds
+  if (p.two) b += (size_t)tc3_parts(p.dpad) * ((size_t)p.cap * 2 / std::max(1, tc3_parts(p.dpad)) * 8 + 4);
+  b += (size_t)(p.dpad + 16) * 2 + 16;  // query image row + its bounds
+  b += (size_t)k * 24 + 64;             // staged outputs, fallback bookkeeping
+  return b;
+}
+
+// run_knn over [q_begin, q_begin + q_count), in chunks of 128-row multiples when
+// ctx->cfg.workspace_bytes is set and one call would exceed it.  Rows are
+// independent (per-row thresholds, bounds and certificate; the reference-side
+// quantization constants are global), so the outputs are bit-identical.
+tod_status run_knn_auto(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, int64_t q_begin,
+                        int64_t q_count, int d, int k, KnnOutDev out, tod_stats* stats, Timer& tm,
+                        int* launches) {
+  int64_t rows = q_count;
+  if (ctx->cfg.workspace_bytes > 0 && q_count > 128) {
+    Plan plan;
+    TOD_TRY(make_plan(ctx, n, q_count, d, k, &plan));
+    const size_t per = knn_bytes_per_row(plan, k);
+    rows = std::max<int64_t>(128, (int64_t)(ctx->cfg.workspace_bytes / per) / 128 * 128);
+  }
+  if (rows >= q_count) {
+    TOD_TRY(run_knn(ctx, dX, n, dQ, q_begin, q_count, d, k, out, stats, tm, launches));
+    if (stats) stats->query_chunks = 1;
+    return TOD_OK;
+  }
+  Timer off{ctx, false};
+  tm.mark();  // 1: chunked mode reports the whole compute as one phase (see finish_stats)
+  tod_stats acc{};
+  int nch = 0;
+  for (int64_t r0 = 0; r0 < q_count; r0 += rows, ++nch) {
+    const int64_t qc = std::min<int64_t>(rows, q_count - r0);
+    KnnOutDev o = out;
+    auto sh = [&](auto* p, int64_t per_row) { return p ? p + r0 * per_row : p; };
+    o.idx = sh(out.idx, k);
+    o.dist = sh(out.dist, k);
+    o.dist64 = sh(out.dist64, k);
+    o.score_kth = sh(out.score_kth, 1);
+    o.score_mean = sh(out.score_mean, 1);
+    o.kdist64 = sh(out.kdist64, 1);
+    tod_stats cs{};
+    TOD_TRY(run_knn(ctx, dX, n, dQ ? dQ + r0 * d : nullptr, dQ ? 0 : q_begin + r0, qc, d, k, o,
+                    stats ? &cs : nullptr, off, launches));
+    if (nch == 0) acc = cs;
+    else {
+      acc.rows += cs.rows;
+      acc.certified += cs.certified;
+      acc.fallback_rows += cs.fallback_rows;
+      acc.cand_groups += cs.cand_groups;
+      acc.visited_groups += cs.visited_groups;
+      acc.cand_columns += cs.cand_columns;
+      acc.max_abs_err = std::max(acc.max_abs_err, cs.max_abs_err);
+    }
+  }
+  for (int i = 0; i < 4; ++i) tm.mark();  // 2..5
+  if (stats) {
+    *stats = acc;
+    stats->query_chunks = nch;
+  }
+  return TOD_OK;
+}
+
 void finish_stats(tod_stats* stats, Timer& tm, int launches, int i_lof_end) {
   if (!stats) return;
   stats->kernel_launches = launches;
@@ -714,6 +779,8 @@ void finish_stats(tod_stats* stats, Timer& tm, int launches, int i_lof_end) {
   stats->ms_fallback = tm.between(4, 5);
   stats->ms_lof = i_lof_end > 0 ? tm.between(5, i_lof_end) : 0.f;
   stats->ms_total = tm.between(0, tm.n - 1);
+  if (stats->query_chunks > 1)  // chunked: phases interleave, only the totals are meaningful
+    stats->ms_prep = stats->ms_main = stats->ms_certify = stats->ms_fallback = stats->ms_main_kernel = 0.f;
 }
 
 }  // namespace
@@ -809,7 +876,7 @@ tod_status tod_knn(tod_ctx* ctx, const float* X, int64_t n, int32_t d, int32_t k
   TOD_TRY(stage_input(ctx, X, (size_t)n * d, B_X, &dX));
   OutStage os;
   TOD_TRY(stage_outputs(ctx, out, q_count, k, &os));
-  if (q_count > 0) TOD_TRY(run_knn(ctx, dX, n, nullptr, q_begin, q_count, d, k, os.dev, stats, tm, &launches));
+  if (q_count > 0) TOD_TRY(run_knn_auto(ctx, dX, n, nullptr, q_begin, q_count, d, k, os.dev, stats, tm, &launches));
   TOD_TRY(unstage_outputs(ctx, out, q_count, k, os));
   tm.mark();
   TOD_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -833,7 +900,7 @@ tod_status tod_knn_query(tod_ctx* ctx, const float* Q, int64_t nq, const float* 
   if (nq > 0) TOD_TRY(stage_input(ctx, Q, (size_t)nq * d, B_Q, &dQ));
   OutStage os;
   TOD_TRY(stage_outputs(ctx, out, nq, k, &os));
-  if (nq > 0) TOD_TRY(run_knn(ctx, dX, n, dQ, 0, nq, d, k, os.dev, stats, tm, &launches));
+  if (nq > 0) TOD_TRY(run_knn_auto(ctx, dX, n, dQ, 0, nq, d, k, os.dev, stats, tm, &launches));
   TOD_TRY(unstage_outputs(ctx, out, nq, k, os));
   tm.mark();
   TOD_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -926,7 +993,7 @@ tod_status tod_abod(tod_ctx* ctx, const float* X, int64_t n, int32_t d, int32_t 
   bool st_s;
   TOD_TRY(dev_view(ctx, score, (size_t)q_count, B_ABOD, &dscore, &st_s));
   if (q_count > 0) {
-    TOD_TRY(run_knn(ctx, dX, n, nullptr, q_begin, q_count, d, k, os.dev, stats, tm, &launches));
+    TOD_TRY(run_knn_auto(ctx, dX, n, nullptr, q_begin, q_count, d, k, os.dev, stats, tm, &launches));
     TOD_CUDA(launch_abod(dX, q_begin, q_count, d, k, os.dev.idx, dscore, ctx->stream, &launches));
   }
   TOD_TRY(unstage_outputs(ctx, knn_out, q_count, k, os));
@@ -969,7 +1036,7 @@ tod_status tod_knn_classify(tod_ctx* ctx, const float* Q, int64_t nq, const floa
   TOD_TRY(ensure(ctx, B_IDX, (size_t)std::max<int64_t>(nq, 1) * k * 8, &p));
   kd.idx = static_cast<int64_t*>(p);
   if (nq > 0) {
-    TOD_TRY(run_knn(ctx, dX, n, dQ, 0, nq, d, k, kd, stats, tm, &launches));
+    TOD_TRY(run_knn_auto(ctx, dX, n, dQ, 0, nq, d, k, kd, stats, tm, &launches));
     TOD_CUDA(launch_knn_classify(nq, k, kd.idx, dlab, dpred, ctx->stream, &launches));
   }
   if (st_p && nq > 0)
@@ -1008,7 +1075,7 @@ tod_status tod_lof(tod_ctx* ctx, const float* X, int64_t n, int32_t d, int32_t k
     TOD_TRY(ensure(ctx, B_KD64, (size_t)n * 8, &p));
     os.dev.kdist64 = static_cast<double*>(p);
   }
-  TOD_TRY(run_knn(ctx, dX, n, nullptr, 0, n, d, k, os.dev, stats, tm, &launches));
+  TOD_TRY(run_knn_auto(ctx, dX, n, nullptr, 0, n, d, k, os.dev, stats, tm, &launches));
   TOD_TRY(ensure(ctx, B_LRD64, (size_t)n * 8, &p));
   double* lrd64 = static_cast<double*>(p);
   float *dlof, *dlrd;

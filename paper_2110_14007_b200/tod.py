@@ -40,7 +40,7 @@ class TodError(RuntimeError):
 class Config(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("format", ctypes.c_int32), ("kprime", ctypes.c_int32),
                 ("flags", ctypes.c_uint32), ("stream", ctypes.c_void_p), ("chunks", ctypes.c_int32),
-                ("epilogue_split", ctypes.c_int32)]
+                ("epilogue_split", ctypes.c_int32), ("workspace_bytes", ctypes.c_size_t)]
 
 
 class Stats(ctypes.Structure):
@@ -55,7 +55,7 @@ class Stats(ctypes.Structure):
                 ("cand_groups", ctypes.c_int64), ("visited_groups", ctypes.c_int64),
                 ("cand_columns", ctypes.c_int64), ("ms_main_kernel", ctypes.c_float),
                 ("main_kernel", ctypes.c_int32), ("sample_pass", ctypes.c_int32),
-                ("reserved_", ctypes.c_int32)]
+                ("query_chunks", ctypes.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -68,6 +68,9 @@ class KnnOut(ctypes.Structure):
 
 
 _lib = None
+
+
+ABI_VERSION = 2  # include/tod.h TOD_ABI_VERSION
 
 
 def load_library(path: str = LIB_PATH):
@@ -105,6 +108,9 @@ def load_library(path: str = LIB_PATH):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
+    if lib.tod_abi_version() != ABI_VERSION:  # a stale build: struct layouts would disagree
+        raise ImportError("libtod.so ABI %d, binding expects %d; rebuild (__graft_entry__.build())"
+                          % (lib.tod_abi_version(), ABI_VERSION))
     _lib = lib
     return lib
 
@@ -165,10 +171,11 @@ class Context:
     """Owns a tod_ctx (device workspace + stream binding)."""
 
     def __init__(self, device: int = 0, fmt: str = "auto", kprime: int = 0, chunks: int = 0,
-                 flags: int = 0, stream=None, split: int = 0):
+                 flags: int = 0, stream=None, split: int = 0, workspace_bytes: int = 0):
         self.lib = load_library()
         cfg = Config(device=device, format=FORMATS[fmt], kprime=kprime, flags=flags,
-                     stream=stream, chunks=chunks, epilogue_split=split)
+                     stream=stream, chunks=chunks, epilogue_split=split,
+                     workspace_bytes=workspace_bytes)
         h = ctypes.c_void_p()
         st = self.lib.tod_create(ctypes.byref(cfg), ctypes.byref(h))
         if st != TOD_OK:

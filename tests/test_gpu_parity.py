@@ -471,3 +471,28 @@ def test_tensor_core_accumulation_model(pkg, dt):
             err = (C - Ad @ Bd.t()).abs() / (Ad.abs() @ Bd.abs().t() * 2.0 ** -24)
             worst = max(worst, err.max().item())
         assert worst < model / 2, (K, worst, model)
+
+
+# ------------------------------------------------ automatic batching (workspace_bytes)
+@pytest.mark.parametrize("d,fmt", [(32, "fp16"), (64, "bf16"), (10, "auto")])
+def test_workspace_budget_chunks_queries_bit_identical(pkg, d, fmt):
+    # SURVEY 8(a) level 3: a small workspace budget splits the query rows into
+    # 128-row-multiple chunks; every output equals the unchunked call bit for bit
+    n, k = 12_345, 15
+    X = torch.from_numpy(datagen.gaussian_mixture(n, d, seed=3 + d)).cuda()
+    with _ctx(pkg, fmt=fmt) as ctx:
+        ref = ctx.knn(X, k)
+        ref_q = ctx.knn_query(X[:1000] + 0.25, X, k)
+        lof_ref = ctx.lof(X, k)
+    with _ctx(pkg, fmt=fmt, workspace_bytes=3 << 20) as ctx:
+        got = ctx.knn(X, k, q_begin=77, q_count=n - 77)
+        got_q = ctx.knn_query(X[:1000] + 0.25, X, k)
+        lof_got = ctx.lof(X, k)
+    assert got.stats["query_chunks"] > 2, got.stats["query_chunks"]
+    assert got.stats["rows"] == n - 77
+    for f in ("idx", "dist", "dist64", "score_kth", "score_mean", "kdist64"):
+        assert torch.equal(getattr(got, f), getattr(ref, f)[77:]), f
+        assert torch.equal(getattr(got_q, f), getattr(ref_q, f)), f
+    assert torch.equal(lof_got[0], lof_ref[0]) and torch.equal(lof_got[1], lof_ref[1])
+    assert lof_got[3]["query_chunks"] > 2
+    _check_rows(ref, _np(X), k, np.arange(0, n, n // 8))
