@@ -44,7 +44,7 @@ struct Workspace {
 enum BufId {
   B_X = 0, B_Q, B_IMG_B, B_A2_B, B_E_B, B_IMG_A, B_A2_A, B_E_A, B_MU, B_PART,
   B_G, B_CIDX, B_CV, B_FAIL, B_SMALL, B_IDX, B_DIST, B_DIST64, B_KTH, B_MEAN, B_KD64,
-  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT, B_FAILUB, B_NWRTAU, B_NWRCNT, B_NWRPTR, B_NWRCOLS, B_SCAN, B_ABOD, B_LABELS, B_PRED, B_SAMP, B_NWRBLK, B_NWRTASK, B_NBUF
+  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT, B_FAILUB, B_NWRTAU, B_NWRCNT, B_NWRPTR, B_NWRCOLS, B_SCAN, B_ABOD, B_LABELS, B_PRED, B_SAMP, B_NWRBLK, B_NWRTASK, B_RRWS, B_NBUF
 };
 static_assert(B_NBUF <= 48, "Workspace::bufs too small");
 
@@ -495,9 +495,14 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     }
     return TOD_OK;
   }
+  void* rr_ws = nullptr;
+  if (plan.kind == PASS_TC && rerank_use_split(d)) {
+    TOD_TRY(ensure(ctx, B_RRWS, rerank_split_ws(q_count), &p));
+    rr_ws = p;
+  }
   TOD_CUDA(launch_rerank(dQ, q_begin, q_count, dX, n, d, k, self, cands, plan.two ? &mp : nullptr,
                          cp, out, fail_rows, fail_ub,
-                         &small->fail_count, &small->max_err, small->counters, st, launches));
+                         &small->fail_count, &small->max_err, small->counters, rr_ws, st, launches));
   tm.mark();  // 4: fallback start
   SmallDev h{};
   TOD_CUDA(cudaMemcpyAsync(&h, small, sizeof(SmallDev), cudaMemcpyDeviceToHost, st));
@@ -711,6 +716,8 @@ size_t knn_bytes_per_row(const Plan& p, int k) {
   if (p.two) b += (size_t)tc3_parts(p.dpad) * ((size_t)p.cap * 2 / std::max(1, tc3_parts(p.dpad)) * 8 + 4);
   b += (size_t)(p.dpad + 16) * 2 + 16;  // query image row + its bounds
   b += (size_t)k * 24 + 64;             // staged outputs, fallback bookkeeping
+  if (p.kind == PASS_TC && rerank_use_split(p.dpad))
+    b += rerank_split_ws(1024) / 1024;  // split re-rank: visited groups, kept columns, tasks
   return b;
 }
 

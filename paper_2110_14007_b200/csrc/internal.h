@@ -132,11 +132,13 @@ struct KnnOutDev {
   float* score_mean;
   double* kdist64;
 };
+size_t rerank_split_ws(int64_t q);  // bytes of the split re-rank's workspace (tensor-core pass)
+int rerank_use_split(int d);        // the split re-rank is used at this width (d > 256)
 cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, const float* X,
                           int64_t n, int d, int k, bool self_join, Cands c, const MainPass* mp,
                           CertParams cp,
                           KnnOutDev out, int32_t* fail_rows, double* fail_ub, int32_t* fail_count,
-                          double* max_err, unsigned long long* counters, cudaStream_t st,
+                          double* max_err, unsigned long long* counters, void* split_ws, cudaStream_t st,
                           int* launches);
 int fallback_slices(int nfail, int64_t n, int num_sms);
 size_t fallback_workspace(int nfail, int k, int64_t n, int num_sms);

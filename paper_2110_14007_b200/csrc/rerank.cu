@@ -786,6 +786,380 @@ __global__ void __launch_bounds__(kGrpWarps * 32, 4)
 }
 
 
+// ============================================= split re-rank (two-pass mode)
+// The per-row warp of k_rerank_groups walks its visited groups in ~6 dependent
+// rounds (gather, then a 3*d-step fp64 chain), so the kernel is bound by that
+// per-row latency.  The split form keeps the same arithmetic but flattens the
+// expansion across the whole GPU:
+//   k_rr_plan   (warp per row)  stage the kept groups, kappa, UB, key cut, and
+//               the visited group list -> global;
+//   scan + k_rr_map             task -> (row, round of 4 groups);
+//   k_rr_expand (warp per task) O1 for the round's 32 columns, columns with
+//               D64 <= UB appended to the row's list (slots by atomicAdd);
+//   k_rr_finish (warp per row)  top-k by (D64, index), certificate, outputs.
+// The kept set of a row is the same as in k_rerank_groups (its order differs;
+// the selection is a total order), so outputs are identical.
+constexpr int kRrVis = kSelMax;  // visited groups per row (more: the row goes to the fallback)
+
+struct RrWs {
+  int32_t* nv;     // [q] visited groups
+  int32_t* flags;  // [q] bit 0: overflow (the row cannot be certified)
+  int32_t* G;      // [q] staged groups (telemetry)
+  int32_t* nc;     // [q] kept-column counter
+  float* vmin;     // [q] pass-1 threshold (certificate)
+  double* ub;      // [q] UB on the k-th exact distance
+  int32_t* gid;    // [q][kRrVis]
+  double* ck;      // [q][kColMax] kept columns: D64
+  int32_t* ci;     // [q][kColMax]                index
+  int64_t* tcnt;   // [q] expansion tasks
+  int64_t* toff;   // [q + 1]
+  int64_t* map;    // [q * kRrVis / 4]
+  void* scan;
+};
+
+// carve the workspace at base (base = nullptr: offsets only, for sizing)
+__host__ RrWs rr_layout(void* base, int64_t q, size_t* total = nullptr) {
+  RrWs w;
+  const int64_t q1 = q < 1 ? 1 : q;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* r = base ? static_cast<char*>(base) + off : nullptr;
+    off += (bytes + 255) / 256 * 256;
+    return r;
+  };
+  w.ub = reinterpret_cast<double*>(take(q1 * 8));
+  w.ck = reinterpret_cast<double*>(take((size_t)q1 * kColMax * 8));
+  w.tcnt = reinterpret_cast<int64_t*>(take(q1 * 8));
+  w.toff = reinterpret_cast<int64_t*>(take((q1 + 1) * 8));
+  w.map = reinterpret_cast<int64_t*>(take((size_t)q1 * (kRrVis / 4) * 8));
+  w.scan = take(scan_workspace(q1));
+  w.nv = reinterpret_cast<int32_t*>(take(q1 * 4));
+  w.flags = reinterpret_cast<int32_t*>(take(q1 * 4));
+  w.G = reinterpret_cast<int32_t*>(take(q1 * 4));
+  w.nc = reinterpret_cast<int32_t*>(take(q1 * 4));
+  w.vmin = reinterpret_cast<float*>(take(q1 * 4));
+  w.gid = reinterpret_cast<int32_t*>(take((size_t)q1 * kRrVis * 4));
+  w.ci = reinterpret_cast<int32_t*>(take((size_t)q1 * kColMax * 4));
+  if (total) *total = off;
+  return w;
+}
+
+__global__ void __launch_bounds__(kGrpWarps * 32, 4)
+    k_rr_plan(int64_t q_count, int k, const int32_t* __restrict__ cand_idx,
+              const float* __restrict__ cand_key, const float* __restrict__ cand_v, int kp, int lists,
+              const uint2* __restrict__ mbuf, const int* __restrict__ mcnt, int mcap, int mparts,
+              CertParams cp, RrWs rw) {
+  __shared__ float s_gk[kGrpWarps][kSelMax];
+  __shared__ int s_gi[kGrpWarps][kSelMax];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* gk = s_gk[w];
+  int* gid = s_gi[w];
+  for (int64_t r = (int64_t)blockIdx.x * kGrpWarps + w; r < q_count;
+       r += (int64_t)gridDim.x * kGrpWarps) {
+    __syncwarp();
+    int G = 0;
+    bool overflow = false;
+    const int L = lists * kp;
+    for (int e0 = 0; e0 < L; e0 += 32) {
+      const int e = e0 + lane;
+      const int g = e < L ? cand_idx[r * L + e] : -1;
+      const unsigned live = __ballot_sync(0xffffffffu, g >= 0);
+      const int pos = G + __popc(live & ((1u << lane) - 1u));
+      if (g >= 0 && pos < kSelMax) {
+        gk[pos] = cand_key[r * L + e];
+        gid[pos] = g;
+      }
+      G += __popc(live);
+    }
+    if (mbuf) {
+      int cnt[4] = {0, 0, 0, 0}, off[5];
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+        if (h < mparts) cnt[h] = mcnt[r * mparts + h];
+      off[0] = 0;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        overflow |= cnt[h] > mcap;
+        off[h + 1] = off[h] + min(cnt[h], mcap);
+      }
+      const int M = off[4];
+      for (int e0 = 0; e0 < M; e0 += 128) {
+        uint2 kv[4];
+        int pos[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = e0 + u * 32 + lane;
+          pos[u] = -1;
+          if (e < M) {
+            int h = 0;
+#pragma unroll
+            for (int q = 1; q < 4; ++q) h += e >= off[q];
+            kv[u] = __ldcg(mbuf + (r * mparts + h) * (int64_t)mcap + (e - off[h]));
+            pos[u] = G + e;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (pos[u] >= 0 && pos[u] < kSelMax) {
+            gk[pos[u]] = __uint_as_float(kv[u].x);
+            gid[pos[u]] = (int)kv[u].y;
+          }
+      }
+      G += M;
+    }
+    overflow |= G > kSelMax;
+    if (G > kSelMax) G = kSelMax;
+    float vmin = CUDART_INF_F;
+    for (int c = 0; c < lists; ++c) vmin = fminf(vmin, cand_v[r * lists + c]);
+    __syncwarp();
+    // kappa (the k-th smallest key, to 64 ulps) and UB, as in rerank_groups_row
+    double UB = CUDART_INF;
+    if (G >= k) {
+      uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+      uint32_t ok[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = lane + 32 * u;
+        ok[u] = (e < G) ? f2ord(gk[e]) : 0xFFFFFFFFu;
+        if (e < G) {
+          lo = min(lo, ok[u]);
+          hi = max(hi, ok[u]);
+        }
+      }
+      for (int e = lane + 256; e < G; e += 32) {
+        const uint32_t o = f2ord(gk[e]);
+        lo = min(lo, o);
+        hi = max(hi, o);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      }
+      if (lo < hi) --lo;
+      int chi = G;
+      for (int it = 0; it < 32 && hi - lo > 64 && chi > k; ++it) {
+        const uint32_t mid = lo + ((hi - lo) >> 1);
+        int c = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c += ok[u] <= mid;
+        for (int e = lane + 256; e < G; e += 32) c += f2ord(gk[e]) <= mid;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (c >= k) {
+          hi = mid;
+          chi = c;
+        } else {
+          lo = mid;
+        }
+      }
+      const float kappa = ord2f(hi);
+      if (kappa < CUDART_INF_F) UB = ub2_from_key(cp, r, (double)kappa);
+    }
+    // the visited groups, compacted straight to the row's global list
+    const float kcut = key_cut_from_ub(cp, r, UB);
+    int32_t* gout = rw.gid + r * kRrVis;
+    int nv = 0;
+    for (int e0 = 0; e0 < G; e0 += 32) {
+      const int e = e0 + lane;
+      const bool vis = e < G && gk[e] <= kcut;
+      const unsigned vm = __ballot_sync(0xffffffffu, vis);
+      const int pos = nv + __popc(vm & ((1u << lane) - 1u));
+      if (vis && pos < kRrVis) gout[pos] = gid[e];
+      nv += __popc(vm);
+    }
+    if (nv > kRrVis) {
+      overflow = true;
+      nv = kRrVis;
+    }
+    if (lane == 0) {
+      rw.nv[r] = nv;
+      rw.flags[r] = overflow ? 1 : 0;
+      rw.G[r] = G;
+      rw.nc[r] = 0;
+      rw.vmin[r] = vmin;
+      rw.ub[r] = UB;
+      rw.tcnt[r] = (nv + 3) / 4;
+    }
+  }
+}
+
+__global__ void k_rr_map(int64_t q_count, RrWs rw) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= q_count) return;
+  const int64_t t0 = rw.toff[r];
+  const int nt = (int)(rw.toff[r + 1] - t0);
+  for (int c = 0; c < nt; ++c) rw.map[t0 + c] = (r << 8) | c;
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kGrpWarps * 32)
+    k_rr_expand(const float* __restrict__ Q, int64_t q_begin, const float* __restrict__ X,
+                int64_t n, int d, int self_join, RrWs rw, const int64_t* __restrict__ ntasks) {
+  extern __shared__ double s_xq[];  // [warps][d]
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* xq = s_xq + (size_t)w * d;
+  const int64_t T = *ntasks;
+  for (int64_t task = (int64_t)blockIdx.x * kGrpWarps + w; task < T;
+       task += (int64_t)gridDim.x * kGrpWarps) {
+    const int64_t code = rw.map[task];
+    const int64_t r = code >> 8;
+    const int c = (int)(code & 0xFF);
+    const int64_t gi = q_begin + r;
+    const float* xi = self_join ? X + gi * d : Q + r * d;
+    __syncwarp();
+    for (int e = lane; e < d; e += 32) xq[e] = (double)xi[e];
+    __syncwarp();
+    const int nv = rw.nv[r];
+    const double UB = rw.ub[r];
+    const int gs = 4 * c + (lane >> 3);
+    const int g = gs < nv ? rw.gid[r * kRrVis + gs] : -1;
+    const int64_t j = (int64_t)g * 8 + (lane & 7);
+    double key = CUDART_INF;
+    if (g >= 0 && j < n && !(self_join && j == gi)) {
+      const float* xj = X + j * d;
+      if constexpr (DT > 0) {
+        key = d64_fixed<DT>(xq, xj);
+      } else {
+        double acc = 0.0;  // O1: ascending c, no FMA
+        for (int cc = 0; cc < d; ++cc) {
+          const double t = __dsub_rn(xq[cc], (double)__ldg(xj + cc));
+          acc = __dadd_rn(acc, __dmul_rn(t, t));
+        }
+        key = acc;
+      }
+    }
+    const bool keep = key <= UB && key < CUDART_INF;
+    const unsigned km = __ballot_sync(0xffffffffu, keep);
+    if (km == 0u) continue;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(rw.nc + r, __popc(km));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    const int pos = base + __popc(km & ((1u << lane) - 1u));
+    if (keep && pos < kColMax) {
+      rw.ck[r * kColMax + pos] = key;
+      rw.ci[r * kColMax + pos] = (int)j;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kGrpWarps * 32)
+    k_rr_finish(int64_t q_count, int k, CertParams cp, RrWs rw, KnnOutDev out,
+                int32_t* __restrict__ fail_rows, double* __restrict__ fail_ub,
+                int32_t* __restrict__ fail_count, unsigned long long* __restrict__ max_err_bits,
+                unsigned long long* __restrict__ counters) {
+  __shared__ double s_ck[kGrpWarps][kColMax];
+  __shared__ int s_ci[kGrpWarps][kColMax];
+  __shared__ double s_tk[kGrpWarps][kMaxK];
+  __shared__ int s_ti[kGrpWarps][kMaxK];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  RowTel tel;
+  for (int64_t r = (int64_t)blockIdx.x * kGrpWarps + w; r < q_count;
+       r += (int64_t)gridDim.x * kGrpWarps) {
+    __syncwarp();
+    const int ncr = rw.nc[r];
+    bool overflow = rw.flags[r] != 0 || ncr > kColMax;
+    const int nc = ncr < kColMax ? ncr : kColMax;
+    double* ck = s_ck[w];
+    int* ci = s_ci[w];
+    double* tk = s_tk[w];
+    int* ti = s_ti[w];
+    if (nc > 64) {
+      for (int e = lane; e < nc; e += 32) {
+        ck[e] = rw.ck[r * kColMax + e];
+        ci[e] = rw.ci[r * kColMax + e];
+      }
+    }
+    __syncwarp();
+    if (nc <= 32) {
+      double kk1 = lane < nc ? rw.ck[r * kColMax + lane] : CUDART_INF;
+      int ii1 = lane < nc ? rw.ci[r * kColMax + lane] : INT32_MAX;
+      warp_sort32(kk1, ii1, lane);
+      if (lane < k) {
+        tk[lane] = kk1;
+        ti[lane] = ii1;
+      }
+    } else if (nc <= 64) {
+      double kk[2];
+      int ii[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int p = 2 * lane + e;
+        kk[e] = p < nc ? rw.ck[r * kColMax + p] : CUDART_INF;
+        ii[e] = p < nc ? rw.ci[r * kColMax + p] : INT32_MAX;
+      }
+      warp_sort64(kk, ii, lane);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int p = 2 * lane + e;
+        if (p < k) {
+          tk[p] = kk[e];
+          ti[p] = ii[e];
+        }
+      }
+    } else {
+      auto slice_min = [&](double& mk, int& mi, int& mp) {
+        mk = CUDART_INF;
+        mi = INT32_MAX;
+        mp = -1;
+        for (int e = lane; e < nc; e += 32)
+          if (key_less(ck[e], ci[e], mk, mi)) {
+            mk = ck[e];
+            mi = ci[e];
+            mp = e;
+          }
+      };
+      double lk;
+      int li, lp;
+      slice_min(lk, li, lp);
+      for (int m = 0; m < k; ++m) {
+        double bk = lk;
+        int bi = li;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (key_less(ok, oi, bk, bi)) {
+            bk = ok;
+            bi = oi;
+          }
+        }
+        if (lane == 0) {
+          tk[m] = bk;
+          ti[m] = bi;
+        }
+        if (lp >= 0 && li == bi && bi != INT32_MAX) {
+          ck[lp] = CUDART_INF;
+          ci[lp] = INT32_MAX;
+          slice_min(lk, li, lp);
+        }
+      }
+    }
+    __syncwarp();
+    double err = 0.0;
+    const bool have = nc >= k;
+    bool cert = !overflow && have && row_certified(cp, r, rw.vmin[r], tk[k - 1], &err);
+    if (cp.force_fail) cert = false;
+    tel.maxerr = fmax(tel.maxerr, err);
+    tel.G += (unsigned long long)rw.G[r];
+    tel.nv += (unsigned long long)rw.nv[r];
+    tel.nc += (unsigned long long)nc;
+    if (cert) {
+      write_row(out, r, k, tk, ti, lane, 32);
+    } else if (lane == 0) {
+      const int slot = atomicAdd(fail_count, 1);
+      fail_rows[slot] = (int32_t)r;
+      fail_ub[slot] = fmin(rw.ub[r], have ? tk[k - 1] : CUDART_INF);
+    }
+  }
+  if (lane == 0) {
+    if (tel.maxerr > 0.0) atomicMax(max_err_bits, (unsigned long long)__double_as_longlong(tel.maxerr));
+    if (tel.G) atomicAdd(counters + 0, tel.G);
+    if (tel.nv) atomicAdd(counters + 1, tel.nv);
+    if (tel.nc) atomicAdd(counters + 2, tel.nc);
+  }
+}
+
 // ===================================================================== NWR
 // Neighbours within range (§5.3): {j != i : D_ij <= phi},
 // D_ij the squared distance of Eq. (3) evaluated as the oracle's O1.  Provable
@@ -1604,17 +1978,61 @@ cudaError_t launch_scan(const int64_t* counts, int64_t q, int64_t* row_ptr, void
   return cudaGetLastError();
 }
 
+int rerank_use_split(int d) {
+  const char* se = getenv("TOD_RR_SPLIT");  // experiment knob: 0 / 1 forces the choice
+  return se ? atoi(se) != 0 : d > 256;
+}
+
+size_t rerank_split_ws(int64_t q) {
+  size_t total = 0;
+  (void)rr_layout(nullptr, q, &total);
+  return total;
+}
+
 cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, const float* X,
                           int64_t n, int d, int k, bool self_join, Cands c, const MainPass* mp,
                           CertParams cp, KnnOutDev out, int32_t* fail_rows, double* fail_ub,
                           int32_t* fail_count, double* max_err, unsigned long long* counters,
-                          cudaStream_t st, int* launches) {
+                          void* split_ws, cudaStream_t st, int* launches) {
   if (k > kMaxK) return cudaErrorInvalidValue;
   if (cp.kind == PASS_TC) {  // group candidates
     if (c.lists * c.kp > kSelMax || !c.key) return cudaErrorInvalidValue;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // Split form for wide rows only: measured on B200, C5 width (d = 512, k = 50) 83 -> 57 ms
+    // at n = 2e5; slower at d <= 256 (C2 0.61 -> 0.79 ms, d = 128 5.7 -> 6.5 ms), where the
+    // per-row gathers are short and the extra passes over the row state cost more.
+    if (split_ws && rerank_use_split(d)) {
+      if (q_count <= 0) return cudaSuccess;
+      const RrWs rw = rr_layout(split_ws, q_count);
+      const unsigned rb = (unsigned)std::min<int64_t>((q_count + kGrpWarps - 1) / kGrpWarps, (int64_t)sms * 8);
+      k_rr_plan<<<rb, kGrpWarps * 32, 0, st>>>(q_count, k, c.idx, c.key, c.v, c.kp, c.lists,
+                                              mp ? mp->buf : nullptr, mp ? mp->cnt : nullptr,
+                                              mp ? mp->cap : 0, mp ? mp->parts : 0, cp, rw);
+      cudaError_t e = launch_scan(rw.tcnt, q_count, rw.toff, rw.scan, st, launches);
+      if (e != cudaSuccess) return e;
+      k_rr_map<<<(unsigned)((q_count + 255) / 256), 256, 0, st>>>(q_count, rw);
+      const size_t smem = (size_t)kGrpWarps * d * 8;
+      if (smem > 160 * 1024) return cudaErrorInvalidValue;
+      const bool al = ((reinterpret_cast<uintptr_t>(X) & 31) == 0);
+      auto kx = (al && d == 16) ? k_rr_expand<16>
+              : (al && d == 32) ? k_rr_expand<32>
+              : (al && d == 64) ? k_rr_expand<64>
+              : (al && d == 128) ? k_rr_expand<128>
+              : (al && d == 256) ? k_rr_expand<256>
+              : (al && d == 512) ? k_rr_expand<512> : k_rr_expand<0>;
+      e = cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      kx<<<(unsigned)(sms * 16), kGrpWarps * 32, smem, st>>>(Q, q_begin, X, n, d, self_join ? 1 : 0,
+                                                             rw, rw.toff + q_count);
+      k_rr_finish<<<rb, kGrpWarps * 32, 0, st>>>(q_count, k, cp, rw, out, fail_rows, fail_ub,
+                                                fail_count,
+                                                reinterpret_cast<unsigned long long*>(max_err),
+                                                counters);
+      *launches += 4;
+      return cudaGetLastError();
+    }
     int mult = 8;
     if (const char* e = getenv("TOD_RR_GRID")) mult = std::max(1, atoi(e));  // experiment knob
     const int64_t gb = std::min<int64_t>((q_count + kGrpWarps - 1) / kGrpWarps, (int64_t)sms * mult);

@@ -496,3 +496,20 @@ def test_workspace_budget_chunks_queries_bit_identical(pkg, d, fmt):
     assert torch.equal(lof_got[0], lof_ref[0]) and torch.equal(lof_got[1], lof_ref[1])
     assert lof_got[3]["query_chunks"] > 2
     _check_rows(ref, _np(X), k, np.arange(0, n, n // 8))
+
+
+@pytest.mark.parametrize("n,d,k", [(20_000, 32, 20), (9000, 300, 12)])
+def test_split_rerank_matches_one_kernel_rerank(pkg, n, d, k, monkeypatch):
+    # the split re-rank (plan -> flat expansion -> finish; default at d > 256) and
+    # the one-kernel re-rank keep the same columns: outputs bit-identical, both
+    # equal to the oracle on sampled rows
+    X = torch.from_numpy(datagen.gaussian_mixture(n, d, seed=11 + d)).cuda()
+    res = {}
+    for split in ("0", "1"):
+        monkeypatch.setenv("TOD_RR_SPLIT", split)
+        with _ctx(pkg, fmt="fp16") as ctx:
+            res[split] = ctx.knn(X, k)
+    for f in ("idx", "dist64", "score_mean"):
+        assert torch.equal(getattr(res["0"], f), getattr(res["1"], f)), f
+    assert res["0"].stats["certified"] == res["1"].stats["certified"]
+    _check_rows(res["1"], _np(X), k, np.arange(0, n, n // 6))

@@ -21,7 +21,7 @@ X = torch.from_numpy(datagen.gaussian_mixture(a.n, a.d, seed=0)).cuda()
 ref = None
 for var in a.variants.split(","):
     env = dict(kv.split("=") for kv in var.split("+"))
-    for key in ("MAIN_PAIR", "RR_GRID", "SAMPLE_V1", "SAMPLE_R"):
+    for key in ("MAIN_PAIR", "RR_GRID", "RR_SPLIT", "SAMPLE_V1", "SAMPLE_R"):
         os.environ.pop("TOD_" + key, None)
     for key, v in env.items():
         os.environ["TOD_" + key] = v
