@@ -153,16 +153,21 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
   const int kmax_list = p->kind == PASS_TC ? 64 : 128;
   int kp_policy = kp;  // uncapped (the two-pass main pass has no list capacity)
   if (kp <= 0) {
-    if (fmt == TOD_FMT_FP16) kp = roundup(k + 24, 8);
+    // fp16: k + 24 (C2: 99.999 % certified); wide rows carry more quantization
+    // error per key, so more candidates (measured at d = 512, k = 50: K' 80 -> 96
+    // cuts the uncertified rows 134 -> 5 of 2e5 and the fallback 6.7 -> 0.4 ms)
+    if (fmt == TOD_FMT_FP16) kp = d > 128 ? roundup(3 * k / 2 + 16, 8) : roundup(k + 24, 8);
     else if (fmt == TOD_FMT_BF16) kp = roundup(std::max(6 * k, k + 40), 16);
     else kp = roundup(std::max(k + 8, 16), 8);
     kp_policy = kp;
     kp = std::min(kp, kmax_list);
   }
   if (kp < k) kp = k;  // never fewer candidates than outputs
-  if (kp > kmax_list)
-    return fail(ctx, TOD_E_UNSUPPORTED, "K'=%d exceeds this pass's list capacity %d (k=%d)", kp,
-                kmax_list, k);
+  if (kp_policy < kp) kp_policy = kp;
+  // an explicit K' above the list capacity is only honoured by the two-pass
+  // selection (its main pass has no list): checked once the pass is chosen
+  const int kp_req = kp;
+  if (kp > kmax_list) kp = kmax_list;
   p->kp = kp;
   int S = ctx->cfg.chunks;
   p->two = 0;
@@ -184,7 +189,7 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
       const int v = atoi(e);
       if (v >= 2 && v <= 64 && (v & (v - 1)) == 0) p->R = v;
     }
-    const int kps = std::min(64, std::max(8, roundup((2 * kp + p->R - 1) / p->R, 4)));
+    const int kps = std::min(64, std::max(8, roundup((2 * p->kp_target + p->R - 1) / p->R, 4)));
     const double img_bytes = (double)bt256 * 256 * (p->dpad + 16) * 2;
     p->main_S = std::max(1, (int)std::ceil(img_bytes / (48.0 * 1024 * 1024)));
     p->cap = roundup(std::max(64, 2 * (p->R - 1) * kps), 32);
@@ -192,6 +197,9 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
   }
   if (p->kind == PASS_TC && !p->two && p->dpad > 128)
     return fail(ctx, TOD_E_UNSUPPORTED, "d=%d needs the two-pass tensor-core path", d);
+  if (!p->two && kp_req > kmax_list)
+    return fail(ctx, TOD_E_UNSUPPORTED, "K'=%d exceeds this pass's list capacity %d (k=%d)",
+                kp_req, kmax_list, k);
   if (p->kind == PASS_TC && !p->two && p->dpad <= 64) bt_v1 = bt256;
   if (p->kind == PASS_TC) {
     // Reference chunks: each chunk's operand image should stay L2-resident
