@@ -32,7 +32,7 @@ struct Buf {
 };
 
 struct Workspace {
-  Buf bufs[48];
+  Buf bufs[64];
   void release() {
     for (auto& b : bufs) {
       if (b.p) cudaFree(b.p);
@@ -44,9 +44,9 @@ struct Workspace {
 enum BufId {
   B_X = 0, B_Q, B_IMG_B, B_A2_B, B_E_B, B_IMG_A, B_A2_A, B_E_A, B_MU, B_PART,
   B_G, B_CIDX, B_CV, B_FAIL, B_SMALL, B_IDX, B_DIST, B_DIST64, B_KTH, B_MEAN, B_KD64,
-  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT, B_FAILUB, B_NWRTAU, B_NWRCNT, B_NWRPTR, B_NWRCOLS, B_SCAN, B_ABOD, B_LABELS, B_PRED, B_SAMP, B_NWRBLK, B_NWRTASK, B_RRWS, B_NBUF
+  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT, B_FAILUB, B_NWRTAU, B_NWRCNT, B_NWRPTR, B_NWRCOLS, B_SCAN, B_ABOD, B_LABELS, B_PRED, B_SAMP, B_NWRBLK, B_NWRTASK, B_RRWS, B_T2ROWS, B_T2Q, B_T2IDX, B_T2D64, B_NBUF
 };
-static_assert(B_NBUF <= 48, "Workspace::bufs too small");
+static_assert(B_NBUF <= 64, "Workspace::bufs too small");
 
 }  // namespace
 
@@ -516,7 +516,36 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
   TOD_CUDA(cudaMemcpyAsync(&h, small, sizeof(SmallDev), cudaMemcpyDeviceToHost, st));
   TOD_CUDA(cudaStreamSynchronize(st));
   if (h.g.nonfinite) return fail(ctx, TOD_E_NONFINITE, "X (or Q) contains NaN or Inf");
-  if (h.fail_count > 0) {
+  const int nf = h.fail_count;
+  // TOD_TIER2 (testing knob): 0 = off, 1 = default (not under TOD_F_NO_CERTIFY, which
+  // exercises the brute-force tier), 2 = also under TOD_F_NO_CERTIFY
+  const char* t2e = getenv("TOD_TIER2");
+  const int t2 = t2e ? atoi(t2e) : 1;
+  if (nf > 0 && plan.fmt == TOD_FMT_BF16 && t2 != 0 &&
+      (t2 == 2 || !(ctx->cfg.flags & TOD_F_NO_CERTIFY)) && (int64_t)k + (self ? 1 : 0) <= n) {
+    // bf16 rows not certified: the fp16 pass on just those rows (its own
+    // fallback answers whatever it cannot certify), then scattered back
+    TOD_TRY(ensure(ctx, B_T2ROWS, (size_t)nf * 4, &p));
+    int32_t* rows = static_cast<int32_t*>(p);
+    TOD_CUDA(cudaMemcpyAsync(rows, fail_rows, (size_t)nf * 4, cudaMemcpyDeviceToDevice, st));
+    TOD_TRY(ensure(ctx, B_T2Q, (size_t)nf * d * 4, &p));
+    float* qf = static_cast<float*>(p);
+    TOD_CUDA(launch_gather_rows(self ? dX : dQ, self ? q_begin : 0, rows, nf, d, qf, st, launches));
+    const int k2 = self ? k + 1 : k;
+    KnnOutDev o2{};
+    TOD_TRY(ensure(ctx, B_T2IDX, (size_t)nf * k2 * 8, &p));
+    o2.idx = static_cast<int64_t*>(p);
+    TOD_TRY(ensure(ctx, B_T2D64, (size_t)nf * k2 * 8, &p));
+    o2.dist64 = static_cast<double*>(p);
+    const int fmt_saved = ctx->cfg.format;
+    ctx->cfg.format = TOD_FMT_FP16;
+    Timer off{ctx, false};
+    const tod_status s2 = run_knn(ctx, dX, n, qf, 0, nf, d, k2, o2, nullptr, off, launches);
+    ctx->cfg.format = fmt_saved;
+    if (s2 != TOD_OK) return s2;
+    TOD_CUDA(launch_tier2_scatter(rows, nf, q_begin, self, k, k2, o2.idx, o2.dist64, out, st,
+                                  launches));
+  } else if (nf > 0) {
     TOD_TRY(ensure(ctx, B_FBPART, fallback_workspace(h.fail_count, k, n, ctx->num_sms), &p));
     TOD_CUDA(launch_fallback(dQ, q_begin, dX, n, d, k, self, fail_rows, fail_ub, h.fail_count, out, p,
                              ctx->num_sms, st, launches));

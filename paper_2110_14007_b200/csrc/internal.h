@@ -142,6 +142,12 @@ cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, cons
                           int* launches);
 int fallback_slices(int nfail, int64_t n, int num_sms);
 size_t fallback_workspace(int nfail, int k, int64_t n, int num_sms);
+// second tier for bf16 passes (rerank.cu)
+cudaError_t launch_gather_rows(const float* src, int64_t base, const int32_t* rows, int nr, int d,
+                               float* dst, cudaStream_t st, int* launches);
+cudaError_t launch_tier2_scatter(const int32_t* rows, int nr, int64_t q_begin, bool self_join, int k,
+                                 int k2, const int64_t* idx2, const double* dd2, KnnOutDev out,
+                                 cudaStream_t st, int* launches);
 cudaError_t launch_fallback(const float* Q, int64_t q_begin, const float* X, int64_t n, int d,
                             int k, bool self_join, const int32_t* fail_rows,
                             const double* fail_ub, int nfail,

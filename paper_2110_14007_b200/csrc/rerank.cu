@@ -1160,6 +1160,60 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
   }
 }
 
+// ============================================ second tier for bf16 first passes
+// Rows a bf16 pass could not certify are re-answered by an fp16 pass (a finer
+// quantization of the same method, SURVEY 8(a) a4 tier 1): their rows are
+// gathered as queries, the library runs them against all of X with k+1
+// neighbours and no exclusion (k for query-mode calls), and the scatter drops
+// the row's own index (or, if it is not among the k+1 -- k+1 exact duplicates
+// with smaller indices -- the last entry), writing the outputs as write_row does.
+__global__ void k_gather_rows(const float* __restrict__ src, int64_t base,
+                              const int32_t* __restrict__ rows, int nr, int d,
+                              float* __restrict__ dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)nr * d) return;
+  const int64_t r = i / d, c = i - r * d;
+  dst[i] = src[(base + rows[r]) * d + c];
+}
+
+__global__ void k_tier2_scatter(const int32_t* __restrict__ rows, int nr, int64_t q_begin,
+                                int self_join, int k, int k2, const int64_t* __restrict__ idx2,
+                                const double* __restrict__ dd2, KnnOutDev out) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= nr) return;
+  const int64_t r = rows[w];
+  const int64_t self = self_join ? q_begin + r : -1;
+  // position of the self entry among the k2 (k2 - 1 = drop the last when absent)
+  int drop = k2 > k ? k2 - 1 : k2;
+  for (int m0 = 0; m0 < k2; m0 += 32) {
+    const int m = m0 + lane;
+    const unsigned hit = __ballot_sync(0xffffffffu, m < k2 && idx2[(int64_t)w * k2 + m] == self);
+    if (hit && drop == k2 - 1 && k2 > k) drop = m0 + __ffs(hit) - 1;
+  }
+  double acc = 0.0;
+  for (int m0 = 0; m0 < k; m0 += 32) {
+    const int m = m0 + lane;
+    double dd = 0.0;
+    if (m < k) {
+      const int src = m < drop ? m : m + 1;
+      dd = dd2[(int64_t)w * k2 + src];
+      const int64_t j = idx2[(int64_t)w * k2 + src];
+      if (out.idx) out.idx[r * k + m] = j;
+      if (out.dist64) out.dist64[r * k + m] = dd;
+      if (out.dist) out.dist[r * k + m] = __double2float_rn(dd);
+      if (m == k - 1) {
+        if (out.kdist64) out.kdist64[r] = dd;
+        if (out.score_kth) out.score_kth[r] = __double2float_rn(dd);
+      }
+    }
+    if (out.score_mean) {
+      const int cnt = k - m0 < 32 ? k - m0 : 32;
+      for (int t = 0; t < cnt; ++t) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, dd, t));
+    }
+  }
+  if (lane == 0 && out.score_mean) out.score_mean[r] = __double2float_rn(__ddiv_rn(acc, (double)k));
+}
+
 // ===================================================================== NWR
 // Neighbours within range (§5.3): {j != i : D_ij <= phi},
 // D_ij the squared distance of Eq. (3) evaluated as the oracle's O1.  Provable
@@ -1962,6 +2016,25 @@ cudaError_t launch_nwr_brute(const float* Q, int64_t q_begin, const float* X, in
 }
 
 int nwr_brute_slices() { return kNwrSlices; }
+
+cudaError_t launch_gather_rows(const float* src, int64_t base, const int32_t* rows, int nr, int d,
+                               float* dst, cudaStream_t st, int* launches) {
+  if (nr <= 0) return cudaSuccess;
+  const int64_t tot = (int64_t)nr * d;
+  k_gather_rows<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(src, base, rows, nr, d, dst);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tier2_scatter(const int32_t* rows, int nr, int64_t q_begin, bool self_join, int k,
+                                 int k2, const int64_t* idx2, const double* dd2, KnnOutDev out,
+                                 cudaStream_t st, int* launches) {
+  if (nr <= 0) return cudaSuccess;
+  k_tier2_scatter<<<(unsigned)((nr + 3) / 4), 128, 0, st>>>(rows, nr, q_begin, self_join ? 1 : 0, k,
+                                                           k2, idx2, dd2, out);
+  *launches += 1;
+  return cudaGetLastError();
+}
 
 size_t scan_workspace(int64_t q) { return (size_t)((q + 1023) / 1024 + 2) * 8; }
 

@@ -513,3 +513,30 @@ def test_split_rerank_matches_one_kernel_rerank(pkg, n, d, k, monkeypatch):
         assert torch.equal(getattr(res["0"], f), getattr(res["1"], f)), f
     assert res["0"].stats["certified"] == res["1"].stats["certified"]
     _check_rows(res["1"], _np(X), k, np.arange(0, n, n // 6))
+
+
+@pytest.mark.parametrize("case", ["mixture", "duplicates"])
+def test_bf16_second_tier_matches_brute_force_tier(pkg, case, monkeypatch):
+    # rows a bf16 pass cannot certify are re-answered by the fp16 pass on just
+    # those rows (self dropped from k+1 neighbours); the outputs must equal the
+    # fp64 brute-force tier's bit for bit, including rows with exact duplicates
+    if case == "mixture":
+        X = datagen.gaussian_mixture(60_000, 64, seed=8)
+    else:
+        X = datagen.with_duplicates(datagen.lattice(20_000, 64, seed=9, extent=3), frac=0.2, seed=10)
+    Xd = torch.from_numpy(X).cuda()
+    k = 10
+    # duplicates: every row forced through the tiers (TOD_F_NO_CERTIFY; knob 2 keeps
+    # the second tier on), so the self-drop among exact-duplicate neighbours runs
+    flags, on = (0, "1") if case == "mixture" else (pkg.F_NO_CERTIFY, "2")
+    res = {}
+    for t2 in (on, "0"):
+        monkeypatch.setenv("TOD_TIER2", t2)
+        with _ctx(pkg, fmt="bf16", flags=flags) as ctx:
+            res[t2] = ctx.knn(Xd, k)
+    res["1"] = res[on]
+    assert res["1"].stats["fallback_rows"] == res["0"].stats["fallback_rows"]
+    print("bf16 uncertified rows:", res["1"].stats["fallback_rows"])
+    for f in ("idx", "dist", "dist64", "score_kth", "score_mean", "kdist64"):
+        assert torch.equal(getattr(res["1"], f), getattr(res["0"], f)), f
+    _check_rows(res["1"], X, k, np.arange(0, X.shape[0], X.shape[0] // 8))
