@@ -385,29 +385,6 @@ struct RowTel {
   double maxerr = 0.0;
 };
 
-// fp32 screen distance (difference form, FMA, 4 independent partial sums): all
-// terms are >= 0, so |D32 - rho^2| <= gamma_{d+2}(2^-24) rho^2 whatever the order.
-template <int DT>
-__device__ __forceinline__ float d32_fixed(const float* __restrict__ xqf, const float* xj) {
-  float v[DT];
-#pragma unroll
-  for (int u = 0; u < DT / 8; ++u) ldg8(xj + 8 * u, v + 8 * u);
-  float a[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-  for (int c = 0; c < DT; c += 4) {
-    const float4 q = *reinterpret_cast<const float4*>(xqf + c);
-    float t = q.x - v[c];
-    a[0] = fmaf(t, t, a[0]);
-    t = q.y - v[c + 1];
-    a[1] = fmaf(t, t, a[1]);
-    t = q.z - v[c + 2];
-    a[2] = fmaf(t, t, a[2]);
-    t = q.w - v[c + 3];
-    a[3] = fmaf(t, t, a[3]);
-  }
-  return (a[0] + a[1]) + (a[2] + a[3]);
-}
-
 template <int DT>
 __device__ __forceinline__ void rerank_groups_row(
     const float* __restrict__ Q, int64_t q_begin, int64_t q_count, const float* __restrict__ X,
@@ -423,7 +400,6 @@ __device__ __forceinline__ void rerank_groups_row(
   __shared__ int s_ci[kGrpWarps][kColMax];        //                    index
   __shared__ double s_tk[kGrpWarps][kMaxK];       // selected top-k
   __shared__ int s_ti[kGrpWarps][kMaxK];
-  __shared__ __align__(16) float s_xqf[kGrpWarps][64];  // fp32 query row (screen, DT > 0)
   extern __shared__ double s_xq[];                // [warps][d] query row in fp64
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t gi = q_begin + r;
@@ -558,48 +534,6 @@ __device__ __forceinline__ void rerank_groups_row(
   double* ck = s_ck[w];
   int* ci = s_ci[w];
   int nc = 0;
-  if constexpr (DT < 0) {  // fp32 screen: measured no faster on B200 (gathers dominate); kept off
-    // phase 1: fp32 screen of every column of the visited groups; a column can
-    // only have D64 <= UB if D32 <= T32 := UB (1 + g32) / (1 - g64), rounded up
-    const double g32 = gamma_up(DT + 2, 5.9604644775390625e-08);
-    const double g64 = gamma_up(DT + 2, 1.1102230246251565e-16);
-    const float T32 = UB < CUDART_INF
-                          ? __double2float_ru(UB * (1.0 + g32) / (1.0 - g64) * (1.0 + 1e-7) + 1e-30)
-                          : CUDART_INF_F;
-    const float* xqf = s_xqf[w];
-    int ns = 0;
-    for (int b0 = 0; b0 < nv; b0 += 4) {
-      const int gs = b0 + (lane >> 3);
-      const int g = gs < nv ? gid[gs] : -1;
-      const int64_t j = (int64_t)g * 8 + (lane & 7);
-      bool pass = false;
-      if (g >= 0 && j < n && !(self_join && j == gi)) pass = d32_fixed<DT>(xqf, X + j * d) <= T32;
-      const unsigned pm = __ballot_sync(0xffffffffu, pass);
-      const int pos = ns + __popc(pm & ((1u << lane) - 1u));
-      if (pass && pos < kColMax) ci[pos] = (int)j;
-      ns += __popc(pm);
-    }
-    overflow |= ns > kColMax;
-    if (ns > kColMax) ns = kColMax;
-    __syncwarp();
-    // phase 2: the oracle's exact D64 for the survivors only (compacted in place)
-    for (int s0 = 0; s0 < ns; s0 += 32) {
-      const int e = s0 + lane;
-      const int j = e < ns ? ci[e] : -1;
-      double key = CUDART_INF;
-      if (j >= 0) key = d64_fixed<DT>(xq, X + (int64_t)j * d);
-      const bool keep = key <= UB && key < CUDART_INF;
-      const unsigned km = __ballot_sync(0xffffffffu, keep);
-      const int pos = nc + __popc(km & ((1u << lane) - 1u));
-      __syncwarp();
-      if (keep) {
-        ck[pos] = key;
-        ci[pos] = j;
-      }
-      nc += __popc(km);
-      __syncwarp();
-    }
-  } else {
   for (int b0 = 0; b0 < nv; b0 += 4) {
     const int gs = b0 + (lane >> 3);
     const int g = gs < nv ? gid[gs] : -1;
@@ -659,7 +593,6 @@ __device__ __forceinline__ void rerank_groups_row(
       ci[pos] = (int)j;
     }
     nc += __popc(km);
-  }
   }
   overflow |= nc > kColMax;
   if (nc > kColMax) nc = kColMax;

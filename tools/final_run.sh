@@ -4,6 +4,7 @@ timeout -s KILL 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider > g
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/prof/smoke.txt 2>&1; tail -1 gpurun_out/prof/smoke.txt
 timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/prof/bench_c2_line.json 2> gpurun_out/prof/bench_c2.err
 timeout 900 python bench.py --config c3f16 --steps 5 --warmup 3 --no-cpu > gpurun_out/prof/bench_c3f16_line.json 2> /dev/null
+timeout 900 python bench.py --config c3 --steps 5 --warmup 3 --no-cpu > gpurun_out/prof/bench_c3_line.json 2> /dev/null
 timeout 900 python bench.py --config c5s --steps 2 --warmup 3 --no-cpu > gpurun_out/prof/bench_c5s_line.json 2> /dev/null
 timeout 600 python bench.py --config nwr --steps 10 --warmup 3 > gpurun_out/prof/bench_nwr_line.json 2> /dev/null
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/prof/bench_ref_line.json 2> /dev/null
