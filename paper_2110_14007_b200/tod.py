@@ -152,7 +152,10 @@ def _empty_like_host_or_dev(ref, shape, dtype_np):
         import torch
         tmap = {np.int64: torch.int64, np.int32: torch.int32, np.float32: torch.float32,
                 np.float64: torch.float64}
-        return torch.empty(shape, dtype=tmap[dtype_np], device=ref.device)
+        # host outputs of a pinned host input are pinned too (torch's caching host
+        # allocator), so the library's device->host copies run at DMA speed
+        pin = ref.device.type == "cpu" and ref.is_pinned()
+        return torch.empty(shape, dtype=tmap[dtype_np], device=ref.device, pin_memory=pin)
     return np.empty(shape, dtype=dtype_np)
 
 
