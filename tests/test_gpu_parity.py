@@ -535,6 +535,14 @@ def test_bf16_second_tier_matches_brute_force_tier(pkg, case, monkeypatch):
         with _ctx(pkg, fmt="bf16", flags=flags) as ctx:
             res[t2] = ctx.knn(Xd, k)
     res["1"] = res[on]
+    if case == "duplicates":  # query mode (no self to drop) through the same tier
+        q = {}
+        for t2 in (on, "0"):
+            monkeypatch.setenv("TOD_TIER2", t2)
+            with _ctx(pkg, fmt="bf16", flags=flags) as ctx:
+                q[t2] = ctx.knn_query(Xd[:3000], Xd, k)
+        for f in ("idx", "dist64", "score_mean"):
+            assert torch.equal(getattr(q[on], f), getattr(q["0"], f)), f
     assert res["1"].stats["fallback_rows"] == res["0"].stats["fallback_rows"]
     print("bf16 uncertified rows:", res["1"].stats["fallback_rows"])
     for f in ("idx", "dist", "dist64", "score_kth", "score_mean", "kdist64"):
