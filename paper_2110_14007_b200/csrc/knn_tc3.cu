@@ -1,5 +1,5 @@
-// knn_tc3.cu — K2 main pass (dpad <= 64): fused tile distance + threshold filter
-// on tcgen05 tensor cores, append-only.
+// knn_tc3.cu — K2 main pass and key-only sample pass (dpad <= 512): fused tile
+// distance + threshold filter on tcgen05 tensor cores, append-only.
 //
 // Arithmetic: the tensor core produces, per (query row i,
 // reference column j),
@@ -10,23 +10,25 @@
 // is appended to the row's candidate buffer in HBM (operator fusion of cdist
 // and topk: the n x n matrix is never stored).
 //
-// tau_i comes from the SAMPLE pass (knn_tc.cu run on every R-th reference tile
-// with a small candidate list): it is that list's threshold, so every group
-// NOT appended anywhere -- sample or main -- has key >= tau_i, which is all the
-// certificate needs.  With tau_i
-// fixed for the whole pass there is no per-row set to maintain: the epilogue
-// is a pure stream (min trees, one compare, predicated shared-memory append),
-// and chunks of the same row may run concurrently (slots are reserved with one
-// atomicAdd per flush).
+// tau_i comes from the SAMPLE pass over every R-th reference tile (this kernel's
+// sample mode, keys only, or knn_tc.cu's list-based pass): every group NOT kept
+// anywhere has key >= tau_i, which is all the certificate needs (DESIGN.md
+// "Two-pass candidate selection").  With tau_i fixed for the whole pass there is
+// no per-row set to maintain: the epilogue is a pure stream (min trees, one
+// compare, predicated shared-memory append), and chunks of the same row may run
+// concurrently (slots are reserved with one atomicAdd per flush).
 //
 // Structure (one CTA per SM, persistent; items = query tile x reference
 // chunk, chunk-major so all SMs sweep the same L2-resident chunk):
 //   warp 0     producer: bulk async copies (TMA engine) of the query tile and
-//              a ring of 256-column reference tiles, mbarrier complete_tx.
+//              a ring of 256-column reference tiles (dpad <= 64: A resident;
+//              dpad > 64: A and B streamed per 64-wide K chunk), mbarrier
+//              complete_tx.
 //   warp 1     TMEM allocator + MMA issuer: (dpad+16)/16 MMAs 128x256x16 per
 //              tile into one of two 256-column TMEM accumulators.
-//   warps 2-9  filter: warp (q, h) owns TMEM lane quarter q (32 rows) and
-//              column half h (128 columns) of every tile.
+//   warps 2..  FW filter warps (16, or 8 when fewer operand stages fit): warp
+//              (q, h) owns TMEM lane quarter q (32 rows) and column part h
+//              (256 / (FW/4) columns) of every tile.
 #include <math_constants.h>
 
 #include <algorithm>
