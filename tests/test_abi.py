@@ -73,3 +73,18 @@ def test_product_package_never_imports_oracle():
                 txt = open(os.path.join(dp, f)).read()
                 assert not re.search(r"^\s*(import|from)\s+oracle\b", txt, re.M), f
                 assert "knn_oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_every_environment_knob_is_documented():
+    # the library's experiment knobs (getenv) must be listed in DESIGN.md
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    csrc = os.path.join(root, "paper_2110_14007_b200", "csrc")
+    names = set()
+    for f in os.listdir(csrc):
+        if f.endswith((".cu", ".cuh", ".h")):
+            with open(os.path.join(csrc, f)) as fh:
+                names |= set(re.findall(r'getenv\("([A-Z_0-9]+)"\)', fh.read()))
+    with open(os.path.join(root, "DESIGN.md")) as fh:
+        design = fh.read()
+    missing = sorted(n for n in names if n not in design)
+    assert not missing, missing
