@@ -485,11 +485,8 @@ __device__ __forceinline__ void rerank_groups_row(
       lo = min(lo, o);
       hi = max(hi, o);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
     // invariant: count(key <= hi) >= k; shrink hi towards the k-th key (a tight
     // kappa keeps UB, and with it the visited set, small).  Stopping within
     // 64 ulps of it (relative 2^-17, far below the bound's own slack) saves the
@@ -502,8 +499,7 @@ __device__ __forceinline__ void rerank_groups_row(
 #pragma unroll
       for (int u = 0; u < 8; ++u) c += ok[u] <= mid;
       for (int e = lane + 256; e < G; e += 32) c += f2ord(gk[e]) <= mid;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      c = __reduce_add_sync(0xffffffffu, c);  // one REDUX instead of a 5-step shuffle tree
       if (c >= k) {
         hi = mid;
         chi = c;
@@ -864,11 +860,8 @@ __global__ void __launch_bounds__(kGrpWarps * 32, 4)
         lo = min(lo, o);
         hi = max(hi, o);
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-      }
+      lo = __reduce_min_sync(0xffffffffu, lo);
+      hi = __reduce_max_sync(0xffffffffu, hi);
       if (lo < hi) --lo;
       int chi = G;
       for (int it = 0; it < 32 && hi - lo > 64 && chi > k; ++it) {
@@ -877,8 +870,7 @@ __global__ void __launch_bounds__(kGrpWarps * 32, 4)
 #pragma unroll
         for (int u = 0; u < 8; ++u) c += ok[u] <= mid;
         for (int e = lane + 256; e < G; e += 32) c += f2ord(gk[e]) <= mid;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        c = __reduce_add_sync(0xffffffffu, c);
         if (c >= k) {
           hi = mid;
           chi = c;
