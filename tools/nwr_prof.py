@@ -1,3 +1,4 @@
+"""tod_nwr phase timings on the C2 data at two radii (profiling aid)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, datagen

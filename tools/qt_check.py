@@ -1,4 +1,4 @@
-"""A/B experiment knobs (TOD_<KEY>=v, e.g. MAIN_PAIR=0+RR_MINB=6): identical outputs, timings."""
+"""A/B experiment knobs (TOD_<KEY>=v, e.g. MAIN_PAIR=0+RR_SPLIT=1): identical outputs, timings."""
 import argparse
 import os
 import sys
