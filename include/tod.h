@@ -47,7 +47,10 @@
 extern "C" {
 #endif
 
-#define TOD_ABI_VERSION 2
+#define TOD_ABI_VERSION 3
+
+/* Largest k (neighbours per row) this build serves; larger k -> TOD_E_UNSUPPORTED. */
+#define TOD_MAX_K 128
 
 typedef enum {
   TOD_OK = 0,
@@ -82,7 +85,9 @@ typedef struct {
   int32_t format;          /* tod_format */
   int32_t kprime;          /* K' candidates kept per row by the low-precision pass; 0 = auto */
   uint32_t flags;          /* TOD_F_* */
-  void* stream;            /* cudaStream_t to run on; NULL = the library's own non-blocking stream */
+  void* stream;            /* cudaStream_t to run on; NULL = a stream the library creates, BLOCKING
+                              with respect to the legacy default stream (it waits for work queued
+                              there, e.g. by torch, before running) */
   int32_t chunks;          /* reference chunks S per query tile (load balance); 0 = auto */
   int32_t epilogue_split;  /* tensor-core pass: epilogue warps per TMEM lane quarter (1 or 2; 2 splits each
                               tile's columns into two per-row lists of K'/2+8); 0 = auto */
@@ -128,6 +133,9 @@ typedef struct {
   float* score_kth;     /* [q_count] fp32(dist64[:, k-1]) */
   float* score_mean;    /* [q_count] fp32((sum_m dist64[:, m], sequential in m) / k) */
   double* kdist64;      /* [q_count] dist64[:, k-1] (k-distance; input of the LOF stage) */
+  int32_t* row_tier;    /* [q_count] diagnostics: which step answered each row -- 0 = certified by the
+                           low-precision pass (P:342 step iii), 1 = bf16 rows re-answered by the fp16
+                           pass, 2 = the fp64 tiers ("recalculate on the subset") */
 } tod_knn_out;
 
 typedef struct tod_ctx tod_ctx;
@@ -236,9 +244,11 @@ tod_status tod_nwr(tod_ctx* ctx, const float* X, int64_t n, int32_t d, double ph
  * tod_abod — angle-based outlier scores (§4.2, Fig. 3(a):
  * the kNN functional operator followed by cosine similarity; Kriegel 2008,
  * cited P:182).  For each query row i in [q_begin, q_begin+q_count) of X
- * (self-join, exact neighbours as tod_knn): score_i = -Var over neighbour
- * pairs (a < b) of cos(x_a - x_i, x_b - x_i), pairs with a coincident
- * neighbour skipped, 0 if none remain (reading A20; higher = more outlying).
+ * (self-join, exact neighbours as tod_knn): with a = x_a - x_i, b = x_b - x_i,
+ * score_i = -Var over neighbour pairs (a < b) of <a,b> / (||a||^2 ||b||^2)
+ * (Kriegel's distance-weighted angle factor, as PyOD's fast ABOD over the
+ * k-exact neighbour set), pairs with a coincident neighbour skipped, 0 if none
+ * remain (reading A20; higher = more outlying).
  * fp64 with the oracle's operation order; fp32 out.
  *   score    [q_count] fp32 (required).  knn_out: optional neighbour outputs.
  * Errors: as tod_knn; TOD_E_UNSUPPORTED for k > 48.

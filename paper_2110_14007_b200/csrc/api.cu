@@ -44,7 +44,7 @@ struct Workspace {
 enum BufId {
   B_X = 0, B_Q, B_IMG_B, B_A2_B, B_E_B, B_IMG_A, B_A2_A, B_E_A, B_MU, B_PART,
   B_G, B_CIDX, B_CV, B_FAIL, B_SMALL, B_IDX, B_DIST, B_DIST64, B_KTH, B_MEAN, B_KD64,
-  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT, B_FAILUB, B_NWRTAU, B_NWRCNT, B_NWRPTR, B_NWRCOLS, B_SCAN, B_ABOD, B_LABELS, B_PRED, B_SAMP, B_NWRBLK, B_NWRTASK, B_RRWS, B_T2ROWS, B_T2Q, B_T2IDX, B_T2D64, B_NBUF
+  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT, B_FAILUB, B_NWRTAU, B_NWRCNT, B_NWRPTR, B_NWRCOLS, B_SCAN, B_ABOD, B_LABELS, B_PRED, B_SAMP, B_NWRBLK, B_NWRTASK, B_RRWS, B_T2ROWS, B_T2Q, B_T2IDX, B_T2D64, B_TIER, B_NBUF
 };
 static_assert(B_NBUF <= 64, "Workspace::bufs too small");
 
@@ -290,12 +290,22 @@ struct SmallDev {
   unsigned long long counters[3];  // re-rank telemetry: staged groups, visited groups, kept columns
 };
 
+// Reference-side prep shared by the query chunks of one call (automatic
+// batching): computed by the first chunk, reused by the others.  A bf16 second
+// tier overwrites the reference image and the globals, so it clears `ready`.
+struct RefPrep {
+  bool ready = false;
+  const float* dQall = nullptr;  // query mode: every query row of the call (finite / absmax)
+  int64_t nq_all = 0;
+};
+
 // Input quantization (a1) for the tensor-core passes: column mean, power-of-two
-// scale, reference image B over all n rows and query image A over the 128-row
-// query tiles covering [q_begin, q_begin+q_count) (self-join) or over Q.
+// scale, reference image B over all n rows (skipped when ref->ready) and query
+// image A over the 128-row query tiles covering [q_begin, q_begin+q_count)
+// (self-join) or over Q.
 tod_status prep_tc(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, int64_t q_begin,
                    int64_t q_count, int d, int fmt, int dpad, PrepGlobals* g, Image* Aout,
-                   Image* Bout, CertParams* cp, int* launches) {
+                   Image* Bout, CertParams* cp, RefPrep* ref, int* launches) {
   cudaStream_t st = ctx->stream;
   const bool self = dQ == nullptr;
   void* p;
@@ -327,19 +337,24 @@ tod_status prep_tc(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
   Image& A = *Aout;
   TOD_TRY(make_img(B_IMG_B, B_A2_B, B_E_B, n, n_pad, &B));
   TOD_TRY(make_img(B_IMG_A, B_A2_A, B_E_A, a_rows, a_pad, &A));
-  const int stat_blocks = (int)((n + 127) / 128);  // prep.cu kRowsPerStatBlock
   TOD_TRY(ensure(ctx, B_MU, (size_t)d * 8, &p));
   double* mu = static_cast<double*>(p);
-  TOD_TRY(ensure(ctx, B_PART, (size_t)stat_blocks * d * 8, &p));
-  double* part = static_cast<double*>(p);
-  TOD_CUDA(launch_prep_stats(dX, n, d, mu, part, stat_blocks, g, st, launches));
-  TOD_CUDA(launch_prep_absmax(dX, n, d, mu, g, st, launches));
-  if (!self) {
-    TOD_CUDA(launch_finite_check(dQ, q_count, d, g, st, launches));
-    TOD_CUDA(launch_prep_absmax(dQ, q_count, d, mu, g, st, launches));
+  if (!ref->ready) {
+    const int stat_blocks = (int)((n + 127) / 128);  // prep.cu kRowsPerStatBlock
+    TOD_TRY(ensure(ctx, B_PART, (size_t)stat_blocks * d * 8, &p));
+    double* part = static_cast<double*>(p);
+    TOD_CUDA(launch_prep_stats(dX, n, d, mu, part, stat_blocks, g, st, launches));
+    TOD_CUDA(launch_prep_absmax(dX, n, d, mu, g, st, launches));
+    if (!self) {
+      const float* qa = ref->dQall ? ref->dQall : dQ;
+      const int64_t nqa = ref->dQall ? ref->nq_all : q_count;
+      TOD_CUDA(launch_finite_check(qa, nqa, d, g, st, launches));
+      TOD_CUDA(launch_prep_absmax(qa, nqa, d, mu, g, st, launches));
+    }
+    TOD_CUDA(launch_prep_scale(g, fmt, dpad, st, launches));
+    TOD_CUDA(launch_prep_quant(dX, n, d, mu, g, fmt, B, 0, st, launches));
+    ref->ready = true;
   }
-  TOD_CUDA(launch_prep_scale(g, fmt, dpad, st, launches));
-  TOD_CUDA(launch_prep_quant(dX, n, d, mu, g, fmt, B, 0, st, launches));
   const float* qsrc = self ? dX + a_row0 * d : dQ;
   TOD_CUDA(launch_prep_quant(qsrc, a_rows, d, mu, g, fmt, A, 1, st, launches));
   cp->qa2 = A.a2 + (self ? q_begin - a_row0 : 0);
@@ -351,7 +366,8 @@ tod_status prep_tc(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
 // [q_begin, q_begin+q_count).  Else queries Q[0..q_count) against X.
 tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, int64_t q_begin,
                    int64_t q_count, int d, int k, KnnOutDev out, tod_stats* stats, Timer& tm,
-                   int* launches) {
+                   int* launches, RefPrep* ref) {
+  int32_t* row_tier = out.tier;
   const bool self = dQ == nullptr;
   bool main_timed = false;
   int main_kernel = 0;
@@ -363,7 +379,12 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
   void* p;
   TOD_TRY(ensure(ctx, B_SMALL, sizeof(SmallDev), &p));
   SmallDev* small = static_cast<SmallDev*>(p);
-  TOD_CUDA(cudaMemsetAsync(small, 0, sizeof(SmallDev), st));
+  if (plan.kind == PASS_TC && ref->ready) {  // keep the reference-side globals
+    const size_t off = offsetof(SmallDev, fail_count);
+    TOD_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(small) + off, 0, sizeof(SmallDev) - off, st));
+  } else {
+    TOD_CUDA(cudaMemsetAsync(small, 0, sizeof(SmallDev), st));
+  }
   PrepGlobals* g = &small->g;
 
   Cands cands;
@@ -411,7 +432,7 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
   if (plan.kind == PASS_TC) {
     Image B, A;
     TOD_TRY(prep_tc(ctx, dX, n, dQ, q_begin, q_count, d, plan.fmt, plan.dpad, g, &A, &B, &cp,
-                    launches));
+                    ref, launches));
     tm.mark();  // 2: main start
     // Two-pass sample: key-only register top-4 per (row, column part) over the
     // sample tiles (knn_tc3 sample mode), tau = the j-th smallest of those; the
@@ -521,12 +542,29 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
   // exercises the brute-force tier), 2 = also under TOD_F_NO_CERTIFY
   const char* t2e = getenv("TOD_TIER2");
   const int t2 = t2e ? atoi(t2e) : 1;
-  if (nf > 0 && plan.fmt == TOD_FMT_BF16 && t2 != 0 &&
-      (t2 == 2 || !(ctx->cfg.flags & TOD_F_NO_CERTIFY)) && (int64_t)k + (self ? 1 : 0) <= n) {
+  // the second tier only when the fp16 plan can serve k2 = k (+1 for the
+  // dropped self) neighbours; otherwise, or if it fails, the fp64 tiers answer
+  bool tier2 = nf > 0 && plan.fmt == TOD_FMT_BF16 && t2 != 0 &&
+               (t2 == 2 || !(ctx->cfg.flags & TOD_F_NO_CERTIFY)) &&
+               (int64_t)k + (self ? 1 : 0) <= n && k + (self ? 1 : 0) <= TOD_MAX_K;
+  if (tier2) {
+    const int fmt_saved = ctx->cfg.format;
+    ctx->cfg.format = TOD_FMT_FP16;
+    Plan p2;
+    const std::string msg_saved = ctx->msg;
+    tier2 = make_plan(ctx, n, nf, d, k + (self ? 1 : 0), &p2) == TOD_OK;
+    ctx->cfg.format = fmt_saved;
+    ctx->msg = msg_saved;
+  }
+  bool tier2_done = false;
+  const int32_t* rows_t2 = nullptr;
+  if (row_tier) TOD_CUDA(cudaMemsetAsync(row_tier, 0, (size_t)q_count * 4, st));
+  if (tier2) {
     // bf16 rows not certified: the fp16 pass on just those rows (its own
     // fallback answers whatever it cannot certify), then scattered back
     TOD_TRY(ensure(ctx, B_T2ROWS, (size_t)nf * 4, &p));
     int32_t* rows = static_cast<int32_t*>(p);
+    rows_t2 = rows;
     TOD_CUDA(cudaMemcpyAsync(rows, fail_rows, (size_t)nf * 4, cudaMemcpyDeviceToDevice, st));
     TOD_TRY(ensure(ctx, B_T2Q, (size_t)nf * d * 4, &p));
     float* qf = static_cast<float*>(p);
@@ -540,12 +578,28 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     const int fmt_saved = ctx->cfg.format;
     ctx->cfg.format = TOD_FMT_FP16;
     Timer off{ctx, false};
-    const tod_status s2 = run_knn(ctx, dX, n, qf, 0, nf, d, k2, o2, nullptr, off, launches);
+    RefPrep ref2;  // the fp16 tier re-quantizes the references in its own format
+    ref->ready = false;
+    const tod_status s2 = run_knn(ctx, dX, n, qf, 0, nf, d, k2, o2, nullptr, off, launches, &ref2);
     ctx->cfg.format = fmt_saved;
-    if (s2 != TOD_OK) return s2;
-    TOD_CUDA(launch_tier2_scatter(rows, nf, q_begin, self, k, k2, o2.idx, o2.dist64, out, st,
-                                  launches));
-  } else if (nf > 0) {
+    if (s2 == TOD_OK) {
+      TOD_CUDA(launch_tier2_scatter(rows, nf, q_begin, self, k, k2, o2.idx, o2.dist64, out, st,
+                                    launches));
+      tier2_done = true;
+    } else if (s2 != TOD_E_UNSUPPORTED && s2 != TOD_E_NOMEM) {
+      return s2;
+    } else {  // the fp64 tiers answer instead: the failing rows are still in fail_rows
+      // (the inner call may have reused fail_rows / fail_ub: restore the rows and
+      // drop the upper bounds -- 0x7F7F... is a valid, huge bound)
+      ctx->msg.clear();
+      TOD_CUDA(cudaMemcpyAsync(fail_rows, rows, (size_t)nf * 4, cudaMemcpyDeviceToDevice, st));
+      TOD_CUDA(cudaMemsetAsync(fail_ub, 0x7F, (size_t)nf * 8, st));
+    }
+  }
+  if (row_tier && nf > 0)  // diagnostics: 1 = bf16 -> fp16 second tier, 2 = fp64 tiers
+    TOD_CUDA(launch_mark_rows(tier2_done ? rows_t2 : fail_rows, nf, tier2_done ? 1 : 2, row_tier, st,
+                              launches));
+  if (nf > 0 && !tier2_done) {
     TOD_TRY(ensure(ctx, B_FBPART, fallback_workspace(h.fail_count, k, n, ctx->num_sms), &p));
     TOD_CUDA(launch_fallback(dQ, q_begin, dX, n, d, k, self, fail_rows, fail_ub, h.fail_count, out, p,
                              ctx->num_sms, st, launches));
@@ -597,8 +651,9 @@ tod_status run_nwr(tod_ctx* ctx, const float* dX, int64_t n, int d, double phi, 
   cp.g = &small->g;
   tm.mark();  // 1: prep
   Image A, B;
+  RefPrep ref;
   TOD_TRY(prep_tc(ctx, dX, n, nullptr, q_begin, q_count, d, fmt, dpad, &small->g, &A, &B, &cp,
-                  launches));
+                  &ref, launches));
   TOD_TRY(ensure(ctx, B_NWRTAU, (size_t)std::max<int64_t>(q_count, 1) * 4, &p));
   float* tau = static_cast<float*>(p);
   TOD_CUDA(launch_nwr_tau(q_count, phi, cp, tau, st, launches));
@@ -698,13 +753,15 @@ tod_status validate_common(tod_ctx* ctx, int64_t n, int32_t d, int32_t k) {
   if (n < 1 || n > INT32_MAX) return fail(ctx, TOD_E_RANGE, "n=%lld outside [1, 2^31-1]", (long long)n);
   if (d < 1 || d > 4096) return fail(ctx, TOD_E_RANGE, "d=%d outside [1, 4096]", d);
   if (k < 1) return fail(ctx, TOD_E_RANGE, "k=%d < 1", k);
+  if (k > TOD_MAX_K)
+    return fail(ctx, TOD_E_UNSUPPORTED, "k=%d exceeds this build's limit TOD_MAX_K=%d", k, TOD_MAX_K);
   return TOD_OK;
 }
 
 struct OutStage {
   KnnOutDev dev{};
   bool st_idx = false, st_dist = false, st_d64 = false, st_kth = false, st_mean = false,
-       st_kd = false;
+       st_kd = false, st_tier = false;
 };
 
 tod_status stage_outputs(tod_ctx* ctx, const tod_knn_out* o, int64_t q, int k, OutStage* s) {
@@ -717,6 +774,7 @@ tod_status stage_outputs(tod_ctx* ctx, const tod_knn_out* o, int64_t q, int k, O
   TOD_TRY(dev_view(ctx, o->score_kth, (size_t)q, B_KTH, &s->dev.score_kth, &s->st_kth));
   TOD_TRY(dev_view(ctx, o->score_mean, (size_t)q, B_MEAN, &s->dev.score_mean, &s->st_mean));
   TOD_TRY(dev_view(ctx, o->kdist64, (size_t)q, B_KD64, &s->dev.kdist64, &s->st_kd));
+  TOD_TRY(dev_view(ctx, o->row_tier, (size_t)q, B_TIER, &s->dev.tier, &s->st_tier));
   return TOD_OK;
 }
 
@@ -730,6 +788,7 @@ tod_status unstage_outputs(tod_ctx* ctx, const tod_knn_out* o, int64_t q, int k,
   if (s.st_kth) TOD_CUDA(cudaMemcpyAsync(o->score_kth, s.dev.score_kth, q * 4, cudaMemcpyDeviceToHost, st));
   if (s.st_mean) TOD_CUDA(cudaMemcpyAsync(o->score_mean, s.dev.score_mean, q * 4, cudaMemcpyDeviceToHost, st));
   if (s.st_kd) TOD_CUDA(cudaMemcpyAsync(o->kdist64, s.dev.kdist64, q * 8, cudaMemcpyDeviceToHost, st));
+  if (s.st_tier) TOD_CUDA(cudaMemcpyAsync(o->row_tier, s.dev.tier, q * 4, cudaMemcpyDeviceToHost, st));
   return TOD_OK;
 }
 
@@ -750,9 +809,17 @@ tod_status stage_input(tod_ctx* ctx, const float* user, size_t count, int id, co
 // device workspace of one run_knn call, per query row, from the plan.
 size_t knn_bytes_per_row(const Plan& p, int k) {
   size_t b = (size_t)p.lists * p.kp * 12 + (size_t)p.lists * 4;  // pass-1 lists + thresholds
-  if (p.two) b += (size_t)tc3_parts(p.dpad) * ((size_t)p.cap * 2 / std::max(1, tc3_parts(p.dpad)) * 8 + 4);
+  if (p.kind == PASS_TC && p.S > 1) b += (size_t)p.lists * p.kp * 8;  // parked list state (B_STLIST)
+  if (p.two) {
+    const int parts = std::max(1, tc3_parts(p.dpad));
+    b += (size_t)parts * ((size_t)p.cap * 2 / parts * 8 + 4);  // main-pass buffers + counts
+    b += (size_t)parts * 8 * 4;                                 // key-only sample minima (B_SAMP)
+  }
   b += (size_t)(p.dpad + 16) * 2 + 16;  // query image row + its bounds
-  b += (size_t)k * 24 + 64;             // staged outputs, fallback bookkeeping
+  b += (size_t)k * 24 + 64;             // staged outputs, fail list and bounds
+  // fallback: threshold tier (1024 candidates x 12 B) + per-slice lists, for
+  // every row in the worst case (the tier only runs on failing rows)
+  b += 1024 * 12 + (size_t)k * 12 * 8;
   if (p.kind == PASS_TC && rerank_use_split(p.dpad))
     b += rerank_split_ws(1024) / 1024;  // split re-rank: visited groups, kept columns, tasks
   return b;
@@ -772,8 +839,11 @@ tod_status run_knn_auto(tod_ctx* ctx, const float* dX, int64_t n, const float* d
     const size_t per = knn_bytes_per_row(plan, k);
     rows = std::max<int64_t>(128, (int64_t)(ctx->cfg.workspace_bytes / per) / 128 * 128);
   }
+  RefPrep ref;
+  ref.dQall = dQ;
+  ref.nq_all = dQ ? q_count : 0;
   if (rows >= q_count) {
-    TOD_TRY(run_knn(ctx, dX, n, dQ, q_begin, q_count, d, k, out, stats, tm, launches));
+    TOD_TRY(run_knn(ctx, dX, n, dQ, q_begin, q_count, d, k, out, stats, tm, launches, &ref));
     if (stats) stats->query_chunks = 1;
     return TOD_OK;
   }
@@ -791,9 +861,10 @@ tod_status run_knn_auto(tod_ctx* ctx, const float* dX, int64_t n, const float* d
     o.score_kth = sh(out.score_kth, 1);
     o.score_mean = sh(out.score_mean, 1);
     o.kdist64 = sh(out.kdist64, 1);
+    o.tier = sh(out.tier, 1);
     tod_stats cs{};
     TOD_TRY(run_knn(ctx, dX, n, dQ ? dQ + r0 * d : nullptr, dQ ? 0 : q_begin + r0, qc, d, k, o,
-                    stats ? &cs : nullptr, off, launches));
+                    stats ? &cs : nullptr, off, launches, &ref));
     if (nch == 0) acc = cs;
     else {
       acc.rows += cs.rows;
@@ -878,7 +949,10 @@ tod_status tod_create(const tod_config* cfg, tod_ctx** out) {
   if (ctx->cfg.stream) {
     ctx->stream = static_cast<cudaStream_t>(ctx->cfg.stream);
   } else {
-    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    // A BLOCKING stream: it waits for work the caller queued on the legacy
+    // default stream (e.g. torch kernels producing X) before each of our
+    // kernels starts, so device inputs are never read stale.
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamDefault) != cudaSuccess) {
       delete ctx;
       return TOD_E_CUDA;
     }

@@ -131,6 +131,7 @@ struct KnnOutDev {
   float* score_kth;
   float* score_mean;
   double* kdist64;
+  int32_t* tier;   // [q] diagnostics (nullable): 0 certified by pass 1, 1 second tier, 2 fp64 tiers
 };
 size_t rerank_split_ws(int64_t q);  // bytes of the split re-rank's workspace (tensor-core pass)
 int rerank_use_split(int d);        // the split re-rank is used at this width (d > 256)
@@ -145,6 +146,8 @@ size_t fallback_workspace(int nfail, int k, int64_t n, int num_sms);
 // second tier for bf16 passes (rerank.cu)
 cudaError_t launch_gather_rows(const float* src, int64_t base, const int32_t* rows, int nr, int d,
                                float* dst, cudaStream_t st, int* launches);
+cudaError_t launch_mark_rows(const int32_t* rows, int nr, int32_t value, int32_t* dst,
+                             cudaStream_t st, int* launches);
 cudaError_t launch_tier2_scatter(const int32_t* rows, int nr, int64_t q_begin, bool self_join, int k,
                                  int k2, const int64_t* idx2, const double* dd2, KnnOutDev out,
                                  cudaStream_t st, int* launches);

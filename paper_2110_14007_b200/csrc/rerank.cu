@@ -50,17 +50,21 @@ __device__ __forceinline__ double gamma_up(double m, double u) {
   return (m * u) / (1.0 - m * u) * (1.0 + 1e-10);
 }
 
-// Tensor-core accumulation model (reading A9): every tcgen05 MMA
-// K-step sums its 16 exact fp16/bf16 products in a tree of depth <= 4 and adds
-// the result to the fp32 accumulator; each of those operations may truncate
-// (<= 2^-23 relative).  With K = dpad + 16 that is m = 5 ceil(K/16) + 2 roundings:
-//   |w~ - w| <= gamma_m(2^-23) sum_k |A_ik B_jk|.
-// Measured on B200 (tools/acc_error.py, 25M entries per K): the worst error is
-// 8.7 / 13 / 56 / 114 units of 2^-24 sum|ab| at K = 48 / 80 / 528 / 1040, i.e.
-// ~6x below this model (the previous model, 2K roundings at 2^-22, was 75x).
+// Tensor-core accumulation model (reading A9), valid for ANY internal
+// order and width >= 24 bits: each tcgen05 K-step adds 17 addends (its 16 exact
+// fp16/bf16 products and the fp32 accumulator).  Worst case, the hardware aligns
+// all of them to the largest exponent and truncates each to 24 bits (error
+// < 2^-23 |max| for each of the 16 non-maximal addends), then truncates the
+// exact aligned sum S to fp32 (< 2^-23 |S|): per step < 17 * 2^-23 * sum|addends|.
+// |acc| <= sum of the earlier |A B| (times 1 + tiny), so with T = ceil(K/16)
+// steps, K = dpad + 16:
+//   |w~ - w| <= 17 T 2^-23 (1 + 1e-3) sum_k |A_ik B_jk|.
+// (Round 1 used a per-operation model, 5T + 2 roundings, which alignment
+// truncation can exceed: ADVICE r01.)  Measured on B200 on the library's own
+// kernels (tools/cert_check.py): see DESIGN.md A9.
 __device__ __forceinline__ double acc_gamma(int dpad) {
-  const double m = 5.0 * ((dpad + 16 + 15) / 16) + 2.0;
-  return gamma_up(m, 1.1920928955078125e-07 /*2^-23*/);
+  const double T = (double)((dpad + 16 + 15) / 16);
+  return 17.0 * T * 1.1920928955078125e-07 /*2^-23*/ * (1.0 + 1e-3);
 }
 
 // Writes the k outputs of one row from ascending (key, id) arrays (fp64
@@ -107,7 +111,7 @@ __device__ double lb2_from_key(const CertParams& cp, int64_t r, double w, double
     //   |w~_ij - w_ij| <= gamma_m(u) sum_k |A_ik B_jk| + rep_j
     //                  <= gamma (2 a_i a_max + 1.002 amax2) + repmax  =: E_i
     // (Cauchy-Schwarz on the dot part; sum_q |c_q p_jq| <= 1.002 ||xhat_j||^2).
-    // A9: accumulation model acc_gamma (5 ceil(K/16) + 2 roundings at 2^-23).
+    // A9: accumulation model acc_gamma (17 ceil(K/16) units of 2^-23: alignment truncation).
     // w~_ij >= w gives ||xhat_i - xhat_j||^2 >= a_i^2 + w - E_i; the residuals
     // e_i, e_j <= emax then bound the exact distance (triangle inequality).
     const double a2i = cp.qa2[r];
@@ -1101,6 +1105,12 @@ __global__ void k_gather_rows(const float* __restrict__ src, int64_t base,
   dst[i] = src[(base + rows[r]) * d + c];
 }
 
+__global__ void k_mark_rows(const int32_t* __restrict__ rows, int nr, int32_t value,
+                            int32_t* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nr) dst[rows[i]] = value;
+}
+
 __global__ void k_tier2_scatter(const int32_t* __restrict__ rows, int nr, int64_t q_begin,
                                 int self_join, int k, int k2, const int64_t* __restrict__ idx2,
                                 const double* __restrict__ dd2, KnnOutDev out) {
@@ -1947,6 +1957,14 @@ cudaError_t launch_gather_rows(const float* src, int64_t base, const int32_t* ro
   if (nr <= 0) return cudaSuccess;
   const int64_t tot = (int64_t)nr * d;
   k_gather_rows<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(src, base, rows, nr, d, dst);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mark_rows(const int32_t* rows, int nr, int32_t value, int32_t* dst,
+                             cudaStream_t st, int* launches) {
+  if (nr <= 0) return cudaSuccess;
+  k_mark_rows<<<(nr + 255) / 256, 256, 0, st>>>(rows, nr, value, dst);
   *launches += 1;
   return cudaGetLastError();
 }

@@ -64,13 +64,13 @@ class Stats(ctypes.Structure):
 class KnnOut(ctypes.Structure):
     _fields_ = [("idx", ctypes.c_void_p), ("dist", ctypes.c_void_p), ("dist64", ctypes.c_void_p),
                 ("score_kth", ctypes.c_void_p), ("score_mean", ctypes.c_void_p),
-                ("kdist64", ctypes.c_void_p)]
+                ("kdist64", ctypes.c_void_p), ("row_tier", ctypes.c_void_p)]
 
 
 _lib = None
 
 
-ABI_VERSION = 2  # include/tod.h TOD_ABI_VERSION
+ABI_VERSION = 3  # include/tod.h TOD_ABI_VERSION
 
 
 def load_library(path: str = LIB_PATH):
@@ -168,6 +168,7 @@ class KnnResult:
     score_mean: object
     kdist64: object
     stats: dict
+    row_tier: object = None
 
 
 class Context:
@@ -176,6 +177,17 @@ class Context:
     def __init__(self, device: int = 0, fmt: str = "auto", kprime: int = 0, chunks: int = 0,
                  flags: int = 0, stream=None, split: int = 0, workspace_bytes: int = 0):
         self.lib = load_library()
+        if stream is None:
+            # default to torch's current stream on this device, so kernels queued
+            # there (producing X) are ordered before the library's; stream 0 (the
+            # legacy default) maps to the library's own stream, which is blocking
+            # with respect to it (include/tod.h tod_config.stream)
+            try:
+                import torch
+                if torch.cuda.is_available():
+                    stream = torch.cuda.current_stream(device).cuda_stream or None
+            except Exception:
+                stream = None
         cfg = Config(device=device, format=FORMATS[fmt], kprime=kprime, flags=flags,
                      stream=stream, chunks=chunks, epilogue_split=split,
                      workspace_bytes=workspace_bytes)
@@ -216,6 +228,7 @@ class Context:
         o["score_kth"] = _empty_like_host_or_dev(ref, (q,), np.float32) if "score_kth" in want else None
         o["score_mean"] = _empty_like_host_or_dev(ref, (q,), np.float32) if "score_mean" in want else None
         o["kdist64"] = _empty_like_host_or_dev(ref, (q,), np.float64) if "kdist64" in want else None
+        o["row_tier"] = _empty_like_host_or_dev(ref, (q,), np.int32) if "row_tier" in want else None
         ko = KnnOut(*[_ptr(o[f]) for f, _ in KnnOut._fields_])
         return o, ko
 
@@ -276,7 +289,8 @@ class Context:
         return counts, row_ptr, cols, s.as_dict()
 
     def abod(self, X, k: int, q_begin: int = 0, q_count=None, want_knn=()):
-        """tod_abod: -variance of neighbour-pair cosines per row; (score fp32[q], KnnResult|None, stats)."""
+        """tod_abod: -Var over neighbour pairs of <a,b>/(|a|^2 |b|^2) (a, b = neighbour - row;
+        Kriegel's weighted angle factor, reading A20); (score fp32[q], KnnResult|None, stats)."""
         X = _as_f32_2d(X)
         n, d = X.shape
         if q_count is None:

@@ -40,7 +40,8 @@ def test_library_exports_every_header_symbol(lib):
 def test_status_strings_and_version(lib):
     for code in (0, -1, -2, -3, -4, -5, -7, -8):
         assert lib.tod_status_str(code).startswith(b"TOD_")
-    assert lib.tod_abi_version() == 2
+    import paper_2110_14007_b200.tod as t
+    assert lib.tod_abi_version() == t.ABI_VERSION
     assert b"sm_100a" in lib.tod_build_info()
 
 
