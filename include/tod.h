@@ -59,6 +59,7 @@ typedef enum {
   TOD_E_RANGE = -3,        /* k < 1, k > n-1 (k > n for queries), n > 2^31-1, d < 1 or d > 4096, q range outside [0,n) */
   TOD_E_NOMEM = -4,        /* workspace allocation failed */
   TOD_E_CUDA = -5,         /* a CUDA runtime error (message has cudaGetErrorString) */
+  TOD_E_NCCL = -6,         /* an NCCL error in the sharded path, or libnccl.so.2 not loadable */
   TOD_E_UNSUPPORTED = -7,  /* valid request this build cannot serve (message says why) */
   TOD_E_INTERNAL = -8      /* invariant violated inside the library (a bug) */
 } tod_status;
@@ -270,6 +271,80 @@ tod_status tod_knn_classify(tod_ctx* ctx, const float* Q, int64_t nq, const floa
 
 tod_status tod_knn_query(tod_ctx* ctx, const float* Q, int64_t nq, const float* X, int64_t n,
                          int32_t d, int32_t k, const tod_knn_out* out, tod_stats* stats);
+
+/* ===================================================================== *
+ * Sharded multi-GPU path (§6.2: one process per GPU,    *
+ * "subtasks are split equally").     *
+ * ===================================================================== *
+ * Rank r of W holds only its row block X_r = rows [row_offset, row_offset +
+ * n_local) of X.  It answers the kNN of its own rows while the quantized
+ * reference blocks circulate over an NCCL ring (double-buffered, overlapped with
+ * the tensor-core pass); the fp32 rows the exact re-rank needs are all-gathered
+ * once.  Outputs are bit-identical to tod_knn / tod_lof for every W.
+ *
+ * Communicator: the library creates its own NCCL communicator (libnccl.so.2 is
+ * loaded at run time; when torch is loaded it is torch's copy) from an id that
+ * rank 0 creates with tod_comm_id_create and the job broadcasts (e.g. with
+ * torch.distributed).  Every rank then calls tod_comm_init on its context.  A
+ * context without a communicator runs the sharded calls as a world of 1.
+ * tod_comm_init_loopback (testing) makes the context run `world` VIRTUAL ranks
+ * in this one process on its one GPU: the same schedule, every collective and
+ * ring transfer replaced by device-to-device copies; the sharded calls then take
+ * all rows (row_offset 0, n_local n) and write every rank's outputs.
+ *
+ * Shards must tile [0, n) in rank order with row_offset % 256 == 0; use
+ * tod_shard_rows for the balanced split.  Every rank must make the same
+ * sequence of sharded calls with the same (n, d, k).
+ */
+
+/* Opaque 128-byte communicator id (an ncclUniqueId). */
+typedef struct {
+  char bytes[128];
+} tod_comm_id;
+
+/* Rank 0: a fresh id (TOD_E_NCCL if libnccl.so.2 cannot be loaded). */
+tod_status tod_comm_id_create(tod_comm_id* id);
+
+/* Attach an NCCL communicator of `world` ranks to ctx (collective: every rank
+ * calls it with the same id).  ctx's device must be this rank's GPU. */
+tod_status tod_comm_init(tod_ctx* ctx, const tod_comm_id* id, int32_t rank, int32_t world);
+
+/* Testing: `world` virtual ranks in this process (see above). */
+tod_status tod_comm_init_loopback(tod_ctx* ctx, int32_t world);
+
+/* Balanced split of n rows over `world` ranks on 256-row boundaries (host-only). */
+tod_status tod_shard_rows(int64_t n, int32_t world, int32_t rank, int64_t* row_offset,
+                          int64_t* n_local);
+
+/*
+ * tod_knn_sharded — tod_knn for this rank's rows of a sharded X.
+ *   X_local          fp32 [n_local x d], rows [row_offset, row_offset + n_local) of X.
+ *   n                global row count; 1 <= k <= n-1.
+ *   out              this rank's rows (n_local), as tod_knn_out (nullable fields).
+ *   score_kth_all, score_mean_all   [n] fp32 scores of ALL rows, gathered (nullable).
+ * Errors: as tod_knn; TOD_E_ARG if the shards do not tile [0, n); TOD_E_NCCL.
+ */
+tod_status tod_knn_sharded(tod_ctx* ctx, const float* X_local, int64_t n_local, int64_t row_offset,
+                           int64_t n, int32_t d, int32_t k, const tod_knn_out* out,
+                           float* score_kth_all, float* score_mean_all, tod_stats* stats);
+
+/*
+ * tod_lof_sharded — tod_lof over a sharded X: kNN of own rows (ring), k-distances
+ * all-gathered, lrd of own rows, lrd all-gathered, LOF of own rows, then LOF and
+ * lrd of ALL rows gathered into lof_all / lrd_all ([n] fp32, nullable).
+ *   out      this rank's kNN outputs (nullable).
+ */
+tod_status tod_lof_sharded(tod_ctx* ctx, const float* X_local, int64_t n_local, int64_t row_offset,
+                           int64_t n, int32_t d, int32_t k, float* lof_all, float* lrd_all,
+                           const tod_knn_out* out, tod_stats* stats);
+
+/*
+ * tod_workspace_size — estimated device bytes one tod_knn call over q_count
+ * query rows of an n x d dataset allocates (reference image, per-row candidate
+ * state, re-rank and fallback bookkeeping; excluding X and caller outputs), for
+ * choosing cfg->workspace_bytes.  0 if the request is invalid.  Host-only.
+ */
+size_t tod_workspace_size(int64_t n, int32_t d, int32_t k, int64_t q_count, const tod_config* cfg);
 
 #ifdef __cplusplus
 }

@@ -6,9 +6,11 @@ processes (dist.py).  It never imports the CPU oracle (oracle/), and it has no
 CPU fallback.
 """
 from .tod import (Context, KnnResult, TodError, load_library, header_symbols, LIB_PATH,  # noqa: F401
-                  F_NO_CERTIFY, F_TIMING, F_PASS1_V1, F_MAIN_1SM, FORMATS)
+                  F_NO_CERTIFY, F_TIMING, F_PASS1_V1, F_MAIN_1SM, FORMATS, MAX_K,
+                  comm_id_create, shard_rows, workspace_size)
 
 from . import detectors  # noqa: F401,E402  (PyOD-style fit/decision_scores_/labels_)
 
 __all__ = ["detectors", "Context", "KnnResult", "TodError", "load_library", "header_symbols", "LIB_PATH",
-           "F_NO_CERTIFY", "F_TIMING", "F_PASS1_V1", "F_MAIN_1SM", "FORMATS"]
+           "F_NO_CERTIFY", "F_TIMING", "F_PASS1_V1", "F_MAIN_1SM", "FORMATS", "MAX_K",
+           "comm_id_create", "shard_rows", "workspace_size"]

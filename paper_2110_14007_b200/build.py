@@ -63,7 +63,7 @@ def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> 
     objs = [os.path.join(BUILD, os.path.basename(s) + ".o") for s in srcs]
     if jobs or not os.path.exists(OUT) or os.path.getmtime(OUT) < max(os.path.getmtime(o) for o in objs):
         tmp = OUT + ".tmp%d" % os.getpid()
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

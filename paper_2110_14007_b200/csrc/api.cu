@@ -16,6 +16,7 @@
 #include <string>
 
 #include "../../include/tod.h"
+#include "ctx.h"
 #include "internal.h"
 
 #ifndef TOD_BUILD_INFO
@@ -23,46 +24,10 @@
 #endif
 
 using namespace tod;
+using namespace todapi;
 
-namespace {
 
-struct Buf {
-  void* p = nullptr;
-  size_t bytes = 0;
-};
-
-struct Workspace {
-  Buf bufs[64];
-  void release() {
-    for (auto& b : bufs) {
-      if (b.p) cudaFree(b.p);
-      b = Buf{};
-    }
-  }
-};
-
-enum BufId {
-  B_X = 0, B_Q, B_IMG_B, B_A2_B, B_E_B, B_IMG_A, B_A2_A, B_E_A, B_MU, B_PART,
-  B_G, B_CIDX, B_CV, B_FAIL, B_SMALL, B_IDX, B_DIST, B_DIST64, B_KTH, B_MEAN, B_KD64,
-  B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT, B_FAILUB, B_NWRTAU, B_NWRCNT, B_NWRPTR, B_NWRCOLS, B_SCAN, B_ABOD, B_LABELS, B_PRED, B_SAMP, B_NWRBLK, B_NWRTASK, B_RRWS, B_T2ROWS, B_T2Q, B_T2IDX, B_T2D64, B_TIER, B_NBUF
-};
-static_assert(B_NBUF <= 64, "Workspace::bufs too small");
-
-}  // namespace
-
-struct tod_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-  tod_config cfg{};
-  int num_sms = 148;
-  std::string msg;
-  Workspace ws;
-  cudaEvent_t ev[8] = {};
-  cudaEvent_t evk[2] = {};  // around the main-pass kernel (two-pass mode)
-};
-
-namespace {
+namespace todapi {
 
 tod_status fail(tod_ctx* ctx, tod_status s, const char* fmt, ...) {
   if (ctx) {
@@ -76,16 +41,9 @@ tod_status fail(tod_ctx* ctx, tod_status s, const char* fmt, ...) {
   return s;
 }
 
-#define TOD_CUDA(call)                                                                    \
-  do {                                                                                    \
-    cudaError_t e_ = (call);                                                              \
-    if (e_ != cudaSuccess)                                                                \
-      return fail(ctx, e_ == cudaErrorMemoryAllocation ? TOD_E_NOMEM : TOD_E_CUDA,       \
-                  "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
-  } while (0)
 
-tod_status ensure(tod_ctx* ctx, int id, size_t bytes, void** out) {
-  Buf& b = ctx->ws.bufs[id];
+tod_status ensure_ws(tod_ctx* ctx, Workspace& ws, int id, size_t bytes, void** out) {
+  Buf& b = ws.bufs[id];
   if (bytes == 0) bytes = 16;
   if (b.bytes < bytes) {
     if (b.p) cudaFree(b.p);
@@ -101,11 +59,6 @@ tod_status ensure(tod_ctx* ctx, int id, size_t bytes, void** out) {
   return TOD_OK;
 }
 
-#define TOD_TRY(expr)                  \
-  do {                                 \
-    tod_status s_ = (expr);            \
-    if (s_ != TOD_OK) return s_;       \
-  } while (0)
 
 // Is p device memory of this context's device?  Host (pageable/pinned) -> false.
 bool is_device_ptr(const void* p, int device) {
@@ -118,22 +71,6 @@ bool is_device_ptr(const void* p, int device) {
   }
   return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) && a.device == device;
 }
-
-int roundup(int x, int m) { return (x + m - 1) / m * m; }
-
-struct Plan {
-  int fmt;       // 1 fp16, 2 bf16, 3 fp32 simt
-  int kind;      // PASS_TC / PASS_SIMT
-  int dpad;
-  int kp;
-  int S;
-  int lists;     // candidate lists per row (TC: epilogue split; SIMT: S)
-  int two;       // TC: two-pass candidate selection (sample pass + append-only main pass)
-  int R;         // two-pass: sample stride over 256-column reference tiles
-  int main_S;    // two-pass: main-pass reference chunks
-  int kp_target; // two-pass: K' (target count of kept groups)
-  int cap;       // two-pass: main-pass buffer slots per (row, column half)
-};
 
 tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k, Plan* p) {
   int fmt = ctx->cfg.format;
@@ -267,37 +204,8 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
   return TOD_OK;
 }
 
-struct Timer {
-  tod_ctx* ctx;
-  bool on;
-  int n = 0;
-  void mark() {
-    if (on && n < 8) cudaEventRecord(ctx->ev[n++], ctx->stream);
-  }
-  float between(int a, int b) {
-    if (!on || b >= n) return 0.f;
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, ctx->ev[a], ctx->ev[b]);
-    return ms;
-  }
-};
 
-struct SmallDev {
-  PrepGlobals g;
-  int32_t fail_count;
-  int32_t pad;
-  double max_err;
-  unsigned long long counters[3];  // re-rank telemetry: staged groups, visited groups, kept columns
-};
 
-// Reference-side prep shared by the query chunks of one call (automatic
-// batching): computed by the first chunk, reused by the others.  A bf16 second
-// tier overwrites the reference image and the globals, so it clears `ready`.
-struct RefPrep {
-  bool ready = false;
-  const float* dQall = nullptr;  // query mode: every query row of the call (finite / absmax)
-  int64_t nq_all = 0;
-};
 
 // Input quantization (a1) for the tensor-core passes: column mean, power-of-two
 // scale, reference image B over all n rows (skipped when ref->ready) and query
@@ -367,7 +275,6 @@ tod_status prep_tc(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
 tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, int64_t q_begin,
                    int64_t q_count, int d, int k, KnnOutDev out, tod_stats* stats, Timer& tm,
                    int* launches, RefPrep* ref) {
-  int32_t* row_tier = out.tier;
   const bool self = dQ == nullptr;
   bool main_timed = false;
   int main_kernel = 0;
@@ -415,11 +322,6 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     cands.st_done = static_cast<int*>(p);
     TOD_CUDA(cudaMemsetAsync(cands.st_done, 0, (size_t)nqt * 4, st));
   }
-  TOD_TRY(ensure(ctx, B_FAIL, (size_t)std::max<int64_t>(q_count, 1) * 4, &p));
-  int32_t* fail_rows = static_cast<int32_t*>(p);
-  TOD_TRY(ensure(ctx, B_FAILUB, (size_t)std::max<int64_t>(q_count, 1) * 8, &p));
-  double* fail_ub = static_cast<double*>(p);
-
   CertParams cp{};
   cp.kind = plan.kind;
   cp.d = d;
@@ -524,12 +426,33 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     }
     return TOD_OK;
   }
+  PassInfo pi;
+  pi.main_kernel = main_kernel;
+  pi.sample_pass = sample_pass;
+  pi.main_timed = main_timed;
+  return finish_rows(ctx, dX, n, dQ, q_begin, q_count, d, k, plan, cands, plan.two ? &mp : nullptr,
+                     cp, small, out, stats, tm, launches, ref, pi);
+}
+
+tod_status finish_rows(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, int64_t q_begin,
+                       int64_t q_count, int d, int k, const Plan& plan, Cands cands,
+                       const MainPass* mp, CertParams cp, SmallDev* small, KnnOutDev out,
+                       tod_stats* stats, Timer& tm, int* launches, RefPrep* ref,
+                       const PassInfo& pi) {
+  const bool self = dQ == nullptr;
+  cudaStream_t st = ctx->stream;
+  int32_t* row_tier = out.tier;
+  void* p;
+  TOD_TRY(ensure(ctx, B_FAIL, (size_t)std::max<int64_t>(q_count, 1) * 4, &p));
+  int32_t* fail_rows = static_cast<int32_t*>(p);
+  TOD_TRY(ensure(ctx, B_FAILUB, (size_t)std::max<int64_t>(q_count, 1) * 8, &p));
+  double* fail_ub = static_cast<double*>(p);
   void* rr_ws = nullptr;
   if (plan.kind == PASS_TC && rerank_use_split(d)) {
     TOD_TRY(ensure(ctx, B_RRWS, rerank_split_ws(q_count), &p));
     rr_ws = p;
   }
-  TOD_CUDA(launch_rerank(dQ, q_begin, q_count, dX, n, d, k, self, cands, plan.two ? &mp : nullptr,
+  TOD_CUDA(launch_rerank(dQ, q_begin, q_count, dX, n, d, k, self, cands, mp,
                          cp, out, fail_rows, fail_ub,
                          &small->fail_count, &small->max_err, small->counters, rr_ws, st, launches));
   tm.mark();  // 4: fallback start
@@ -615,10 +538,10 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     stats->dpad = plan.dpad;
     stats->scale = plan.kind == PASS_TC ? h.g.s : 1.0;
     stats->max_abs_err = h.max_err;
-    stats->main_kernel = main_kernel;
-    stats->sample_pass = sample_pass;
+    stats->main_kernel = pi.main_kernel;
+    stats->sample_pass = pi.sample_pass;
     stats->ms_main_kernel = 0.f;
-    if (main_timed) cudaEventElapsedTime(&stats->ms_main_kernel, ctx->evk[0], ctx->evk[1]);
+    if (pi.main_timed) cudaEventElapsedTime(&stats->ms_main_kernel, ctx->evk[0], ctx->evk[1]);
     stats->cand_groups = (int64_t)h.counters[0];
     stats->visited_groups = (int64_t)h.counters[1];
     stats->cand_columns = (int64_t)h.counters[2];
@@ -729,24 +652,6 @@ tod_status run_nwr(tod_ctx* ctx, const float* dX, int64_t n, int d, double phi, 
   return TOD_OK;
 }
 
-// Resolve a caller buffer: device pointer as is, host pointer -> staging buffer.
-template <class T>
-tod_status dev_view(tod_ctx* ctx, T* user, size_t count, int id, T** dev, bool* staged) {
-  *staged = false;
-  if (!user) {
-    *dev = nullptr;
-    return TOD_OK;
-  }
-  if (is_device_ptr(user, ctx->device)) {
-    *dev = user;
-    return TOD_OK;
-  }
-  void* p;
-  TOD_TRY(ensure(ctx, id, count * sizeof(T), &p));
-  *dev = static_cast<T*>(p);
-  *staged = true;
-  return TOD_OK;
-}
 
 tod_status validate_common(tod_ctx* ctx, int64_t n, int32_t d, int32_t k) {
   if (!ctx) return TOD_E_ARG;
@@ -758,11 +663,6 @@ tod_status validate_common(tod_ctx* ctx, int64_t n, int32_t d, int32_t k) {
   return TOD_OK;
 }
 
-struct OutStage {
-  KnnOutDev dev{};
-  bool st_idx = false, st_dist = false, st_d64 = false, st_kth = false, st_mean = false,
-       st_kd = false, st_tier = false;
-};
 
 tod_status stage_outputs(tod_ctx* ctx, const tod_knn_out* o, int64_t q, int k, OutStage* s) {
   tod_knn_out z{};
@@ -898,7 +798,7 @@ void finish_stats(tod_stats* stats, Timer& tm, int launches, int i_lof_end) {
     stats->ms_prep = stats->ms_main = stats->ms_certify = stats->ms_fallback = stats->ms_main_kernel = 0.f;
 }
 
-}  // namespace
+}  // namespace todapi
 
 extern "C" {
 
@@ -913,6 +813,7 @@ const char* tod_status_str(tod_status s) {
     case TOD_E_RANGE: return "TOD_E_RANGE: size or k out of range";
     case TOD_E_NOMEM: return "TOD_E_NOMEM: device allocation failed";
     case TOD_E_CUDA: return "TOD_E_CUDA: CUDA runtime error";
+    case TOD_E_NCCL: return "TOD_E_NCCL: NCCL error";
     case TOD_E_UNSUPPORTED: return "TOD_E_UNSUPPORTED: not supported by this build";
     case TOD_E_INTERNAL: return "TOD_E_INTERNAL: internal error";
   }
@@ -974,6 +875,9 @@ tod_status tod_destroy(tod_ctx* ctx) {
   for (auto ev : ctx->evk)
     if (ev) cudaEventDestroy(ev);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  for (auto& w : ctx->rank_ws) w.release();
+  if (ctx->nccl_comm) tod_comm_release(ctx);
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   delete ctx;
   return TOD_OK;
 }

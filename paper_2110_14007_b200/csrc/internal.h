@@ -67,6 +67,11 @@ cudaError_t launch_prep_scale(PrepGlobals* g, int fmt, int dpad, cudaStream_t st
 // side 1 = query image A (-2 xhat | constants).
 cudaError_t launch_prep_quant(const float* X, int64_t n, int d, const double* mu, PrepGlobals* g,
                               int fmt, Image img, int side, cudaStream_t st, int* launches);
+cudaError_t launch_prep_colsum(const float* X, int64_t n, int d, double* partial, PrepGlobals* g,
+                               cudaStream_t st, int* launches);
+cudaError_t launch_prep_colmean(const double* partial, int blocks, int64_t n, int d, double* mu,
+                                cudaStream_t st, int* launches);
+int prep_stat_rows();  // rows per column-sum partial block (128)
 cudaError_t launch_finite_check(const float* X, int64_t n, int d, PrepGlobals* g, cudaStream_t st,
                                 int* launches);
 
@@ -94,6 +99,8 @@ struct MainPass {
   float* samp = nullptr;      // sample mode (knn_tc3 only): [q_count][parts][samp_t] smallest
                               // group minima over the sample tiles t = 0, R, 2R, ... (no appends)
   int samp_t = 4;             // 4 or 8
+  int samp_acc = 0;           // sample mode: merge into the minima already in samp (ring of blocks)
+  int64_t col0 = 0;           // global index of reference row 0 of the image (a ring block; % 256 == 0)
 };
 cudaError_t launch_tau_combine(int64_t q, int nv, int j, const float* samp, float* tau,
                                cudaStream_t st, int* launches);

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
               int self_join, int S, int R, int nstage,
               const float* __restrict__ tau_v, int tau_lists,
               uint2* __restrict__ mbuf, int* __restrict__ mcnt, int cap,
-              float* __restrict__ samp) {
+              float* __restrict__ samp, int64_t col0, int samp_acc) {
   using C = Cfg3<DPAD>;
   constexpr int SMP = MODE >= 4 ? MODE : 0;
   constexpr int SKIP = MODE == 1 ? 1 : 0;
@@ -387,9 +387,13 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
       const int64_t r = valid ? row - q_begin : 0;
       const int self = self_join ? (int)row : -1;
       // tiles that may need masking: the one holding this query tile's own
-      // columns (self-join) and the last (padded) one
-      const int t_self = self_join ? (int)(((qt0 + qtl) * kBM) / kBN) : -1;
+      // columns (self-join; the reference rows are the block [col0, col0 + n_ref)
+      // of the global index space) and the last (padded) one
+      const int64_t qrow0 = (qt0 + qtl) * kBM;
+      const int t_self = (self_join && qrow0 >= col0 && qrow0 < col0 + n_ref)
+                             ? (int)((qrow0 - col0) / kBN) : -1;
       const int t_last = (int)((n_ref - 1) / kBN);
+      const int scol0 = (int)col0;
       float tau = -CUDART_INF_F;  // rows outside the range append nothing
       if (valid) {
         tau = CUDART_INF_F;
@@ -413,7 +417,8 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
       constexpr int T = SMP > 0 ? SMP : 1;  // sample pass: T smallest minima per (row, part)
       float top[T];
 #pragma unroll
-      for (int i = 0; i < T; ++i) top[i] = CUDART_INF_F;
+      for (int i = 0; i < T; ++i)  // a ring of blocks accumulates over launches
+        top[i] = (SMP && samp_acc && valid) ? samp[(r * H + h) * T + i] : CUDART_INF_F;
       Seq<SMP, SKIP> ts;
       ts.begin(b_tiles, S, R, c);
       for (; ts.more(); ts.next()) {
@@ -440,7 +445,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
         if (t == t_self || t == t_last) {
 #pragma unroll
           for (int e = 0; e < BH; ++e)
-            v[e] = (j0 + e == self || j0 + e >= n_ref) ? CUDART_INF_F : v[e];
+            v[e] = (scol0 + j0 + e == self || j0 + e >= n_ref) ? CUDART_INF_F : v[e];
         }
         // independent min trees first (full ILP), then the appends
         float m[BH / 8];
@@ -458,7 +463,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
           }
           continue;
         }
-        const int gbase = j0 >> 3;
+        const int gbase = (scol0 + j0) >> 3;  // global group index (col0 % 256 == 0)
 #pragma unroll
         for (int hh = 0; hh < BH / 64; ++hh) {
           if (__any_sync(0xffffffffu, pa > pbase + (kPend - 8) * SLOT)) flush();
@@ -510,7 +515,7 @@ cudaError_t launch3(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
       reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(), A.extra_offset(),
       reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
       B.n_pad / kBN, B.n, qt0, qt1 - qt0, q_begin, q_begin + q_count, self_join ? 1 : 0, m.S,
-      m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap, m.samp);
+      m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap, m.samp, m.col0, m.samp_acc);
   return cudaGetLastError();
 }
 

@@ -112,7 +112,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
               int64_t n_ref, int64_t qt0, int64_t n_qpairs, int64_t q_begin, int64_t q_end,
               int self_join, int S, int R, int nstage,
               const float* __restrict__ tau_v, int tau_lists,
-              uint2* __restrict__ mbuf, int* __restrict__ mcnt, int cap) {
+              uint2* __restrict__ mbuf, int* __restrict__ mcnt, int cap, int64_t col0) {
   using C = Cfg4<DPAD>;
   constexpr int H = FW / 4;
   constexpr int BH = kBN / H;
@@ -315,8 +315,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
       const bool valid = row >= q_begin && row < q_end;
       const int64_t r = valid ? row - q_begin : 0;
       const int self = self_join ? (int)row : -1;
-      const int t_self = self_join ? (int)(((qt0 + qtl) * kBM) / kBN) : -1;
+      // reference rows = the block [col0, col0 + n_ref) of the global index space
+      const int64_t qrow0 = (qt0 + qtl) * kBM;
+      const int t_self = (self_join && qrow0 >= col0 && qrow0 < col0 + n_ref)
+                             ? (int)((qrow0 - col0) / kBN) : -1;
       const int t_last = (int)((n_ref - 1) / kBN);
+      const int scol0 = (int)col0;
       float tau = -CUDART_INF_F;
       if (valid) {
         tau = CUDART_INF_F;
@@ -363,12 +367,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
         if (t == t_self || t == t_last) {
 #pragma unroll
           for (int e = 0; e < BH; ++e)
-            v[e] = (j0 + e == self || j0 + e >= n_ref) ? CUDART_INF_F : v[e];
+            v[e] = (scol0 + j0 + e == self || j0 + e >= n_ref) ? CUDART_INF_F : v[e];
         }
         float m[BH / 8];
 #pragma unroll
         for (int g = 0; g < BH / 8; ++g) m[g] = min8(v + 8 * g);
-        const int gbase = j0 >> 3;
+        const int gbase = (scol0 + j0) >> 3;  // global group index (col0 % 256 == 0)
 #pragma unroll
         for (int hh = 0; hh < BH / 64; ++hh) {
           if (__any_sync(0xffffffffu, pa > pbase + (kPend - 8) * SLOT)) flush();
@@ -414,7 +418,7 @@ cudaError_t launch4(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
       reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(), A.extra_offset(),
       reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
       B.n_pad / kBN, B.n, qt0, n_qpairs, q_begin, q_begin + q_count, self_join ? 1 : 0, m.S,
-      m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap);
+      m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap, m.col0);
   return cudaGetLastError();
 }
 

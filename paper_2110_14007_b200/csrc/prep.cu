@@ -283,6 +283,28 @@ cudaError_t launch_prep_stats(const float* X, int64_t n, int d, double* mu, doub
   return cudaGetLastError();
 }
 
+// The two halves of launch_prep_stats, for the sharded path: each rank writes
+// the partials of its own 128-row blocks (row_offset % 128 == 0, so its local
+// block b is global block row_offset/128 + b); the partials of all ranks,
+// gathered in global block order, then give the same mean as one process.
+cudaError_t launch_prep_colsum(const float* X, int64_t n, int d, double* partial, PrepGlobals* g,
+                               cudaStream_t st, int* launches) {
+  const int blocks = (int)((n + kRowsPerStatBlock - 1) / kRowsPerStatBlock);
+  if (blocks <= 0) return cudaSuccess;
+  k_colsum_partial<<<blocks, kStatThreads, 0, st>>>(X, n, d, partial, g);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prep_colmean(const double* partial, int blocks, int64_t n, int d, double* mu,
+                                cudaStream_t st, int* launches) {
+  k_colmean<<<d, 256, 0, st>>>(partial, blocks, n, d, mu);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+int prep_stat_rows() { return kRowsPerStatBlock; }
+
 cudaError_t launch_finite_check(const float* X, int64_t n, int d, PrepGlobals* g, cudaStream_t st,
                                 int* launches) {
   const int64_t total = n * (int64_t)d;

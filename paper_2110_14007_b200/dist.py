@@ -2,11 +2,18 @@
 "subtasks are split equally", one subprocess per GPU; here torch.distributed
 with NCCL between B200s, gloo in CPU tests).
 
-Partitioning: rank r answers the query rows
-[begin_r, begin_r + count_r) against the full reference set X, which every
-rank holds (the BASELINE configs need <= 4.1 GB of fp32 X per GPU out of 180 GB),
-so the distance pass needs no data-path collective.  The only exchanges are the
-real ones of the method:
+Two forms:
+
+* The RING (north_star): each rank holds only its row
+  block X_r; ``init_comm`` attaches the library's own NCCL communicator (id
+  broadcast through the torch process group), and ``knn_ring`` / ``lof_ring``
+  call tod_knn_sharded / tod_lof_sharded, where the quantized reference blocks
+  circulate over NCCL send/recv with a running candidate state and the scores
+  are all-gathered -- all inside libtod.so.
+
+* The REPLICATED form below (``knn_scores`` / ``lof_scores``): every rank holds
+  all of X and answers its query rows [begin_r, begin_r + count_r); the only
+  exchanges are the real ones of the method:
   * kNN scores / neighbour tables -> all_gather (output assembly);
   * LOF: all_gather of the k-distances before the lrd stage, and of lrd before
     the final ratio (reach-dist and LOF of a row read its neighbours' values,
@@ -23,7 +30,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-ROW_ALIGN = 128  # tensor-core query tile: shard edges on tile boundaries
+ROW_ALIGN = 256  # reference tile: shard edges on tile boundaries (= tod_shard_rows)
 
 
 def shard_rows(n: int, world: int, rank: int, align: int = ROW_ALIGN):
@@ -102,3 +109,34 @@ def lof_scores(X, k: int, stages, group=None):
     if world == 1:
         return lof_loc, lrd32_loc
     return _gather_rows(lof_loc, n, world, group), _gather_rows(lrd32_loc, n, world, group)
+
+
+# ------------------------------------------------------------------ the ring
+def init_comm(ctx, group=None):
+    """Attach an NCCL communicator over the process group's ranks to ``ctx``
+    (tod_comm_init): rank 0 creates the id, the group broadcasts it."""
+    from . import tod
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    obj = [tod.comm_id_create() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    ctx.comm_init(rank, world, obj[0])
+    return rank, world
+
+
+def local_block(X, world: int, rank: int):
+    """(X_local, row_offset) of this rank's 256-row-aligned block of X."""
+    b, c = shard_rows(X.shape[0], world, rank)
+    return X[b:b + c], b
+
+
+def knn_ring(ctx, X_local, n: int, row_offset: int, k: int, want=("idx", "dist64")):
+    """Sharded kNN through the library's NCCL ring: (local KnnResult,
+    score_kth[n], score_mean[n]) with the scores of all rows."""
+    return ctx.knn_sharded(X_local, n, row_offset, k, want=want, gather_scores=True)
+
+
+def lof_ring(ctx, X_local, n: int, row_offset: int, k: int):
+    """Sharded LOF through the library's NCCL ring: (lof[n], lrd[n], stats)."""
+    lof, lrd, _, st = ctx.lof_sharded(X_local, n, row_offset, k)
+    return lof, lrd, st

@@ -23,7 +23,9 @@ HEADER = os.path.join(os.path.dirname(_HERE), "include", "tod.h")
 
 TOD_OK = 0
 STATUS = {0: "TOD_OK", -1: "TOD_E_ARG", -2: "TOD_E_NONFINITE", -3: "TOD_E_RANGE",
-          -4: "TOD_E_NOMEM", -5: "TOD_E_CUDA", -7: "TOD_E_UNSUPPORTED", -8: "TOD_E_INTERNAL"}
+          -4: "TOD_E_NOMEM", -5: "TOD_E_CUDA", -6: "TOD_E_NCCL", -7: "TOD_E_UNSUPPORTED",
+          -8: "TOD_E_INTERNAL"}
+MAX_K = 128  # include/tod.h TOD_MAX_K
 FORMATS = {"auto": 0, "fp16": 1, "bf16": 2, "fp32": 3}
 F_NO_CERTIFY = 0x1
 F_TIMING = 0x2
@@ -103,6 +105,16 @@ def load_library(path: str = LIB_PATH):
         "tod_nwr": ([P, P, I64, I32, ctypes.c_double, I64, I64, P, P, P, I64,
                      ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(Stats)], ctypes.c_int),
         "tod_lof_finish": ([P, I64, I32, I64, I64, P, P, P, P], ctypes.c_int),
+        "tod_comm_id_create": ([P], ctypes.c_int),
+        "tod_comm_init": ([P, P, I32, I32], ctypes.c_int),
+        "tod_comm_init_loopback": ([P, I32], ctypes.c_int),
+        "tod_shard_rows": ([I64, I32, I32, ctypes.POINTER(ctypes.c_int64),
+                            ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+        "tod_knn_sharded": ([P, P, I64, I64, I64, I32, I32, ctypes.POINTER(KnnOut), P, P,
+                             ctypes.POINTER(Stats)], ctypes.c_int),
+        "tod_lof_sharded": ([P, P, I64, I64, I64, I32, I32, P, P, ctypes.POINTER(KnnOut),
+                             ctypes.POINTER(Stats)], ctypes.c_int),
+        "tod_workspace_size": ([I64, I32, I32, I64, ctypes.POINTER(Config)], ctypes.c_size_t),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -113,6 +125,33 @@ def load_library(path: str = LIB_PATH):
                           % (lib.tod_abi_version(), ABI_VERSION))
     _lib = lib
     return lib
+
+
+def comm_id_create() -> bytes:
+    """tod_comm_id_create: a fresh 128-byte communicator id (rank 0 of a job)."""
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    st = lib.tod_comm_id_create(buf)
+    if st != TOD_OK:
+        raise TodError(st, "tod_comm_id_create failed (libnccl.so.2 not loadable?)")
+    return buf.raw
+
+
+def shard_rows(n: int, world: int, rank: int):
+    """tod_shard_rows: the library's balanced 256-row-aligned split (row_offset, n_local)."""
+    lib = load_library()
+    b, c = ctypes.c_int64(), ctypes.c_int64()
+    st = lib.tod_shard_rows(n, world, rank, ctypes.byref(b), ctypes.byref(c))
+    if st != TOD_OK:
+        raise TodError(st, "tod_shard_rows(n=%d, world=%d, rank=%d)" % (n, world, rank))
+    return b.value, c.value
+
+
+def workspace_size(n: int, d: int, k: int, q_count: int, fmt: str = "auto", kprime: int = 0) -> int:
+    """tod_workspace_size: estimated device bytes of one tod_knn call."""
+    lib = load_library()
+    cfg = Config(device=0, format=FORMATS[fmt], kprime=kprime)
+    return int(lib.tod_workspace_size(n, d, k, q_count, ctypes.byref(cfg)))
 
 
 def header_symbols(header: str = HEADER):
@@ -329,6 +368,50 @@ class Context:
         s = Stats()
         self._check(self.lib.tod_lof(self.h, _ptr(X), n, d, k, _ptr(lof), _ptr(lrd),
                                      ctypes.byref(ko) if want_knn else None, ctypes.byref(s)))
+        res = KnnResult(**o, stats=s.as_dict()) if want_knn else None
+        return lof, lrd, res, s.as_dict()
+
+    # ---------------------------------------------------------- sharded path
+    def comm_init(self, rank: int, world: int, comm_id: bytes):
+        """tod_comm_init: attach this rank's NCCL communicator (collective)."""
+        buf = ctypes.create_string_buffer(bytes(comm_id), 128)
+        self._check(self.lib.tod_comm_init(self.h, buf, rank, world))
+        self.rank, self.world = rank, world
+
+    def comm_init_loopback(self, world: int):
+        """tod_comm_init_loopback (testing): `world` virtual ranks on this GPU."""
+        self._check(self.lib.tod_comm_init_loopback(self.h, world))
+        self.rank, self.world = 0, world
+
+    def knn_sharded(self, X_local, n: int, row_offset: int, k: int, want=("idx", "dist64"),
+                    gather_scores: bool = True):
+        """tod_knn_sharded: kNN of this rank's rows; returns (KnnResult of the local
+        rows, score_kth fp32[n] | None, score_mean fp32[n] | None) -- the scores of
+        ALL rows, gathered."""
+        X_local = _as_f32_2d(X_local)
+        nl, d = X_local.shape
+        o, ko = self._alloc_knn(X_local, nl, k, want)
+        kth = _empty_like_host_or_dev(X_local, (n,), np.float32) if gather_scores else None
+        mean = _empty_like_host_or_dev(X_local, (n,), np.float32) if gather_scores else None
+        s = Stats()
+        self._check(self.lib.tod_knn_sharded(self.h, _ptr(X_local), nl, row_offset, n, d, k,
+                                             ctypes.byref(ko), _ptr(kth), _ptr(mean),
+                                             ctypes.byref(s)))
+        return KnnResult(**o, stats=s.as_dict()), kth, mean
+
+    def lof_sharded(self, X_local, n: int, row_offset: int, k: int, want_knn=()):
+        """tod_lof_sharded: returns (lof fp32[n], lrd fp32[n], KnnResult of the local
+        rows | None, stats)."""
+        X_local = _as_f32_2d(X_local)
+        nl, d = X_local.shape
+        lof = _empty_like_host_or_dev(X_local, (n,), np.float32)
+        lrd = _empty_like_host_or_dev(X_local, (n,), np.float32)
+        o, ko = self._alloc_knn(X_local, nl, k, want_knn)
+        s = Stats()
+        self._check(self.lib.tod_lof_sharded(self.h, _ptr(X_local), nl, row_offset, n, d, k,
+                                             _ptr(lof), _ptr(lrd),
+                                             ctypes.byref(ko) if want_knn else None,
+                                             ctypes.byref(s)))
         res = KnnResult(**o, stats=s.as_dict()) if want_knn else None
         return lof, lrd, res, s.as_dict()
 

@@ -113,3 +113,31 @@ def test_shard_rows_tile_aligned_and_complete():
             assert pos == n
             counts = [c for _, c in spans]
             assert max(counts) - min(counts) <= tdist.ROW_ALIGN
+
+
+def test_library_shard_rows_matches_dist_split():
+    # tod_shard_rows is host-only: callable without a GPU
+    from paper_2110_14007_b200 import build
+    build.build()
+    import paper_2110_14007_b200 as pkg
+    for n in (1, 255, 256, 257, 20_077, 1_000_000, 10_000_000):
+        for world in (1, 2, 3, 5, 8):
+            spans = [pkg.shard_rows(n, world, r) for r in range(world)]
+            assert spans == [tdist.shard_rows(n, world, r) for r in range(world)]
+            off = 0
+            for b, c in spans:
+                assert b == off and b % 256 == 0
+                off += c
+            assert off == n
+
+
+def test_workspace_size_estimate():
+    from paper_2110_14007_b200 import build
+    build.build()
+    import paper_2110_14007_b200 as pkg
+    a = pkg.workspace_size(1_000_000, 64, 10, 1_000_000, fmt="bf16")
+    b = pkg.workspace_size(1_000_000, 64, 10, 500_000, fmt="bf16")
+    assert a > b > 0
+    # the reference image alone (n x (64+16) x 2 bytes) is a lower bound
+    assert b > 1_000_000 * 80 * 2
+    assert pkg.workspace_size(1, 64, 10, 1) == 0   # n < 2: invalid
