@@ -5,12 +5,15 @@ One STEP = one pass of the whole hot path over one
 synthetic dataset: prep/quantize -> tcgen05 fused distance + top-K' ->
 fp64 re-rank + certificate -> fallback -> kNN scores -> LOF stage.
 
-Default workload (N=1): BASELINE.json configs[1] "C2": kNN + LOF, n=100,000,
-d=32, k=20 (the configuration the metric is quoted on that fits one GPU).
-For N>1 (torchrun, one process per GPU) the same problem family is scaled
-weakly: n_N = round(100,000 * sqrt(N)) so the per-GPU pair count n_N^2/N is
-fixed; query rows are sharded, scores / k-distances / lrd are all-gathered
-over NCCL (paper_2110_14007_b200/dist.py).
+Default workload: BASELINE.json configs[2] "C3": kNN, n=1,000,000, d=64, k=10,
+bf16 provable-quantization path, quoted on 1/2/4/8 B200 (the largest BASELINE
+configuration quoted at one GPU).  It scales STRONGLY: the same n at every N,
+query rows sharded (256-row aligned), and for N > 1 the sharded library path
+(tod_knn_sharded) circulates the quantized reference blocks on an NCCL ring and
+all-gathers the scores.  `--gpus N` launches N ranks itself (torch.distributed.run)
+when not already under torchrun.  Other configs: --config c1 | c2 (kNN + LOF,
+n=100,000, d=32, k=20) | c3f16 | c4 (n=10M, d=64, k=20: each GPU answers one
+1/8 query shard, the whole job at N=8) | c5 | c5s | nwr.
 
 Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle
 (oracle/, the parity reference) on a bounded sample of the same workload.
@@ -39,6 +42,8 @@ CONFIGS = {
     "c3": (1_000_000, 64, 10, False, "bf16", "C3: kNN n=1000000 d=64 k=10 bf16 PQ path"),
     "c3f16": (1_000_000, 64, 10, False, "fp16", "C3 shape, fp16 PQ path"),
     "c5": (2_000_000, 512, 50, False, "fp16", "C5: kNN n=2000000 d=512 k=50 (tensor-bound regime)"),
+    "c4": (10_000_000, 64, 20, False, "fp16",
+           "C4: kNN n=10000000 d=64 k=20 (1/8 query shard per GPU; the whole job on 8 GPUs)"),
     "c5s": (500_000, 512, 50, False, "fp16", "C5 shape at n=500000 (1-GPU sample of C5)"),
     # NEXT-2: NWR on the C2-shaped data; phi = 12 on the squared
     # distance (86 % of rows have no neighbour, mean 39, max ~1900: the paper's
@@ -120,10 +125,7 @@ def _dist_env():
 
 
 def _workload(cfg_name, world):
-    n, d, k, lof, fmt, desc = CONFIGS[cfg_name]
-    if world > 1:
-        n = int(round(n * math.sqrt(world)))
-    return n, d, k, lof, fmt, desc
+    return CONFIGS[cfg_name]
 
 
 def run_reference(args):
@@ -159,10 +161,10 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak" if args.config == "c4" else "strong",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (Gaussian mixture + uniform outliers, seed 0)",
-        "config": {"workload": desc + (" (n scaled to %d for N=%d)" % (n, world) if world > 1 else ""),
-                   "n": n, "d": d, "k": k, "lof": lof},
+        "config": {"workload": desc, "n": n, "d": d, "k": k, "lof": lof},
         "dist_evals_per_s": qps * n,
         "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "oracle",
                          "sample": sample, "cpu": platform.processor() or platform.machine()},
@@ -274,6 +276,24 @@ def run_gpu_nwr(args):
     return 0
 
 
+def _sharding(cfg_name, n, world, rank):
+    """(q_begin, q_count, mode) of this rank's work.
+
+    Strong scaling (every config but c4): the n rows are split over the world;
+    world > 1 runs the NCCL ring (tod_knn_sharded / tod_lof_sharded).
+    c4 (BASELINE configs[3], quoted on 8 GPUs): each rank answers its 1/8 query
+    shard of the n = 10M job, so per-GPU work is fixed ("weak") and N=8 is the
+    whole job on the ring; N < 8 runs ranks 0..N-1's shards, each against the
+    full reference set resident on its GPU (the 1-GPU line measures exactly one
+    rank's share of the target)."""
+    from paper_2110_14007_b200 import dist as tdist
+    if cfg_name == "c4":
+        b, c = tdist.shard_rows(n, 8, rank)
+        return b, c, ("ring" if world == 8 else "shard8")
+    b, c = tdist.shard_rows(n, world, rank)
+    return b, c, ("ring" if world > 1 else "single")
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -287,35 +307,46 @@ def run_gpu(args):
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.cuda.current_device()
-    n, d, k, lof, fmt, desc = _workload(args.config, world)
+    n, d, k, lof, fmt, desc = CONFIGS[args.config]
     if args.fmt:
         fmt = args.fmt
+    if args.config == "c4" and world > 8:
+        raise SystemExit("c4 is defined for up to 8 GPUs")
+    qb, qc, mode = _sharding(args.config, n, world, rank)
     X = datagen.gaussian_mixture(n, d, seed=0)
-    Xd = torch.from_numpy(X).cuda()
     stream = torch.cuda.current_stream()
     ctx = tod.Context(device=dev, fmt=fmt, flags=tod.F_TIMING, stream=stream.cuda_stream)
-    stages = tdist.CudaStages(ctx)
+    if mode == "ring":
+        r_, w_ = tdist.init_comm(ctx)
+        import ctypes
+        ver = ctypes.c_int(0)
+        try:
+            ctypes.CDLL("libnccl.so.2").ncclGetVersion(ctypes.byref(ver))
+        except Exception:
+            pass
+        print("[rank %d] NCCL communicator attached: world=%d, device cuda:%d, NCCL %d" %
+              (r_, w_, dev, ver.value), file=sys.stderr, flush=True)
+        Xl = torch.from_numpy(X[qb:qb + qc]).cuda()
+        Xd = None
+    else:
+        Xd = torch.from_numpy(X).cuda()
+        Xl = None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    main_ms, kern_ms, launches, last_stats = [], [], [], {}
+    last = {}
 
     def step():
-        if lof:
-            lof_v, _ = tdist.lof_scores(Xd, k, stages)
+        if mode == "ring":
+            if lof:
+                _, _, _, st = ctx.lof_sharded(Xl, n, qb, k)
+            else:
+                r, _, _ = ctx.knn_sharded(Xl, n, qb, k, want=())
+                st = r.stats
+        elif lof:
+            _, _, _, st = ctx.lof(Xd, k)
         else:
-            out = tdist.knn_scores(Xd, k, stages)
-        return
-
-    # The per-phase CUDA-event times come from the library (TOD_F_TIMING) via
-    # the stats of the knn stage; wrap the stage to capture them.
-    orig_knn = stages.knn
-
-    def knn_capture(*a, **kw):
-        r = orig_knn(*a, **kw)
-        last_stats.clear()
-        last_stats.update(r["stats"])
-        return r
-
-    stages.knn = knn_capture
+            st = ctx.knn(Xd, k, qb, qc, want=("score_kth", "score_mean")).stats
+        last.clear()
+        last.update(st)
 
     # the clock sampler starts before the warm-up (it keeps only the samples inside
     # the timed window), so the GPU never idles between warm-up and timing
@@ -324,88 +355,92 @@ def run_gpu(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    torch.cuda.synchronize()
+    main_ms, kern_ms, launches = [], [], []
     if world > 1:
         dist.barrier()
+    torch.cuda.synchronize()
     t0 = time.time()
     for i in range(args.steps):
         flush.fill_(float(i))               # L2 flush (256 MiB write) between steps, untimed
         evs[i][0].record(stream)
         step()
         evs[i][1].record(stream)
-        main_ms.append(last_stats.get("ms_main", 0.0))
-        kern_ms.append(last_stats.get("ms_main_kernel", 0.0))
-        launches.append(last_stats.get("kernel_launches", 0) + (2 if lof else 0))
+        main_ms.append(last.get("ms_main", 0.0))
+        kern_ms.append(last.get("ms_main_kernel", 0.0))
+        launches.append(last.get("kernel_launches", 0))
     torch.cuda.synchronize()
     t1 = time.time()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop(t0, t1)
-    step_ms = np.array([a.elapsed_time(b) for a, b in evs])
-    ms = float(step_ms.mean())
-    main = float(np.mean(main_ms))
-    kmain = float(np.mean(kern_ms))
-    if world > 1:
+    ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    main, kmain = float(np.mean(main_ms)), float(np.mean(kern_ms))
+    stats = dict(last)
+    if world > 1:  # max over ranks of the device times
         t = torch.tensor([ms, main, kmain], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, main, kmain = float(t[0]), float(t[1]), float(t[2])
 
-    # ---- e2e: the same step through the C ABI with HOST buffers (pinned),
-    # H2D of X and D2H of the scores inside the timed region (rank-local shard).
+    # ---- e2e: the same step through the C ABI with HOST buffers (pinned): the
+    # H2D of this rank's X and the D2H of the scores are inside the timed region
     e2e_ms = []
-    b, c = tdist.shard_rows(n, world, rank)
-    Xh = torch.from_numpy(X).pin_memory()
-    h2d = n * d * 4
-    if lof and world == 1:
-        d2h = n * 4 * 4   # lof, lrd, score_kth, score_mean (fp32)
-        for i in range(args.warmup + min(args.steps, 20)):
-            flush.fill_(float(i))
-            torch.cuda.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            lof_h, lrd_h, kr, _ = ctx.lof(Xh, k, want_knn=("score_kth", "score_mean"))
-            e1.record(stream)
-            torch.cuda.synchronize()
-            if i >= args.warmup:
-                e2e_ms.append(e0.elapsed_time(e1))
+    if mode == "ring":
+        Xh = torch.from_numpy(X[qb:qb + qc]).pin_memory()
+        h2d = qc * d * 4
+        d2h = n * 4 * 2
     else:
-        d2h = c * 4 * 2
-        for i in range(args.warmup + min(args.steps, 20)):
-            flush.fill_(float(i))
-            torch.cuda.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            ctx.knn(Xh, k, b, c, want=("score_kth", "score_mean"))
-            e1.record(stream)
-            torch.cuda.synchronize()
-            if i >= args.warmup:
-                e2e_ms.append(e0.elapsed_time(e1))
+        Xh = torch.from_numpy(X).pin_memory()
+        h2d = n * d * 4
+        d2h = (n * 4 * 4) if lof else (qc * 4 * 2)
+    for i in range(args.warmup + min(args.steps, 10)):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        if mode == "ring":
+            if lof:
+                ctx.lof_sharded(Xh, n, qb, k)
+            else:
+                ctx.knn_sharded(Xh, n, qb, k, want=())
+        elif lof:
+            ctx.lof(Xh, k, want_knn=("score_kth", "score_mean"))
+        else:
+            ctx.knn(Xh, k, qb, qc, want=("score_kth", "score_mean"))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            e2e_ms.append(e0.elapsed_time(e1))
     e2e = float(np.mean(e2e_ms))
     if world > 1:
         t = torch.tensor([e2e], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = float(t[0])
 
+    # queries answered by the whole job per step
+    if args.config == "c4":
+        q_job = sum(tdist.shard_rows(n, 8, r)[1] for r in range(world))
+    else:
+        q_job = n
     if rank == 0:
         peak_b, peak_s, hbm, peak_src = _peaks()
         # Dominant kernel: the tensor-core main pass (k_knn_tc3 single-SM or
-        # k_knn_tc4 CTA pairs), timed with CUDA events around its launch on the
-        # launching stream.  Algorithmic work per (query, reference) pair = 2d
-        # flops of the -2XY^T contraction; the main pass covers
-        # every reference column (key-only sample, d <= 32) or every column
-        # outside the sample tiles (list sample, d = 64), for this rank's rows.
-        rows = tdist.shard_rows(n, world, rank)[1]
-        mk = last_stats.get("main_kernel", 0)
+        # k_knn_tc4 CTA pairs), timed with CUDA events around its launch(es) on
+        # the launching stream (the ring: around the W main-pass launches, which
+        # also contain any wait for a block transfer).  Algorithmic work per
+        # (query, reference) pair = 2d flops of the -2XY^T contraction (DESIGN.md
+        # §7); the main pass covers every reference column (key-only sample) or
+        # every column outside the sample tiles (list sample, d = 64 in one
+        # process), for this rank's rows.
+        rows = qc
+        mk = stats.get("main_kernel", 0)
         if mk:
             bt = (n + 255) // 256
             samp_cols = sum(min(256, n - 256 * t) for t in range(0, bt, 8))
-            if last_stats.get("sample_pass") == 2:   # key-only sample: main covers every tile
+            if stats.get("sample_pass") == 2:   # key-only sample: main covers every tile
                 samp_cols = 0
             pairs_main = rows * (n - samp_cols)
             kname = {3: "k_knn_tc3 (single-SM tcgen05 main pass)",
@@ -418,38 +453,50 @@ def run_gpu(args):
         flops = 2.0 * pairs_main * d          # algorithmic contraction flops per launch (per GPU)
         achieved = flops / (kms * 1e-3) / 1e12
         pass1_tf = 2.0 * rows * n * d / (main * 1e-3) / 1e12
-        qps = n / (ms * 1e-3)
+        # peak: the sustained GEMM figure for a kernel that runs tens of ms inside a
+        # long step, the burst figure for a short one (B200_PROFILING.md)
+        long_kernel = kms >= 20.0
+        peak = peak_s if long_kernel else peak_b
+        qps = q_job / (ms * 1e-3)
         line = {
             "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f16 operands/f32 accumulate (pass 1), f64 re-rank",
+            "higher_is_better": True,
+            "scaling": "weak" if args.config == "c4" else "strong",
+            "vs_baseline": None,
+            "dtype": "%s operands/f32 accumulate (pass 1), f64 re-rank" %
+                     {1: "f16", 2: "bf16", 3: "f32"}.get(stats.get("format"), "?"),
             "data": "synthetic (Gaussian mixture + uniform outliers, seed 0)",
-            "config": {"workload": desc + (" (n scaled to %d for N=%d: weak scaling)" % (n, world)
-                                           if world > 1 else ""),
-                       "n": n, "d": d, "k": k, "lof": lof, "format": last_stats.get("format"),
-                       "kprime": last_stats.get("kprime"), "chunks": last_stats.get("chunks"),
+            "config": {"workload": desc, "n": n, "d": d, "k": k, "lof": lof,
+                       "queries_per_step": q_job, "queries_this_rank": qc,
+                       "format": stats.get("format"), "kprime": stats.get("kprime"),
+                       "chunks": stats.get("chunks"),
                        "l2": "flushed between steps (256 MiB write)",
-                       "parallelism": "query-sharded dp%d" % world},
+                       "parallelism": ("query-sharded dp%d, reference blocks on an NCCL ring" % world
+                                       if mode == "ring" else
+                                       "one rank's 1/8 query shard per GPU, references resident"
+                                       if mode == "shard8" else "single GPU")},
             "dist_evals_per_s": qps * n,
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_b,
-                         "unit": "TFLOP/s", "frac": achieved / peak_b,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak,
+                         "frac_of_burst_peak": achieved / peak_b,
                          "traffic": _traffic(args.config),
                          "kernel": kname, "kernel_ms": kms, "flops_per_launch": flops,
-                         "pass1": {"kernels": "sample k_knn_tc + main" if mk else "k_knn_tc",
-                                   "ms": main, "achieved_tflops": pass1_tf,
-                                   "frac": pass1_tf / peak_b},
-                         "peak_source": "%s bf16_tflops (fp16 dense rate = bf16 on B200)" % peak_src},
-            "phase_ms": {kk: last_stats.get(kk) for kk in
+                         "pass1": {"kernels": "sample + main", "ms": main,
+                                   "achieved_tflops": pass1_tf, "frac": pass1_tf / peak},
+                         "peak_source": "%s %s (fp16 dense rate = bf16 on B200)" %
+                                        (peak_src, "bf16_tflops_sustained" if long_kernel
+                                         else "bf16_tflops")},
+            "phase_ms": {kk: stats.get(kk) for kk in
                          ("ms_prep", "ms_main", "ms_main_kernel", "ms_certify", "ms_fallback",
                           "ms_lof")},
             "candidates_per_row": {
-                "staged_groups": last_stats.get("cand_groups", 0) / max(1, rows),
-                "visited_groups": last_stats.get("visited_groups", 0) / max(1, rows),
-                "kept_columns": last_stats.get("cand_columns", 0) / max(1, rows)},
-            "certified_rows": last_stats.get("certified"),
-            "fallback_rows": last_stats.get("fallback_rows"),
-            "e2e": {"value": n / (e2e * 1e-3),
+                "staged_groups": stats.get("cand_groups", 0) / max(1, rows),
+                "visited_groups": stats.get("visited_groups", 0) / max(1, rows),
+                "kept_columns": stats.get("cand_columns", 0) / max(1, rows)},
+            "certified_rows": stats.get("certified"),
+            "fallback_rows": stats.get("fallback_rows"),
+            "e2e": {"value": q_job / (e2e * 1e-3),
                     "unit": "queries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e},
             "gpu_launches": int(sum(launches)),
@@ -464,13 +511,23 @@ def run_gpu(args):
     return 0
 
 
+def _relaunch_distributed(args):
+    """`--gpus N` without torchrun: start N ranks with torch.distributed.run."""
+    import random
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+           "--master-port", str(random.randint(20000, 40000)), os.path.abspath(__file__)]
+    cmd += [a for a in sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--fmt", default=None, choices=[None, "fp16", "bf16", "fp32", "auto"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
@@ -478,6 +535,12 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _relaunch_distributed(args)
+    if world != args.gpus and int(os.environ.get("RANK", "0")) == 0:
+        print("bench.py: --gpus %d but WORLD_SIZE=%d; using %d ranks" % (args.gpus, world, world),
+              file=sys.stderr)
     if args.impl == "reference":
         return run_reference(args)
     if args.config == "nwr":
