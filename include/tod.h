@@ -272,6 +272,24 @@ tod_status tod_knn_classify(tod_ctx* ctx, const float* Q, int64_t nq, const floa
 tod_status tod_knn_query(tod_ctx* ctx, const float* Q, int64_t nq, const float* X, int64_t n,
                          int32_t d, int32_t k, const tod_knn_out* out, tod_stats* stats);
 
+/*
+ * tod_debug_mainpass — diagnostics for the certificate's tensor-core error
+ * model (reading A9; the verification step (iii) of PAPER.md
+ * P:341-343 rests on it).  Quantizes X as tod_knn would (cfg->format), runs the
+ * production main-pass kernel (single-SM or CTA-pair, as tod_knn would) for
+ * query rows [0, 128) against all n rows, and returns:
+ *   w      [128 x n] fp32: the raw tensor-core accumulators w~_ij (self and
+ *          padding unmasked);
+ *   a_ops  [128 x K] fp32: the query operand row i as multiplied (-2 xhat_i, then
+ *          the norm-piece constants), K = dpad + 16;
+ *   b_ops  [n x K] fp32: the reference operand row j (xhat_j, then the norm pieces),
+ * so that w_ij = sum_c a_ops[i,c] b_ops[j,c] exactly (every product is exact in
+ * fp32) and |w~_ij - w_ij| can be checked against the model.  All pointers are
+ * DEVICE pointers; n >= 128.  *K_out = K; *main_kernel = 3 (single SM) or 4 (pair).
+ */
+tod_status tod_debug_mainpass(tod_ctx* ctx, const float* X, int64_t n, int32_t d, float* w,
+                              float* a_ops, float* b_ops, int32_t* K_out, int32_t* main_kernel);
+
 /* ===================================================================== *
  * Sharded multi-GPU path (§6.2: one process per GPU,    *
  * "subtasks are split equally").     *

@@ -1117,6 +1117,53 @@ tod_status tod_lof(tod_ctx* ctx, const float* X, int64_t n, int32_t d, int32_t k
   return TOD_OK;
 }
 
+tod_status tod_debug_mainpass(tod_ctx* ctx, const float* X, int64_t n, int32_t d, float* w,
+                              float* a_ops, float* b_ops, int32_t* K_out, int32_t* main_kernel) {
+  TOD_TRY(validate_common(ctx, n, d, 1));
+  if (n < 128) return fail(ctx, TOD_E_RANGE, "tod_debug_mainpass needs n >= 128");
+  if (!X || !w || !a_ops || !b_ops || !K_out)
+    return fail(ctx, TOD_E_ARG, "null pointer");
+  for (const void* q : {(const void*)X, (const void*)w, (const void*)a_ops, (const void*)b_ops})
+    if (!is_device_ptr(q, ctx->device)) return fail(ctx, TOD_E_ARG, "tod_debug_mainpass takes device pointers");
+  TOD_CUDA(cudaSetDevice(ctx->device));
+  Plan plan;
+  TOD_TRY(make_plan(ctx, n, 128, d, 1, &plan));
+  if (plan.kind != PASS_TC || !tc3_fits(plan.dpad))
+    return fail(ctx, TOD_E_UNSUPPORTED, "tensor-core main pass not used for this shape/format");
+  cudaStream_t st = ctx->stream;
+  int launches = 0;
+  void* p;
+  TOD_TRY(ensure(ctx, B_SMALL, sizeof(SmallDev), &p));
+  SmallDev* small = static_cast<SmallDev*>(p);
+  TOD_CUDA(cudaMemsetAsync(small, 0, sizeof(SmallDev), st));
+  CertParams cp{};
+  Image A, B;
+  RefPrep ref;
+  TOD_TRY(prep_tc(ctx, X, n, nullptr, 0, 128, d, plan.fmt, plan.dpad, &small->g, &A, &B, &cp, &ref,
+                  &launches));
+  MainPass mp;
+  mp.S = 1;
+  mp.R = 0;
+  mp.parts = tc3_parts(plan.dpad);
+  mp.tau_v = nullptr;
+  mp.tau_lists = 0;
+  mp.buf = reinterpret_cast<uint2*>(w);  // dump: [128 x n] fp32, ld = n
+  mp.cap = (int)n;
+  mp.cnt = nullptr;
+  const char* pe = getenv("TOD_MAIN_PAIR");
+  const bool pair = (pe ? atoi(pe) != 0 : tc4_preferred(plan.dpad) != 0) &&
+                    !(ctx->cfg.flags & TOD_F_MAIN_1SM) && tc4_fits(plan.dpad, mp.parts);
+  if (pair) TOD_CUDA(launch_knn_tc4(A, B, 0, 128, true, plan.fmt, mp, ctx->num_sms, 4, st, &launches));
+  else TOD_CUDA(launch_knn_tc3(A, B, 0, 128, true, plan.fmt, mp, ctx->num_sms, 4, st, &launches));
+  TOD_CUDA(launch_image_decode(A, plan.fmt, 128, a_ops, st, &launches));
+  TOD_CUDA(launch_image_decode(B, plan.fmt, n, b_ops, st, &launches));
+  TOD_CUDA(cudaStreamSynchronize(st));
+  *K_out = plan.dpad + 16;
+  if (main_kernel) *main_kernel = pair ? 4 : 3;
+  ctx->msg.clear();
+  return TOD_OK;
+}
+
 tod_status tod_lof_lrd(tod_ctx* ctx, int64_t n, int32_t k, int64_t q_count, const int64_t* idx,
                        const double* dist64, const double* kdist64_all, double* lrd64_out) {
   if (!ctx) return TOD_E_ARG;

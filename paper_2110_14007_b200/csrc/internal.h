@@ -72,6 +72,8 @@ cudaError_t launch_prep_colsum(const float* X, int64_t n, int d, double* partial
 cudaError_t launch_prep_colmean(const double* partial, int blocks, int64_t n, int d, double* mu,
                                 cudaStream_t st, int* launches);
 int prep_stat_rows();  // rows per column-sum partial block (128)
+cudaError_t launch_image_decode(const Image& img, int fmt, int64_t rows, float* out, cudaStream_t st,
+                                int* launches);  // diagnostics: 16-bit image -> fp32 [rows][dpad+16]
 cudaError_t launch_finite_check(const float* X, int64_t n, int d, PrepGlobals* g, cudaStream_t st,
                                 int* launches);
 

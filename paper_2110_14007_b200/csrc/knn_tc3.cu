@@ -440,6 +440,17 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
         if (DBG & 3) continue;  // profiling: pipeline without the filter work
         const int t = ts.t;
         const int j0 = t * kBN + h * BH;
+        if constexpr ((DBG & 4) != 0) {
+          // diagnostics (tod_debug_mainpass): the raw accumulators w~ of the first
+          // query tile, [128 x ld] fp32 in mbuf, ld = cap; no appends
+          if (qtl == 0) {
+            float* dump = reinterpret_cast<float*>(mbuf);
+#pragma unroll
+            for (int e = 0; e < BH; ++e)
+              if (j0 + e < n_ref) dump[(int64_t)rt * cap + j0 + e] = v[e];
+          }
+          continue;
+        }
         // the self column and padding columns (>= n_ref) are never candidates;
         // only the query tile's own reference tile and the last tile need masks
         if (t == t_self || t == t_last) {
@@ -514,7 +525,7 @@ cudaError_t launch3(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
   kern<<<grid, 64 + 32 * FW, smem, st>>>(
       reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(), A.extra_offset(),
       reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
-      B.n_pad / kBN, B.n, qt0, qt1 - qt0, q_begin, q_begin + q_count, self_join ? 1 : 0, m.S,
+      (B.n + kBN - 1) / kBN, B.n, qt0, qt1 - qt0, q_begin, q_begin + q_count, self_join ? 1 : 0, m.S,
       m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap, m.samp, m.col0, m.samp_acc);
   return cudaGetLastError();
 }
@@ -586,6 +597,9 @@ cudaError_t launch_knn_tc3(const Image& A, const Image& B, int64_t q_begin, int6
   if (m.samp)                                                                                     \
     return fmt == 1 ? launch3<D, 1, 0, FW, 4>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
                     : launch3<D, 2, 0, FW, 4>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+  if (dbg & 4)                                                                                    \
+    return fmt == 1 ? launch3<D, 1, 4, FW, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
+                    : launch3<D, 2, 4, FW, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
   if ((dbg & 3) == 1 && fmt == 1)                                                                 \
     return launch3<D, 1, 1, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st);            \
   if (dbg & 3)                                                                                    \

@@ -364,6 +364,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
         if (DBG & 3) continue;
         const int t = ts.t;
         const int j0 = t * kBN + h * BH;
+        if constexpr ((DBG & 4) != 0) {
+          // diagnostics (tod_debug_mainpass): raw w~ of the first query tile (CTA 0)
+          if (qtl == 0) {
+            float* dump = reinterpret_cast<float*>(mbuf);
+#pragma unroll
+            for (int e = 0; e < BH; ++e)
+              if (j0 + e < n_ref) dump[(int64_t)rt * cap + j0 + e] = v[e];
+          }
+          continue;
+        }
         if (t == t_self || t == t_last) {
 #pragma unroll
           for (int e = 0; e < BH; ++e)
@@ -417,7 +427,7 @@ cudaError_t launch4(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
   kern<<<(unsigned)(2 * pairs), 64 + 32 * FW, smem, st>>>(
       reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(), A.extra_offset(),
       reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
-      B.n_pad / kBN, B.n, qt0, n_qpairs, q_begin, q_begin + q_count, self_join ? 1 : 0, m.S,
+      (B.n + kBN - 1) / kBN, B.n, qt0, n_qpairs, q_begin, q_begin + q_count, self_join ? 1 : 0, m.S,
       m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap, m.col0);
   return cudaGetLastError();
 }
@@ -445,6 +455,9 @@ cudaError_t launch_knn_tc4(const Image& A, const Image& B, int64_t q_begin, int6
   *launches += 1;
 #define TOD_TC4_CASE(D)                                                                          \
   case D:                                                                                       \
+    if (dbg & 4)                                                                                \
+      return fmt == 1 ? launch4<D, 1, 4, 16>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
+                      : launch4<D, 2, 4, 16>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
     if (dbg & 3)                                                                                \
       return fmt == 1 ? launch4<D, 1, 2, 16>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
                       : launch4<D, 2, 2, 16>(A, B, q_begin, q_count, self_join, m, num_sms, st); \

@@ -271,7 +271,46 @@ __global__ void k_quant(const float* __restrict__ X, int64_t n, int d,
   }
 }
 
+// Diagnostics (tod_debug_mainpass): the 16-bit operand image decoded to fp32,
+// out[r][c], c < dpad from the main regions, c in [dpad, dpad + 16) from the
+// extra region -- exactly the values the tensor core multiplies.
+template <int FMT>
+__global__ void k_image_decode(Image img, int64_t rows, float* __restrict__ out) {
+  const int K = img.dpad + 16;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * K) return;
+  const int64_t r = i / K;
+  const int c = (int)(i - r * K);
+  const uint8_t* base = reinterpret_cast<const uint8_t*>(img.data);
+  uint64_t phys;
+  const uint8_t* reg;
+  if (c < img.dpad) {
+    const int epr = img.rb / 2;
+    const unsigned M = img.layout == 2 ? 7u : (img.layout == 4 ? 3u : 1u);
+    const uint64_t o = (uint64_t)r * img.rb + (uint64_t)(c % epr) * 2u;
+    phys = o ^ (((o >> 7) & M) << 4);
+    reg = base + (size_t)(c / epr) * img.region_bytes();
+  } else {
+    const uint64_t o = (uint64_t)r * 32u + (uint64_t)(c - img.dpad) * 2u;
+    phys = o ^ (((o >> 7) & 1u) << 4);
+    reg = base + img.extra_offset();
+  }
+  const uint16_t h = *reinterpret_cast<const uint16_t*>(reg + phys);
+  out[i] = (float)widen16<FMT>(h);
+}
+
 }  // namespace
+
+cudaError_t launch_image_decode(const Image& img, int fmt, int64_t rows, float* out, cudaStream_t st,
+                                int* launches) {
+  const int64_t tot = rows * (img.dpad + 16);
+  if (tot <= 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((tot + 255) / 256);
+  if (fmt == 1) k_image_decode<1><<<blocks, 256, 0, st>>>(img, rows, out);
+  else k_image_decode<2><<<blocks, 256, 0, st>>>(img, rows, out);
+  *launches += 1;
+  return cudaGetLastError();
+}
 
 cudaError_t launch_prep_stats(const float* X, int64_t n, int d, double* mu, double* partial,
                               int partial_blocks, PrepGlobals* g, cudaStream_t st, int* launches) {

@@ -105,6 +105,8 @@ def load_library(path: str = LIB_PATH):
         "tod_nwr": ([P, P, I64, I32, ctypes.c_double, I64, I64, P, P, P, I64,
                      ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(Stats)], ctypes.c_int),
         "tod_lof_finish": ([P, I64, I32, I64, I64, P, P, P, P], ctypes.c_int),
+        "tod_debug_mainpass": ([P, P, I64, I32, P, P, P, ctypes.POINTER(ctypes.c_int32),
+                                ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),
         "tod_comm_id_create": ([P], ctypes.c_int),
         "tod_comm_init": ([P, P, I32, I32], ctypes.c_int),
         "tod_comm_init_loopback": ([P, I32], ctypes.c_int),
@@ -370,6 +372,25 @@ class Context:
                                      ctypes.byref(ko) if want_knn else None, ctypes.byref(s)))
         res = KnnResult(**o, stats=s.as_dict()) if want_knn else None
         return lof, lrd, res, s.as_dict()
+
+    def debug_mainpass(self, X):
+        """tod_debug_mainpass (diagnostics, CUDA tensors): raw tensor-core
+        accumulators of query rows [0, 128) against all rows, and the operands
+        as multiplied.  Returns (w [128, n], a_ops [128, K], b_ops [n, K], kernel)."""
+        import torch
+        X = _as_f32_2d(X)
+        n, d = X.shape
+        K = ((d + 15) // 16) * 16
+        K = (16 if d <= 16 else 32 if d <= 32 else 64 if d <= 64 else 128 if d <= 128
+             else 256 if d <= 256 else 512) + 16
+        w = torch.empty((128, n), dtype=torch.float32, device=X.device)
+        a = torch.empty((128, K), dtype=torch.float32, device=X.device)
+        b = torch.empty((n, K), dtype=torch.float32, device=X.device)
+        k_out, mk = ctypes.c_int32(0), ctypes.c_int32(0)
+        self._check(self.lib.tod_debug_mainpass(self.h, _ptr(X), n, d, _ptr(w), _ptr(a), _ptr(b),
+                                                ctypes.byref(k_out), ctypes.byref(mk)))
+        assert k_out.value == K
+        return w, a, b, mk.value
 
     # ---------------------------------------------------------- sharded path
     def comm_init(self, rank: int, world: int, comm_id: bytes):

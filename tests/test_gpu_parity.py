@@ -269,30 +269,6 @@ def _sample_rows(n, labels, m, seed):
     return np.unique(rows)
 
 
-def test_c2_full_size_sampled(pkg):
-    # configs[1]: kNN + LOF, n=100,000, d=32, k=20 on 1xB200 (bench launch config)
-    X, lab = datagen.gaussian_mixture(100_000, 32, seed=0, return_labels=True)
-    k = 20
-    with _ctx(pkg) as ctx:
-        lof, lrd, res, st = ctx.lof(torch.from_numpy(X).cuda(), k,
-                                    want_knn=("idx", "dist", "dist64", "score_kth", "score_mean"))
-    rows = _sample_rows(100_000, lab, 48, seed=1)
-    _check_rows(res, X, k, rows)
-    lr = oracle.lof_rows(X, k, rows[:3])
-    assert np.array_equal(_np(lof)[rows[:3]], lr["lof"].astype(np.float32))
-    assert st["certified"] >= 0.99 * 100_000, st
-
-
-def test_c3_full_size_sampled_bf16(pkg):
-    # configs[2]: n=1,000,000, d=64, k=10, bf16 provable-quantization path
-    X, lab = datagen.gaussian_mixture(1_000_000, 64, seed=0, return_labels=True)
-    k = 10
-    with _ctx(pkg, fmt="bf16") as ctx:
-        res = ctx.knn(torch.from_numpy(X).cuda(), k)
-    rows = _sample_rows(1_000_000, lab, 16, seed=2)
-    _check_rows(res, X, k, rows)
-
-
 # ------------------------------------------------------------ NWR (NEXT-2)
 def _nwr_check(got, X, phi, rows):
     counts, ptr, cols, st = got
