@@ -472,6 +472,8 @@ __device__ __forceinline__ void rerank_groups_row(
   __syncwarp();
   // ---- 1. kappa and UB
   double UB = CUDART_INF;
+  float kappa = CUDART_INF_F;
+  int chi = G;  // staged groups with key <= kappa
   if (G >= k) {
     uint32_t lo = 0xFFFFFFFFu, hi = 0u;
     uint32_t ok[8];  // this lane's ordered keys (G <= 256), 0xFFFFFFFF = none
@@ -496,7 +498,6 @@ __device__ __forceinline__ void rerank_groups_row(
     // 64 ulps of it (relative 2^-17, far below the bound's own slack) saves the
     // last halvings; any hi with count >= k gives a valid UB.
     if (lo < hi) --lo;  // count(key <= lo) < k unless lo is the minimum itself
-    int chi = G;
     for (int it = 0; it < 32 && hi - lo > 64 && chi > k; ++it) {
       const uint32_t mid = lo + ((hi - lo) >> 1);
       int c = 0;
@@ -511,32 +512,44 @@ __device__ __forceinline__ void rerank_groups_row(
         lo = mid;
       }
     }
-    const float kappa = ord2f(hi);
+    kappa = ord2f(hi);
     if (kappa < CUDART_INF_F) UB = ub2_from_key(cp, r, (double)kappa);
   }
-  // ---- 2. expand the groups that can hold a top-k column
-  // (compacted in place into gid[0, nv), then 4 groups = 32 columns per step)
-  int nv = 0;
-  const float kcut = key_cut_from_ub(cp, r, UB);
-  for (int e0 = 0; e0 < G; e0 += 32) {
-    const int e = e0 + lane;
-    bool vis = false;
-    int g = -1;
-    if (e < G) {
-      vis = gk[e] <= kcut;
-      g = gid[e];
-    }
-    const unsigned vm = __ballot_sync(0xffffffffu, vis);
-    if (vis) gid[nv + __popc(vm & ((1u << lane) - 1u))] = g;
-    nv += __popc(vm);
-  }
-  __syncwarp();
+  // ---- 2. expand the groups that can hold a top-k column, 4 groups = 32
+  // columns per step.  Two rounds when the groups at or below kappa fit the
+  // column store: round 1 evaluates exactly those (>= k distinct real columns),
+  // whose k-th smallest exact D64 is itself an upper bound UB1 on the k-th
+  // distance -- tighter than UB from kappa, which carries the pass-1 error on top
+  // of the key -- so round 2 only visits the remaining groups whose lower bound
+  // can reach min(UB, UB1).
   double* ck = s_ck[w];
   int* ci = s_ci[w];
   int nc = 0;
-  for (int b0 = 0; b0 < nv; b0 += 4) {
+  int nv = 0;
+  const bool two_round = G >= k && chi <= kColMax / 8 && chi <= kMaxK && kappa < CUDART_INF_F;
+  int* glist = gid;  // groups to expand in the current round
+  auto compact_groups = [&](int* dst, float lo_excl, float hi_incl) {
+    int m = 0;
+    for (int e0 = 0; e0 < G; e0 += 32) {
+      const int e = e0 + lane;
+      bool vis = false;
+      int g = -1;
+      if (e < G) {
+        const float kk = gk[e];
+        vis = kk <= hi_incl && !(kk <= lo_excl);
+        g = gid[e];
+      }
+      const unsigned vm = __ballot_sync(0xffffffffu, vis);
+      if (vis) dst[m + __popc(vm & ((1u << lane) - 1u))] = g;
+      m += __popc(vm);
+    }
+    __syncwarp();
+    return m;
+  };
+  auto expand = [&](const int* gl, int ng, double cut) {
+  for (int b0 = 0; b0 < ng; b0 += 4) {
     const int gs = b0 + (lane >> 3);
-    const int g = gs < nv ? gid[gs] : -1;
+    const int g = gs < ng ? gl[gs] : -1;
     const int64_t j = (int64_t)g * 8 + (lane & 7);
     double key = CUDART_INF;
     if (g >= 0 && j < n && !(self_join && j == gi)) {
@@ -585,7 +598,7 @@ __device__ __forceinline__ void rerank_groups_row(
       }
       key = acc;
     }
-    const bool keep = key <= UB && key < CUDART_INF;
+    const bool keep = key <= cut && key < CUDART_INF;
     const unsigned km = __ballot_sync(0xffffffffu, keep);
     const int pos = nc + __popc(km & ((1u << lane) - 1u));
     if (keep && pos < kColMax) {
@@ -593,6 +606,77 @@ __device__ __forceinline__ void rerank_groups_row(
       ci[pos] = (int)j;
     }
     nc += __popc(km);
+  }
+  };
+  if (two_round) {
+    // round 1: every column of the chi groups at or below kappa (s_ti as the list)
+    int* l1 = s_ti[w];
+    const int n1 = compact_groups(l1, -CUDART_INF_F, kappa);
+    expand(l1, n1, CUDART_INF);
+    __syncwarp();
+    nv = n1;
+    // UB1: the k-th smallest exact D64 among them (bisection on the bits of
+    // non-negative doubles, stopped within 2^20 ulps: any value with >= k
+    // columns at or below it is a valid bound)
+    if (nc >= k) {
+      unsigned long long blo = ~0ull, bhi = 0ull;
+      for (int e = lane; e < nc; e += 32) {
+        const unsigned long long b = (unsigned long long)__double_as_longlong(ck[e]);
+        blo = min(blo, b);
+        bhi = max(bhi, b);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        blo = min(blo, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)blo, o));
+        bhi = max(bhi, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)bhi, o));
+      }
+      if (blo > 0) --blo;  // count(<= blo) < k unless blo is the minimum itself
+      int cb = nc;
+      for (int it = 0; it < 64 && bhi - blo > (1ull << 20) && cb > k; ++it) {
+        const unsigned long long mid = blo + ((bhi - blo) >> 1);
+        int c = 0;
+        for (int e = lane; e < nc; e += 32)
+          c += (unsigned long long)__double_as_longlong(ck[e]) <= mid;
+        c = __reduce_add_sync(0xffffffffu, c);
+        if (c >= k) {
+          bhi = mid;
+          cb = c;
+        } else {
+          blo = mid;
+        }
+      }
+      UB = fmin(UB, __longlong_as_double((long long)bhi));
+    }
+    // keep the round-1 columns at or below UB (in-place ballot compaction)
+    int m = 0;
+    for (int e0 = 0; e0 < nc; e0 += 32) {
+      const int e = e0 + lane;
+      double kk = 0.0;
+      int ii = 0;
+      bool keep = false;
+      if (e < nc) {
+        kk = ck[e];
+        ii = ci[e];
+        keep = kk <= UB;
+      }
+      const unsigned km = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        ck[m + __popc(km & ((1u << lane) - 1u))] = kk;
+        ci[m + __popc(km & ((1u << lane) - 1u))] = ii;
+      }
+      m += __popc(km);
+    }
+    nc = m;
+    __syncwarp();
+    // round 2: groups above kappa whose lower bound can still reach UB
+    const float kcut = key_cut_from_ub(cp, r, UB);
+    const int n2 = compact_groups(glist, kappa, kcut);
+    expand(glist, n2, UB);
+    nv += n2;
+  } else {
+    const float kcut = key_cut_from_ub(cp, r, UB);
+    nv = compact_groups(glist, -CUDART_INF_F, kcut);
+    expand(glist, nv, UB);
   }
   overflow |= nc > kColMax;
   if (nc > kColMax) nc = kColMax;
@@ -1575,7 +1659,7 @@ __global__ void k_scan_final(const int64_t* __restrict__ c, int64_t q, const int
 // SM's bandwidth.
 constexpr int kFbThreads = 256;
 constexpr int kFbCap = 1024;   // collected columns per failing row (threshold tier)
-constexpr int kFbQB = 4;       // failing rows per block of the collect kernel
+constexpr int kFbQB = 16;      // failing rows per block of the collect kernel
 
 // Threshold tier of the fallback: every column whose D64 (oracle formula O1)
 // is <= ub_f -- an upper bound on row f's k-th distance handed over by the
@@ -1587,59 +1671,80 @@ __global__ void __launch_bounds__(kFbThreads)
                  int64_t n, int d, int self_join, const int32_t* __restrict__ fail_rows,
                  const double* __restrict__ fail_ub, int nfail, int P,
                  double* __restrict__ ck, int* __restrict__ ci, int* __restrict__ ccnt) {
-  extern __shared__ double s_q[];  // [kFbQB][d]
+  // A cheap fp32 screen first (difference form, one FFMA per term: |D~ - rho^2| <=
+  // gamma_{d+2}(2^-24) rho^2, the SIMT pass's bound), then the oracle's fp64 O1
+  // only for columns that can be at or below the row's bound -- the exact
+  // evaluation decides, the screen only skips columns that provably cannot.
+  extern __shared__ float s_q32[];  // [kFbQB][d] query rows (fp32, exact)
   const int t = threadIdx.x, lane = t & 31;
   const int p = blockIdx.y, f0 = blockIdx.x * kFbQB;  // x: row groups (large), y: slices
   const int nq = min(kFbQB, nfail - f0);
   int64_t gq[kFbQB];
   double ub[kFbQB];
+  float thr[kFbQB];
+  const double g32 = gamma_up(d + 2, 5.9604644775390625e-08);
+  const double g64 = gamma_up(d + 2, 1.1102230246251565e-16);
 #pragma unroll
   for (int q = 0; q < kFbQB; ++q) {
     const int f = f0 + (q < nq ? q : 0);
     const int64_t r = fail_rows[f];
     gq[q] = q_begin + r;
     ub[q] = q < nq ? fail_ub[f] : -1.0;
+    // D64 <= ub  =>  rho^2 <= ub / (1 - g64)  =>  D~ <= ub (1 + g32) / (1 - g64)
+    const double th = ub[q] * (1.0 + g32) / (1.0 - g64) * (1.0 + 9.5367431640625e-07) +
+                      (d + 2) * 1.1754943508222875e-38;
+    thr[q] = q < nq ? __double2float_ru(th) : -1.0f;
     const float* xi = self_join ? X + gq[q] * d : Q + r * d;
-    for (int c = t; c < d; c += kFbThreads) s_q[q * d + c] = (double)xi[c];
+    for (int c = t; c < d; c += kFbThreads) s_q32[q * d + c] = xi[c];
   }
   __syncthreads();
   const int64_t j_lo = n * p / P, j_hi = n * (p + 1) / P;
   const bool vec8 = (d & 7) == 0 && (reinterpret_cast<uintptr_t>(X) & 31) == 0;
   for (int64_t jb = j_lo; jb < j_hi; jb += kFbThreads) {
     const int64_t j = jb + t;
-    double acc[kFbQB];
+    float acc[kFbQB];
 #pragma unroll
-    for (int q = 0; q < kFbQB; ++q) acc[q] = 0.0;
+    for (int q = 0; q < kFbQB; ++q) acc[q] = 0.0f;
+    const float* xj = X + (j < j_hi ? j : j_lo) * d;
     if (j < j_hi) {
-      const float* xj = X + j * d;
-      if (vec8) {  // 32-byte loads, 8 dims at a time, same per-row order
+      if (vec8) {
         for (int c8 = 0; c8 < d; c8 += 8) {
           float v[8];
           ldg8(xj + c8, v);
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const double xv = (double)v[u];
+          for (int u = 0; u < 8; ++u)
 #pragma unroll
             for (int q = 0; q < kFbQB; ++q) {
-              const double tt = __dsub_rn(s_q[q * d + c8 + u], xv);
-              acc[q] = __dadd_rn(acc[q], __dmul_rn(tt, tt));
+              const float tt = s_q32[q * d + c8 + u] - v[u];
+              acc[q] = fmaf(tt, tt, acc[q]);
             }
-          }
         }
       } else {
-        for (int c = 0; c < d; ++c) {  // O1 per row: ascending c, no FMA
-          const double xv = (double)__ldg(xj + c);
+        for (int c = 0; c < d; ++c) {
+          const float xv = __ldg(xj + c);
 #pragma unroll
           for (int q = 0; q < kFbQB; ++q) {
-            const double tt = __dsub_rn(s_q[q * d + c], xv);
-            acc[q] = __dadd_rn(acc[q], __dmul_rn(tt, tt));
+            const float tt = s_q32[q * d + c] - xv;
+            acc[q] = fmaf(tt, tt, acc[q]);
           }
         }
       }
     }
 #pragma unroll
     for (int q = 0; q < kFbQB; ++q) {
-      const bool keep = j < j_hi && !(self_join && j == gq[q]) && acc[q] <= ub[q];
+      bool keep = false;
+      double dd = 0.0;
+      // NaN / inf (fp32 overflow) also go to the exact evaluation
+      if (j < j_hi && !(self_join && j == gq[q]) && !(acc[q] > thr[q])) {
+        const float* xi = s_q32 + q * d;
+        double a64 = 0.0;  // O1: ascending c, no FMA
+        for (int c = 0; c < d; ++c) {
+          const double tt = __dsub_rn((double)xi[c], (double)__ldg(xj + c));
+          a64 = __dadd_rn(a64, __dmul_rn(tt, tt));
+        }
+        dd = a64;
+        keep = a64 <= ub[q];
+      }
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (m) {
         int base = 0;
@@ -1647,7 +1752,7 @@ __global__ void __launch_bounds__(kFbThreads)
         base = __shfl_sync(0xffffffffu, base, 0);
         const int pos = base + __popc(m & ((1u << lane) - 1u));
         if (keep && pos < kFbCap) {
-          ck[(int64_t)(f0 + q) * kFbCap + pos] = acc[q];
+          ck[(int64_t)(f0 + q) * kFbCap + pos] = dd;
           ci[(int64_t)(f0 + q) * kFbCap + pos] = (int)j;
         }
       }
@@ -2105,7 +2210,7 @@ cudaError_t launch_fallback(const float* Q, int64_t q_begin, const float* X, int
   if (nfail <= 0) return cudaSuccess;
   if (k > kMaxK) return cudaErrorInvalidValue;
   const int P = fallback_slices(nfail, n, num_sms);
-  const bool thr = nfail <= kFbThrMaxRows && (size_t)kFbQB * d * 8 <= 96 * 1024;
+  const bool thr = nfail <= kFbThrMaxRows && (size_t)kFbQB * d * 4 <= 96 * 1024;
   // workspace: [ck nfail*cap f64][pk nfail*P*k f64][pi nfail*P*k i32][ci nfail*cap i32][done][ccnt]
   double* ck = static_cast<double*>(ws);
   double* pk = ck + (thr ? (size_t)nfail * kFbCap : 0);
@@ -2117,10 +2222,10 @@ cudaError_t launch_fallback(const float* Q, int64_t q_begin, const float* X, int
   if (e != cudaSuccess) return e;
   if (thr) {
     const int qb = (nfail + kFbQB - 1) / kFbQB;
-    int Pt = (2 * num_sms + qb - 1) / qb;
+    int Pt = (4 * num_sms + qb - 1) / qb;
     while (Pt > 1 && n / Pt < 1024) --Pt;
     if (Pt < 1) Pt = 1;
-    const size_t smem = (size_t)kFbQB * d * 8;
+    const size_t smem = (size_t)kFbQB * d * 4;
     e = cudaFuncSetAttribute(k_fb_collect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_fb_collect<<<dim3(qb, Pt), kFbThreads, smem, st>>>(Q, q_begin, X, n, d, self_join ? 1 : 0,

@@ -524,3 +524,14 @@ def test_bf16_second_tier_matches_brute_force_tier(pkg, case, monkeypatch):
     for f in ("idx", "dist", "dist64", "score_kth", "score_mean", "kdist64"):
         assert torch.equal(getattr(res["1"], f), getattr(res["0"], f)), f
     _check_rows(res["1"], X, k, np.arange(0, X.shape[0], X.shape[0] // 8))
+
+
+def test_abod_weighted_golden_on_gpu(pkg, golden_dir):
+    # the non-unit hand golden (tests/golden/abod_clf_examples.json): -2/81, not the
+    # plain-cosine -2/9 (reading A20)
+    import json
+    g = json.load(open(os.path.join(golden_dir, "abod_clf_examples.json")))
+    X = np.array(g["abod_weighted_X"], np.float32)
+    with _ctx(pkg) as ctx:
+        s, _, _ = ctx.abod(torch.from_numpy(X).cuda(), g["abod_weighted_k"])
+    assert _np(s)[0] == np.float32(g["abod_weighted_row0"])

@@ -329,6 +329,18 @@ def test_abod_golden_row0(golden_dir):
     assert s[0] == np.float32(g["abod_row0"])
 
 
+def test_abod_golden_weighted_factor_not_cosine(golden_dir):
+    # non-unit neighbour vectors: the distance-weighted factor (-2/81) and the
+    # plain-cosine reading (-2/9) differ; the oracle must give the former
+    g = _load(golden_dir, "abod_clf_examples.json")
+    X = np.array(g["abod_weighted_X"], np.float32)
+    idx, _ = oracle.knn(X, g["abod_weighted_k"])
+    assert list(idx[0]) == [1, 2, 3]
+    s = oracle.abod_from_knn(X, idx)
+    assert s[0] == np.float32(g["abod_weighted_row0"])
+    assert s[0] != np.float32(g["abod_cosine_reading_row0"])
+
+
 def test_abod_k2_is_zero_and_duplicates_skipped():
     X = datagen.gaussian_mixture(50, 4, seed=3)
     idx, _ = oracle.knn(X, 2)
