@@ -124,10 +124,28 @@ __device__ double lb2_from_key(const CertParams& cp, int64_t r, double w, double
     const double gam = acc_gamma(cp.dpad);
     const double E = (gam * (2.0 * ai * am + 1.002 * amax2) + rep) * (1.0 + 1e-6) + 1e-300;
     const double slack = (cp.d + 8) * 2.0 * u53 * (fabs(a2i) + fabs(w) + E);
+    // (1) with a_j <= a_max:  R^2 = ||xhat_i - xhat_j||^2 = a_i^2 + w_ij >= a_i^2 + w - E
     const double R2 = a2i + w - E - slack;
     *err = E + slack;
-    if (!(R2 > 0.0)) return -1.0;
-    const double Rh = sqrt(R2) * (1.0 - 2.0 * u53);
+    double Rh = R2 > 0.0 ? sqrt(R2) * (1.0 - 2.0 * u53) : 0.0;
+    // (2) with a_j <= a_i + R (triangle inequality), the column's own error term
+    //   E_ij <= gam (3.002 a_i^2 + 4.004 a_i R + 1.002 R^2) + rep
+    // turns R^2 >= a_i^2 + w - E_ij into a quadratic in R:
+    //   (1 + 1.002 gam) R^2 + 4.004 gam a_i R - C >= 0,  C = a_i^2 + w - 3.002 gam a_i^2 - rep,
+    // so R >= 2C / (b + sqrt(b^2 + 4 a C)).  Much tighter than (1) when a_max is far
+    // above a_i + R (outlying rows set a_max); the larger of the two bounds holds.
+    {
+      const double g2 = gam * (1.0 + 1e-6);
+      const double qa = 1.0 + 1.002 * g2;
+      const double qb = 4.004 * g2 * ai;
+      const double C = a2i + w - 3.002 * g2 * a2i * (1.0 + 4.0 * u53) - rep * (1.0 + 1e-6) - slack;
+      if (C > 0.0) {
+        const double Rb = 2.0 * C / (qb + sqrt(qb * qb + 4.0 * qa * C) * (1.0 + 4.0 * u53)) *
+                           (1.0 - 1e-12);
+        Rh = fmax(Rh, Rb);
+      }
+    }
+    if (!(Rh > 0.0)) return -1.0;
     const double LB = (Rh - ei - emax) * (1.0 - 8.0 * u53);
     if (!(LB > 0.0)) return -1.0;
     const double lbo = LB / cp.g->s;  // s = 2^e: exact
