@@ -313,10 +313,21 @@ def run_gpu(args):
     if args.config == "c4" and world > 8:
         raise SystemExit("c4 is defined for up to 8 GPUs")
     qb, qc, mode = _sharding(args.config, n, world, rank)
+    if args.loopback > 1:
+        if world > 1:
+            raise SystemExit("--loopback runs on one GPU")
+        qb, qc, mode = 0, n, "loopback"
     X = datagen.gaussian_mixture(n, d, seed=0)
     stream = torch.cuda.current_stream()
     ctx = tod.Context(device=dev, fmt=fmt, flags=tod.F_TIMING, stream=stream.cuda_stream)
-    if mode == "ring":
+    if mode == "loopback":
+        # the ring schedule of `args.loopback` virtual ranks on this one GPU
+        # (collectives and block transfers become device copies): validates the
+        # multi-GPU path at full size; NOT a multi-GPU throughput
+        ctx.comm_init_loopback(args.loopback)
+        Xl = torch.from_numpy(X).cuda()
+        Xd = None
+    elif mode == "ring":
         r_, w_ = tdist.init_comm(ctx)
         import ctypes
         ver = ctypes.c_int(0)
@@ -335,7 +346,7 @@ def run_gpu(args):
     last = {}
 
     def step():
-        if mode == "ring":
+        if mode in ("ring", "loopback"):
             if lof:
                 _, _, _, st = ctx.lof_sharded(Xl, n, qb, k)
             else:
@@ -386,7 +397,7 @@ def run_gpu(args):
     # ---- e2e: the same step through the C ABI with HOST buffers (pinned): the
     # H2D of this rank's X and the D2H of the scores are inside the timed region
     e2e_ms = []
-    if mode == "ring":
+    if mode in ("ring", "loopback"):
         Xh = torch.from_numpy(X[qb:qb + qc]).pin_memory()
         h2d = qc * d * 4
         d2h = n * 4 * 2
@@ -401,7 +412,7 @@ def run_gpu(args):
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        if mode == "ring":
+        if mode in ("ring", "loopback"):
             if lof:
                 ctx.lof_sharded(Xh, n, qb, k)
             else:
@@ -421,7 +432,7 @@ def run_gpu(args):
         e2e = float(t[0])
 
     # queries answered by the whole job per step
-    if args.config == "c4":
+    if args.config == "c4" and mode != "loopback":
         q_job = sum(tdist.shard_rows(n, 8, r)[1] for r in range(world))
     else:
         q_job = n
@@ -474,6 +485,9 @@ def run_gpu(args):
                        "l2": "flushed between steps (256 MiB write)",
                        "parallelism": ("query-sharded dp%d, reference blocks on an NCCL ring" % world
                                        if mode == "ring" else
+                                       "LOOPBACK: the %d-rank ring schedule run by %d virtual ranks "
+                                       "on 1 GPU (validation, not a multi-GPU number)"
+                                       % (args.loopback, args.loopback) if mode == "loopback" else
                                        "one rank's 1/8 query shard per GPU, references resident"
                                        if mode == "shard8" else "single GPU")},
             "dist_evals_per_s": qps * n,
@@ -532,6 +546,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     ap.add_argument("--ref-step-s", type=float, default=3.0)
+    ap.add_argument("--loopback", type=int, default=0,
+                    help="run the W-rank ring schedule as W virtual ranks on one GPU (validation)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

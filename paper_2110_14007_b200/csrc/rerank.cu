@@ -490,8 +490,6 @@ __device__ __forceinline__ void rerank_groups_row(
   __syncwarp();
   // ---- 1. kappa and UB
   double UB = CUDART_INF;
-  float kappa = CUDART_INF_F;
-  int chi = G;  // staged groups with key <= kappa
   if (G >= k) {
     uint32_t lo = 0xFFFFFFFFu, hi = 0u;
     uint32_t ok[8];  // this lane's ordered keys (G <= 256), 0xFFFFFFFF = none
@@ -516,6 +514,7 @@ __device__ __forceinline__ void rerank_groups_row(
     // 64 ulps of it (relative 2^-17, far below the bound's own slack) saves the
     // last halvings; any hi with count >= k gives a valid UB.
     if (lo < hi) --lo;  // count(key <= lo) < k unless lo is the minimum itself
+    int chi = G;
     for (int it = 0; it < 32 && hi - lo > 64 && chi > k; ++it) {
       const uint32_t mid = lo + ((hi - lo) >> 1);
       int c = 0;
@@ -530,44 +529,32 @@ __device__ __forceinline__ void rerank_groups_row(
         lo = mid;
       }
     }
-    kappa = ord2f(hi);
+    const float kappa = ord2f(hi);
     if (kappa < CUDART_INF_F) UB = ub2_from_key(cp, r, (double)kappa);
   }
-  // ---- 2. expand the groups that can hold a top-k column, 4 groups = 32
-  // columns per step.  Two rounds when the groups at or below kappa fit the
-  // column store: round 1 evaluates exactly those (>= k distinct real columns),
-  // whose k-th smallest exact D64 is itself an upper bound UB1 on the k-th
-  // distance -- tighter than UB from kappa, which carries the pass-1 error on top
-  // of the key -- so round 2 only visits the remaining groups whose lower bound
-  // can reach min(UB, UB1).
+  // ---- 2. expand the groups that can hold a top-k column
+  // (compacted in place into gid[0, nv), then 4 groups = 32 columns per step)
+  int nv = 0;
+  const float kcut = key_cut_from_ub(cp, r, UB);
+  for (int e0 = 0; e0 < G; e0 += 32) {
+    const int e = e0 + lane;
+    bool vis = false;
+    int g = -1;
+    if (e < G) {
+      vis = gk[e] <= kcut;
+      g = gid[e];
+    }
+    const unsigned vm = __ballot_sync(0xffffffffu, vis);
+    if (vis) gid[nv + __popc(vm & ((1u << lane) - 1u))] = g;
+    nv += __popc(vm);
+  }
+  __syncwarp();
   double* ck = s_ck[w];
   int* ci = s_ci[w];
   int nc = 0;
-  int nv = 0;
-  const bool two_round = G >= k && chi <= kColMax / 8 && chi <= kMaxK && kappa < CUDART_INF_F;
-  int* glist = gid;  // groups to expand in the current round
-  auto compact_groups = [&](int* dst, float lo_excl, float hi_incl) {
-    int m = 0;
-    for (int e0 = 0; e0 < G; e0 += 32) {
-      const int e = e0 + lane;
-      bool vis = false;
-      int g = -1;
-      if (e < G) {
-        const float kk = gk[e];
-        vis = kk <= hi_incl && !(kk <= lo_excl);
-        g = gid[e];
-      }
-      const unsigned vm = __ballot_sync(0xffffffffu, vis);
-      if (vis) dst[m + __popc(vm & ((1u << lane) - 1u))] = g;
-      m += __popc(vm);
-    }
-    __syncwarp();
-    return m;
-  };
-  auto expand = [&](const int* gl, int ng, double cut) {
-  for (int b0 = 0; b0 < ng; b0 += 4) {
+  for (int b0 = 0; b0 < nv; b0 += 4) {
     const int gs = b0 + (lane >> 3);
-    const int g = gs < ng ? gl[gs] : -1;
+    const int g = gs < nv ? gid[gs] : -1;
     const int64_t j = (int64_t)g * 8 + (lane & 7);
     double key = CUDART_INF;
     if (g >= 0 && j < n && !(self_join && j == gi)) {
@@ -616,7 +603,7 @@ __device__ __forceinline__ void rerank_groups_row(
       }
       key = acc;
     }
-    const bool keep = key <= cut && key < CUDART_INF;
+    const bool keep = key <= UB && key < CUDART_INF;
     const unsigned km = __ballot_sync(0xffffffffu, keep);
     const int pos = nc + __popc(km & ((1u << lane) - 1u));
     if (keep && pos < kColMax) {
@@ -624,77 +611,6 @@ __device__ __forceinline__ void rerank_groups_row(
       ci[pos] = (int)j;
     }
     nc += __popc(km);
-  }
-  };
-  if (two_round) {
-    // round 1: every column of the chi groups at or below kappa (s_ti as the list)
-    int* l1 = s_ti[w];
-    const int n1 = compact_groups(l1, -CUDART_INF_F, kappa);
-    expand(l1, n1, CUDART_INF);
-    __syncwarp();
-    nv = n1;
-    // UB1: the k-th smallest exact D64 among them (bisection on the bits of
-    // non-negative doubles, stopped within 2^20 ulps: any value with >= k
-    // columns at or below it is a valid bound)
-    if (nc >= k) {
-      unsigned long long blo = ~0ull, bhi = 0ull;
-      for (int e = lane; e < nc; e += 32) {
-        const unsigned long long b = (unsigned long long)__double_as_longlong(ck[e]);
-        blo = min(blo, b);
-        bhi = max(bhi, b);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        blo = min(blo, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)blo, o));
-        bhi = max(bhi, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)bhi, o));
-      }
-      if (blo > 0) --blo;  // count(<= blo) < k unless blo is the minimum itself
-      int cb = nc;
-      for (int it = 0; it < 64 && bhi - blo > (1ull << 20) && cb > k; ++it) {
-        const unsigned long long mid = blo + ((bhi - blo) >> 1);
-        int c = 0;
-        for (int e = lane; e < nc; e += 32)
-          c += (unsigned long long)__double_as_longlong(ck[e]) <= mid;
-        c = __reduce_add_sync(0xffffffffu, c);
-        if (c >= k) {
-          bhi = mid;
-          cb = c;
-        } else {
-          blo = mid;
-        }
-      }
-      UB = fmin(UB, __longlong_as_double((long long)bhi));
-    }
-    // keep the round-1 columns at or below UB (in-place ballot compaction)
-    int m = 0;
-    for (int e0 = 0; e0 < nc; e0 += 32) {
-      const int e = e0 + lane;
-      double kk = 0.0;
-      int ii = 0;
-      bool keep = false;
-      if (e < nc) {
-        kk = ck[e];
-        ii = ci[e];
-        keep = kk <= UB;
-      }
-      const unsigned km = __ballot_sync(0xffffffffu, keep);
-      if (keep) {
-        ck[m + __popc(km & ((1u << lane) - 1u))] = kk;
-        ci[m + __popc(km & ((1u << lane) - 1u))] = ii;
-      }
-      m += __popc(km);
-    }
-    nc = m;
-    __syncwarp();
-    // round 2: groups above kappa whose lower bound can still reach UB
-    const float kcut = key_cut_from_ub(cp, r, UB);
-    const int n2 = compact_groups(glist, kappa, kcut);
-    expand(glist, n2, UB);
-    nv += n2;
-  } else {
-    const float kcut = key_cut_from_ub(cp, r, UB);
-    nv = compact_groups(glist, -CUDART_INF_F, kcut);
-    expand(glist, nv, UB);
   }
   overflow |= nc > kColMax;
   if (nc > kColMax) nc = kColMax;
