@@ -128,7 +128,9 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
     }
     const int kps = std::min(64, std::max(8, roundup((2 * p->kp_target + p->R - 1) / p->R, 4)));
     const double img_bytes = (double)bt256 * 256 * (p->dpad + 16) * 2;
-    p->main_S = std::max(1, (int)std::ceil(img_bytes / (48.0 * 1024 * 1024)));
+    double chunk_mb = 48.0;  // reference chunk of the main pass (L2 locality)
+    if (const char* e = getenv("TOD_MAIN_CHUNK_MB")) chunk_mb = std::max(4.0, atof(e));  // experiment knob
+    p->main_S = std::max(1, (int)std::ceil(img_bytes / (chunk_mb * 1024 * 1024)));
     p->cap = roundup(std::max(64, 2 * (p->R - 1) * kps), 32);
     bt_v1 = (bt256 + p->R - 1) / p->R;
   }
