@@ -209,6 +209,24 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
 
 
 
+// Main-pass filter: test each part's minimum with a warp vote first when appends
+// are rare.  A row appends ~2K' groups over 4 n/256 (row, part) cells; below
+// n ~ 3e5 most warps hold a candidate in most parts and the vote only adds work
+// (measured: C2 main kernel 1.13 -> 1.21 ms with the vote, C3 no slower).
+// TOD_VOTE (experiment knob) forces it on (1) or off (0).
+int main_vote(int64_t n_ref) {
+  if (const char* e = getenv("TOD_VOTE")) return atoi(e) != 0;
+  return n_ref >= 300000;
+}
+// Staggered sweep start per CTA (TileSeq); TOD_STAGGER=1 (experiment knob)
+// enables it.  Off by default: measured no faster at C2/C3/C5 (CTAs sweeping a
+// chunk in lockstep share its tiles in L2), and the MMA-only pipeline at C2 was
+// 12 % slower staggered.
+int main_stagger() {
+  if (const char* e = getenv("TOD_STAGGER")) return atoi(e) != 0;
+  return 0;
+}
+
 // Input quantization (a1) for the tensor-core passes: column mean, power-of-two
 // scale, reference image B over all n rows (skipped when ref->ready) and query
 // image A over the 128-row query tiles covering [q_begin, q_begin+q_count)
@@ -263,8 +281,12 @@ tod_status prep_tc(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     }
     TOD_CUDA(launch_prep_scale(g, fmt, dpad, st, launches));
     TOD_CUDA(launch_prep_quant(dX, n, d, mu, g, fmt, B, 0, st, launches));
+    TOD_TRY(ensure(ctx, B_EG, (size_t)std::max<int64_t>((n + 7) / 8, 1) * 8, &p));
+    TOD_CUDA(launch_group_emax(B.e, n, static_cast<double*>(p), st, launches));
     ref->ready = true;
   }
+  TOD_TRY(ensure(ctx, B_EG, (size_t)std::max<int64_t>((n + 7) / 8, 1) * 8, &p));
+  cp->eg = static_cast<const double*>(p);
   const float* qsrc = self ? dX + a_row0 * d : dQ;
   TOD_CUDA(launch_prep_quant(qsrc, a_rows, d, mu, g, fmt, A, 1, st, launches));
   cp->qa2 = A.a2 + (self ? q_begin - a_row0 : 0);
@@ -352,6 +374,7 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
       MainPass sm;
       sm.S = 1;
       sm.R = plan.R;
+      sm.stagger = main_stagger();
       sm.parts = tc3_parts(plan.dpad);
       // tau = the j-th smallest sample minimum, j ~ 2K'/R; 8 per (row, part) when
       // 4 per part cannot supply j (large k)
@@ -377,6 +400,9 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
       mp.tau_lists = cands.lists;
       mp.parts = tc3_parts(plan.dpad);
       mp.cap = plan.cap * 2 / mp.parts;  // plan.cap is per column half
+      mp.vote = main_vote(n);
+      mp.stagger = main_stagger();
+      mp.trace = cands.trace;
       TOD_TRY(ensure(ctx, B_MBUF, (size_t)std::max<int64_t>(q_count, 1) * mp.parts * mp.cap * 8, &p));
       mp.buf = static_cast<uint2*>(p);
       TOD_TRY(ensure(ctx, B_MCNT, (size_t)std::max<int64_t>(q_count, 1) * mp.parts * 4, &p));

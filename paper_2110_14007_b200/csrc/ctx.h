@@ -34,7 +34,7 @@ enum BufId {
   B_G, B_CIDX, B_CV, B_FAIL, B_SMALL, B_IDX, B_DIST, B_DIST64, B_KTH, B_MEAN, B_KD64,
   B_LRD64, B_LOF, B_LRD32, B_KDALL, B_STLIST, B_STDONE, B_FBPART, B_CKEY, B_TRACE, B_MBUF, B_MCNT,
   B_FAILUB, B_NWRTAU, B_NWRCNT, B_NWRPTR, B_NWRCOLS, B_SCAN, B_ABOD, B_LABELS, B_PRED, B_SAMP,
-  B_NWRBLK, B_NWRTASK, B_RRWS, B_T2ROWS, B_T2Q, B_T2IDX, B_T2D64, B_TIER,
+  B_NWRBLK, B_NWRTASK, B_RRWS, B_T2ROWS, B_T2Q, B_T2IDX, B_T2D64, B_TIER, B_EG,
   // sharded path (shard.cu)
   B_XALL, B_XSEND, B_XSLOT, B_SHTAB, B_PARTALL, B_GATHER, B_GATHER2,
   B_NBUF
@@ -100,6 +100,8 @@ struct Plan {
   int cap;       // two-pass: main-pass buffer slots per (row, column half)
 };
 tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k, Plan* p);
+int main_vote(int64_t n_ref);   // main-pass filter: part-minimum vote first (rare appends)
+int main_stagger();             // staggered per-CTA sweep start of each chunk
 
 struct Timer {
   tod_ctx* ctx;

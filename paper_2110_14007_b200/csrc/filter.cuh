@@ -1,0 +1,103 @@
+// filter.cuh — the append-only threshold filter of the two-pass main pass
+// (DESIGN.md §5 "Two-pass candidate selection"; operator fusion of cdist and
+// topk), shared by the single-SM (knn_tc3.cu) and CTA-pair
+// (knn_tc4.cu) kernels.
+//
+// One filter warp owns 32 query rows (its TMEM lane quarter) and a part of
+// BH columns of every tile.  Each 8-column group's minimum w~ that is below the
+// row's threshold tau is appended, as (key, group index), to the lane's pending
+// run in shared memory.  Appends are rare (C3: ~0.7 % of the (row, 64-column
+// part) pairs), so the part minimum is tested first with one warp vote and the
+// per-group compares run only when some lane of the warp has a candidate.
+#pragma once
+#include "ptx.cuh"
+
+namespace tod {
+
+constexpr int kPendRun = 16;          // pending slots per lane (flush checked every 8 groups)
+constexpr uint32_t kPendSlot = 32 * 8;  // bytes between a lane's consecutive pending slots
+
+__device__ __forceinline__ float min8(const float* v) {
+  return fminf(fminf(fminf(v[0], v[1]), v[2]),
+               fminf(fminf(v[3], v[4]), fminf(fminf(v[5], v[6]), v[7])));
+}
+
+// v: this lane's BH accumulators of the tile (masked); gbase: global index of
+// the part's first group.  `flush` moves the pending run to HBM.
+// vote: test the part minimum first (worth it when appends are rare: large n;
+// at n = 1e5 most warps hold a candidate in most parts and the test only adds work).
+template <int BH, class Flush>
+__device__ __forceinline__ void filter_part(const float* v, float tau, int gbase, uint32_t& pa,
+                                            uint32_t pbase, bool vote, Flush&& flush) {
+  float m[BH / 8];
+#pragma unroll
+  for (int g = 0; g < BH / 8; ++g) m[g] = min8(v + 8 * g);
+  if (vote) {
+    float pm = m[0];
+#pragma unroll
+    for (int g = 1; g + 1 < BH / 8; g += 2) pm = fminf(pm, fminf(m[g], m[g + 1]));
+    if constexpr ((BH / 8) % 2 == 0) pm = fminf(pm, m[BH / 8 - 1]);
+    if (!__any_sync(0xffffffffu, pm < tau)) return;
+  }
+#pragma unroll
+  for (int hh = 0; hh < BH / 64; ++hh) {
+    if (__any_sync(0xffffffffu, pa > pbase + (kPendRun - 8) * kPendSlot)) flush();
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      const int gg = hh * 8 + g;
+      if (m[gg] < tau) {
+        sts_kv(pa, m[gg], gbase + gg);
+        pa += kPendSlot;
+      }
+    }
+  }
+}
+
+// Tiles of reference chunk c of S: [bt*c/S, bt*(c+1)/S), minus the sample tiles
+// (t % R == 0; R a power of two, 0 = none) when SKIP; the sample pass (SMP)
+// visits only the sample tiles t = si*R, si in [bs*c/S, bs*(c+1)/S).  The
+// sweep starts at a per-CTA rotation of the chunk (rot = cta * len / ncta):
+// CTAs that sweep one L2-resident chunk at the same time would otherwise
+// request the same reference tile together.
+template <int SMP, int SKIP>
+struct TileSeq {
+  int b, len, i, rot, t, R, mask;
+  bool on;
+  __device__ __forceinline__ void begin(int64_t bt, int S, int R_, int c, int64_t cta, int64_t ncta,
+                                        int stagger) {
+    R = R_;
+    on = SKIP && R > 0;
+    mask = R - 1;
+    if constexpr (SMP) {
+      const int64_t bs = (bt + R - 1) / R;
+      b = (int)(bs * c / S);
+      len = (int)(bs * (c + 1) / S) - b;
+    } else {
+      b = (int)(bt * c / S);
+      len = (int)(bt * (c + 1) / S) - b;
+    }
+    rot = (stagger && len > 0) ? (int)(cta * len / ncta) : 0;
+    i = 0;
+    at();
+    skip();
+  }
+  __device__ __forceinline__ void at() {
+    int k = i + rot;
+    if (k >= len) k -= len;
+    t = SMP ? (b + k) * R : b + k;
+  }
+  __device__ __forceinline__ void skip() {
+    while (on && i < len && (t & mask) == 0) {
+      ++i;
+      at();
+    }
+  }
+  __device__ __forceinline__ bool more() const { return i < len; }
+  __device__ __forceinline__ void next() {
+    ++i;
+    at();
+    skip();
+  }
+};
+
+}  // namespace tod

@@ -72,6 +72,8 @@ cudaError_t launch_prep_colsum(const float* X, int64_t n, int d, double* partial
 cudaError_t launch_prep_colmean(const double* partial, int blocks, int64_t n, int d, double* mu,
                                 cudaStream_t st, int* launches);
 int prep_stat_rows();  // rows per column-sum partial block (128)
+// eg[g] = max of e[8g .. 8g+7] (rows < n): per-group residual bound for the re-rank
+cudaError_t launch_group_emax(const double* e, int64_t n, double* eg, cudaStream_t st, int* launches);
 cudaError_t launch_image_decode(const Image& img, int fmt, int64_t rows, float* out, cudaStream_t st,
                                 int* launches);  // diagnostics: 16-bit image -> fp32 [rows][dpad+16]
 cudaError_t launch_finite_check(const float* X, int64_t n, int d, PrepGlobals* g, cudaStream_t st,
@@ -103,6 +105,9 @@ struct MainPass {
   int samp_t = 4;             // 4 or 8
   int samp_acc = 0;           // sample mode: merge into the minima already in samp (ring of blocks)
   int64_t col0 = 0;           // global index of reference row 0 of the image (a ring block; % 256 == 0)
+  int vote = 0;               // filter: test each part's minimum with one warp vote first (rare appends)
+  int stagger = 1;            // CTAs start their sweep of a chunk at staggered tiles (L2 spread)
+  long long* trace = nullptr; // profiling (TOD_F_DEBUG_TRACE): CTA 0's per-tile clock64 stamps
 };
 cudaError_t launch_tau_combine(int64_t q, int nv, int j, const float* samp, float* tau,
                                cudaStream_t st, int* launches);
@@ -131,6 +136,7 @@ struct CertParams {
   const PrepGlobals* g;  // device: amax2, emax (tensor path)
   const double* qa2;     // query ||xhat||^2 (tensor path)
   const double* qe;      // query residual bound (tensor path)
+  const double* eg;      // per 8-row reference group: max residual bound (nullable: emax)
   int force_fail;        // TOD_F_NO_CERTIFY
 };
 struct KnnOutDev {

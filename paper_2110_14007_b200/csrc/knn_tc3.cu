@@ -35,6 +35,7 @@
 
 #include "internal.h"
 #include "ptx.cuh"
+#include "filter.cuh"
 
 namespace tod {
 
@@ -46,7 +47,6 @@ static_assert(kBN == 256, "filter addresses accumulators as acc << 8");
 constexpr int kExtraRB = 32;
 constexpr int kSmemMax = 232448;
 constexpr int kMaxStage = 4;
-constexpr int kPend = 16;       // pending slots per row (checks every 8 groups)
 
 __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
 
@@ -79,7 +79,7 @@ __host__ __device__ constexpr int smem3(int nstage, int* off_b, int* off_p, int*
   *off_b = o;
   o += nstage * (C::KP ? C::KS_BYTES : C::B_STRIDE);
   *off_p = o;
-  o += FW * kPend * 32 * 8;
+  o += FW * kPendRun * 32 * 8;
   *off_bar = o;
   o += 8 * (2 * kMaxStage + 2 + 4) + 16;
   return o + 1024;
@@ -93,50 +93,6 @@ int pick_stages3() {
   return 0;
 }
 
-// Tiles of chunk c: [bt*c/S, bt*(c+1)/S) minus the sample tiles (t % R == 0;
-// R is a power of two, 0 = no sample pass).
-// SMP (sample pass): chunk c covers sample tiles t = si*R, si in [bs*c/S, bs*(c+1)/S).
-template <int SMP, int SKIP = 1>
-struct Seq {
-  int t, end;
-  int mask;
-  int R;
-  bool on;
-  __device__ __forceinline__ void begin(int64_t bt, int S, int R_, int c) {
-    R = R_;
-    if constexpr (SMP) {
-      const int64_t bs = (bt + R - 1) / R;
-      t = (int)(bs * c / S) * R;
-      end = (int)(bs * (c + 1) / S) * R;
-      if (end > bt) end = (int)bt;
-      return;
-    }
-    on = R > 0;
-    mask = R - 1;
-    t = (int)(bt * c / S);
-    end = (int)(bt * (c + 1) / S);
-    skip();
-  }
-  __device__ __forceinline__ void skip() {
-    if constexpr (SKIP)
-      if (on && (t & mask) == 0) ++t;
-  }
-  __device__ __forceinline__ bool more() const { return t < end; }
-  __device__ __forceinline__ void next() {
-    if constexpr (SMP) {
-      t += R;
-      return;
-    }
-    ++t;
-    skip();
-  }
-};
-
-__device__ __forceinline__ float min8(const float* v) {
-  return fminf(fminf(fminf(v[0], v[1]), v[2]),
-               fminf(fminf(v[3], v[4]), fminf(fminf(v[5], v[6]), v[7])));
-}
-
 // MODE: 0 = main pass over every tile, 1 = main pass skipping the sample tiles
 // (t % R == 0), 4 / 8 = sample pass keeping that many minima per (row, part).
 template <int DPAD, int FMT, int DBG, int FW, int MODE>
@@ -147,7 +103,14 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
               int self_join, int S, int R, int nstage,
               const float* __restrict__ tau_v, int tau_lists,
               uint2* __restrict__ mbuf, int* __restrict__ mcnt, int cap,
-              float* __restrict__ samp, int64_t col0, int samp_acc) {
+              float* __restrict__ samp, int64_t col0, int samp_acc, int vote, int stagger,
+              long long* __restrict__ trace) {
+  // trace (profiling): CTA 0, per tile in sweep order, [8] clock64 stamps:
+  // 0 MMA: before the B-tile wait, 1 after it, 2 after the accumulator wait;
+  // 3 filter warp 2: before the t_full wait, 4 after it, 5 accumulator released,
+  // 6 filter done; 7 producer: B-tile copy issued.
+  constexpr int kTraceTiles = 4096;
+  const bool tron = trace != nullptr && blockIdx.x == 0;
   using C = Cfg3<DPAD>;
   constexpr int SMP = MODE >= 4 ? MODE : 0;
   constexpr int SKIP = MODE == 1 ? 1 : 0;
@@ -199,8 +162,8 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t qtl = item % n_qtiles;
       const int c = (int)(item / n_qtiles);
-      Seq<SMP, SKIP> ts;
-      ts.begin(b_tiles, S, R, c);
+      TileSeq<SMP, SKIP> ts;
+      ts.begin(b_tiles, S, R, c, blockIdx.x, gridDim.x, stagger);
       for (; ts.more(); ts.next()) {
         const int64_t t = ts.t;
         for (int kb = 0; kb <= C::NKB; ++kb) {
@@ -236,8 +199,8 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
     uint32_t phase = 0, acc_phase = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int c = (int)(item / n_qtiles);
-      Seq<SMP, SKIP> ts;
-      ts.begin(b_tiles, S, R, c);
+      TileSeq<SMP, SKIP> ts;
+      ts.begin(b_tiles, S, R, c, blockIdx.x, gridDim.x, stagger);
       for (; ts.more(); ts.next()) {
         mbar_wait(&t_empty[acc], acc_phase ^ 1);
         for (int kb = 0; kb <= C::NKB; ++kb) {
@@ -274,11 +237,12 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
     // -------------------------------------------------------------- producer
     int stage = 0;
     uint32_t phase = 0, aphase = 0;
+    int ptr = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t qtl = item % n_qtiles;
       const int c = (int)(item / n_qtiles);
-      Seq<SMP, SKIP> ts;
-      ts.begin(b_tiles, S, R, c);
+      TileSeq<SMP, SKIP> ts;
+      ts.begin(b_tiles, S, R, c, blockIdx.x, gridDim.x, stagger);
       int issued = 0;
       bool a_done = false;
       auto load_a = [&]() {
@@ -299,6 +263,8 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
         // the item's first B tiles are fetched while the MMA drains the previous item
         if (!a_done && issued == nstage - 1) load_a();
         mbar_wait_backoff(&empty[stage], phase ^ 1);
+        if (tron && lane == 0 && ptr < kTraceTiles) trace[ptr * 8 + 7] = clock64();
+        ++ptr;
         if (elect_one()) {
           mbar_arrive_expect_tx(&full[stage], C::B_BYTES);
           uint8_t* dst = sB + stage * C::B_STRIDE;
@@ -336,16 +302,22 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
     bdesc[C::KSTEPS] = smem_desc(b_base + C::B_EXTRA, 8 * kExtraRB, 6);
     int stage = 0, acc = 0;
     uint32_t phase = 0, acc_phase = 0, aphase = 0;
+    int mtr = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int c = (int)(item / n_qtiles);
-      Seq<SMP, SKIP> ts;
-      ts.begin(b_tiles, S, R, c);
+      TileSeq<SMP, SKIP> ts;
+      ts.begin(b_tiles, S, R, c, blockIdx.x, gridDim.x, stagger);
       mbar_wait(a_full, aphase);
       aphase ^= 1;
       tc_fence_after();
       for (; ts.more(); ts.next()) {
+        const bool tr = tron && lane == 0 && mtr < kTraceTiles;
+        if (tr) trace[mtr * 8 + 0] = clock64();
         mbar_wait(&full[stage], phase);
+        if (tr) trace[mtr * 8 + 1] = clock64();
         mbar_wait(&t_empty[acc], acc_phase ^ 1);
+        if (tr) trace[mtr * 8 + 2] = clock64();
+        ++mtr;
         tc_fence_after();
         const uint64_t bst = (uint64_t)((stage * C::B_STRIDE) >> 4);
         if (elect_one()) {
@@ -374,11 +346,12 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
     const int q = warp & 3;           // TMEM lane quarter
     const int h = f >> 2;             // column part of every tile
     const int rt = q * 32 + lane;     // row within the query tile
-    constexpr uint32_t SLOT = 32 * 8;
-    const uint32_t pbase = s_pend + (f * kPend * 32 + lane) * 8;
+    constexpr uint32_t SLOT = kPendSlot;
+    const uint32_t pbase = s_pend + (f * kPendRun * 32 + lane) * 8;
     uint32_t pa = pbase;
     uint32_t tcount = 0;  // tiles consumed: accumulator = tcount & 1, phase = (tcount >> 1) & 1
     const uint32_t taddr0 = tmem_base + ((uint32_t)(q * 32) << 16) + h * BH;
+    const uint32_t s_tfull = smem_u32(t_full), s_tempty = smem_u32(t_empty);
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t qtl = item % n_qtiles;
       const int c = (int)(item / n_qtiles);
@@ -419,11 +392,15 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
 #pragma unroll
       for (int i = 0; i < T; ++i)  // a ring of blocks accumulates over launches
         top[i] = (SMP && samp_acc && valid) ? samp[(r * H + h) * T + i] : CUDART_INF_F;
-      Seq<SMP, SKIP> ts;
-      ts.begin(b_tiles, S, R, c);
+      TileSeq<SMP, SKIP> ts;
+      ts.begin(b_tiles, S, R, c, blockIdx.x, gridDim.x, stagger);
       for (; ts.more(); ts.next()) {
         const uint32_t acc = tcount & 1u;
-        mbar_wait(&t_full[acc], (tcount >> 1) & 1u);
+        const int etr = (int)tcount;
+        const bool tr = tron && warp == 2 && lane == 0 && etr < kTraceTiles;
+        if (tr) trace[etr * 8 + 3] = clock64();
+        mbar_wait_u32(s_tfull + acc * 8, (tcount >> 1) & 1u);
+        if (tr) trace[etr * 8 + 4] = clock64();
         tc_fence_after();
         float v[BH];
         const uint32_t taddr = taddr0 + (acc << 8);  // acc * kBN
@@ -435,7 +412,8 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&t_empty[acc]);
+        if (lane == 0) mbar_arrive_u32(s_tempty + acc * 8);
+        if (tr) trace[etr * 8 + 5] = clock64();
         ++tcount;
         if (DBG & 3) continue;  // profiling: pipeline without the filter work
         const int t = ts.t;
@@ -458,11 +436,10 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
           for (int e = 0; e < BH; ++e)
             v[e] = (scol0 + j0 + e == self || j0 + e >= n_ref) ? CUDART_INF_F : v[e];
         }
-        // independent min trees first (full ILP), then the appends
-        float m[BH / 8];
-#pragma unroll
-        for (int g = 0; g < BH / 8; ++g) m[g] = min8(v + 8 * g);
         if constexpr (SMP) {
+          float m[BH / 8];
+#pragma unroll
+          for (int g = 0; g < BH / 8; ++g) m[g] = min8(v + 8 * g);
           // sample pass: the T smallest group minima of this (row, part), keys
           // only, by a branch-free insertion network (new_i = min(r_i, max(r_i-1, x)))
 #pragma unroll
@@ -474,19 +451,8 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
           }
           continue;
         }
-        const int gbase = (scol0 + j0) >> 3;  // global group index (col0 % 256 == 0)
-#pragma unroll
-        for (int hh = 0; hh < BH / 64; ++hh) {
-          if (__any_sync(0xffffffffu, pa > pbase + (kPend - 8) * SLOT)) flush();
-#pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            const int gg = hh * 8 + g;
-            if (m[gg] < tau) {
-              sts_kv(pa, m[gg], gbase + gg);
-              pa += SLOT;
-            }
-          }
-        }
+        filter_part<BH>(v, tau, (scol0 + j0) >> 3, pa, pbase, vote != 0, flush);  // col0 % 256 == 0
+        if (tr) trace[etr * 8 + 6] = clock64();
       }
       if constexpr (SMP) {
         if (valid) {
@@ -526,7 +492,8 @@ cudaError_t launch3(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
       reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(), A.extra_offset(),
       reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
       (B.n + kBN - 1) / kBN, B.n, qt0, qt1 - qt0, q_begin, q_begin + q_count, self_join ? 1 : 0, m.S,
-      m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap, m.samp, m.col0, m.samp_acc);
+      m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap, m.samp, m.col0, m.samp_acc, m.vote,
+      m.stagger, m.trace);
   return cudaGetLastError();
 }
 

@@ -27,6 +27,7 @@
 
 #include "internal.h"
 #include "ptx.cuh"
+#include "filter.cuh"
 
 namespace tod {
 
@@ -39,7 +40,6 @@ constexpr int kBNH = 128;       // reference rows of each tile staged per CTA
 constexpr int kExtraRB = 32;
 constexpr int kSmemMax = 232448;
 constexpr int kMaxStage = 6;
-constexpr int kPend = 16;
 
 __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
 
@@ -65,7 +65,7 @@ __host__ __device__ constexpr int smem4(int nstage, int* off_b, int* off_p, int*
   *off_b = o;
   o += nstage * C::B_STRIDE;
   *off_p = o;
-  o += FW * kPend * 32 * 8;
+  o += FW * kPendRun * 32 * 8;
   *off_bar = o;
   o += 8 * (2 * kMaxStage + 2 + 4) + 16;
   return o + 1024;
@@ -79,32 +79,6 @@ int pick_stages4() {
   return 0;
 }
 
-struct Seq {
-  int t, end;
-  int mask;
-  bool on;
-  __device__ __forceinline__ void begin(int64_t bt, int S, int R, int c) {
-    on = R > 0;
-    mask = R - 1;
-    t = (int)(bt * c / S);
-    end = (int)(bt * (c + 1) / S);
-    skip();
-  }
-  __device__ __forceinline__ void skip() {
-    if (on && (t & mask) == 0) ++t;
-  }
-  __device__ __forceinline__ bool more() const { return t < end; }
-  __device__ __forceinline__ void next() {
-    ++t;
-    skip();
-  }
-};
-
-__device__ __forceinline__ float min8(const float* v) {
-  return fminf(fminf(fminf(v[0], v[1]), v[2]),
-               fminf(fminf(v[3], v[4]), fminf(fminf(v[5], v[6]), v[7])));
-}
-
 template <int DPAD, int FMT, int DBG, int FW>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
     k_knn_tc4(const uint8_t* __restrict__ a_img, size_t a_region, size_t a_extra,
@@ -112,7 +86,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
               int64_t n_ref, int64_t qt0, int64_t n_qpairs, int64_t q_begin, int64_t q_end,
               int self_join, int S, int R, int nstage,
               const float* __restrict__ tau_v, int tau_lists,
-              uint2* __restrict__ mbuf, int* __restrict__ mcnt, int cap, int64_t col0) {
+              uint2* __restrict__ mbuf, int* __restrict__ mcnt, int cap, int64_t col0, int vote,
+              int stagger) {
   using C = Cfg4<DPAD>;
   constexpr int H = FW / 4;
   constexpr int BH = kBN / H;
@@ -167,8 +142,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
     for (int64_t item = cid; item < n_items; item += ncl) {
       const int64_t qtl = (item % n_qpairs) * 2 + rank;
       const int c = (int)(item / n_qpairs);
-      Seq ts;
-      ts.begin(b_tiles, S, R, c);
+      TileSeq<0, 1> ts;
+      ts.begin(b_tiles, S, R, c, cid, ncl, stagger);
       int issued = 0;
       bool a_done = false;
       auto load_a = [&]() {
@@ -227,8 +202,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
     uint32_t phase = 0, acc_phase = 0, aphase = 0;
     for (int64_t item = cid; item < n_items; item += ncl) {
       const int c = (int)(item / n_qpairs);
-      Seq ts;
-      ts.begin(b_tiles, S, R, c);
+      TileSeq<0, 1> ts;
+      ts.begin(b_tiles, S, R, c, cid, ncl, stagger);
       mbar_wait_cl(a_full, aphase);
       aphase ^= 1;
       tc_fence_after();
@@ -266,8 +241,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
     uint32_t phase = 0, aphase = 0;
     for (int64_t item = cid; item < n_items; item += ncl) {
       const int c = (int)(item / n_qpairs);
-      Seq ts;
-      ts.begin(b_tiles, S, R, c);
+      TileSeq<0, 1> ts;
+      ts.begin(b_tiles, S, R, c, cid, ncl, stagger);
       // the producer may issue up to nstage-1 B tiles before the A tile: the
       // forwarder must not block on A first (the leader needs those B tiles
       // to finish the previous item, which releases A)
@@ -302,12 +277,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
     const int q = warp & 3;
     const int h = f >> 2;
     const int rt = q * 32 + lane;
-    constexpr uint32_t SLOT = 32 * 8;
-    const uint32_t pbase = s_pend + (f * kPend * 32 + lane) * 8;
+    constexpr uint32_t SLOT = kPendSlot;
+    const uint32_t pbase = s_pend + (f * kPendRun * 32 + lane) * 8;
     uint32_t pa = pbase;
     uint32_t tcount = 0;  // tiles consumed: accumulator = tcount & 1, phase = (tcount >> 1) & 1
     const uint32_t taddr0 = tmem_base + ((uint32_t)(q * 32) << 16) + h * BH;
     const uint32_t r_tempty = mapa_shared(smem_u32(t_empty), 0);
+    const uint32_t s_tfull = smem_u32(t_full), s_tempty = smem_u32(t_empty);
     for (int64_t item = cid; item < n_items; item += ncl) {
       const int64_t qtl = (item % n_qpairs) * 2 + rank;
       const int c = (int)(item / n_qpairs);
@@ -340,11 +316,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
         }
         pa = pbase;
       };
-      Seq ts;
-      ts.begin(b_tiles, S, R, c);
+      TileSeq<0, 1> ts;
+      ts.begin(b_tiles, S, R, c, cid, ncl, stagger);
       for (; ts.more(); ts.next()) {
         const uint32_t acc = tcount & 1u;
-        mbar_wait_cl(&t_full[acc], (tcount >> 1) & 1u);
+        mbar_wait_u32(s_tfull + acc * 8, (tcount >> 1) & 1u);
         tc_fence_after();
         float v[BH];
         const uint32_t taddr = taddr0 + (acc << 8);  // acc * kBN
@@ -357,7 +333,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if (leader) mbar_arrive(&t_empty[acc]);
+          if (leader) mbar_arrive_u32(s_tempty + acc * 8);
           else mbar_arrive_cluster(r_tempty + acc * 8);
         }
         ++tcount;
@@ -379,22 +355,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
           for (int e = 0; e < BH; ++e)
             v[e] = (scol0 + j0 + e == self || j0 + e >= n_ref) ? CUDART_INF_F : v[e];
         }
-        float m[BH / 8];
-#pragma unroll
-        for (int g = 0; g < BH / 8; ++g) m[g] = min8(v + 8 * g);
-        const int gbase = (scol0 + j0) >> 3;  // global group index (col0 % 256 == 0)
-#pragma unroll
-        for (int hh = 0; hh < BH / 64; ++hh) {
-          if (__any_sync(0xffffffffu, pa > pbase + (kPend - 8) * SLOT)) flush();
-#pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            const int gg = hh * 8 + g;
-            if (m[gg] < tau) {
-              sts_kv(pa, m[gg], gbase + gg);
-              pa += SLOT;
-            }
-          }
-        }
+        filter_part<BH>(v, tau, (scol0 + j0) >> 3, pa, pbase, vote != 0, flush);  // col0 % 256 == 0
       }
       flush();
     }
@@ -428,7 +389,7 @@ cudaError_t launch4(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
       reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(), A.extra_offset(),
       reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
       (B.n + kBN - 1) / kBN, B.n, qt0, n_qpairs, q_begin, q_begin + q_count, self_join ? 1 : 0, m.S,
-      m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap, m.col0);
+      m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap, m.col0, m.vote, m.stagger);
   return cudaGetLastError();
 }
 

@@ -386,4 +386,29 @@ cudaError_t launch_prep_quant(const float* X, int64_t n, int d, const double* mu
   return cudaGetLastError();
 }
 
+// Per 8-row group of the reference image: e_g = max residual bound of its rows
+// (rows >= n count 0).  The re-rank bounds a group's columns with e_g instead of
+// the global e_max (DESIGN.md §5 "Re-rank"): the triangle inequality only needs
+// e_j <= e_g for the columns j of the group.
+__global__ void k_group_emax(const double* __restrict__ e, int64_t n, int64_t ngroups,
+                             double* __restrict__ eg) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ngroups) return;
+  double m = 0.0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int64_t j = g * 8 + u;
+    if (j < n) m = fmax(m, e[j]);
+  }
+  eg[g] = m;
+}
+
+cudaError_t launch_group_emax(const double* e, int64_t n, double* eg, cudaStream_t st, int* launches) {
+  const int64_t ng = (n + 7) / 8;
+  if (ng <= 0) return cudaSuccess;
+  k_group_emax<<<(unsigned)((ng + 255) / 256), 256, 0, st>>>(e, n, ng, eg);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
 }  // namespace tod

@@ -238,55 +238,66 @@ __global__ void __launch_bounds__(kRerankWarps * 32)
 // group's minimum is >= v), so the same certificate applies.
 constexpr int kGrpWarps = 4;
 
-// Upper bound, in original units, on the exact squared distance D64 of row r to
-// the best column of a group whose pass-1 key is w (the group's minimum w~):
-// that column has w_ij <= w + E_i, so ||xhat_i - xhat_j||^2 <= a_i^2 + w + E_i,
-// and the residuals e_i, e_j <= emax bound the exact distance from above.
-// (Mirror image of lb2_from_key; tensor-core pass only.)
-__device__ double ub2_from_key(const CertParams& cp, int64_t r, double w) {
+// Per-row terms of the pass-1 bounds (tensor-core pass): a_i^2, e_i and the
+// accumulation error E_i = gamma (2 a_i a_max + 1.002 a_max^2) + rep (lb2_from_key).
+struct RowBound {
+  double a2i, ei, E;
+};
+__device__ __forceinline__ RowBound row_bound(const CertParams& cp, int64_t r) {
   const double u53 = 1.1102230246251565e-16;
-  const double a2i = cp.qa2[r];
-  const double ei = cp.qe[r];
+  RowBound b;
+  b.a2i = cp.qa2[r];
+  b.ei = cp.qe[r];
   const double amax2 = cp.g->amax2;
-  const double emax = cp.g->emax;
-  const double rep = cp.g->repmax;
-  const double ai = sqrt(a2i) * (1.0 + 4 * u53);
+  const double ai = sqrt(b.a2i) * (1.0 + 4 * u53);
   const double am = sqrt(amax2) * (1.0 + 4 * u53);
-  const double gam = acc_gamma(cp.dpad);
-  const double E = (gam * (2.0 * ai * am + 1.002 * amax2) + rep) * (1.0 + 1e-6) + 1e-300;
-  const double slack = (cp.d + 8) * 2.0 * u53 * (fabs(a2i) + fabs(w) + E);
-  double R2 = a2i + w + E + slack;
+  b.E = (acc_gamma(cp.dpad) * (2.0 * ai * am + 1.002 * amax2) + cp.g->repmax) * (1.0 + 1e-6) + 1e-300;
+  return b;
+}
+
+// Upper bound, in original units, on the exact squared distance D64 of row r
+// to the best column of a group whose pass-1 key is w (the group's minimum w~)
+// and whose rows have residual bounds <= ej: that column has w_ij <= w + E_i, so
+// ||xhat_i - xhat_j||^2 <= a_i^2 + w + E_i, and the residuals e_i, e_j bound the
+// exact distance from above.  (Mirror image of lb2_from_key; tensor-core pass only.)
+__device__ double ub2_key_e(const CertParams& cp, const RowBound& b, double w, double ej) {
+  const double u53 = 1.1102230246251565e-16;
+  const double slack = (cp.d + 8) * 2.0 * u53 * (fabs(b.a2i) + fabs(w) + b.E);
+  double R2 = b.a2i + w + b.E + slack;
   if (!(R2 > 0.0)) R2 = 0.0;
   const double Rh = sqrt(R2) * (1.0 + 2.0 * u53);
-  const double UB = (Rh + ei + emax) * (1.0 + 8.0 * u53);
+  const double UB = (Rh + b.ei + ej) * (1.0 + 8.0 * u53);
   const double ubo = UB / cp.g->s;  // s = 2^e: exact
   return ubo * ubo * (1.0 + 8.0 * u53) * (1.0 + gamma_up(cp.d + 2, u53));
 }
+__device__ double ub2_from_key(const CertParams& cp, int64_t r, double w) {
+  return ub2_key_e(cp, row_bound(cp, r), w, cp.g->emax);
+}
 
-// Largest pass-1 key w (rounded up to fp32) for which lb2_from_key(w)(1-gamma)
-// could still be <= UB: lb2_from_key is increasing in w, so inverting it with
-// every rounding pushed upward gives a cutoff above which a group provably holds
-// no column at distance <= UB.  (A larger cutoff only visits more groups.)
-__device__ float key_cut_from_ub(const CertParams& cp, int64_t r, double UB) {
-  if (!(UB < CUDART_INF)) return CUDART_INF_F;
+// Key cut (DESIGN.md §5 "Re-rank"): the largest pass-1 key w (rounded up to
+// fp32) for which lb2_from_key(w)(1-gamma) -- with the group's residual bound ej
+// in place of e_max -- could still be <= UB.  lb2_from_key is increasing in w,
+// so inverting it with every rounding pushed upward gives a cutoff above which a
+// group provably holds no column at distance <= UB.  (A larger cutoff only
+// visits more groups.)  Ts = cut_scaled(UB) is the row's part.
+__device__ double cut_scaled(const CertParams& cp, double UB) {
   const double u53 = 1.1102230246251565e-16;
-  const double a2i = cp.qa2[r];
-  const double ei = cp.qe[r];
-  const double amax2 = cp.g->amax2;
-  const double emax = cp.g->emax;
-  const double rep = cp.g->repmax;
-  const double ai = sqrt(a2i) * (1.0 + 4 * u53);
-  const double am = sqrt(amax2) * (1.0 + 4 * u53);
-  const double gam = acc_gamma(cp.dpad);
-  const double E = (gam * (2.0 * ai * am + 1.002 * amax2) + rep) * (1.0 + 1e-6) + 1e-300;
   const double g64 = gamma_up(cp.d + 2, u53);
   const double T = sqrt(UB / ((1.0 - 8.0 * u53) * (1.0 - g64))) * (1.0 + 4 * u53);
-  const double Z = (T * cp.g->s / (1.0 - 8.0 * u53) + ei + emax) * (1.0 + 4 * u53);
+  return T * cp.g->s / (1.0 - 8.0 * u53);
+}
+__device__ float key_cut_e(const CertParams& cp, const RowBound& b, double Ts, double ej) {
+  const double u53 = 1.1102230246251565e-16;
+  const double Z = (Ts + b.ei + ej) * (1.0 + 4 * u53);
   const double Zr = Z / (1.0 - 2.0 * u53) * (1.0 + 4 * u53);
-  const double w0 = Zr * Zr - a2i + E;
-  const double slack = (cp.d + 8) * 2.0 * u53 * (fabs(a2i) + fabs(w0) + E);
-  const double w = w0 + 2.0 * slack + 1e-9 * (fabs(a2i) + fabs(w0) + E);
+  const double w0 = Zr * Zr - b.a2i + b.E;
+  const double slack = (cp.d + 8) * 2.0 * u53 * (fabs(b.a2i) + fabs(w0) + b.E);
+  const double w = w0 + 2.0 * slack + 1e-9 * (fabs(b.a2i) + fabs(w0) + b.E);
   return __double2float_ru(w);
+}
+__device__ float key_cut_from_ub(const CertParams& cp, int64_t r, double UB) {
+  if (!(UB < CUDART_INF)) return CUDART_INF_F;
+  return key_cut_e(cp, row_bound(cp, r), cut_scaled(cp, UB), cp.g->emax);
 }
 
 // Group candidates (DESIGN.md §5 "Re-rank").  A row's kept groups come from its
@@ -369,6 +380,96 @@ __device__ __forceinline__ void warp_sort64(double (&k)[2], int (&id)[2], int la
   }
 }
 
+// A value h (ordered bits) with count(arr[e] <= h, e < G) >= k, at most ~64 ulps
+// above the k-th smallest (bisection on the ordered key bits; G >= k).  Stopping
+// within 64 ulps (relative 2^-17, far below the bounds' own slack) saves the last
+// halvings; any h with count >= k gives a valid upper bound.
+__device__ __forceinline__ uint32_t kth_from_above(const float* arr, int G, int k, int lane) {
+  uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+  uint32_t ok[8];  // this lane's ordered keys (G <= 256), 0xFFFFFFFF = none
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int e = lane + 32 * u;
+    ok[u] = (e < G) ? f2ord(arr[e]) : 0xFFFFFFFFu;
+    if (e < G) {
+      lo = min(lo, ok[u]);
+      hi = max(hi, ok[u]);
+    }
+  }
+  for (int e = lane + 256; e < G; e += 32) {
+    const uint32_t o = f2ord(arr[e]);
+    lo = min(lo, o);
+    hi = max(hi, o);
+  }
+  lo = __reduce_min_sync(0xffffffffu, lo);
+  hi = __reduce_max_sync(0xffffffffu, hi);
+  if (lo < hi) --lo;  // count(key <= lo) < k unless lo is the minimum itself
+  int chi = G;
+  for (int it = 0; it < 32 && hi - lo > 64 && chi > k; ++it) {
+    const uint32_t mid = lo + ((hi - lo) >> 1);
+    int c = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) c += ok[u] <= mid;
+    for (int e = lane + 256; e < G; e += 32) c += f2ord(arr[e]) <= mid;
+    c = __reduce_add_sync(0xffffffffu, c);  // one REDUX instead of a 5-step shuffle tree
+    if (c >= k) {
+      hi = mid;
+      chi = c;
+    } else {
+      lo = mid;
+    }
+  }
+  return hi;
+}
+
+// Steps 1-2 of a row's re-rank (one warp; DESIGN.md §5 "Re-rank") over its G
+// staged groups (keys gk, indices gid):
+//  1. UB >= the k-th exact distance.  Each staged group holds a distinct column
+//     with D64 <= ub_g (ub2_key_e with the group's residual bound e_g, or e_max
+//     when cp.eg is null), so UB = the k-th smallest ub_g.  (With e_max the ub_g
+//     order is the key order: UB = ub2_from_key(kappa), kappa the k-th key.)
+//  2. Only groups whose lower bound can be <= UB are visited (key_cut_e with e_g).
+// The visited group indices are compacted to vis[0, nv) (vis may alias gid;
+// entries beyond viscap are dropped: the caller checks nv).  gu: G floats of
+// scratch.
+__device__ __forceinline__ void plan_row(const CertParams& cp, int64_t r, int k, const float* gk,
+                                         int* gid, float* gu, int G, int* vis, int viscap,
+                                         double& UB, int& nv, int lane) {
+  UB = CUDART_INF;
+  const RowBound b = row_bound(cp, r);
+  if (G >= k) {
+    if (cp.eg) {
+      for (int e = lane; e < G; e += 32)
+        gu[e] = __double2float_ru(ub2_key_e(cp, b, (double)gk[e], cp.eg[gid[e]]));
+      __syncwarp();
+      const float ubk = ord2f(kth_from_above(gu, G, k, lane));
+      if (ubk < CUDART_INF_F) UB = (double)ubk;
+    } else {
+      const float kappa = ord2f(kth_from_above(gk, G, k, lane));
+      if (kappa < CUDART_INF_F) UB = ub2_key_e(cp, b, (double)kappa, cp.g->emax);
+    }
+  }
+  const bool fin = UB < CUDART_INF;
+  const double Ts = fin ? cut_scaled(cp, UB) : 0.0;
+  const float kcut = fin ? key_cut_e(cp, b, Ts, cp.g->emax) : CUDART_INF_F;
+  nv = 0;
+  for (int e0 = 0; e0 < G; e0 += 32) {
+    const int e = e0 + lane;
+    bool v = false;
+    int g = -1;
+    if (e < G) {
+      g = gid[e];
+      const float cut = (fin && cp.eg) ? key_cut_e(cp, b, Ts, cp.eg[g]) : kcut;
+      v = gk[e] <= cut;
+    }
+    const unsigned vm = __ballot_sync(0xffffffffu, v);
+    const int pos = nv + __popc(vm & ((1u << lane) - 1u));
+    if (v && pos < viscap) vis[pos] = g;
+    nv += __popc(vm);
+  }
+  __syncwarp();
+}
+
 // 256-bit read-only global load (sm_100: LDG.E.ENL2.256); p must be 32-byte aligned.
 __device__ __forceinline__ void ldg8(const float* p, float* v) {
   asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -418,6 +519,7 @@ __device__ __forceinline__ void rerank_groups_row(
     int32_t* __restrict__ fail_count, int64_t r, RowTel& tel) {
   __shared__ float s_gk[kGrpWarps][kSelMax];      // staged group keys
   __shared__ int s_gi[kGrpWarps][kSelMax];        // staged group indices
+  __shared__ float s_gu[kGrpWarps][kSelMax];      // per-group upper bounds (scratch)
   __shared__ double s_ck[kGrpWarps][kColMax];     // surviving columns: D64
   __shared__ int s_ci[kGrpWarps][kColMax];        //                    index
   __shared__ double s_tk[kGrpWarps][kMaxK];       // selected top-k
@@ -488,67 +590,11 @@ __device__ __forceinline__ void rerank_groups_row(
   float vmin = CUDART_INF_F;
   for (int c = 0; c < lists; ++c) vmin = fminf(vmin, cand_v[r * lists + c]);
   __syncwarp();
-  // ---- 1. kappa and UB
-  double UB = CUDART_INF;
-  if (G >= k) {
-    uint32_t lo = 0xFFFFFFFFu, hi = 0u;
-    uint32_t ok[8];  // this lane's ordered keys (G <= 256), 0xFFFFFFFF = none
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = lane + 32 * u;
-      ok[u] = (e < G) ? f2ord(gk[e]) : 0xFFFFFFFFu;
-      if (e < G) {
-        lo = min(lo, ok[u]);
-        hi = max(hi, ok[u]);
-      }
-    }
-    for (int e = lane + 256; e < G; e += 32) {
-      const uint32_t o = f2ord(gk[e]);
-      lo = min(lo, o);
-      hi = max(hi, o);
-    }
-    lo = __reduce_min_sync(0xffffffffu, lo);
-    hi = __reduce_max_sync(0xffffffffu, hi);
-    // invariant: count(key <= hi) >= k; shrink hi towards the k-th key (a tight
-    // kappa keeps UB, and with it the visited set, small).  Stopping within
-    // 64 ulps of it (relative 2^-17, far below the bound's own slack) saves the
-    // last halvings; any hi with count >= k gives a valid UB.
-    if (lo < hi) --lo;  // count(key <= lo) < k unless lo is the minimum itself
-    int chi = G;
-    for (int it = 0; it < 32 && hi - lo > 64 && chi > k; ++it) {
-      const uint32_t mid = lo + ((hi - lo) >> 1);
-      int c = 0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) c += ok[u] <= mid;
-      for (int e = lane + 256; e < G; e += 32) c += f2ord(gk[e]) <= mid;
-      c = __reduce_add_sync(0xffffffffu, c);  // one REDUX instead of a 5-step shuffle tree
-      if (c >= k) {
-        hi = mid;
-        chi = c;
-      } else {
-        lo = mid;
-      }
-    }
-    const float kappa = ord2f(hi);
-    if (kappa < CUDART_INF_F) UB = ub2_from_key(cp, r, (double)kappa);
-  }
-  // ---- 2. expand the groups that can hold a top-k column
-  // (compacted in place into gid[0, nv), then 4 groups = 32 columns per step)
-  int nv = 0;
-  const float kcut = key_cut_from_ub(cp, r, UB);
-  for (int e0 = 0; e0 < G; e0 += 32) {
-    const int e = e0 + lane;
-    bool vis = false;
-    int g = -1;
-    if (e < G) {
-      vis = gk[e] <= kcut;
-      g = gid[e];
-    }
-    const unsigned vm = __ballot_sync(0xffffffffu, vis);
-    if (vis) gid[nv + __popc(vm & ((1u << lane) - 1u))] = g;
-    nv += __popc(vm);
-  }
-  __syncwarp();
+  // ---- 1-2. UB and the groups that can hold a top-k column (compacted in place
+  // into gid[0, nv)), then 4 groups = 32 columns per step
+  double UB;
+  int nv;
+  plan_row(cp, r, k, gk, gid, s_gu[w], G, gid, kSelMax, UB, nv, lane);
   double* ck = s_ck[w];
   int* ci = s_ci[w];
   int nc = 0;
@@ -802,6 +848,7 @@ __global__ void __launch_bounds__(kGrpWarps * 32, 4)
               CertParams cp, RrWs rw) {
   __shared__ float s_gk[kGrpWarps][kSelMax];
   __shared__ int s_gi[kGrpWarps][kSelMax];
+  __shared__ float s_gu[kGrpWarps][kSelMax];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* gk = s_gk[w];
   int* gid = s_gi[w];
@@ -863,58 +910,10 @@ __global__ void __launch_bounds__(kGrpWarps * 32, 4)
     float vmin = CUDART_INF_F;
     for (int c = 0; c < lists; ++c) vmin = fminf(vmin, cand_v[r * lists + c]);
     __syncwarp();
-    // kappa (the k-th smallest key, to 64 ulps) and UB, as in rerank_groups_row
-    double UB = CUDART_INF;
-    if (G >= k) {
-      uint32_t lo = 0xFFFFFFFFu, hi = 0u;
-      uint32_t ok[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int e = lane + 32 * u;
-        ok[u] = (e < G) ? f2ord(gk[e]) : 0xFFFFFFFFu;
-        if (e < G) {
-          lo = min(lo, ok[u]);
-          hi = max(hi, ok[u]);
-        }
-      }
-      for (int e = lane + 256; e < G; e += 32) {
-        const uint32_t o = f2ord(gk[e]);
-        lo = min(lo, o);
-        hi = max(hi, o);
-      }
-      lo = __reduce_min_sync(0xffffffffu, lo);
-      hi = __reduce_max_sync(0xffffffffu, hi);
-      if (lo < hi) --lo;
-      int chi = G;
-      for (int it = 0; it < 32 && hi - lo > 64 && chi > k; ++it) {
-        const uint32_t mid = lo + ((hi - lo) >> 1);
-        int c = 0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) c += ok[u] <= mid;
-        for (int e = lane + 256; e < G; e += 32) c += f2ord(gk[e]) <= mid;
-        c = __reduce_add_sync(0xffffffffu, c);
-        if (c >= k) {
-          hi = mid;
-          chi = c;
-        } else {
-          lo = mid;
-        }
-      }
-      const float kappa = ord2f(hi);
-      if (kappa < CUDART_INF_F) UB = ub2_from_key(cp, r, (double)kappa);
-    }
-    // the visited groups, compacted straight to the row's global list
-    const float kcut = key_cut_from_ub(cp, r, UB);
-    int32_t* gout = rw.gid + r * kRrVis;
-    int nv = 0;
-    for (int e0 = 0; e0 < G; e0 += 32) {
-      const int e = e0 + lane;
-      const bool vis = e < G && gk[e] <= kcut;
-      const unsigned vm = __ballot_sync(0xffffffffu, vis);
-      const int pos = nv + __popc(vm & ((1u << lane) - 1u));
-      if (vis && pos < kRrVis) gout[pos] = gid[e];
-      nv += __popc(vm);
-    }
+    // UB and the visited groups, as in rerank_groups_row, straight to the row's global list
+    double UB;
+    int nv;
+    plan_row(cp, r, k, gk, gid, s_gu[w], G, rw.gid + r * kRrVis, kRrVis, UB, nv, lane);
     if (nv > kRrVis) {
       overflow = true;
       nv = kRrVis;
