@@ -262,7 +262,7 @@ def run_gpu_nwr(args):
             "dist_evals_per_s": n * n / (ms * 1e-3),
             "roofline": {"bound": "tensor", "achieved": ach, "peak": peak_b, "unit": "TFLOP/s",
                          "frac": ach / peak_b, "traffic": None,
-                         "kernel": {3: "k_knn_tc3", 4: "k_knn_tc4"}.get(stats.get("main_kernel"), "?"),
+                         "kernel": {3: "k_knn_tc3", 4: "k_knn_tc4", 5: "k_knn_tc5"}.get(stats.get("main_kernel"), "?"),
                          "kernel_ms": km, "flops_per_launch": flops,
                          "peak_source": "%s bf16_tflops" % peak_src},
             "fallback_rows": stats.get("fallback_rows"),
@@ -438,8 +438,8 @@ def run_gpu(args):
         q_job = n
     if rank == 0:
         peak_b, peak_s, hbm, peak_src = _peaks()
-        # Dominant kernel: the tensor-core main pass (k_knn_tc3 single-SM or
-        # k_knn_tc4 CTA pairs), timed with CUDA events around its launch(es) on
+        # Dominant kernel: the tensor-core main pass (k_knn_tc3 / k_knn_tc5 single-SM
+        # or k_knn_tc4 CTA pairs), timed with CUDA events around its launch(es) on
         # the launching stream (the ring: around the W main-pass launches, which
         # also contain any wait for a block transfer).  Algorithmic work per
         # (query, reference) pair = 2d flops of the -2XY^T contraction (DESIGN.md
@@ -455,7 +455,8 @@ def run_gpu(args):
                 samp_cols = 0
             pairs_main = rows * (n - samp_cols)
             kname = {3: "k_knn_tc3 (single-SM tcgen05 main pass)",
-                     4: "k_knn_tc4 (CTA-pair tcgen05 cta_group::2 main pass)"}[mk]
+                     4: "k_knn_tc4 (CTA-pair tcgen05 cta_group::2 main pass)",
+                     5: "k_knn_tc5 (single-SM tcgen05 main pass, 3-deep accumulator ring)"}[mk]
             kms = kmain
         else:
             pairs_main = rows * n

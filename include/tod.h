@@ -117,7 +117,8 @@ typedef struct {
   int64_t visited_groups;  /* groups the re-rank expanded to exact fp64 distances, summed over rows */
   int64_t cand_columns;    /* exact distances at or below the per-row bound kept for the final selection */
   float ms_main_kernel;    /* two-pass mode, TOD_F_TIMING: the main-pass kernel alone (ms_main also has the sample pass) */
-  int32_t main_kernel;     /* main-pass kernel used: 0 = none (single pass), 3 = single-SM, 4 = CTA pairs */
+  int32_t main_kernel;     /* main-pass kernel used: 0 = none (single pass), 3 = single-SM, 4 = CTA pairs,
+                              5 = single-SM with a 3-deep accumulator ring */
   int32_t sample_pass;     /* two-pass sample: 0 = none, 1 = list-based (main pass skips the sample
                               tiles), 2 = key-only (main pass covers every tile) */
   int32_t query_chunks;    /* query-row chunks the call was split into (workspace_bytes); 1 = none */
@@ -135,8 +136,9 @@ typedef struct {
   float* score_mean;    /* [q_count] fp32((sum_m dist64[:, m], sequential in m) / k) */
   double* kdist64;      /* [q_count] dist64[:, k-1] (k-distance; input of the LOF stage) */
   int32_t* row_tier;    /* [q_count] diagnostics: which step answered each row -- 0 = certified by the
-                           low-precision pass (P:342 step iii), 1 = bf16 rows re-answered by the fp16
-                           pass, 2 = the fp64 tiers ("recalculate on the subset") */
+                           low-precision pass (P:342 step iii), 1 = re-answered by the second tier
+                           (the fp16 two-pass path on just the failing rows: bf16 -> fp16, fp16 ->
+                           twice K'), 2 = the fp64 tiers ("recalculate on the subset") */
 } tod_knn_out;
 
 typedef struct tod_ctx tod_ctx;

@@ -131,6 +131,13 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
     double chunk_mb = 48.0;  // reference chunk of the main pass (L2 locality)
     if (const char* e = getenv("TOD_MAIN_CHUNK_MB")) chunk_mb = std::max(4.0, atof(e));  // experiment knob
     p->main_S = std::max(1, (int)std::ceil(img_bytes / (chunk_mb * 1024 * 1024)));
+    {
+      // few query tiles (a second tier, small query calls): split the references
+      // so the (query tile x chunk) items still cover every SM
+      const int64_t units = (q_count + 255) / 256 + 1;  // CTA-pair tile pairs (or ~half the tiles)
+      const int64_t want = (ctx->num_sms + units - 1) / units;
+      if (want > p->main_S) p->main_S = (int)std::min<int64_t>(want, std::max<int64_t>(1, bt256 / 4));
+    }
     p->cap = roundup(std::max(64, 2 * (p->R - 1) * kps), 32);
     bt_v1 = (bt256 + p->R - 1) / p->R;
   }
@@ -218,6 +225,23 @@ int main_vote(int64_t n_ref) {
   if (const char* e = getenv("TOD_VOTE")) return atoi(e) != 0;
   return n_ref >= 300000;
 }
+// The single-SM main pass with a three-deep accumulator ring (knn_tc5.cu) for
+// dpad <= 32 when the main pass covers every tile (key-only sample) and no
+// profiling mode is on; TOD_MAIN_RING3 (experiment knob) forces it on (1, also
+// dpad = 64) or off (0).
+int main_ring3(int dpad, const MainPass& mp, int dbg) {
+  if (mp.R != 0 || mp.parts != 4 || (dbg & 7) != 0 || !tc5_fits(dpad)) return 0;
+  if (const char* e = getenv("TOD_MAIN_RING3")) return atoi(e) != 0;
+  return dpad <= 32;
+}
+
+// Accumulator hand-off waits of the main pass: poll (1) or suspend (0);
+// TOD_SPIN (experiment knob).
+int main_spin() {
+  if (const char* e = getenv("TOD_SPIN")) return atoi(e) != 0;
+  return 0;
+}
+
 // Staggered sweep start per CTA (TileSeq); TOD_STAGGER=1 (experiment knob)
 // enables it.  Off by default: measured no faster at C2/C3/C5 (CTAs sweeping a
 // chunk in lockstep share its tiles in L2), and the MMA-only pipeline at C2 was
@@ -403,6 +427,7 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
       mp.vote = main_vote(n);
       mp.stagger = main_stagger();
       mp.trace = cands.trace;
+      mp.spin = main_spin();
       TOD_TRY(ensure(ctx, B_MBUF, (size_t)std::max<int64_t>(q_count, 1) * mp.parts * mp.cap * 8, &p));
       mp.buf = static_cast<uint2*>(p);
       TOD_TRY(ensure(ctx, B_MCNT, (size_t)std::max<int64_t>(q_count, 1) * mp.parts * 4, &p));
@@ -412,13 +437,18 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
       const bool pair = pe ? atoi(pe) != 0 : tc4_preferred(plan.dpad) != 0;
       if (tm.on) cudaEventRecord(ctx->evk[0], st);
       main_timed = tm.on;
-      if (pair && !(ctx->cfg.flags & TOD_F_MAIN_1SM) && tc4_fits(plan.dpad, mp.parts))
+      const bool use4 = pair && !(ctx->cfg.flags & TOD_F_MAIN_1SM) && tc4_fits(plan.dpad, mp.parts);
+      const bool use5 = !use4 && main_ring3(plan.dpad, mp, cands.dbg);
+      if (use4)
         TOD_CUDA(launch_knn_tc4(A, B, self ? q_begin : 0, q_count, self, plan.fmt, mp,
                                 ctx->num_sms, cands.dbg, st, launches));
+      else if (use5)
+        TOD_CUDA(launch_knn_tc5(A, B, self ? q_begin : 0, q_count, self, plan.fmt, mp,
+                                ctx->num_sms, st, launches));
       else
         TOD_CUDA(launch_knn_tc3(A, B, self ? q_begin : 0, q_count, self, plan.fmt, mp,
                                 ctx->num_sms, cands.dbg, st, launches));
-      main_kernel = (pair && !(ctx->cfg.flags & TOD_F_MAIN_1SM) && tc4_fits(plan.dpad, mp.parts)) ? 4 : 3;
+      main_kernel = use4 ? 4 : (use5 ? 5 : 3);
       if (tm.on) cudaEventRecord(ctx->evk[1], st);
     }
   } else {
@@ -490,21 +520,34 @@ tod_status finish_rows(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ
   if (h.g.nonfinite) return fail(ctx, TOD_E_NONFINITE, "X (or Q) contains NaN or Inf");
   const int nf = h.fail_count;
   // TOD_TIER2 (testing knob): 0 = off, 1 = default (not under TOD_F_NO_CERTIFY, which
-  // exercises the brute-force tier), 2 = also under TOD_F_NO_CERTIFY
+  // exercises the brute-force tier), 2 = forced (also under TOD_F_NO_CERTIFY, and
+  // an fp16 pass's re-run regardless of its cost estimate)
   const char* t2e = getenv("TOD_TIER2");
   const int t2 = t2e ? atoi(t2e) : 1;
-  // the second tier only when the fp16 plan can serve k2 = k (+1 for the
-  // dropped self) neighbours; otherwise, or if it fails, the fp64 tiers answer
-  bool tier2 = nf > 0 && plan.fmt == TOD_FMT_BF16 && t2 != 0 &&
-               (t2 == 2 || !(ctx->cfg.flags & TOD_F_NO_CERTIFY)) &&
+  // Second tier (SURVEY 8(a) a4 tier 1): the rows pass 1 could not certify are
+  // re-answered as queries by the fp16 two-pass path on just those rows -- for a
+  // bf16 pass at the fp16 default K' (finer quantization), for an fp16 pass with
+  // twice its K' on the references already prepared (a wider candidate set:
+  // C5 2,484 failing rows of 2e6, 371 ms as fp64 threshold passes over X).  Only
+  // when the fp16 plan can serve k2 = k (+1 for the dropped self) neighbours, and
+  // never nested; otherwise, or if it fails, the fp64 tiers answer.
+  // (the fp16 re-run costs about one main pass of ceil(nf/128) query tiles over
+  // all references; the fp64 threshold tier one fp64 pass over X per 4 rows:
+  // the re-run wins once nf * n * d is large -- C4, C5 -- not for C2's 1 row)
+  const bool t2_fp16 = plan.fmt == TOD_FMT_FP16 && plan.two && (t2 == 2 || (double)nf * n * d >= 2e10);
+  const int kp2 = t2_fp16 ? std::min(2 * plan.kp_target, 256) : 0;
+  bool tier2 = nf > 0 && (plan.fmt == TOD_FMT_BF16 || t2_fp16) && t2 != 0 &&
+               ctx->tier_depth == 0 && (t2 == 2 || !(ctx->cfg.flags & TOD_F_NO_CERTIFY)) &&
                (int64_t)k + (self ? 1 : 0) <= n && k + (self ? 1 : 0) <= TOD_MAX_K;
   if (tier2) {
-    const int fmt_saved = ctx->cfg.format;
+    const int fmt_saved = ctx->cfg.format, kp_saved = ctx->cfg.kprime;
     ctx->cfg.format = TOD_FMT_FP16;
+    ctx->cfg.kprime = kp2;
     Plan p2;
     const std::string msg_saved = ctx->msg;
-    tier2 = make_plan(ctx, n, nf, d, k + (self ? 1 : 0), &p2) == TOD_OK;
+    tier2 = make_plan(ctx, n, nf, d, k + (self ? 1 : 0), &p2) == TOD_OK && (!t2_fp16 || p2.two);
     ctx->cfg.format = fmt_saved;
+    ctx->cfg.kprime = kp_saved;
     ctx->msg = msg_saved;
   }
   bool tier2_done = false;
@@ -526,13 +569,23 @@ tod_status finish_rows(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ
     o2.idx = static_cast<int64_t*>(p);
     TOD_TRY(ensure(ctx, B_T2D64, (size_t)nf * k2 * 8, &p));
     o2.dist64 = static_cast<double*>(p);
-    const int fmt_saved = ctx->cfg.format;
+    const int fmt_saved = ctx->cfg.format, kp_saved = ctx->cfg.kprime;
     ctx->cfg.format = TOD_FMT_FP16;
+    ctx->cfg.kprime = kp2;
     Timer off{ctx, false};
-    RefPrep ref2;  // the fp16 tier re-quantizes the references in its own format
-    ref->ready = false;
-    const tod_status s2 = run_knn(ctx, dX, n, qf, 0, nf, d, k2, o2, nullptr, off, launches, &ref2);
+    // a bf16 pass: the fp16 tier re-quantizes the references in its own format;
+    // an fp16 pass: its reference image (and scale, bounds) serve as they are
+    RefPrep ref2;
+    RefPrep* rp = ref;
+    if (!t2_fp16) {
+      ref->ready = false;
+      rp = &ref2;
+    }
+    ++ctx->tier_depth;
+    const tod_status s2 = run_knn(ctx, dX, n, qf, 0, nf, d, k2, o2, nullptr, off, launches, rp);
+    --ctx->tier_depth;
     ctx->cfg.format = fmt_saved;
+    ctx->cfg.kprime = kp_saved;
     if (s2 == TOD_OK) {
       TOD_CUDA(launch_tier2_scatter(rows, nf, q_begin, self, k, k2, o2.idx, o2.dist64, out, st,
                                     launches));

@@ -59,6 +59,7 @@ struct tod_ctx {
   void* nccl_comm = nullptr;                 // ncclComm_t when a real NCCL communicator is attached
   cudaStream_t comm_stream = nullptr;        // NCCL transfers overlap compute on this stream
   std::vector<todapi::Workspace> rank_ws;    // per (virtual) rank state of a sharded call
+  int tier_depth = 0;                        // > 0 inside a second-tier re-run (no nesting)
 };
 
 namespace todapi {
@@ -102,6 +103,8 @@ struct Plan {
 tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k, Plan* p);
 int main_vote(int64_t n_ref);   // main-pass filter: part-minimum vote first (rare appends)
 int main_stagger();             // staggered per-CTA sweep start of each chunk
+int main_spin();                // main-pass hand-off waits poll instead of suspending
+int main_ring3(int dpad, const MainPass& mp, int dbg);  // use knn_tc5 (3-deep accumulator ring)
 
 struct Timer {
   tod_ctx* ctx;

@@ -39,12 +39,12 @@ __device__ __forceinline__ void filter_part(const float* v, float tau, int gbase
     if constexpr ((BH / 8) % 2 == 0) pm = fminf(pm, m[BH / 8 - 1]);
     if (!__any_sync(0xffffffffu, pm < tau)) return;
   }
+  static_assert(BH % 8 == 0, "parts hold whole 8-column groups");
 #pragma unroll
-  for (int hh = 0; hh < BH / 64; ++hh) {
+  for (int g0 = 0; g0 < BH / 8; g0 += 8) {
     if (__any_sync(0xffffffffu, pa > pbase + (kPendRun - 8) * kPendSlot)) flush();
 #pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      const int gg = hh * 8 + g;
+    for (int gg = g0; gg < g0 + 8 && gg < BH / 8; ++gg) {
       if (m[gg] < tau) {
         sts_kv(pa, m[gg], gbase + gg);
         pa += kPendSlot;

@@ -24,7 +24,10 @@ struct Image {
   int dpad = 0, rb = 0, nkb = 0, layout = 0;  // layout: 2=SW128, 4=SW64, 6=SW32
   __host__ __device__ size_t region_bytes() const { return (size_t)n_pad * rb; }
   __host__ __device__ size_t extra_offset() const { return (size_t)nkb * n_pad * rb; }
-  __host__ __device__ size_t total_bytes() const { return extra_offset() + (size_t)n_pad * 32; }
+  // + 256 rows of slack after the last (extra) region: kernels whose reference
+  // tiles are not 256-row aligned (knn_tc5.cu, 160-row tiles) read up to one
+  // tile past n_pad (masked columns).
+  __host__ __device__ size_t total_bytes() const { return extra_offset() + (size_t)(n_pad + 256) * 32; }
 };
 
 // Global prep scalars, device resident.
@@ -108,12 +111,18 @@ struct MainPass {
   int vote = 0;               // filter: test each part's minimum with one warp vote first (rare appends)
   int stagger = 1;            // CTAs start their sweep of a chunk at staggered tiles (L2 spread)
   long long* trace = nullptr; // profiling (TOD_F_DEBUG_TRACE): CTA 0's per-tile clock64 stamps
+  int spin = 0;               // accumulator hand-off waits poll (test_wait) instead of suspending
 };
 cudaError_t launch_tau_combine(int64_t q, int nv, int j, const float* samp, float* tau,
                                cudaStream_t st, int* launches);
 int tc3_fits(int dpad);
 int tc3_parts(int dpad);      // column parts (= filter warps / 4) the main pass uses
 // ---- knn_tc4.cu  (the same main pass on CTA pairs: tcgen05 cta_group::2, M = 256)
+// ---- knn_tc5.cu  (single-SM main pass, three 160-column accumulators; MainPass.R == 0 only)
+int tc5_fits(int dpad);
+cudaError_t launch_knn_tc5(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
+                           bool self_join, int fmt, const MainPass& m, int num_sms, cudaStream_t st,
+                           int* launches);
 int tc4_fits(int dpad, int parts);
 int tc4_preferred(int dpad);   // shapes where the pair beats the single-SM main pass
 cudaError_t launch_knn_tc4(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,

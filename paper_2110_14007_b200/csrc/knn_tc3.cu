@@ -104,12 +104,13 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
               const float* __restrict__ tau_v, int tau_lists,
               uint2* __restrict__ mbuf, int* __restrict__ mcnt, int cap,
               float* __restrict__ samp, int64_t col0, int samp_acc, int vote, int stagger,
-              long long* __restrict__ trace) {
+              long long* __restrict__ trace, int spin) {
   // trace (profiling): CTA 0, per tile in sweep order, [8] clock64 stamps:
   // 0 MMA: before the B-tile wait, 1 after it, 2 after the accumulator wait;
   // 3 filter warp 2: before the t_full wait, 4 after it, 5 accumulator released,
   // 6 filter done; 7 producer: B-tile copy issued.
-  constexpr int kTraceTiles = 4096;
+  constexpr int kTraceTiles = 2048;  // x 16 stamps
+  constexpr int kFWlast = FW;         // warp 1 + FW = the last filter warp
   const bool tron = trace != nullptr && blockIdx.x == 0;
   using C = Cfg3<DPAD>;
   constexpr int SMP = MODE >= 4 ? MODE : 0;
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
         // the item's first B tiles are fetched while the MMA drains the previous item
         if (!a_done && issued == nstage - 1) load_a();
         mbar_wait_backoff(&empty[stage], phase ^ 1);
-        if (tron && lane == 0 && ptr < kTraceTiles) trace[ptr * 8 + 7] = clock64();
+        if (tron && lane == 0 && ptr < kTraceTiles) trace[ptr * 16 + 7] = clock64();
         ++ptr;
         if (elect_one()) {
           mbar_arrive_expect_tx(&full[stage], C::B_BYTES);
@@ -312,11 +313,11 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
       tc_fence_after();
       for (; ts.more(); ts.next()) {
         const bool tr = tron && lane == 0 && mtr < kTraceTiles;
-        if (tr) trace[mtr * 8 + 0] = clock64();
-        mbar_wait(&full[stage], phase);
-        if (tr) trace[mtr * 8 + 1] = clock64();
-        mbar_wait(&t_empty[acc], acc_phase ^ 1);
-        if (tr) trace[mtr * 8 + 2] = clock64();
+        if (tr) trace[mtr * 16 + 0] = clock64();
+        mbar_wait_sel(smem_u32(&full[stage]), phase, spin);
+        if (tr) trace[mtr * 16 + 1] = clock64();
+        mbar_wait_sel(smem_u32(&t_empty[acc]), acc_phase ^ 1, spin);
+        if (tr) trace[mtr * 16 + 2] = clock64();
         ++mtr;
         tc_fence_after();
         const uint64_t bst = (uint64_t)((stage * C::B_STRIDE) >> 4);
@@ -328,6 +329,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
           tc_commit(&empty[stage]);
         }
         __syncwarp();
+        if (tr) trace[(mtr - 1) * 16 + 8] = clock64();
         if (++stage == nstage) {
           stage = 0;
           phase ^= 1;
@@ -398,9 +400,9 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
         const uint32_t acc = tcount & 1u;
         const int etr = (int)tcount;
         const bool tr = tron && warp == 2 && lane == 0 && etr < kTraceTiles;
-        if (tr) trace[etr * 8 + 3] = clock64();
-        mbar_wait_u32(s_tfull + acc * 8, (tcount >> 1) & 1u);
-        if (tr) trace[etr * 8 + 4] = clock64();
+        if (tr) trace[etr * 16 + 3] = clock64();
+        mbar_wait_sel(s_tfull + acc * 8, (tcount >> 1) & 1u, spin);
+        if (tr) trace[etr * 16 + 4] = clock64();
         tc_fence_after();
         float v[BH];
         const uint32_t taddr = taddr0 + (acc << 8);  // acc * kBN
@@ -410,10 +412,12 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
             tmem_ld64(taddr + 64 * u, *reinterpret_cast<float(*)[64]>(v + 64 * u));
           tmem_ld_wait();
         }
+        if (tr) trace[etr * 16 + 9] = clock64();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_u32(s_tempty + acc * 8);
-        if (tr) trace[etr * 8 + 5] = clock64();
+        if (tr) trace[etr * 16 + 5] = clock64();
+        if (tron && warp == 1 + kFWlast && lane == 0 && etr < kTraceTiles) trace[etr * 16 + 10] = clock64();
         ++tcount;
         if (DBG & 3) continue;  // profiling: pipeline without the filter work
         const int t = ts.t;
@@ -452,7 +456,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
           continue;
         }
         filter_part<BH>(v, tau, (scol0 + j0) >> 3, pa, pbase, vote != 0, flush);  // col0 % 256 == 0
-        if (tr) trace[etr * 8 + 6] = clock64();
+        if (tr) trace[etr * 16 + 6] = clock64();
       }
       if constexpr (SMP) {
         if (valid) {
@@ -493,7 +497,7 @@ cudaError_t launch3(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
       reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
       (B.n + kBN - 1) / kBN, B.n, qt0, qt1 - qt0, q_begin, q_begin + q_count, self_join ? 1 : 0, m.S,
       m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap, m.samp, m.col0, m.samp_acc, m.vote,
-      m.stagger, m.trace);
+      m.stagger, m.trace, m.spin);
   return cudaGetLastError();
 }
 

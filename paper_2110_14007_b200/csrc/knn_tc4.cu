@@ -87,7 +87,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
               int self_join, int S, int R, int nstage,
               const float* __restrict__ tau_v, int tau_lists,
               uint2* __restrict__ mbuf, int* __restrict__ mcnt, int cap, int64_t col0, int vote,
-              int stagger) {
+              int stagger, int spin) {
   using C = Cfg4<DPAD>;
   constexpr int H = FW / 4;
   constexpr int BH = kBN / H;
@@ -208,8 +208,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
       aphase ^= 1;
       tc_fence_after();
       for (; ts.more(); ts.next()) {
-        mbar_wait_cl(&full[stage], phase);
-        mbar_wait_cl(&t_empty[acc], acc_phase ^ 1);
+        mbar_wait_sel(smem_u32(&full[stage]), phase, spin);
+        mbar_wait_sel(smem_u32(&t_empty[acc]), acc_phase ^ 1, spin);
         tc_fence_after();
         const uint64_t bst = (uint64_t)((stage * C::B_STRIDE) >> 4);
         if (elect_one()) {
@@ -320,7 +320,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
       ts.begin(b_tiles, S, R, c, cid, ncl, stagger);
       for (; ts.more(); ts.next()) {
         const uint32_t acc = tcount & 1u;
-        mbar_wait_u32(s_tfull + acc * 8, (tcount >> 1) & 1u);
+        mbar_wait_sel(s_tfull + acc * 8, (tcount >> 1) & 1u, spin);
         tc_fence_after();
         float v[BH];
         const uint32_t taddr = taddr0 + (acc << 8);  // acc * kBN
@@ -389,7 +389,7 @@ cudaError_t launch4(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
       reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(), A.extra_offset(),
       reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
       (B.n + kBN - 1) / kBN, B.n, qt0, n_qpairs, q_begin, q_begin + q_count, self_join ? 1 : 0, m.S,
-      m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap, m.col0, m.vote, m.stagger);
+      m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap, m.col0, m.vote, m.stagger, m.spin);
   return cudaGetLastError();
 }
 

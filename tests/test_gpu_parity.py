@@ -122,6 +122,31 @@ def test_two_pass_parity(pkg, n, d, k, fmt, chunks, pair):
         assert res.stats["certified"] >= 0.99 * n, res.stats
 
 
+@pytest.mark.parametrize("n,d,k,fmt", [
+    (20_000, 32, 20, "fp16"),    # C2 shape: the default main pass at dpad 32
+    (17_001, 32, 10, "bf16"),    # ragged last 160-row tile, bf16
+    (9_000, 16, 6, "fp16"),      # SW32 operands
+    (20_000, 64, 10, "fp16"),    # dpad 64 (forced: the default there is the CTA pair)
+    (12_345, 64, 10, "bf16"),
+])
+def test_main_ring3_parity(pkg, n, d, k, fmt):
+    # knn_tc5: single-SM main pass with three 160-column accumulators (160-row
+    # reference tiles; a query tile's own columns can straddle two of them)
+    X = datagen.gaussian_mixture(n, d, seed=n + 5 * d)
+    env = {"TOD_MAIN_RING3": "1", "TOD_SAMPLE_V1": "0", "TOD_MAIN_PAIR": "0"}
+    os.environ.update(env)
+    try:
+        with _ctx(pkg, fmt=fmt) as ctx:
+            res = ctx.knn(torch.from_numpy(X).cuda(), k)
+    finally:
+        for e in env:
+            os.environ.pop(e, None)
+    assert res.stats["main_kernel"] == 5, res.stats
+    _check_rows(res, X, k, np.arange(n))
+    if fmt == "fp16":
+        assert res.stats["certified"] >= 0.99 * n, res.stats
+
+
 @pytest.mark.parametrize("n,d,k", [
     (3000, 200, 10),     # dpad 256, small n: two-pass forced (K-pipelined main pass)
     (12_000, 100, 12),   # dpad 128, K-pipelined two-pass
@@ -524,6 +549,36 @@ def test_bf16_second_tier_matches_brute_force_tier(pkg, case, monkeypatch):
     for f in ("idx", "dist", "dist64", "score_kth", "score_mean", "kdist64"):
         assert torch.equal(getattr(res["1"], f), getattr(res["0"], f)), f
     _check_rows(res["1"], X, k, np.arange(0, X.shape[0], X.shape[0] // 8))
+
+
+@pytest.mark.parametrize("case", ["mixture", "duplicates"])
+def test_fp16_second_tier_matches_brute_force_tier(pkg, case, monkeypatch):
+    # rows an fp16 two-pass call cannot certify are re-answered by the same path
+    # on just those rows with twice its K' (references reused); outputs must
+    # equal the fp64 tiers' bit for bit.  K' = 12 for k = 10 leaves many rows
+    # uncertified by pass 1.
+    if case == "mixture":  # TOD_TIER2=2: the re-run regardless of its cost estimate
+        X = datagen.gaussian_mixture(40_000, 32, seed=18)
+        flags, on = 0, "2"
+    else:
+        X = datagen.with_duplicates(datagen.lattice(20_000, 32, seed=19, extent=3), frac=0.2, seed=20)
+        flags, on = pkg.F_NO_CERTIFY, "2"
+    Xd = torch.from_numpy(X).cuda()
+    k = 10
+    res = {}
+    for t2 in (on, "0"):
+        monkeypatch.setenv("TOD_TIER2", t2)
+        with _ctx(pkg, fmt="fp16", kprime=12, flags=flags) as ctx:
+            res[t2] = ctx.knn(Xd, k, want=("idx", "dist", "dist64", "score_kth", "score_mean",
+                                           "kdist64", "row_tier"))
+    assert res[on].stats["fallback_rows"] == res["0"].stats["fallback_rows"] > 0
+    tier = _np(res[on].row_tier)
+    assert (tier == 1).sum() == res[on].stats["fallback_rows"], "every failing row went to the second tier"
+    for f in ("idx", "dist", "dist64", "score_kth", "score_mean", "kdist64"):
+        assert torch.equal(getattr(res[on], f), getattr(res["0"], f)), f
+    rows = np.unique(np.concatenate([np.arange(0, X.shape[0], X.shape[0] // 8),
+                                     np.nonzero(tier)[0][:200]]))
+    _check_rows(res[on], X, k, rows)
 
 
 def test_abod_weighted_golden_on_gpu(pkg, golden_dir):

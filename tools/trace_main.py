@@ -27,8 +27,9 @@ with tod.Context(fmt=a.fmt, flags=tod.F_TIMING | (8 << 8)) as ctx:
         r = ctx.knn(X, a.k, want=("idx",))
         torch.cuda.synchronize()
 print("pass 1 %.3f ms (main kernel %.3f ms)" % (r.stats["ms_main"], r.stats.get("ms_main_kernel", 0)))
-t = np.fromfile(a.out, dtype=np.int64).reshape(-1, 8)
-ok = (t[:, 0] > 0) & (t[:, 2] > 0) & (t[:, 3] > 0) & (t[:, 6] > 0) & (t[:, 7] > 0)
+t = np.fromfile(a.out, dtype=np.int64).reshape(-1, 16)
+nacc = 3 if r.stats.get("main_kernel") == 5 else 2
+ok = (t[:, 0] > 0) & (t[:, 2] > 0) & (t[:, 3] > 0) & (t[:, 6] > 0) & (t[:, 7] > 0) & (t[:, 8] > 0)
 t = t[ok][50:]
 
 
@@ -36,15 +37,18 @@ def q(x):
     return "p10 %6.0f  p50 %6.0f  p90 %6.0f  mean %6.0f" % (*np.percentile(x, [10, 50, 90]), np.mean(x))
 
 
-print("tiles", len(t))
-print("MMA  period            ", q(np.diff(t[:, 0])))
-print("MMA  wait B tile       ", q(t[:, 1] - t[:, 0]))
-print("MMA  wait accumulator  ", q(t[:, 2] - t[:, 1]))
-print("FILT period            ", q(np.diff(t[:, 3])))
-print("FILT wait t_full       ", q(t[:, 4] - t[:, 3]))
-print("FILT ldtm + release    ", q(t[:, 5] - t[:, 4]))
-print("FILT filter work       ", q(t[:, 6] - t[:, 5]))
-print("MMA issue -> FILT full ", q(t[:, 4] - t[:, 2]))
-print("FILT release(t) -> MMA acc ok(t+2)", q(t[2:, 2] - t[:-2, 5]))
+rel = np.maximum(t[:, 5], t[:, 10])  # accumulator free: the later of warp 2's and the last warp's release
+print("tiles", len(t), "accumulators", nacc)
+print("MMA  period               ", q(np.diff(t[:, 0])))
+print("MMA  wait B tile          ", q(t[:, 1] - t[:, 0]))
+print("MMA  wait accumulator     ", q(t[:, 2] - t[:, 1]))
+print("MMA  issue (MMAs+commits) ", q(t[:, 8] - t[:, 2]))
+print("FILT period               ", q(np.diff(t[:, 3])))
+print("FILT wait t_full          ", q(t[:, 4] - t[:, 3]))
+print("FILT ldtm (warp 2)        ", q(t[:, 9] - t[:, 4]))
+print("FILT release (warp 2)     ", q(t[:, 5] - t[:, 4]))
+print("FILT release skew last-w2 ", q(t[:, 10] - t[:, 5]))
+print("FILT filter work          ", q(t[:, 6] - t[:, 5]))
+print("MMA issued -> FILT full   ", q(t[:, 4] - t[:, 8]))
+print("acc free(t) -> MMA acc ok(t+%d)" % nacc, q(t[nacc:, 2] - rel[:-nacc]))
 print("PROD copy issue -> MMA got B", q(t[:, 1] - t[:, 7]))
-print("PROD period            ", q(np.diff(t[:, 7])))
