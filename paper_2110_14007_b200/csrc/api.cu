@@ -235,6 +235,19 @@ int main_ring3(int dpad, const MainPass& mp, int dbg) {
   return dpad <= 32;
 }
 
+// Column candidates (filter.cuh COL): with rare appends (the vote), the main
+// pass appends each column below tau of a passing group, and the re-rank
+// evaluates only those columns instead of all 8 columns of every visited group
+// (a list-based sample's candidates stay groups: the re-rank takes both).  The
+// filter then holds the accumulator until its vote (it re-reads passing groups'
+// columns from TMEM), which costs a two-deep ring: default only where the tile's
+// MMA is long (dpad > 64; C5: re-rank 198 -> 71 ms at n = 5e5), not at d = 64
+// (C3: re-rank -10 ms, main pass +61 ms).  TOD_COLMODE (experiment knob) 1 / 0.
+int main_colmode(const MainPass& mp, int dpad) {
+  if (const char* e = getenv("TOD_COLMODE")) return atoi(e) != 0;
+  return mp.vote && dpad > 64;
+}
+
 // Accumulator hand-off waits of the main pass: poll (1) or suspend (0);
 // TOD_SPIN (experiment knob).
 int main_spin() {
@@ -311,6 +324,7 @@ tod_status prep_tc(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
   }
   TOD_TRY(ensure(ctx, B_EG, (size_t)std::max<int64_t>((n + 7) / 8, 1) * 8, &p));
   cp->eg = static_cast<const double*>(p);
+  cp->ecol = B.e;
   const float* qsrc = self ? dX + a_row0 * d : dQ;
   TOD_CUDA(launch_prep_quant(qsrc, a_rows, d, mu, g, fmt, A, 1, st, launches));
   cp->qa2 = A.a2 + (self ? q_begin - a_row0 : 0);
@@ -428,6 +442,7 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
       mp.stagger = main_stagger();
       mp.trace = cands.trace;
       mp.spin = main_spin();
+      mp.colmode = main_colmode(mp, plan.dpad);
       TOD_TRY(ensure(ctx, B_MBUF, (size_t)std::max<int64_t>(q_count, 1) * mp.parts * mp.cap * 8, &p));
       mp.buf = static_cast<uint2*>(p);
       TOD_TRY(ensure(ctx, B_MCNT, (size_t)std::max<int64_t>(q_count, 1) * mp.parts * 4, &p));

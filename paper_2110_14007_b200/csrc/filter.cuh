@@ -26,20 +26,53 @@ __device__ __forceinline__ float min8(const float* v) {
 // the part's first group.  `flush` moves the pending run to HBM.
 // vote: test the part minimum first (worth it when appends are rare: large n;
 // at n = 1e5 most warps hold a candidate in most parts and the test only adds work).
-template <int BH, class Flush>
+// COL: append each COLUMN below tau of the groups whose minimum is below it, as
+// (w~, column index), instead of (group minimum, group index): the re-rank then
+// evaluates only those columns (DESIGN.md §5 "Column candidates"); every column
+// not appended still has w~ >= tau, so the certificate is unchanged.  Used with
+// the vote (rare appends).  In this mode the caller has NOT released the
+// accumulator yet: it is released here right after the vote when no lane has a
+// candidate (the common case), else after the passing groups' columns are re-read
+// from TMEM (reload(gg, c8): a warp-collective tcgen05.ld of the group's 8
+// columns, masked as v was) and appended -- so v, like in the group mode, dies
+// with the min tree and the filter keeps its register budget.
+template <int BH, bool COL, class Flush, class Reload, class Release>
 __device__ __forceinline__ void filter_part(const float* v, float tau, int gbase, uint32_t& pa,
-                                            uint32_t pbase, bool vote, Flush&& flush) {
+                                            uint32_t pbase, bool vote, Flush&& flush,
+                                            Reload&& reload, Release&& release) {
   float m[BH / 8];
 #pragma unroll
   for (int g = 0; g < BH / 8; ++g) m[g] = min8(v + 8 * g);
-  if (vote) {
+  if (vote || COL) {
     float pm = m[0];
 #pragma unroll
     for (int g = 1; g + 1 < BH / 8; g += 2) pm = fminf(pm, fminf(m[g], m[g + 1]));
     if constexpr ((BH / 8) % 2 == 0) pm = fminf(pm, m[BH / 8 - 1]);
-    if (!__any_sync(0xffffffffu, pm < tau)) return;
+    if (!__any_sync(0xffffffffu, pm < tau)) {
+      if constexpr (COL) release();
+      return;
+    }
   }
   static_assert(BH % 8 == 0, "parts hold whole 8-column groups");
+  if constexpr (COL) {
+#pragma unroll 1
+    for (int gg = 0; gg < BH / 8; ++gg) {
+      if (!__any_sync(0xffffffffu, m[gg] < tau)) continue;
+      if (__any_sync(0xffffffffu, pa > pbase + (kPendRun - 8) * kPendSlot)) flush();
+      float c8[8];
+      reload(gg, c8);  // warp-collective
+      if (m[gg] < tau) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (c8[e] < tau) {
+            sts_kv(pa, c8[e], (gbase + gg) * 8 + e);
+            pa += kPendSlot;
+          }
+      }
+    }
+    release();
+    return;
+  }
 #pragma unroll
   for (int g0 = 0; g0 < BH / 8; g0 += 8) {
     if (__any_sync(0xffffffffu, pa > pbase + (kPendRun - 8) * kPendSlot)) flush();

@@ -112,6 +112,7 @@ struct MainPass {
   int stagger = 1;            // CTAs start their sweep of a chunk at staggered tiles (L2 spread)
   long long* trace = nullptr; // profiling (TOD_F_DEBUG_TRACE): CTA 0's per-tile clock64 stamps
   int spin = 0;               // accumulator hand-off waits poll (test_wait) instead of suspending
+  int colmode = 0;            // appends are (w~, column) of each column below tau, not group minima
 };
 cudaError_t launch_tau_combine(int64_t q, int nv, int j, const float* samp, float* tau,
                                cudaStream_t st, int* launches);
@@ -146,7 +147,9 @@ struct CertParams {
   const double* qa2;     // query ||xhat||^2 (tensor path)
   const double* qe;      // query residual bound (tensor path)
   const double* eg;      // per 8-row reference group: max residual bound (nullable: emax)
+  const double* ecol;    // per reference row: residual bound e_j (column candidates; nullable: eg/emax)
   int force_fail;        // TOD_F_NO_CERTIFY
+  int colmode;           // two-pass candidates are single columns (MainPass.colmode), not 8-column groups
 };
 struct KnnOutDev {
   int64_t* idx;

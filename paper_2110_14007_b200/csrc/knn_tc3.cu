@@ -95,7 +95,7 @@ int pick_stages3() {
 
 // MODE: 0 = main pass over every tile, 1 = main pass skipping the sample tiles
 // (t % R == 0), 4 / 8 = sample pass keeping that many minima per (row, part).
-template <int DPAD, int FMT, int DBG, int FW, int MODE>
+template <int DPAD, int FMT, int DBG, int FW, int MODE, bool COL>
 __global__ void __launch_bounds__(64 + 32 * FW, 1)
     k_knn_tc3(const uint8_t* __restrict__ a_img, size_t a_region, size_t a_extra,
               const uint8_t* __restrict__ b_img, size_t b_region, size_t b_extra, int64_t b_tiles,
@@ -413,9 +413,13 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
           tmem_ld_wait();
         }
         if (tr) trace[etr * 16 + 9] = clock64();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_u32(s_tempty + acc * 8);
+        auto release = [=]() {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_u32(s_tempty + acc * 8);
+        };
+        // column candidates (COL): filter_part releases after its vote
+        if (!COL || SMP != 0 || DBG != 0) release();
         if (tr) trace[etr * 16 + 5] = clock64();
         if (tron && warp == 1 + kFWlast && lane == 0 && etr < kTraceTiles) trace[etr * 16 + 10] = clock64();
         ++tcount;
@@ -435,7 +439,8 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
         }
         // the self column and padding columns (>= n_ref) are never candidates;
         // only the query tile's own reference tile and the last tile need masks
-        if (t == t_self || t == t_last) {
+        const bool need_mask = t == t_self || t == t_last;
+        if (need_mask) {
 #pragma unroll
           for (int e = 0; e < BH; ++e)
             v[e] = (scol0 + j0 + e == self || j0 + e >= n_ref) ? CUDART_INF_F : v[e];
@@ -455,7 +460,19 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
           }
           continue;
         }
-        filter_part<BH>(v, tau, (scol0 + j0) >> 3, pa, pbase, vote != 0, flush);  // col0 % 256 == 0
+        auto reload = [=](int gg, float* c8) {
+          tmem_ld8(taddr + 8 * gg, c8);
+          tmem_ld_wait();
+          if (need_mask) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int jj = j0 + 8 * gg + e;
+              if (scol0 + jj == self || jj >= n_ref) c8[e] = CUDART_INF_F;
+            }
+          }
+        };
+        filter_part<BH, COL>(v, tau, (scol0 + j0) >> 3, pa, pbase, vote != 0, flush, reload,
+                             release);  // col0 % 256 == 0
         if (tr) trace[etr * 16 + 6] = clock64();
       }
       if constexpr (SMP) {
@@ -476,7 +493,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
   }
 }
 
-template <int DPAD, int FMT, int DBG, int FW, int MODE>
+template <int DPAD, int FMT, int DBG, int FW, int MODE, bool COL = false>
 cudaError_t launch3(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                     bool self_join, const MainPass& m, int num_sms, cudaStream_t st) {
   const int nstage = pick_stages3<DPAD, FW>();
@@ -484,7 +501,7 @@ cudaError_t launch3(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
   if (m.parts != FW / 4) return cudaErrorInvalidValue;
   int a, b, c;
   const int smem = smem3<DPAD, FW>(nstage, &a, &b, &c);
-  auto kern = k_knn_tc3<DPAD, FMT, DBG, FW, MODE>;
+  auto kern = k_knn_tc3<DPAD, FMT, DBG, FW, MODE, COL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t qt0 = q_begin / kBM;
@@ -576,9 +593,15 @@ cudaError_t launch_knn_tc3(const Image& A, const Image& B, int64_t q_begin, int6
   if (dbg & 3)                                                                                    \
     return fmt == 1 ? launch3<D, 1, 2, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
                     : launch3<D, 2, 2, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+  if (m.R > 0 && m.colmode)                                                                      \
+    return fmt == 1 ? launch3<D, 1, 0, FW, 1, true>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
+                    : launch3<D, 2, 0, FW, 1, true>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
   if (m.R > 0)                                                                                    \
     return fmt == 1 ? launch3<D, 1, 0, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
                     : launch3<D, 2, 0, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+  if (m.colmode)                                                                                  \
+    return fmt == 1 ? launch3<D, 1, 0, FW, 0, true>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
+                    : launch3<D, 2, 0, FW, 0, true>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
   return fmt == 1 ? launch3<D, 1, 0, FW, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st)    \
                   : launch3<D, 2, 0, FW, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st);
 #define TOD_TC3_CASE(D)          \

@@ -79,7 +79,7 @@ int pick_stages4() {
   return 0;
 }
 
-template <int DPAD, int FMT, int DBG, int FW>
+template <int DPAD, int FMT, int DBG, int FW, bool COL>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
     k_knn_tc4(const uint8_t* __restrict__ a_img, size_t a_region, size_t a_extra,
               const uint8_t* __restrict__ b_img, size_t b_region, size_t b_extra, int64_t b_tiles,
@@ -330,12 +330,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
             tmem_ld64(taddr + 64 * u, *reinterpret_cast<float(*)[64]>(v + 64 * u));
           tmem_ld_wait();
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (leader) mbar_arrive_u32(s_tempty + acc * 8);
-          else mbar_arrive_cluster(r_tempty + acc * 8);
-        }
+        auto release = [=]() {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (leader) mbar_arrive_u32(s_tempty + acc * 8);
+            else mbar_arrive_cluster(r_tempty + acc * 8);
+          }
+        };
+        // column candidates (COL): filter_part releases after its vote
+        if (!COL || DBG != 0) release();
         ++tcount;
         if (DBG & 3) continue;
         const int t = ts.t;
@@ -350,12 +354,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
           }
           continue;
         }
-        if (t == t_self || t == t_last) {
+        const bool need_mask = t == t_self || t == t_last;
+        if (need_mask) {
 #pragma unroll
           for (int e = 0; e < BH; ++e)
             v[e] = (scol0 + j0 + e == self || j0 + e >= n_ref) ? CUDART_INF_F : v[e];
         }
-        filter_part<BH>(v, tau, (scol0 + j0) >> 3, pa, pbase, vote != 0, flush);  // col0 % 256 == 0
+        auto reload = [=](int gg, float* c8) {
+          tmem_ld8(taddr + 8 * gg, c8);
+          tmem_ld_wait();
+          if (need_mask) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int jj = j0 + 8 * gg + e;
+              if (scol0 + jj == self || jj >= n_ref) c8[e] = CUDART_INF_F;
+            }
+          }
+        };
+        filter_part<BH, COL>(v, tau, (scol0 + j0) >> 3, pa, pbase, vote != 0, flush, reload,
+                             release);  // col0 % 256 == 0
       }
       flush();
     }
@@ -368,7 +385,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
   }
 }
 
-template <int DPAD, int FMT, int DBG, int FW>
+template <int DPAD, int FMT, int DBG, int FW, bool COL>
 cudaError_t launch4(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                     bool self_join, const MainPass& m, int num_sms, cudaStream_t st) {
   const int nstage = pick_stages4<DPAD, FW>();
@@ -376,7 +393,7 @@ cudaError_t launch4(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
   if (m.parts != FW / 4) return cudaErrorInvalidValue;
   int a, b, c;
   const int smem = smem4<DPAD, FW>(nstage, &a, &b, &c);
-  auto kern = k_knn_tc4<DPAD, FMT, DBG, FW>;
+  auto kern = k_knn_tc4<DPAD, FMT, DBG, FW, COL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t qt0 = q_begin / kBM;
@@ -417,13 +434,16 @@ cudaError_t launch_knn_tc4(const Image& A, const Image& B, int64_t q_begin, int6
 #define TOD_TC4_CASE(D)                                                                          \
   case D:                                                                                       \
     if (dbg & 4)                                                                                \
-      return fmt == 1 ? launch4<D, 1, 4, 16>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
-                      : launch4<D, 2, 4, 16>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+      return fmt == 1 ? launch4<D, 1, 4, 16, false>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
+                      : launch4<D, 2, 4, 16, false>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
     if (dbg & 3)                                                                                \
-      return fmt == 1 ? launch4<D, 1, 2, 16>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
-                      : launch4<D, 2, 2, 16>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
-    return fmt == 1 ? launch4<D, 1, 0, 16>(A, B, q_begin, q_count, self_join, m, num_sms, st)   \
-                    : launch4<D, 2, 0, 16>(A, B, q_begin, q_count, self_join, m, num_sms, st);
+      return fmt == 1 ? launch4<D, 1, 2, 16, false>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
+                      : launch4<D, 2, 2, 16, false>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+    if (m.colmode)                                                                              \
+      return fmt == 1 ? launch4<D, 1, 0, 16, true>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
+                      : launch4<D, 2, 0, 16, true>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+    return fmt == 1 ? launch4<D, 1, 0, 16, false>(A, B, q_begin, q_count, self_join, m, num_sms, st)   \
+                    : launch4<D, 2, 0, 16, false>(A, B, q_begin, q_count, self_join, m, num_sms, st);
   switch (A.dpad) {
     TOD_TC4_CASE(16)
     TOD_TC4_CASE(32)

@@ -98,7 +98,7 @@ __device__ __forceinline__ void tmem_ld_part(uint32_t taddr, float* v) {
   if constexpr ((BH % 16) == 8) tmem_ld8(taddr + c, v + c);
 }
 
-template <int DPAD, int FMT, int NB>
+template <int DPAD, int FMT, int NB, bool COL>
 __global__ void __launch_bounds__(64 + 32 * kFW, 1)
     k_knn_tc5(const uint8_t* __restrict__ a_img, size_t a_region, size_t a_extra,
               const uint8_t* __restrict__ b_img, size_t b_region, size_t b_extra, int64_t b_tiles,
@@ -308,9 +308,13 @@ __global__ void __launch_bounds__(64 + 32 * kFW, 1)
         tmem_ld_part<BH>(taddr0 + acc * NB, v);
         tmem_ld_wait();
         if (tr) trace[etr * 16 + 9] = clock64();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_u32(s_tempty + acc * 8);
+        const uint32_t acc_now = acc;
+        auto release = [=]() {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_u32(s_tempty + acc_now * 8);
+        };
+        if (!COL) release();  // column candidates: filter_part releases after its vote
         if (tr) trace[etr * 16 + 5] = clock64();
         if (tron && warp == 1 + kFW && lane == 0 && etr < kTraceTiles) trace[etr * 16 + 10] = clock64();
         ++etr;
@@ -319,12 +323,26 @@ __global__ void __launch_bounds__(64 + 32 * kFW, 1)
           acc_phase ^= 1;
         }
         const int64_t j0 = (int64_t)t * NB + h * BH;  // block-relative first column of the part
-        if ((uint64_t)(selfc - j0) < (uint64_t)BH || j0 + BH > n_ref) {
+        const bool need_mask = (uint64_t)(selfc - j0) < (uint64_t)BH || j0 + BH > n_ref;
+        if (need_mask) {
 #pragma unroll
           for (int e = 0; e < BH; ++e)
             v[e] = (j0 + e == selfc || j0 + e >= n_ref) ? CUDART_INF_F : v[e];
         }
-        filter_part<BH>(v, tau, (int)((col0 + j0) >> 3), pa, pbase, vote != 0, flush);
+        const uint32_t taddr = taddr0 + acc_now * NB;
+        auto reload = [=](int gg, float* c8) {
+          tmem_ld8(taddr + 8 * gg, c8);
+          tmem_ld_wait();
+          if (need_mask) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int64_t jj = j0 + 8 * gg + e;
+              if (jj == selfc || jj >= n_ref) c8[e] = CUDART_INF_F;
+            }
+          }
+        };
+        filter_part<BH, COL>(v, tau, (int)((col0 + j0) >> 3), pa, pbase, vote != 0, flush, reload,
+                             release);
         if (tr) trace[(etr - 1) * 16 + 6] = clock64();
       }
       flush();
@@ -338,7 +356,7 @@ __global__ void __launch_bounds__(64 + 32 * kFW, 1)
   }
 }
 
-template <int DPAD, int FMT, int NB>
+template <int DPAD, int FMT, int NB, bool COL>
 cudaError_t launch5(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                     bool self_join, const MainPass& m, int num_sms, cudaStream_t st) {
   const int nstage = pick_stages5<DPAD, NB>();
@@ -346,7 +364,7 @@ cudaError_t launch5(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
   if (m.parts != 4 || m.R != 0) return cudaErrorInvalidValue;
   int a, b, c;
   const int smem = smem5<DPAD, NB>(nstage, &a, &b, &c);
-  auto kern = k_knn_tc5<DPAD, FMT, NB>;
+  auto kern = k_knn_tc5<DPAD, FMT, NB, COL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t qt0 = q_begin / kBM;
@@ -381,17 +399,19 @@ cudaError_t launch_knn_tc5(const Image& A, const Image& B, int64_t q_begin, int6
                            bool self_join, int fmt, const MainPass& m, int num_sms, cudaStream_t st,
                            int* launches) {
   *launches += 1;
+#define TOD_TC5_CASE(D)                                                                          \
+  case D:                                                                                       \
+    if (m.colmode)                                                                              \
+      return fmt == 1 ? launch5<D, 1, kNB, true>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
+                      : launch5<D, 2, kNB, true>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+    return fmt == 1 ? launch5<D, 1, kNB, false>(A, B, q_begin, q_count, self_join, m, num_sms, st)   \
+                    : launch5<D, 2, kNB, false>(A, B, q_begin, q_count, self_join, m, num_sms, st);
   switch (A.dpad) {
-    case 16:
-      return fmt == 1 ? launch5<16, 1, kNB>(A, B, q_begin, q_count, self_join, m, num_sms, st)
-                      : launch5<16, 2, kNB>(A, B, q_begin, q_count, self_join, m, num_sms, st);
-    case 32:
-      return fmt == 1 ? launch5<32, 1, kNB>(A, B, q_begin, q_count, self_join, m, num_sms, st)
-                      : launch5<32, 2, kNB>(A, B, q_begin, q_count, self_join, m, num_sms, st);
-    case 64:
-      return fmt == 1 ? launch5<64, 1, kNB>(A, B, q_begin, q_count, self_join, m, num_sms, st)
-                      : launch5<64, 2, kNB>(A, B, q_begin, q_count, self_join, m, num_sms, st);
+    TOD_TC5_CASE(16)
+    TOD_TC5_CASE(32)
+    TOD_TC5_CASE(64)
   }
+#undef TOD_TC5_CASE
   return cudaErrorInvalidValue;
 }
 

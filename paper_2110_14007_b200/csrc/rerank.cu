@@ -422,50 +422,77 @@ __device__ __forceinline__ uint32_t kth_from_above(const float* arr, int G, int 
   return hi;
 }
 
+// Staged candidates are 8-column groups (list entries; main-pass appends in group
+// mode) or single columns (main-pass appends in column mode, MainPass.colmode),
+// told apart by bit 30 of the staged index (column mode needs n < 2^30).
+constexpr int kColFlag = 1 << 30;
+
 // Steps 1-2 of a row's re-rank (one warp; DESIGN.md §5 "Re-rank") over its G
-// staged groups (keys gk, indices gid):
+// staged candidates (keys gk, tagged indices gid):
 //  1. UB >= the k-th exact distance.  Each staged group holds a distinct column
-//     with D64 <= ub_g (ub2_key_e with the group's residual bound e_g, or e_max
-//     when cp.eg is null), so UB = the k-th smallest ub_g.  (With e_max the ub_g
-//     order is the key order: UB = ub2_from_key(kappa), kappa the k-th key.)
-//  2. Only groups whose lower bound can be <= UB are visited (key_cut_e with e_g).
-// The visited group indices are compacted to vis[0, nv) (vis may alias gid;
-// entries beyond viscap are dropped: the caller checks nv).  gu: G floats of
-// scratch.
+//     with D64 <= ub (ub2_key_e with the candidate's residual bound: a column's
+//     own e_j, a group's e_g = max over its rows, or e_max when those arrays are
+//     null), so UB = the k-th smallest ub.  (With e_max everywhere the ub order is
+//     the key order: UB = ub2_from_key(kappa), kappa the k-th key.)
+//  2. Only candidates whose lower bound can be <= UB are visited (key_cut_e with
+//     the same residual bound).
+// The visited groups are compacted to visg[0, nvg) (visg may alias gid) and the
+// visited columns to visc[i * cstride], i < nvc; the caller checks the counts
+// against its capacities (entries beyond them are dropped).  gu: G floats of scratch
+// (free again on return: visc may alias it).
 __device__ __forceinline__ void plan_row(const CertParams& cp, int64_t r, int k, const float* gk,
-                                         int* gid, float* gu, int G, int* vis, int viscap,
-                                         double& UB, int& nv, int lane) {
+                                         int* gid, float* gu, int G, int* visg, int capg, int* visc,
+                                         int capc, int cstride, double& UB, int& nvg, int& nvc,
+                                         int lane) {
   UB = CUDART_INF;
   const RowBound b = row_bound(cp, r);
+  const double emax = cp.g->emax;
+  auto ej_of = [&](int t) {
+    if (t & kColFlag) return cp.ecol ? cp.ecol[t & (kColFlag - 1)] : emax;
+    return cp.eg ? cp.eg[t] : emax;
+  };
+  const bool per_cand = cp.eg || (cp.colmode && cp.ecol);
   if (G >= k) {
-    if (cp.eg) {
+    if (per_cand) {
       for (int e = lane; e < G; e += 32)
-        gu[e] = __double2float_ru(ub2_key_e(cp, b, (double)gk[e], cp.eg[gid[e]]));
+        gu[e] = __double2float_ru(ub2_key_e(cp, b, (double)gk[e], ej_of(gid[e])));
       __syncwarp();
       const float ubk = ord2f(kth_from_above(gu, G, k, lane));
       if (ubk < CUDART_INF_F) UB = (double)ubk;
     } else {
       const float kappa = ord2f(kth_from_above(gk, G, k, lane));
-      if (kappa < CUDART_INF_F) UB = ub2_key_e(cp, b, (double)kappa, cp.g->emax);
+      if (kappa < CUDART_INF_F) UB = ub2_key_e(cp, b, (double)kappa, emax);
     }
   }
+  __syncwarp();  // gu reads done (visc may alias it)
   const bool fin = UB < CUDART_INF;
   const double Ts = fin ? cut_scaled(cp, UB) : 0.0;
-  const float kcut = fin ? key_cut_e(cp, b, Ts, cp.g->emax) : CUDART_INF_F;
-  nv = 0;
+  const float kcut = fin ? key_cut_e(cp, b, Ts, emax) : CUDART_INF_F;
+  nvg = 0;
+  nvc = 0;
   for (int e0 = 0; e0 < G; e0 += 32) {
     const int e = e0 + lane;
     bool v = false;
-    int g = -1;
+    int t = 0;
     if (e < G) {
-      g = gid[e];
-      const float cut = (fin && cp.eg) ? key_cut_e(cp, b, Ts, cp.eg[g]) : kcut;
+      t = gid[e];
+      const float cut = (fin && per_cand) ? key_cut_e(cp, b, Ts, ej_of(t)) : kcut;
       v = gk[e] <= cut;
     }
-    const unsigned vm = __ballot_sync(0xffffffffu, v);
-    const int pos = nv + __popc(vm & ((1u << lane) - 1u));
-    if (v && pos < viscap) vis[pos] = g;
-    nv += __popc(vm);
+    const bool col = (t & kColFlag) != 0;
+    const unsigned vg = __ballot_sync(0xffffffffu, v && !col);
+    const unsigned vc = __ballot_sync(0xffffffffu, v && col);
+    const unsigned below = (1u << lane) - 1u;
+    if (v && !col) {
+      const int pos = nvg + __popc(vg & below);
+      if (pos < capg) visg[pos] = t;
+    }
+    if (v && col) {
+      const int pos = nvc + __popc(vc & below);
+      if (pos < capc) visc[pos * cstride] = t & (kColFlag - 1);
+    }
+    nvg += __popc(vg);
+    nvc += __popc(vc);
   }
   __syncwarp();
 }
@@ -561,6 +588,7 @@ __device__ __forceinline__ void rerank_groups_row(
       off[h + 1] = off[h] + min(cnt[h], mcap);
     }
     const int M = off[4];
+    const int colflag = cp.colmode ? kColFlag : 0;  // main-pass appends are columns
     for (int e0 = 0; e0 < M; e0 += 128) {
       uint2 kv[4];
       int pos[4];
@@ -580,7 +608,7 @@ __device__ __forceinline__ void rerank_groups_row(
       for (int u = 0; u < 4; ++u)
         if (pos[u] >= 0 && pos[u] < kSelMax) {
           gk[pos[u]] = __uint_as_float(kv[u].x);
-          gid[pos[u]] = (int)kv[u].y;
+          gid[pos[u]] = (int)kv[u].y | colflag;
         }
     }
     G += M;
@@ -590,18 +618,30 @@ __device__ __forceinline__ void rerank_groups_row(
   float vmin = CUDART_INF_F;
   for (int c = 0; c < lists; ++c) vmin = fminf(vmin, cand_v[r * lists + c]);
   __syncwarp();
-  // ---- 1-2. UB and the groups that can hold a top-k column (compacted in place
-  // into gid[0, nv)), then 4 groups = 32 columns per step
+  // ---- 1-2. UB and the candidates that can hold a top-k column: groups compacted
+  // in place into gid[0, nvg), columns into the (then free) ub scratch; groups
+  // expand 4 per step (4 x 8 columns), then columns 32 per step
   double UB;
-  int nv;
-  plan_row(cp, r, k, gk, gid, s_gu[w], G, gid, kSelMax, UB, nv, lane);
+  int nvg, nvc;
+  int* visc = reinterpret_cast<int*>(s_gu[w]);
+  plan_row(cp, r, k, gk, gid, s_gu[w], G, gid, kSelMax, visc, kSelMax, 1, UB, nvg, nvc, lane);
+  const int nv = nvg + nvc;
   double* ck = s_ck[w];
   int* ci = s_ci[w];
   int nc = 0;
-  for (int b0 = 0; b0 < nv; b0 += 4) {
-    const int gs = b0 + (lane >> 3);
-    const int g = gs < nv ? gid[gs] : -1;
-    const int64_t j = (int64_t)g * 8 + (lane & 7);
+  const int gsteps = (nvg + 3) / 4;
+  for (int st = 0; st < gsteps + (nvc + 31) / 32; ++st) {
+    int64_t j;
+    int g;
+    if (st < gsteps) {
+      const int gs = 4 * st + (lane >> 3);
+      g = gs < nvg ? gid[gs] : -1;
+      j = (int64_t)g * 8 + (lane & 7);
+    } else {
+      const int cs = 32 * (st - gsteps) + lane;
+      g = cs < nvc ? visc[cs] : -1;
+      j = g;
+    }
     double key = CUDART_INF;
     if (g >= 0 && j < n && !(self_join && j == gi)) {
       const float* xj = X + j * d;
@@ -799,7 +839,8 @@ __global__ void __launch_bounds__(kGrpWarps * 32, 4)
 constexpr int kRrVis = kSelMax;  // visited groups per row (more: the row goes to the fallback)
 
 struct RrWs {
-  int32_t* nv;     // [q] visited groups
+  int32_t* nv;     // [q] visited groups (front of gid)
+  int32_t* nvc;    // [q] visited column candidates (back of gid, descending)
   int32_t* flags;  // [q] bit 0: overflow (the row cannot be certified)
   int32_t* G;      // [q] staged groups (telemetry)
   int32_t* nc;     // [q] kept-column counter
@@ -831,6 +872,7 @@ __host__ RrWs rr_layout(void* base, int64_t q, size_t* total = nullptr) {
   w.map = reinterpret_cast<int64_t*>(take((size_t)q1 * (kRrVis / 4) * 8));
   w.scan = take(scan_workspace(q1));
   w.nv = reinterpret_cast<int32_t*>(take(q1 * 4));
+  w.nvc = reinterpret_cast<int32_t*>(take(q1 * 4));
   w.flags = reinterpret_cast<int32_t*>(take(q1 * 4));
   w.G = reinterpret_cast<int32_t*>(take(q1 * 4));
   w.nc = reinterpret_cast<int32_t*>(take(q1 * 4));
@@ -881,6 +923,7 @@ __global__ void __launch_bounds__(kGrpWarps * 32, 4)
         off[h + 1] = off[h] + min(cnt[h], mcap);
       }
       const int M = off[4];
+      const int colflag = cp.colmode ? kColFlag : 0;  // main-pass appends are columns
       for (int e0 = 0; e0 < M; e0 += 128) {
         uint2 kv[4];
         int pos[4];
@@ -900,7 +943,7 @@ __global__ void __launch_bounds__(kGrpWarps * 32, 4)
         for (int u = 0; u < 4; ++u)
           if (pos[u] >= 0 && pos[u] < kSelMax) {
             gk[pos[u]] = __uint_as_float(kv[u].x);
-            gid[pos[u]] = (int)kv[u].y;
+            gid[pos[u]] = (int)kv[u].y | colflag;
           }
       }
       G += M;
@@ -912,20 +955,24 @@ __global__ void __launch_bounds__(kGrpWarps * 32, 4)
     __syncwarp();
     // UB and the visited groups, as in rerank_groups_row, straight to the row's global list
     double UB;
-    int nv;
-    plan_row(cp, r, k, gk, gid, s_gu[w], G, rw.gid + r * kRrVis, kRrVis, UB, nv, lane);
+    int nvg, nvc;
+    plan_row(cp, r, k, gk, gid, s_gu[w], G, rw.gid + r * kRrVis, kRrVis,
+             rw.gid + r * kRrVis + (kRrVis - 1), kRrVis, -1, UB, nvg, nvc, lane);
+    int nv = nvg + nvc;  // groups from the front of the row's list, columns from its back
     if (nv > kRrVis) {
       overflow = true;
-      nv = kRrVis;
+      nvg = nvc = 0;
+      nv = 0;
     }
     if (lane == 0) {
-      rw.nv[r] = nv;
+      rw.nv[r] = nvg;
+      rw.nvc[r] = nvc;
       rw.flags[r] = overflow ? 1 : 0;
       rw.G[r] = G;
       rw.nc[r] = 0;
       rw.vmin[r] = vmin;
       rw.ub[r] = UB;
-      rw.tcnt[r] = (nv + 3) / 4;
+      rw.tcnt[r] = (nvg + 3) / 4 + (nvc + 31) / 32;
     }
   }
 }
@@ -958,9 +1005,18 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
     __syncwarp();
     const int nv = rw.nv[r];
     const double UB = rw.ub[r];
-    const int gs = 4 * c + (lane >> 3);
-    const int g = gs < nv ? rw.gid[r * kRrVis + gs] : -1;
-    const int64_t j = (int64_t)g * 8 + (lane & 7);
+    int g;
+    int64_t j;
+    const int gtasks = (nv + 3) / 4;
+    if (c < gtasks) {  // 4 groups x 8 columns per task
+      const int gs = 4 * c + (lane >> 3);
+      g = gs < nv ? rw.gid[r * kRrVis + gs] : -1;
+      j = (int64_t)g * 8 + (lane & 7);
+    } else {           // 32 column candidates per task (stored from the back)
+      const int cs = 32 * (c - gtasks) + lane;
+      g = cs < rw.nvc[r] ? rw.gid[r * kRrVis + (kRrVis - 1 - cs)] : -1;
+      j = g;
+    }
     double key = CUDART_INF;
     if (g >= 0 && j < n && !(self_join && j == gi)) {
       const float* xj = X + j * d;
@@ -1088,7 +1144,7 @@ __global__ void __launch_bounds__(kGrpWarps * 32)
     if (cp.force_fail) cert = false;
     tel.maxerr = fmax(tel.maxerr, err);
     tel.G += (unsigned long long)rw.G[r];
-    tel.nv += (unsigned long long)rw.nv[r];
+    tel.nv += (unsigned long long)(rw.nv[r] + rw.nvc[r]);
     tel.nc += (unsigned long long)nc;
     if (cert) {
       write_row(out, r, k, tk, ti, lane, 32);
@@ -2049,8 +2105,10 @@ cudaError_t launch_rerank(const float* Q, int64_t q_begin, int64_t q_count, cons
                           int32_t* fail_count, double* max_err, unsigned long long* counters,
                           void* split_ws, cudaStream_t st, int* launches) {
   if (k > kMaxK) return cudaErrorInvalidValue;
-  if (cp.kind == PASS_TC) {  // group candidates
+  if (cp.kind == PASS_TC) {  // group (or column) candidates
     if (c.lists * c.kp > kSelMax || !c.key) return cudaErrorInvalidValue;
+    cp.colmode = mp ? mp->colmode : 0;
+    if (cp.colmode && n >= kColFlag) return cudaErrorInvalidValue;  // tagged column indices
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -147,6 +147,31 @@ def test_main_ring3_parity(pkg, n, d, k, fmt):
         assert res.stats["certified"] >= 0.99 * n, res.stats
 
 
+@pytest.mark.parametrize("n,d,k,fmt,v1,pair", [
+    (20_000, 32, 20, "fp16", "0", "0"),   # key-only sample: column candidates only (tc3)
+    (17_001, 32, 10, "bf16", "0", "0"),   # bf16 (second tier), ragged tail
+    (20_000, 64, 10, "fp16", "1", "1"),   # list sample (group candidates) + CTA-pair main pass (columns)
+    (12_345, 64, 10, "bf16", "1", "0"),   # mixed candidates, single-SM main pass
+    (9_000, 512, 20, "fp16", "0", "0"),   # d = 512: split re-rank with column tasks
+])
+def test_column_candidates_parity(pkg, n, d, k, fmt, v1, pair):
+    # MainPass.colmode: the main pass appends each column below tau of a passing
+    # group (the default for large n); forced on here at sizes the oracle checks
+    X = datagen.gaussian_mixture(n, d, seed=n + 7 * d)
+    env = {"TOD_COLMODE": "1", "TOD_VOTE": "1", "TOD_SAMPLE_V1": v1, "TOD_MAIN_PAIR": pair}
+    os.environ.update(env)
+    try:
+        with _ctx(pkg, fmt=fmt) as ctx:
+            res = ctx.knn(torch.from_numpy(X).cuda(), k)
+    finally:
+        for e in env:
+            os.environ.pop(e, None)
+    rows = np.arange(n) if n <= 20_000 and d <= 64 else np.random.default_rng(1).choice(n, 500, replace=False)
+    _check_rows(res, X, k, np.sort(rows))
+    if fmt == "fp16":
+        assert res.stats["certified"] >= 0.99 * n, res.stats
+
+
 @pytest.mark.parametrize("n,d,k", [
     (3000, 200, 10),     # dpad 256, small n: two-pass forced (K-pipelined main pass)
     (12_000, 100, 12),   # dpad 128, K-pipelined two-pass
