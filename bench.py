@@ -449,8 +449,9 @@ def run_gpu(args):
         rows = qc
         mk = stats.get("main_kernel", 0)
         if mk:
-            bt = (n + 255) // 256
-            samp_cols = sum(min(256, n - 256 * t) for t in range(0, bt, 8))
+            tile = 256
+            bt = (n + tile - 1) // tile
+            samp_cols = sum(min(tile, n - tile * t) for t in range(0, bt, 8))
             if stats.get("sample_pass") == 2:   # key-only sample: main covers every tile
                 samp_cols = 0
             pairs_main = rows * (n - samp_cols)

@@ -120,7 +120,9 @@ typedef struct {
   int32_t main_kernel;     /* main-pass kernel used: 0 = none (single pass), 3 = single-SM, 4 = CTA pairs,
                               5 = single-SM with a 3-deep accumulator ring */
   int32_t sample_pass;     /* two-pass sample: 0 = none, 1 = list-based (main pass skips the sample
-                              tiles), 2 = key-only (main pass covers every tile) */
+                              tiles), 2 = key-only (main pass covers every tile), 3 = three-stage
+                              (key-only pre-sample; the main-pass kernel over the sample tiles,
+                              then over the others) */
   int32_t query_chunks;    /* query-row chunks the call was split into (workspace_bytes); 1 = none */
 } tod_stats;
 

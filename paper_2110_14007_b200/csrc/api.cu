@@ -248,21 +248,15 @@ int main_colmode(const MainPass& mp, int dpad) {
   return mp.vote && dpad > 64;
 }
 
-// Accumulator hand-off waits of the main pass: poll (1) or suspend (0);
-// TOD_SPIN (experiment knob).
-int main_spin() {
-  if (const char* e = getenv("TOD_SPIN")) return atoi(e) != 0;
-  return 0;
+// CTA-pair main pass tile geometry: 160-column tiles with three accumulators
+// when no list-based sample tiles (256-column grid) must be skipped;
+// TOD_MAIN_NB (experiment knob) 160 / 256.
+int main_nb(const MainPass& mp) {
+  int nb = 256;
+  if (const char* e = getenv("TOD_MAIN_NB")) nb = atoi(e) == 160 ? 160 : 256;
+  return mp.R != 0 ? 256 : nb;  // sample tiles are skipped on the 256-column grid
 }
 
-// Staggered sweep start per CTA (TileSeq); TOD_STAGGER=1 (experiment knob)
-// enables it.  Off by default: measured no faster at C2/C3/C5 (CTAs sweeping a
-// chunk in lockstep share its tiles in L2), and the MMA-only pipeline at C2 was
-// 12 % slower staggered.
-int main_stagger() {
-  if (const char* e = getenv("TOD_STAGGER")) return atoi(e) != 0;
-  return 0;
-}
 
 // Input quantization (a1) for the tensor-core passes: column mean, power-of-two
 // scale, reference image B over all n rows (skipped when ref->ready) and query
@@ -398,33 +392,46 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     TOD_TRY(prep_tc(ctx, dX, n, dQ, q_begin, q_count, d, plan.fmt, plan.dpad, g, &A, &B, &cp,
                     ref, launches));
     tm.mark();  // 2: main start
-    // Two-pass sample: key-only register top-4 per (row, column part) over the
-    // sample tiles (knn_tc3 sample mode), tau = the j-th smallest of those; the
-    // main pass then covers every tile.  TOD_SAMPLE_V1=1 (experiment knob)
-    // keeps the list-based sample pass of knn_tc.cu instead.
-    // Measured on B200: key-only sample wins at d <= 32 (C2 pass 1 1.44 -> 1.35 ms), the
-    // list-based sample at d = 64 (C3 132 vs 137 ms: there the main pass would also
-    // have to cover the sample tiles on the CTA-pair kernel).
+    // Candidate selection (DESIGN.md §5 "Two-pass" and "Three-stage"):
+    //  * key-only sample (d <= 32, d >= 128): knn_tc3 sample mode keeps the 4 (or 8)
+    //    smallest group minima per (row, part) over every R-th tile; tau = the j-th
+    //    smallest of those; the main pass covers every tile.
+    //  * three-stage (d = 64 on CTA pairs): a key-only pre-sample over every
+    //    (8R)-th tile gives an over-estimate tau0; the main-pass kernel sweeps the
+    //    sample tiles (t % R == 0) appending everything below tau0; tau = the j-th
+    //    smallest of those appends (<= tau0); the main pass sweeps the other tiles
+    //    below tau.  Every non-kept candidate is >= tau either way.
+    //  * list-based sample (TOD_SAMPLE3=0 at d = 64; TOD_SAMPLE_V1=1): knn_tc.cu's
+    //    running top-K'' lists over the sample tiles, the main pass skips them.
+    const char* pe = getenv("TOD_MAIN_PAIR");  // experiment knob: 1 = force pairs, 0 = never
+    const bool pair = pe ? atoi(pe) != 0 : tc4_preferred(plan.dpad) != 0;
+    const bool use4 = plan.two && pair && !(ctx->cfg.flags & TOD_F_MAIN_1SM) &&
+                      tc4_fits(plan.dpad, tc3_parts(plan.dpad));
     const char* sv = getenv("TOD_SAMPLE_V1");
-    const bool samp_v1 = plan.two && plan.dpad <= 128 && (sv ? atoi(sv) != 0 : plan.dpad == 64);
-    if (plan.two) sample_pass = samp_v1 ? 1 : 2;
+    const char* s3 = getenv("TOD_SAMPLE3");
+    const bool three = plan.two && use4 && (cands.dbg & 7) == 0 && !sv &&
+                       (s3 ? atoi(s3) != 0 : plan.dpad == 64);
+    const bool samp_v1 = plan.two && !three && plan.dpad <= 128 &&
+                         (sv ? atoi(sv) != 0 : plan.dpad == 64);
+    if (plan.two) sample_pass = samp_v1 ? 1 : (three ? 3 : 2);
+    // tau = the j-th smallest sample key, j ~ 2K'/R
+    const int jw = std::max(4, (2 * plan.kp_target + plan.R - 1) / plan.R);
     if (plan.two && !samp_v1) {
       MainPass sm;
       sm.S = 1;
-      sm.R = plan.R;
-      sm.stagger = main_stagger();
+      sm.R = three ? 8 * plan.R : plan.R;
       sm.parts = tc3_parts(plan.dpad);
-      // tau = the j-th smallest sample minimum, j ~ 2K'/R; 8 per (row, part) when
-      // 4 per part cannot supply j (large k)
-      const int jw = std::max(4, (2 * plan.kp_target + plan.R - 1) / plan.R);
-      sm.samp_t = jw > 3 * sm.parts ? 8 : 4;
+      // 8 minima per (row, part) when 4 per part cannot supply j (large k); the
+      // three-stage pre-sample takes the 8th of 16 (an over-estimate of the
+      // stage-2 tau: the (8 x 8R)-th group over all tiles in expectation)
+      const int ja = three ? 8 : jw;
+      sm.samp_t = ja > 3 * sm.parts ? 8 : 4;
       const int nv = sm.parts * sm.samp_t;
       TOD_TRY(ensure(ctx, B_SAMP, (size_t)std::max<int64_t>(q_count, 1) * nv * 4, &p));
       sm.samp = static_cast<float*>(p);
       TOD_CUDA(launch_knn_tc3(A, B, self ? q_begin : 0, q_count, self, plan.fmt, sm, ctx->num_sms,
                               0, st, launches));
-      const int j = std::min(nv, jw);
-      TOD_CUDA(launch_tau_combine(q_count, nv, j, sm.samp, cands.v, st, launches));
+      TOD_CUDA(launch_tau_combine(q_count, nv, std::min(nv, ja), sm.samp, cands.v, st, launches));
       cands.lists = 1;
       cands.kp = 0;
     } else {
@@ -433,26 +440,33 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     }
     if (plan.two) {
       mp.S = plan.main_S;
-      mp.R = samp_v1 ? plan.R : 0;
+      mp.R = (samp_v1 || three) ? plan.R : 0;
       mp.tau_v = cands.v;
       mp.tau_lists = cands.lists;
       mp.parts = tc3_parts(plan.dpad);
       mp.cap = plan.cap * 2 / mp.parts;  // plan.cap is per column half
       mp.vote = main_vote(n);
-      mp.stagger = main_stagger();
       mp.trace = cands.trace;
-      mp.spin = main_spin();
-      mp.colmode = main_colmode(mp, plan.dpad);
+      mp.smode = three ? 1 : 0;
+      mp.colmode = cands.dbg ? 0 : main_colmode(mp, plan.dpad);  // profiling builds: groups
+      mp.nb = main_nb(mp);
       TOD_TRY(ensure(ctx, B_MBUF, (size_t)std::max<int64_t>(q_count, 1) * mp.parts * mp.cap * 8, &p));
       mp.buf = static_cast<uint2*>(p);
       TOD_TRY(ensure(ctx, B_MCNT, (size_t)std::max<int64_t>(q_count, 1) * mp.parts * 4, &p));
       mp.cnt = static_cast<int*>(p);
       TOD_CUDA(cudaMemsetAsync(mp.cnt, 0, (size_t)std::max<int64_t>(q_count, 1) * mp.parts * 4, st));
-      const char* pe = getenv("TOD_MAIN_PAIR");  // experiment knob: 1 = force pairs, 0 = never
-      const bool pair = pe ? atoi(pe) != 0 : tc4_preferred(plan.dpad) != 0;
+      if (three) {
+        // stage 2: the sample tiles below tau0, appended; tau = their j-th smallest key
+        MainPass mb = mp;
+        mb.trace = nullptr;  // the profiling trace records the main sweep (stage 4)
+        TOD_CUDA(launch_knn_tc4(A, B, self ? q_begin : 0, q_count, self, plan.fmt, mb,
+                                ctx->num_sms, 0, st, launches));
+        TOD_CUDA(launch_tau_from_appends(q_count, mp.parts, mp.cap, mp.cnt, mp.buf, jw, cands.v,
+                                         st, launches));
+        mp.smode = 0;
+      }
       if (tm.on) cudaEventRecord(ctx->evk[0], st);
       main_timed = tm.on;
-      const bool use4 = pair && !(ctx->cfg.flags & TOD_F_MAIN_1SM) && tc4_fits(plan.dpad, mp.parts);
       const bool use5 = !use4 && main_ring3(plan.dpad, mp, cands.dbg);
       if (use4)
         TOD_CUDA(launch_knn_tc4(A, B, self ? q_begin : 0, q_count, self, plan.fmt, mp,

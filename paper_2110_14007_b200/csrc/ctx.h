@@ -102,8 +102,7 @@ struct Plan {
 };
 tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k, Plan* p);
 int main_vote(int64_t n_ref);   // main-pass filter: part-minimum vote first (rare appends)
-int main_stagger();             // staggered per-CTA sweep start of each chunk
-int main_spin();                // main-pass hand-off waits poll instead of suspending
+int main_nb(const MainPass& mp);  // CTA-pair main pass: 256-column tiles x 2 or 160 x 3
 int main_colmode(const MainPass& mp, int dpad);  // main pass appends column candidates
 int main_ring3(int dpad, const MainPass& mp, int dbg);  // use knn_tc5 (3-deep accumulator ring)
 

@@ -88,47 +88,71 @@ __device__ __forceinline__ void filter_part(const float* v, float tau, int gbase
 
 // Tiles of reference chunk c of S: [bt*c/S, bt*(c+1)/S), minus the sample tiles
 // (t % R == 0; R a power of two, 0 = none) when SKIP; the sample pass (SMP)
-// visits only the sample tiles t = si*R, si in [bs*c/S, bs*(c+1)/S).  The
-// sweep starts at a per-CTA rotation of the chunk (rot = cta * len / ncta):
-// CTAs that sweep one L2-resident chunk at the same time would otherwise
-// request the same reference tile together.
+// visits only the sample tiles t = si*R, si in [bs*c/S, bs*(c+1)/S).  (A
+// staggered per-CTA start was measured no faster: CTAs sweeping one L2-resident
+// chunk in lockstep share its tiles.)
 template <int SMP, int SKIP>
 struct TileSeq {
-  int b, len, i, rot, t, R, mask;
+  int t, end, R, mask;
   bool on;
-  __device__ __forceinline__ void begin(int64_t bt, int S, int R_, int c, int64_t cta, int64_t ncta,
-                                        int stagger) {
+  __device__ __forceinline__ void begin(int64_t bt, int S, int R_, int c) {
     R = R_;
     on = SKIP && R > 0;
     mask = R - 1;
     if constexpr (SMP) {
       const int64_t bs = (bt + R - 1) / R;
-      b = (int)(bs * c / S);
-      len = (int)(bs * (c + 1) / S) - b;
-    } else {
-      b = (int)(bt * c / S);
-      len = (int)(bt * (c + 1) / S) - b;
+      t = (int)(bs * c / S) * R;
+      end = (int)(bs * (c + 1) / S) * R;
+      if (end > bt) end = (int)bt;
+      return;
     }
-    rot = (stagger && len > 0) ? (int)(cta * len / ncta) : 0;
-    i = 0;
-    at();
+    t = (int)(bt * c / S);
+    end = (int)(bt * (c + 1) / S);
     skip();
   }
-  __device__ __forceinline__ void at() {
-    int k = i + rot;
-    if (k >= len) k -= len;
-    t = SMP ? (b + k) * R : b + k;
+  __device__ __forceinline__ void skip() {
+    if (on && (t & mask) == 0) ++t;
+  }
+  __device__ __forceinline__ bool more() const { return t < end; }
+  __device__ __forceinline__ void next() {
+    if constexpr (SMP) {
+      t += R;
+      return;
+    }
+    ++t;
+    skip();
+  }
+};
+
+// Runtime-mode tile sequence of chunk c of S over bt tiles (no rotation):
+// smode 0: every tile, minus the sample tiles t % R == 0 when R > 0 (R a power
+// of two); smode 1: only the sample tiles t = si * R, si in [bs*c/S, bs*(c+1)/S).
+struct TileSeqRT {
+  int t, end, step, mask;
+  bool skip_on;
+  __device__ __forceinline__ void begin(int64_t bt, int S, int R, int c, int smode) {
+    if (smode) {
+      const int64_t bs = (bt + R - 1) / R;
+      t = (int)(bs * c / S) * R;
+      end = (int)(bs * (c + 1) / S) * R;
+      if (end > bt) end = (int)bt;
+      step = R;
+      skip_on = false;
+    } else {
+      t = (int)(bt * c / S);
+      end = (int)(bt * (c + 1) / S);
+      step = 1;
+      skip_on = R > 0;
+    }
+    mask = R - 1;
+    skip();
   }
   __device__ __forceinline__ void skip() {
-    while (on && i < len && (t & mask) == 0) {
-      ++i;
-      at();
-    }
+    if (skip_on && (t & mask) == 0) ++t;
   }
-  __device__ __forceinline__ bool more() const { return i < len; }
+  __device__ __forceinline__ bool more() const { return t < end; }
   __device__ __forceinline__ void next() {
-    ++i;
-    at();
+    t += step;
     skip();
   }
 };

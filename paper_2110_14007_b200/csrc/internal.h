@@ -109,11 +109,13 @@ struct MainPass {
   int samp_acc = 0;           // sample mode: merge into the minima already in samp (ring of blocks)
   int64_t col0 = 0;           // global index of reference row 0 of the image (a ring block; % 256 == 0)
   int vote = 0;               // filter: test each part's minimum with one warp vote first (rare appends)
-  int stagger = 1;            // CTAs start their sweep of a chunk at staggered tiles (L2 spread)
   long long* trace = nullptr; // profiling (TOD_F_DEBUG_TRACE): CTA 0's per-tile clock64 stamps
-  int spin = 0;               // accumulator hand-off waits poll (test_wait) instead of suspending
   int colmode = 0;            // appends are (w~, column) of each column below tau, not group minima
+  int nb = 256;               // CTA-pair main pass tile: 256 columns x 2 accumulators, or 160 x 3
+  int smode = 0;              // CTA-pair main pass: 1 = sweep only the sample tiles t % R == 0
 };
+cudaError_t launch_tau_from_appends(int64_t q, int parts, int cap, const int* cnt, const uint2* buf,
+                                    int j, float* tau, cudaStream_t st, int* launches);
 cudaError_t launch_tau_combine(int64_t q, int nv, int j, const float* samp, float* tau,
                                cudaStream_t st, int* launches);
 int tc3_fits(int dpad);

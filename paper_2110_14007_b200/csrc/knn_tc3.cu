@@ -103,15 +103,16 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
               int self_join, int S, int R, int nstage,
               const float* __restrict__ tau_v, int tau_lists,
               uint2* __restrict__ mbuf, int* __restrict__ mcnt, int cap,
-              float* __restrict__ samp, int64_t col0, int samp_acc, int vote, int stagger,
-              long long* __restrict__ trace, int spin) {
+              float* __restrict__ samp, int64_t col0, int samp_acc, int vote,
+              long long* __restrict__ trace) {
   // trace (profiling): CTA 0, per tile in sweep order, [8] clock64 stamps:
   // 0 MMA: before the B-tile wait, 1 after it, 2 after the accumulator wait;
   // 3 filter warp 2: before the t_full wait, 4 after it, 5 accumulator released,
   // 6 filter done; 7 producer: B-tile copy issued.
   constexpr int kTraceTiles = 2048;  // x 16 stamps
   constexpr int kFWlast = FW;         // warp 1 + FW = the last filter warp
-  const bool tron = trace != nullptr && blockIdx.x == 0;
+  constexpr bool TRACE = (DBG & 8) != 0;  // profiling build only (no trace code otherwise)
+  const bool tron = TRACE && trace != nullptr && blockIdx.x == 0;
   using C = Cfg3<DPAD>;
   constexpr int SMP = MODE >= 4 ? MODE : 0;
   constexpr int SKIP = MODE == 1 ? 1 : 0;
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
       const int64_t qtl = item % n_qtiles;
       const int c = (int)(item / n_qtiles);
       TileSeq<SMP, SKIP> ts;
-      ts.begin(b_tiles, S, R, c, blockIdx.x, gridDim.x, stagger);
+      ts.begin(b_tiles, S, R, c);
       for (; ts.more(); ts.next()) {
         const int64_t t = ts.t;
         for (int kb = 0; kb <= C::NKB; ++kb) {
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int c = (int)(item / n_qtiles);
       TileSeq<SMP, SKIP> ts;
-      ts.begin(b_tiles, S, R, c, blockIdx.x, gridDim.x, stagger);
+      ts.begin(b_tiles, S, R, c);
       for (; ts.more(); ts.next()) {
         mbar_wait(&t_empty[acc], acc_phase ^ 1);
         for (int kb = 0; kb <= C::NKB; ++kb) {
@@ -243,7 +244,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
       const int64_t qtl = item % n_qtiles;
       const int c = (int)(item / n_qtiles);
       TileSeq<SMP, SKIP> ts;
-      ts.begin(b_tiles, S, R, c, blockIdx.x, gridDim.x, stagger);
+      ts.begin(b_tiles, S, R, c);
       int issued = 0;
       bool a_done = false;
       auto load_a = [&]() {
@@ -264,7 +265,8 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
         // the item's first B tiles are fetched while the MMA drains the previous item
         if (!a_done && issued == nstage - 1) load_a();
         mbar_wait_backoff(&empty[stage], phase ^ 1);
-        if (tron && lane == 0 && ptr < kTraceTiles) trace[ptr * 16 + 7] = clock64();
+        if constexpr (TRACE)
+          if (tron && lane == 0 && ptr < kTraceTiles) trace[ptr * 16 + 7] = clock64();
         ++ptr;
         if (elect_one()) {
           mbar_arrive_expect_tx(&full[stage], C::B_BYTES);
@@ -307,16 +309,16 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int c = (int)(item / n_qtiles);
       TileSeq<SMP, SKIP> ts;
-      ts.begin(b_tiles, S, R, c, blockIdx.x, gridDim.x, stagger);
+      ts.begin(b_tiles, S, R, c);
       mbar_wait(a_full, aphase);
       aphase ^= 1;
       tc_fence_after();
       for (; ts.more(); ts.next()) {
-        const bool tr = tron && lane == 0 && mtr < kTraceTiles;
+        const bool tr = TRACE && tron && lane == 0 && mtr < kTraceTiles;
         if (tr) trace[mtr * 16 + 0] = clock64();
-        mbar_wait_sel(smem_u32(&full[stage]), phase, spin);
+        mbar_wait(&full[stage], phase);
         if (tr) trace[mtr * 16 + 1] = clock64();
-        mbar_wait_sel(smem_u32(&t_empty[acc]), acc_phase ^ 1, spin);
+        mbar_wait(&t_empty[acc], acc_phase ^ 1);
         if (tr) trace[mtr * 16 + 2] = clock64();
         ++mtr;
         tc_fence_after();
@@ -395,13 +397,13 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
       for (int i = 0; i < T; ++i)  // a ring of blocks accumulates over launches
         top[i] = (SMP && samp_acc && valid) ? samp[(r * H + h) * T + i] : CUDART_INF_F;
       TileSeq<SMP, SKIP> ts;
-      ts.begin(b_tiles, S, R, c, blockIdx.x, gridDim.x, stagger);
+      ts.begin(b_tiles, S, R, c);
       for (; ts.more(); ts.next()) {
         const uint32_t acc = tcount & 1u;
         const int etr = (int)tcount;
-        const bool tr = tron && warp == 2 && lane == 0 && etr < kTraceTiles;
+        const bool tr = TRACE && tron && warp == 2 && lane == 0 && etr < kTraceTiles;
         if (tr) trace[etr * 16 + 3] = clock64();
-        mbar_wait_sel(s_tfull + acc * 8, (tcount >> 1) & 1u, spin);
+        mbar_wait_u32(s_tfull + acc * 8, (tcount >> 1) & 1u);
         if (tr) trace[etr * 16 + 4] = clock64();
         tc_fence_after();
         float v[BH];
@@ -421,7 +423,8 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
         // column candidates (COL): filter_part releases after its vote
         if (!COL || SMP != 0 || DBG != 0) release();
         if (tr) trace[etr * 16 + 5] = clock64();
-        if (tron && warp == 1 + kFWlast && lane == 0 && etr < kTraceTiles) trace[etr * 16 + 10] = clock64();
+        if constexpr (TRACE)
+          if (tron && warp == 1 + kFWlast && lane == 0 && etr < kTraceTiles) trace[etr * 16 + 10] = clock64();
         ++tcount;
         if (DBG & 3) continue;  // profiling: pipeline without the filter work
         const int t = ts.t;
@@ -514,7 +517,7 @@ cudaError_t launch3(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
       reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
       (B.n + kBN - 1) / kBN, B.n, qt0, qt1 - qt0, q_begin, q_begin + q_count, self_join ? 1 : 0, m.S,
       m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap, m.samp, m.col0, m.samp_acc, m.vote,
-      m.stagger, m.trace, m.spin);
+      m.trace);
   return cudaGetLastError();
 }
 
@@ -541,7 +544,46 @@ __global__ void k_tau_combine(int64_t q, int nv, int j, const float* __restrict_
   tau[r] = t;
 }
 
+// Three-stage selection, stage 3: tau_r = min(tau0_r, the j-th smallest key the
+// sample-tile sweep appended for row r over its parts) -- every non-appended
+// sample column has w~ >= tau0 >= tau_r.  Fewer than j appends: tau0 stays.
+__global__ void k_tau_from_appends(int64_t q, int parts, int cap, const int* __restrict__ cnt,
+                                   const uint2* __restrict__ buf, int j, float* __restrict__ tau) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= q) return;
+  float top[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) top[i] = CUDART_INF_F;
+  int total = 0;
+  for (int h = 0; h < parts; ++h) {
+    const int c = min(cnt[r * parts + h], cap);
+    total += c;
+    const uint2* b = buf + (r * parts + h) * (int64_t)cap;
+    for (int e = 0; e < c; ++e) {
+      const float x = __uint_as_float(__ldcg(b + e).x);
+#pragma unroll
+      for (int i = 31; i > 0; --i) top[i] = fminf(top[i], fmaxf(top[i - 1], x));
+      top[0] = fminf(top[0], x);
+    }
+  }
+  if (total >= j) {
+    float t = CUDART_INF_F;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) t = (i == j - 1) ? top[i] : t;
+    tau[r] = fminf(tau[r], t);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_tau_from_appends(int64_t q, int parts, int cap, const int* cnt, const uint2* buf,
+                                    int j, float* tau, cudaStream_t st, int* launches) {
+  if (q <= 0) return cudaSuccess;
+  j = j < 1 ? 1 : (j > 32 ? 32 : j);  // a smaller j only lowers tau (fewer candidates, still valid)
+  k_tau_from_appends<<<(unsigned)((q + 127) / 128), 128, 0, st>>>(q, parts, cap, cnt, buf, j, tau);
+  *launches += 1;
+  return cudaGetLastError();
+}
 
 cudaError_t launch_tau_combine(int64_t q, int nv, int j, const float* samp, float* tau,
                                cudaStream_t st, int* launches) {
@@ -593,6 +635,12 @@ cudaError_t launch_knn_tc3(const Image& A, const Image& B, int64_t q_begin, int6
   if (dbg & 3)                                                                                    \
     return fmt == 1 ? launch3<D, 1, 2, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
                     : launch3<D, 2, 2, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+  if ((dbg & 8) && m.R > 0)  /* profiling trace build */                                       \
+    return fmt == 1 ? launch3<D, 1, 8, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
+                    : launch3<D, 2, 8, FW, 1>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+  if (dbg & 8)                                                                                    \
+    return fmt == 1 ? launch3<D, 1, 8, FW, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
+                    : launch3<D, 2, 8, FW, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
   if (m.R > 0 && m.colmode)                                                                      \
     return fmt == 1 ? launch3<D, 1, 0, FW, 1, true>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
                     : launch3<D, 2, 0, FW, 1, true>(A, B, q_begin, q_count, self_join, m, num_sms, st); \

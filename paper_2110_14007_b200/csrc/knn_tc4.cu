@@ -21,6 +21,16 @@
 //   t_full[acc]         to both CTAs.
 //   t_empty[acc]        CTA 0 only: all 32 filter warps of the pair arrive
 //                       (CTA 1's remotely) before the accumulator is reused.
+//
+// Two tile geometries (template NB, NACC): 256-column tiles with two
+// accumulators (2 x 256 TMEM columns; the tile grid of the list-based sample
+// pass), or 160-column tiles with THREE accumulators (3 x 160): the per-tile
+// trace showed the accumulator hand-off on the critical path with two
+// (the MMA of tile t+2 waits for the filter warps of both SMs to release t);
+// with three, two tiles' MMAs are queued while the filter drains the third.
+// A tile is any multiple of 8 rows of the swizzled image (the image keeps 256
+// rows of slack past n_pad for the last 160-row tile).  smode 1 sweeps only the
+// sample tiles t % R == 0 (the three-stage candidate selection).
 #include <math_constants.h>
 
 #include <algorithm>
@@ -34,17 +44,16 @@ namespace tod {
 namespace {
 
 constexpr int kBM = 128;        // query rows per CTA (= TMEM lanes)
-constexpr int kBN = 256;        // reference columns per tile (MMA N)
-static_assert(kBN == 256, "filter addresses accumulators as acc << 8");
-constexpr int kBNH = 128;       // reference rows of each tile staged per CTA
+constexpr int kMaxAcc = 3;      // accumulators in the TMEM ring (NACC <= 3)
 constexpr int kExtraRB = 32;
 constexpr int kSmemMax = 232448;
 constexpr int kMaxStage = 6;
 
 __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
 
-template <int DPAD>
+template <int DPAD, int NB>
 struct Cfg4 {
+  static constexpr int NBH = NB / 2;  // reference rows of each tile staged per CTA
   static constexpr int RB = DPAD * 2 < 128 ? DPAD * 2 : 128;
   static constexpr int NKB = DPAD * 2 / RB;
   static constexpr int LAYOUT = RB == 128 ? 2 : (RB == 64 ? 4 : 6);
@@ -53,33 +62,45 @@ struct Cfg4 {
   static constexpr int A_ONE = kBM * (DPAD + 16) * 2;
   static constexpr int A_STRIDE = align_up(A_ONE, 1024);
   static constexpr int A_EXTRA = kBM * NKB * RB;
-  static constexpr int B_BYTES = kBNH * (DPAD + 16) * 2;   // this CTA's half tile
+  static constexpr int B_BYTES = NBH * (DPAD + 16) * 2;    // this CTA's half tile
   static constexpr int B_STRIDE = align_up(B_BYTES, 1024);
-  static constexpr int B_EXTRA = kBNH * NKB * RB;
+  static constexpr int B_EXTRA = NBH * NKB * RB;
 };
 
-template <int DPAD, int FW>
+template <int DPAD, int FW, int NB>
 __host__ __device__ constexpr int smem4(int nstage, int* off_b, int* off_p, int* off_bar) {
-  using C = Cfg4<DPAD>;
+  using C = Cfg4<DPAD, NB>;
   int o = C::A_STRIDE;
   *off_b = o;
   o += nstage * C::B_STRIDE;
   *off_p = o;
   o += FW * kPendRun * 32 * 8;
   *off_bar = o;
-  o += 8 * (2 * kMaxStage + 2 + 4) + 16;
+  o += 8 * (2 * kMaxStage + 2 + 2 * kMaxAcc) + 16;
   return o + 1024;
 }
 
-template <int DPAD, int FW>
+template <int DPAD, int FW, int NB>
 int pick_stages4() {
   int a, b, c;
   for (int ns = kMaxStage; ns >= 2; --ns)
-    if (smem4<DPAD, FW>(ns, &a, &b, &c) <= kSmemMax) return ns;
+    if (smem4<DPAD, FW, NB>(ns, &a, &b, &c) <= kSmemMax) return ns;
   return 0;
 }
 
-template <int DPAD, int FMT, int DBG, int FW, bool COL>
+// TMEM reads of one filter warp's part: BH consecutive columns (64 or 40).
+template <int BH>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float* v) {
+  static_assert(BH == 64 || BH == 40, "part width");
+  if constexpr (BH == 64) {
+    tmem_ld64(taddr, *reinterpret_cast<float(*)[64]>(v));
+  } else {
+    tmem_ld32(taddr, *reinterpret_cast<float(*)[32]>(v));
+    tmem_ld8(taddr + 32, v + 32);
+  }
+}
+
+template <int DPAD, int FMT, int DBG, int FW, bool COL, int NB, int NACC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
     k_knn_tc4(const uint8_t* __restrict__ a_img, size_t a_region, size_t a_extra,
               const uint8_t* __restrict__ b_img, size_t b_region, size_t b_extra, int64_t b_tiles,
@@ -87,15 +108,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
               int self_join, int S, int R, int nstage,
               const float* __restrict__ tau_v, int tau_lists,
               uint2* __restrict__ mbuf, int* __restrict__ mcnt, int cap, int64_t col0, int vote,
-              int stagger, int spin) {
-  using C = Cfg4<DPAD>;
+              int smode, long long* __restrict__ trace) {
+  // trace (profiling, TOD_F_DEBUG_TRACE): the leader CTA of cluster 0, per tile,
+  // the 16 clock64 stamps of knn_tc3.cu (tools/trace_main.py)
+  constexpr int kTraceTiles = 2048;
+  using C = Cfg4<DPAD, NB>;
   constexpr int H = FW / 4;
-  constexpr int BH = kBN / H;
+  constexpr int BH = NB / H;
+  constexpr int NBH = C::NBH;
+  static_assert(NB * NACC <= 512 && NACC <= kMaxAcc, "accumulator ring must fit TMEM");
   extern __shared__ uint8_t smem_raw[];
   // identical layout in both CTAs: every offset below is valid in the peer too
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   int off_b, off_p, off_bar;
-  smem4<DPAD, FW>(nstage, &off_b, &off_p, &off_bar);
+  smem4<DPAD, FW, NB>(nstage, &off_b, &off_p, &off_bar);
   uint8_t* sA = smem;
   uint8_t* sB = smem + off_b;
   const uint32_t s_pend = smem_u32(smem + off_p);
@@ -104,9 +130,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
   uint64_t* empty = bars + kMaxStage;
   uint64_t* a_full = bars + 2 * kMaxStage;
   uint64_t* a_empty = a_full + 1;
-  uint64_t* t_full = a_empty + 1;   // [2]
-  uint64_t* t_empty = t_full + 2;   // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + 2);
+  uint64_t* t_full = a_empty + 1;      // [NACC]
+  uint64_t* t_empty = t_full + NACC;   // [NACC]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_empty + NACC);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -120,7 +146,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
     }
     mbar_init(a_full, leader ? 2 : 1);
     mbar_init(a_empty, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NACC; ++i) {
       mbar_init(&t_full[i], 1);
       mbar_init(&t_empty[i], 2 * FW);
     }
@@ -133,17 +159,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
   const uint32_t tmem_base = *tmem_slot;
   const int64_t n_items = n_qpairs * S;
   const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  constexpr bool TRACE = (DBG & 8) != 0;  // profiling build only
+  const bool tron = TRACE && trace != nullptr && blockIdx.x == 0;
 
   if (warp == 0) {
     // -------------------------------------------------------------- producer
     // (both CTAs: own query tile, own half of each reference tile)
     int stage = 0;
     uint32_t phase = 0, aphase = 0;
+    int ptr = 0;
     for (int64_t item = cid; item < n_items; item += ncl) {
       const int64_t qtl = (item % n_qpairs) * 2 + rank;
       const int c = (int)(item / n_qpairs);
-      TileSeq<0, 1> ts;
-      ts.begin(b_tiles, S, R, c, cid, ncl, stagger);
+      TileSeqRT ts;
+      ts.begin(b_tiles, S, R, c, smode);
       int issued = 0;
       bool a_done = false;
       auto load_a = [&]() {
@@ -163,14 +192,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
       for (; ts.more(); ts.next()) {
         if (!a_done && issued == nstage - 1) load_a();
         mbar_wait_cl_backoff(&empty[stage], phase ^ 1);
+        if constexpr (TRACE)
+          if (tron && lane == 0 && ptr < kTraceTiles) trace[ptr * 16 + 7] = clock64();
+        ++ptr;
         if (elect_one()) {
           mbar_arrive_expect_tx(&full[stage], C::B_BYTES);
           uint8_t* dst = sB + stage * C::B_STRIDE;
-          const int64_t row0 = (int64_t)ts.t * kBN + rank * kBNH;
+          const int64_t row0 = (int64_t)ts.t * NB + rank * NBH;
           for (int kb = 0; kb < C::NKB; ++kb)
-            bulk_g2s(dst + kb * kBNH * C::RB, b_img + kb * b_region + row0 * C::RB,
-                     kBNH * C::RB, &full[stage]);
-          bulk_g2s(dst + C::B_EXTRA, b_img + b_extra + row0 * kExtraRB, kBNH * kExtraRB,
+            bulk_g2s(dst + kb * NBH * C::RB, b_img + kb * b_region + row0 * C::RB,
+                     NBH * C::RB, &full[stage]);
+          bulk_g2s(dst + C::B_EXTRA, b_img + b_extra + row0 * kExtraRB, NBH * kExtraRB,
                    &full[stage]);
         }
         __syncwarp();
@@ -184,7 +216,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
     }
   } else if (warp == 1 && leader) {
     // --------------------------------------------- MMA issuer (leader CTA)
-    constexpr uint32_t IDESC = idesc_f16(2 * kBM, kBN, FMT == 1 ? 0u : 1u);
+    constexpr uint32_t IDESC = idesc_f16(2 * kBM, NB, FMT == 1 ? 0u : 1u);
     constexpr int NK = C::KSTEPS + 1;
     const uint32_t a_base = smem_u32(sA);
     const uint32_t b_base = smem_u32(sB);
@@ -194,38 +226,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
       const int kb = (ks * 32) / C::RB;
       const int koff = (ks * 32) % C::RB;
       adesc[ks] = smem_desc(a_base + kb * kBM * C::RB + koff, C::SBO, C::LAYOUT);
-      bdesc[ks] = smem_desc(b_base + kb * kBNH * C::RB + koff, C::SBO, C::LAYOUT);
+      bdesc[ks] = smem_desc(b_base + kb * NBH * C::RB + koff, C::SBO, C::LAYOUT);
     }
     adesc[C::KSTEPS] = smem_desc(a_base + C::A_EXTRA, 8 * kExtraRB, 6);
     bdesc[C::KSTEPS] = smem_desc(b_base + C::B_EXTRA, 8 * kExtraRB, 6);
     int stage = 0, acc = 0;
     uint32_t phase = 0, acc_phase = 0, aphase = 0;
+    int mtr = 0;
     for (int64_t item = cid; item < n_items; item += ncl) {
       const int c = (int)(item / n_qpairs);
-      TileSeq<0, 1> ts;
-      ts.begin(b_tiles, S, R, c, cid, ncl, stagger);
+      TileSeqRT ts;
+      ts.begin(b_tiles, S, R, c, smode);
       mbar_wait_cl(a_full, aphase);
       aphase ^= 1;
       tc_fence_after();
       for (; ts.more(); ts.next()) {
-        mbar_wait_sel(smem_u32(&full[stage]), phase, spin);
-        mbar_wait_sel(smem_u32(&t_empty[acc]), acc_phase ^ 1, spin);
+        const bool tr = TRACE && tron && lane == 0 && mtr < kTraceTiles;
+        if (tr) trace[mtr * 16 + 0] = clock64();
+        mbar_wait_cl(&full[stage], phase);
+        if (tr) trace[mtr * 16 + 1] = clock64();
+        mbar_wait_cl(&t_empty[acc], acc_phase ^ 1);
+        if (tr) trace[mtr * 16 + 2] = clock64();
         tc_fence_after();
         const uint64_t bst = (uint64_t)((stage * C::B_STRIDE) >> 4);
         if (elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < NK; ++ks)
-            tc_mma_f16_2cta(tmem_base + acc * kBN, adesc[ks], bdesc[ks] + bst, IDESC,
+            tc_mma_f16_2cta(tmem_base + acc * NB, adesc[ks], bdesc[ks] + bst, IDESC,
                             ks > 0 ? 1u : 0u);
           tc_commit_mc(&t_full[acc], 0x3);
           tc_commit_mc(&empty[stage], 0x3);
         }
         __syncwarp();
+        if (tr) trace[mtr * 16 + 8] = clock64();
+        ++mtr;
         if (++stage == nstage) {
           stage = 0;
           phase ^= 1;
         }
-        if (++acc == 2) {
+        if (++acc == NACC) {
           acc = 0;
           acc_phase ^= 1;
         }
@@ -241,8 +280,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
     uint32_t phase = 0, aphase = 0;
     for (int64_t item = cid; item < n_items; item += ncl) {
       const int c = (int)(item / n_qpairs);
-      TileSeq<0, 1> ts;
-      ts.begin(b_tiles, S, R, c, cid, ncl, stagger);
+      TileSeqRT ts;
+      ts.begin(b_tiles, S, R, c, smode);
       // the producer may issue up to nstage-1 B tiles before the A tile: the
       // forwarder must not block on A first (the leader needs those B tiles
       // to finish the previous item, which releases A)
@@ -280,7 +319,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
     constexpr uint32_t SLOT = kPendSlot;
     const uint32_t pbase = s_pend + (f * kPendRun * 32 + lane) * 8;
     uint32_t pa = pbase;
-    uint32_t tcount = 0;  // tiles consumed: accumulator = tcount & 1, phase = (tcount >> 1) & 1
+    uint32_t acc = 0, acc_phase = 0;  // accumulator ring position of the next tile
+    int etr = 0;
     const uint32_t taddr0 = tmem_base + ((uint32_t)(q * 32) << 16) + h * BH;
     const uint32_t r_tempty = mapa_shared(smem_u32(t_empty), 0);
     const uint32_t s_tfull = smem_u32(t_full), s_tempty = smem_u32(t_empty);
@@ -290,12 +330,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
       const int64_t row = (qt0 + qtl) * kBM + rt;
       const bool valid = row >= q_begin && row < q_end;
       const int64_t r = valid ? row - q_begin : 0;
-      const int self = self_join ? (int)row : -1;
-      // reference rows = the block [col0, col0 + n_ref) of the global index space
-      const int64_t qrow0 = (qt0 + qtl) * kBM;
-      const int t_self = (self_join && qrow0 >= col0 && qrow0 < col0 + n_ref)
-                             ? (int)((qrow0 - col0) / kBN) : -1;
-      const int t_last = (int)((n_ref - 1) / kBN);
+      // reference rows = the block [col0, col0 + n_ref) of the global index space;
+      // the self column (block-relative) and padding columns are never candidates
+      const int64_t selfc = self_join ? row - col0 : -1;
       const int scol0 = (int)col0;
       float tau = -CUDART_INF_F;
       if (valid) {
@@ -316,20 +353,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
         }
         pa = pbase;
       };
-      TileSeq<0, 1> ts;
-      ts.begin(b_tiles, S, R, c, cid, ncl, stagger);
+      TileSeqRT ts;
+      ts.begin(b_tiles, S, R, c, smode);
       for (; ts.more(); ts.next()) {
-        const uint32_t acc = tcount & 1u;
-        mbar_wait_sel(s_tfull + acc * 8, (tcount >> 1) & 1u, spin);
+        const bool tr = TRACE && tron && warp == 2 && lane == 0 && etr < kTraceTiles;
+        if (tr) trace[etr * 16 + 3] = clock64();
+        mbar_wait_u32(s_tfull + acc * 8, acc_phase);
+        if (tr) trace[etr * 16 + 4] = clock64();
         tc_fence_after();
         float v[BH];
-        const uint32_t taddr = taddr0 + (acc << 8);  // acc * kBN
+        const uint32_t taddr = taddr0 + acc * NB;
         if (!(DBG & 2)) {
-#pragma unroll
-          for (int u = 0; u < BH / 64; ++u)
-            tmem_ld64(taddr + 64 * u, *reinterpret_cast<float(*)[64]>(v + 64 * u));
+          tmem_ld_cols<BH>(taddr, v);
           tmem_ld_wait();
         }
+        if (tr) trace[etr * 16 + 9] = clock64();
         auto release = [=]() {
           tc_fence_before();
           __syncwarp();
@@ -340,10 +378,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
         };
         // column candidates (COL): filter_part releases after its vote
         if (!COL || DBG != 0) release();
-        ++tcount;
+        if (tr) trace[etr * 16 + 5] = clock64();
+        if constexpr (TRACE)
+          if (tron && warp == 1 + FW && lane == 0 && etr < kTraceTiles) trace[etr * 16 + 10] = clock64();
+        ++etr;
+        if (++acc == NACC) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
         if (DBG & 3) continue;
         const int t = ts.t;
-        const int j0 = t * kBN + h * BH;
+        const int j0 = t * NB + h * BH;
         if constexpr ((DBG & 4) != 0) {
           // diagnostics (tod_debug_mainpass): raw w~ of the first query tile (CTA 0)
           if (qtl == 0) {
@@ -354,11 +399,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
           }
           continue;
         }
-        const bool need_mask = t == t_self || t == t_last;
+        const bool need_mask = (uint64_t)(selfc - j0) < (uint64_t)BH || j0 + BH > n_ref;
         if (need_mask) {
 #pragma unroll
           for (int e = 0; e < BH; ++e)
-            v[e] = (scol0 + j0 + e == self || j0 + e >= n_ref) ? CUDART_INF_F : v[e];
+            v[e] = (j0 + e == selfc || j0 + e >= n_ref) ? CUDART_INF_F : v[e];
         }
         auto reload = [=](int gg, float* c8) {
           tmem_ld8(taddr + 8 * gg, c8);
@@ -366,13 +411,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
           if (need_mask) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-              const int jj = j0 + 8 * gg + e;
-              if (scol0 + jj == self || jj >= n_ref) c8[e] = CUDART_INF_F;
+              const int64_t jj = j0 + 8 * gg + e;
+              if (jj == selfc || jj >= n_ref) c8[e] = CUDART_INF_F;
             }
           }
         };
         filter_part<BH, COL>(v, tau, (scol0 + j0) >> 3, pa, pbase, vote != 0, flush, reload,
                              release);  // col0 % 256 == 0
+        if (tr) trace[(etr - 1) * 16 + 6] = clock64();
       }
       flush();
     }
@@ -385,15 +431,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
   }
 }
 
-template <int DPAD, int FMT, int DBG, int FW, bool COL>
+template <int DPAD, int FMT, int DBG, int FW, bool COL, int NB, int NACC>
 cudaError_t launch4(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                     bool self_join, const MainPass& m, int num_sms, cudaStream_t st) {
-  const int nstage = pick_stages4<DPAD, FW>();
+  const int nstage = pick_stages4<DPAD, FW, NB>();
   if (nstage < 3) return cudaErrorInvalidValue;
   if (m.parts != FW / 4) return cudaErrorInvalidValue;
   int a, b, c;
-  const int smem = smem4<DPAD, FW>(nstage, &a, &b, &c);
-  auto kern = k_knn_tc4<DPAD, FMT, DBG, FW, COL>;
+  const int smem = smem4<DPAD, FW, NB>(nstage, &a, &b, &c);
+  auto kern = k_knn_tc4<DPAD, FMT, DBG, FW, COL, NB, NACC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t qt0 = q_begin / kBM;
@@ -405,8 +451,8 @@ cudaError_t launch4(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
   kern<<<(unsigned)(2 * pairs), 64 + 32 * FW, smem, st>>>(
       reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(), A.extra_offset(),
       reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
-      (B.n + kBN - 1) / kBN, B.n, qt0, n_qpairs, q_begin, q_begin + q_count, self_join ? 1 : 0, m.S,
-      m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap, m.col0, m.vote, m.stagger, m.spin);
+      (B.n + NB - 1) / NB, B.n, qt0, n_qpairs, q_begin, q_begin + q_count, self_join ? 1 : 0, m.S,
+      m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap, m.col0, m.vote, m.smode, m.trace);
   return cudaGetLastError();
 }
 
@@ -419,13 +465,21 @@ cudaError_t launch4(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
 int tc4_fits(int dpad, int parts) {
   if (parts != 4) return 0;
   switch (dpad) {
-    case 16: return pick_stages4<16, 16>() >= 3;
-    case 32: return pick_stages4<32, 16>() >= 3;
-    case 64: return pick_stages4<64, 16>() >= 3;
+    case 16: return pick_stages4<16, 16, 256>() >= 3 && pick_stages4<16, 16, 160>() >= 3;
+    case 32: return pick_stages4<32, 16, 256>() >= 3 && pick_stages4<32, 16, 160>() >= 3;
+    case 64: return pick_stages4<64, 16, 256>() >= 3 && pick_stages4<64, 16, 160>() >= 3;
   }
   return 0;
 }
 int tc4_preferred(int dpad) { return dpad == 64; }
+
+// MainPass.nb = 160: the three-accumulator ring (160-column tiles); else 256.
+template <int D, int FMT, int DBG, bool COL>
+cudaError_t launch4_nb(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
+                       bool self_join, const MainPass& m, int num_sms, cudaStream_t st) {
+  if (m.nb == 160) return launch4<D, FMT, DBG, 16, COL, 160, 3>(A, B, q_begin, q_count, self_join, m, num_sms, st);
+  return launch4<D, FMT, DBG, 16, COL, 256, 2>(A, B, q_begin, q_count, self_join, m, num_sms, st);
+}
 
 cudaError_t launch_knn_tc4(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                            bool self_join, int fmt, const MainPass& m, int num_sms, int dbg,
@@ -434,16 +488,19 @@ cudaError_t launch_knn_tc4(const Image& A, const Image& B, int64_t q_begin, int6
 #define TOD_TC4_CASE(D)                                                                          \
   case D:                                                                                       \
     if (dbg & 4)                                                                                \
-      return fmt == 1 ? launch4<D, 1, 4, 16, false>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
-                      : launch4<D, 2, 4, 16, false>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+      return fmt == 1 ? launch4_nb<D, 1, 4, false>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
+                      : launch4_nb<D, 2, 4, false>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
     if (dbg & 3)                                                                                \
-      return fmt == 1 ? launch4<D, 1, 2, 16, false>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
-                      : launch4<D, 2, 2, 16, false>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+      return fmt == 1 ? launch4_nb<D, 1, 2, false>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
+                      : launch4_nb<D, 2, 2, false>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+    if (dbg & 8)  /* profiling trace build */                                                   \
+      return fmt == 1 ? launch4_nb<D, 1, 8, false>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
+                      : launch4_nb<D, 2, 8, false>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
     if (m.colmode)                                                                              \
-      return fmt == 1 ? launch4<D, 1, 0, 16, true>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
-                      : launch4<D, 2, 0, 16, true>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
-    return fmt == 1 ? launch4<D, 1, 0, 16, false>(A, B, q_begin, q_count, self_join, m, num_sms, st)   \
-                    : launch4<D, 2, 0, 16, false>(A, B, q_begin, q_count, self_join, m, num_sms, st);
+      return fmt == 1 ? launch4_nb<D, 1, 0, true>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
+                      : launch4_nb<D, 2, 0, true>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+    return fmt == 1 ? launch4_nb<D, 1, 0, false>(A, B, q_begin, q_count, self_join, m, num_sms, st)   \
+                    : launch4_nb<D, 2, 0, false>(A, B, q_begin, q_count, self_join, m, num_sms, st);
   switch (A.dpad) {
     TOD_TC4_CASE(16)
     TOD_TC4_CASE(32)

@@ -98,14 +98,14 @@ __device__ __forceinline__ void tmem_ld_part(uint32_t taddr, float* v) {
   if constexpr ((BH % 16) == 8) tmem_ld8(taddr + c, v + c);
 }
 
-template <int DPAD, int FMT, int NB, bool COL>
+template <int DPAD, int FMT, int NB, bool COL, bool TRACE>
 __global__ void __launch_bounds__(64 + 32 * kFW, 1)
     k_knn_tc5(const uint8_t* __restrict__ a_img, size_t a_region, size_t a_extra,
               const uint8_t* __restrict__ b_img, size_t b_region, size_t b_extra, int64_t b_tiles,
               int64_t n_ref, int64_t qt0, int64_t n_qtiles, int64_t q_begin, int64_t q_end,
               int self_join, int S, int nstage, const float* __restrict__ tau_v, int tau_lists,
               uint2* __restrict__ mbuf, int* __restrict__ mcnt, int cap, int64_t col0, int vote,
-              long long* __restrict__ trace, int spin) {
+              long long* __restrict__ trace) {
   using C = Cfg5<DPAD, NB>;
   constexpr int BH = C::BH;
   constexpr int H = 4;
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(64 + 32 * kFW, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const bool tron = trace != nullptr && blockIdx.x == 0;
+  const bool tron = TRACE && trace != nullptr && blockIdx.x == 0;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < nstage; ++i) {
@@ -179,7 +179,8 @@ __global__ void __launch_bounds__(64 + 32 * kFW, 1)
         // the item's first B tiles are fetched while the MMA drains the previous item
         if (!a_done && issued == nstage - 1) load_a();
         mbar_wait_backoff(&empty[stage], phase ^ 1);
-        if (tron && lane == 0 && ptr < kTraceTiles) trace[ptr * 16 + 7] = clock64();
+        if constexpr (TRACE)
+          if (tron && lane == 0 && ptr < kTraceTiles) trace[ptr * 16 + 7] = clock64();
         ++ptr;
         if (elect_one()) {
           mbar_arrive_expect_tx(&full[stage], C::B_BYTES);
@@ -227,11 +228,11 @@ __global__ void __launch_bounds__(64 + 32 * kFW, 1)
       aphase ^= 1;
       tc_fence_after();
       for (int t = t0; t < t1; ++t) {
-        const bool tr = tron && lane == 0 && mtr < kTraceTiles;
+        const bool tr = TRACE && tron && lane == 0 && mtr < kTraceTiles;
         if (tr) trace[mtr * 16 + 0] = clock64();
-        mbar_wait_sel(s_full + stage * 8, phase, spin);
+        mbar_wait_u32(s_full + stage * 8, phase);
         if (tr) trace[mtr * 16 + 1] = clock64();
-        mbar_wait_sel(s_tempty + acc * 8, acc_phase ^ 1, spin);
+        mbar_wait_u32(s_tempty + acc * 8, acc_phase ^ 1);
         if (tr) trace[mtr * 16 + 2] = clock64();
         ++mtr;
         tc_fence_after();
@@ -299,9 +300,9 @@ __global__ void __launch_bounds__(64 + 32 * kFW, 1)
         pa = pbase;
       };
       for (int t = t0; t < t1; ++t) {
-        const bool tr = tron && warp == 2 && lane == 0 && etr < kTraceTiles;
+        const bool tr = TRACE && tron && warp == 2 && lane == 0 && etr < kTraceTiles;
         if (tr) trace[etr * 16 + 3] = clock64();
-        mbar_wait_sel(s_tfull + acc * 8, acc_phase, spin);
+        mbar_wait_u32(s_tfull + acc * 8, acc_phase);
         if (tr) trace[etr * 16 + 4] = clock64();
         tc_fence_after();
         float v[BH];
@@ -316,7 +317,8 @@ __global__ void __launch_bounds__(64 + 32 * kFW, 1)
         };
         if (!COL) release();  // column candidates: filter_part releases after its vote
         if (tr) trace[etr * 16 + 5] = clock64();
-        if (tron && warp == 1 + kFW && lane == 0 && etr < kTraceTiles) trace[etr * 16 + 10] = clock64();
+        if constexpr (TRACE)
+          if (tron && warp == 1 + kFW && lane == 0 && etr < kTraceTiles) trace[etr * 16 + 10] = clock64();
         ++etr;
         if (++acc == kNacc) {
           acc = 0;
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(64 + 32 * kFW, 1)
   }
 }
 
-template <int DPAD, int FMT, int NB, bool COL>
+template <int DPAD, int FMT, int NB, bool COL, bool TRACE = false>
 cudaError_t launch5(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                     bool self_join, const MainPass& m, int num_sms, cudaStream_t st) {
   const int nstage = pick_stages5<DPAD, NB>();
@@ -364,7 +366,7 @@ cudaError_t launch5(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
   if (m.parts != 4 || m.R != 0) return cudaErrorInvalidValue;
   int a, b, c;
   const int smem = smem5<DPAD, NB>(nstage, &a, &b, &c);
-  auto kern = k_knn_tc5<DPAD, FMT, NB, COL>;
+  auto kern = k_knn_tc5<DPAD, FMT, NB, COL, TRACE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t qt0 = q_begin / kBM;
@@ -378,7 +380,7 @@ cudaError_t launch5(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
       reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(), A.extra_offset(),
       reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(), b_tiles, B.n,
       qt0, qt1 - qt0, q_begin, q_begin + q_count, self_join ? 1 : 0, S, nstage, m.tau_v,
-      m.tau_lists, m.buf, m.cnt, m.cap, m.col0, m.vote, m.trace, m.spin);
+      m.tau_lists, m.buf, m.cnt, m.cap, m.col0, m.vote, m.trace);
   return cudaGetLastError();
 }
 
@@ -401,6 +403,9 @@ cudaError_t launch_knn_tc5(const Image& A, const Image& B, int64_t q_begin, int6
   *launches += 1;
 #define TOD_TC5_CASE(D)                                                                          \
   case D:                                                                                       \
+    if (m.trace)  /* profiling trace build */                                                   \
+      return fmt == 1 ? launch5<D, 1, kNB, false, true>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
+                      : launch5<D, 2, kNB, false, true>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
     if (m.colmode)                                                                              \
       return fmt == 1 ? launch5<D, 1, kNB, true>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
                       : launch5<D, 2, kNB, true>(A, B, q_begin, q_count, self_join, m, num_sms, st); \

@@ -57,30 +57,6 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t saddr, uint32_t parity) {
   while (!mbar_try_wait_u32(saddr, parity)) {
   }
 }
-// Pure polling wait (mbarrier.test_wait, never suspends): for the latency-critical
-// accumulator hand-off between the MMA issuer and the filter warps, where a
-// suspended try_wait's wake-up adds to every tile's critical path.
-__device__ __forceinline__ bool mbar_test_u32(uint32_t saddr, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(saddr), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-// spin: 0 = suspend-hinted try_wait, 1 = poll
-__device__ __forceinline__ void mbar_wait_sel(uint32_t saddr, uint32_t parity, int spin) {
-  if (spin) {
-    while (!mbar_test_u32(saddr, parity)) {
-    }
-  } else {
-    while (!mbar_try_wait_u32(saddr, parity)) {
-    }
-  }
-}
 __device__ __forceinline__ void mbar_arrive_u32(uint32_t saddr) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr) : "memory");
 }

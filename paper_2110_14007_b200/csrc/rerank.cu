@@ -564,6 +564,8 @@ __device__ __forceinline__ void rerank_groups_row(
   int G = 0;
   bool overflow = false;
   const int L = lists * kp;
+  float vmin = CUDART_INF_F;  // the row's certificate threshold
+  for (int c = 0; c < lists; ++c) vmin = fminf(vmin, cand_v[r * lists + c]);
   for (int e0 = 0; e0 < L; e0 += 32) {
     const int e = e0 + lane;
     const int g = e < L ? cand_idx[r * L + e] : -1;
@@ -589,34 +591,39 @@ __device__ __forceinline__ void rerank_groups_row(
     }
     const int M = off[4];
     const int colflag = cp.colmode ? kColFlag : 0;  // main-pass appends are columns
+    // appends at or above the row's certificate threshold vmin are dropped: they
+    // bound nothing a certified row needs (its top-k lies strictly below
+    // LB(vmin)), and UB stays valid over the rest (three-stage: the sample-tile
+    // appends between tau and tau0)
     for (int e0 = 0; e0 < M; e0 += 128) {
       uint2 kv[4];
-      int pos[4];
+      bool keep[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int e = e0 + u * 32 + lane;
-        pos[u] = -1;
+        keep[u] = false;
         if (e < M) {
           int h = 0;
 #pragma unroll
           for (int q = 1; q < 4; ++q) h += e >= off[q];
           kv[u] = __ldcg(mbuf + (r * mparts + h) * (int64_t)mcap + (e - off[h]));
-          pos[u] = G + e;
+          keep[u] = __uint_as_float(kv[u].x) < vmin;
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (pos[u] >= 0 && pos[u] < kSelMax) {
-          gk[pos[u]] = __uint_as_float(kv[u].x);
-          gid[pos[u]] = (int)kv[u].y | colflag;
+      for (int u = 0; u < 4; ++u) {
+        const unsigned bm = __ballot_sync(0xffffffffu, keep[u]);
+        const int pos = G + __popc(bm & ((1u << lane) - 1u));
+        if (keep[u] && pos < kSelMax) {
+          gk[pos] = __uint_as_float(kv[u].x);
+          gid[pos] = (int)kv[u].y | colflag;
         }
+        G += __popc(bm);
+      }
     }
-    G += M;
   }
   overflow |= G > kSelMax;
   if (G > kSelMax) G = kSelMax;
-  float vmin = CUDART_INF_F;
-  for (int c = 0; c < lists; ++c) vmin = fminf(vmin, cand_v[r * lists + c]);
   __syncwarp();
   // ---- 1-2. UB and the candidates that can hold a top-k column: groups compacted
   // in place into gid[0, nvg), columns into the (then free) ub scratch; groups
@@ -900,6 +907,8 @@ __global__ void __launch_bounds__(kGrpWarps * 32, 4)
     int G = 0;
     bool overflow = false;
     const int L = lists * kp;
+    float vmin = CUDART_INF_F;  // the row's certificate threshold
+    for (int c = 0; c < lists; ++c) vmin = fminf(vmin, cand_v[r * lists + c]);
     for (int e0 = 0; e0 < L; e0 += 32) {
       const int e = e0 + lane;
       const int g = e < L ? cand_idx[r * L + e] : -1;
@@ -924,34 +933,39 @@ __global__ void __launch_bounds__(kGrpWarps * 32, 4)
       }
       const int M = off[4];
       const int colflag = cp.colmode ? kColFlag : 0;  // main-pass appends are columns
+      // appends at or above the row's certificate threshold vmin are dropped: they
+      // bound nothing a certified row needs (its top-k lies strictly below
+      // LB(vmin)), and UB stays valid over the rest (three-stage: the sample-tile
+      // appends between tau and tau0)
       for (int e0 = 0; e0 < M; e0 += 128) {
         uint2 kv[4];
-        int pos[4];
+        bool keep[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int e = e0 + u * 32 + lane;
-          pos[u] = -1;
+          keep[u] = false;
           if (e < M) {
             int h = 0;
 #pragma unroll
             for (int q = 1; q < 4; ++q) h += e >= off[q];
             kv[u] = __ldcg(mbuf + (r * mparts + h) * (int64_t)mcap + (e - off[h]));
-            pos[u] = G + e;
+            keep[u] = __uint_as_float(kv[u].x) < vmin;
           }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (pos[u] >= 0 && pos[u] < kSelMax) {
-            gk[pos[u]] = __uint_as_float(kv[u].x);
-            gid[pos[u]] = (int)kv[u].y | colflag;
+        for (int u = 0; u < 4; ++u) {
+          const unsigned bm = __ballot_sync(0xffffffffu, keep[u]);
+          const int pos = G + __popc(bm & ((1u << lane) - 1u));
+          if (keep[u] && pos < kSelMax) {
+            gk[pos] = __uint_as_float(kv[u].x);
+            gid[pos] = (int)kv[u].y | colflag;
           }
+          G += __popc(bm);
+        }
       }
-      G += M;
     }
     overflow |= G > kSelMax;
     if (G > kSelMax) G = kSelMax;
-    float vmin = CUDART_INF_F;
-    for (int c = 0; c < lists; ++c) vmin = fminf(vmin, cand_v[r * lists + c]);
     __syncwarp();
     // UB and the visited groups, as in rerank_groups_row, straight to the row's global list
     double UB;

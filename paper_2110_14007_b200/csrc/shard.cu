@@ -470,9 +470,6 @@ tod_status run_sharded(tod_ctx* ctx, const float* dXl, int64_t n_local, int64_t 
       R.mp.parts = parts;
       R.mp.cap = plan.cap * 2 / parts;
       R.mp.vote = main_vote(n);
-      R.mp.stagger = main_stagger();
-      R.mp.spin = main_spin();
-      R.sm.stagger = main_stagger();
       TOD_TRY(sh.rens(R, R_MBUF, (size_t)q * parts * R.mp.cap * 8, &p));
       R.mp.buf = static_cast<uint2*>(p);
       TOD_TRY(sh.rens(R, R_MCNT, (size_t)q * parts * 4, &p));

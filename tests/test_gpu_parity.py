@@ -155,10 +155,45 @@ def test_main_ring3_parity(pkg, n, d, k, fmt):
     (9_000, 512, 20, "fp16", "0", "0"),   # d = 512: split re-rank with column tasks
 ])
 def test_column_candidates_parity(pkg, n, d, k, fmt, v1, pair):
+    _column_case(pkg, n, d, k, fmt, {"TOD_SAMPLE_V1": v1, "TOD_MAIN_PAIR": pair})
+
+
+@pytest.mark.parametrize("n,d,k,fmt", [
+    (20_000, 64, 10, "fp16"),
+    (12_345, 64, 10, "bf16"),     # ragged tail, second tier
+    (17_001, 64, 20, "fp16"),
+])
+def test_three_stage_selection_parity(pkg, n, d, k, fmt):
+    # the default at d = 64: key-only pre-sample (every 64th tile) -> the CTA-pair
+    # main pass over the sample tiles below tau0 -> tau -> the main pass over the rest
+    X = datagen.gaussian_mixture(n, d, seed=n + 11 * d)
+    with _ctx(pkg, fmt=fmt) as ctx:
+        res = ctx.knn(torch.from_numpy(X).cuda(), k)
+    assert res.stats["sample_pass"] == 3 and res.stats["main_kernel"] == 4, res.stats
+    _check_rows(res, X, k, np.arange(n))
+    if fmt == "fp16":
+        assert res.stats["certified"] >= 0.99 * n, res.stats
+
+
+@pytest.mark.parametrize("n,d,k,fmt,col", [
+    (20_000, 64, 10, "fp16", "0"),
+    (12_345, 64, 10, "bf16", "1"),
+    (17_001, 32, 10, "fp16", "1"),
+    (9_000, 16, 6, "fp16", "0"),
+])
+def test_pair_ring3_parity(pkg, n, d, k, fmt, col):
+    # CTA-pair main pass with 160-column tiles and three accumulators (key-only
+    # sample: the main pass covers every tile), group or column candidates
+    _column_case(pkg, n, d, k, fmt, {"TOD_SAMPLE_V1": "0", "TOD_MAIN_PAIR": "1", "TOD_MAIN_NB": "160",
+                                     "TOD_COLMODE": col}, main_kernel=4)
+
+
+def _column_case(pkg, n, d, k, fmt, extra, main_kernel=None):
     # MainPass.colmode: the main pass appends each column below tau of a passing
     # group (the default for large n); forced on here at sizes the oracle checks
     X = datagen.gaussian_mixture(n, d, seed=n + 7 * d)
-    env = {"TOD_COLMODE": "1", "TOD_VOTE": "1", "TOD_SAMPLE_V1": v1, "TOD_MAIN_PAIR": pair}
+    env = {"TOD_COLMODE": "1", "TOD_VOTE": "1"}
+    env.update(extra)
     os.environ.update(env)
     try:
         with _ctx(pkg, fmt=fmt) as ctx:
@@ -166,6 +201,8 @@ def test_column_candidates_parity(pkg, n, d, k, fmt, v1, pair):
     finally:
         for e in env:
             os.environ.pop(e, None)
+    if main_kernel is not None:
+        assert res.stats["main_kernel"] == main_kernel, res.stats
     rows = np.arange(n) if n <= 20_000 and d <= 64 else np.random.default_rng(1).choice(n, 500, replace=False)
     _check_rows(res, X, k, np.sort(rows))
     if fmt == "fp16":

@@ -20,7 +20,7 @@ ap.add_argument("--fmt", default="fp16")
 ap.add_argument("--out", default="/tmp/tod_trace.bin")
 a = ap.parse_args()
 os.environ["TOD_TRACE_FILE"] = a.out
-os.environ["TOD_MAIN_PAIR"] = "0"
+os.environ.setdefault("TOD_MAIN_PAIR", "0")
 X = torch.from_numpy(datagen.gaussian_mixture(a.n, a.d, seed=0)).cuda()
 with tod.Context(fmt=a.fmt, flags=tod.F_TIMING | (8 << 8)) as ctx:
     for _ in range(3):
