@@ -225,14 +225,14 @@ int main_vote(int64_t n_ref) {
   if (const char* e = getenv("TOD_VOTE")) return atoi(e) != 0;
   return n_ref >= 300000;
 }
-// The single-SM main pass with a three-deep accumulator ring (knn_tc5.cu) for
-// dpad <= 32 when the main pass covers every tile (key-only sample) and no
-// profiling mode is on; TOD_MAIN_RING3 (experiment knob) forces it on (1, also
-// dpad = 64) or off (0).
+// The single-SM main pass with a three-deep accumulator ring (knn_tc5.cu):
+// opt-in only (TOD_MAIN_RING3=1, experiment knob; dpad <= 64, main pass over
+// every tile, no profiling mode) -- measured slower than knn_tc3 at C2
+// (1.41 vs 1.08 ms main kernel, profiles/r02).
 int main_ring3(int dpad, const MainPass& mp, int dbg) {
   if (mp.R != 0 || mp.parts != 4 || (dbg & 7) != 0 || !tc5_fits(dpad)) return 0;
   if (const char* e = getenv("TOD_MAIN_RING3")) return atoi(e) != 0;
-  return dpad <= 32;
+  return 0;
 }
 
 // Column candidates (filter.cuh COL): with rare appends (the vote), the main

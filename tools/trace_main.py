@@ -18,8 +18,12 @@ ap.add_argument("--d", type=int, default=32)
 ap.add_argument("--k", type=int, default=20)
 ap.add_argument("--fmt", default="fp16")
 ap.add_argument("--out", default="/tmp/tod_trace.bin")
+ap.add_argument("--lib", default=None, help="load this libtod.so instead of the in-tree one")
 a = ap.parse_args()
 os.environ["TOD_TRACE_FILE"] = a.out
+if a.lib:
+    import paper_2110_14007_b200.tod as T  # noqa: E402
+    T.load_library(a.lib)
 os.environ.setdefault("TOD_MAIN_PAIR", "0")
 X = torch.from_numpy(datagen.gaussian_mixture(a.n, a.d, seed=0)).cuda()
 with tod.Context(fmt=a.fmt, flags=tod.F_TIMING | (8 << 8)) as ctx:
