@@ -20,7 +20,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_ld(int iters, unsigned long long
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t base = slot + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * 128;
-  float acc = 0.f;
+  float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // independent sums: the
+  // reduction must not be a dependent FADD chain (round 2's first numbers were)
   unsigned long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
     uint32_t r[32];
@@ -38,10 +39,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_ld(int iters, unsigned long long
           : "r"(base + (uint32_t)(c * 32 + (it & 1) * 0)));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int i = 0; i < 32; ++i) acc += __uint_as_float(r[i]);
+      for (int i = 0; i < 32; ++i) acc8[i & 7] += __uint_as_float(r[i]);
     }
   }
   unsigned long long t1 = clock64();
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc += acc8[i];
   if ((threadIdx.x & 31) == 0) cycles[blockIdx.x * NW + warp] = t1 - t0;
   sink[blockIdx.x * NW * 32 + threadIdx.x] = acc;
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -62,7 +66,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_ld4(int iters, unsigned long lon
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t base = slot + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * 128;
-  float acc = 0.f;
+  float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   unsigned long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
     uint32_t r[4][16];
@@ -79,9 +83,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_ld4(int iters, unsigned long lon
 #pragma unroll
     for (int c = 0; c < 4; ++c)
 #pragma unroll
-      for (int i = 0; i < 16; ++i) acc += __uint_as_float(r[c][i]);
+      for (int i = 0; i < 16; ++i) acc8[i & 7] += __uint_as_float(r[c][i]);
   }
   unsigned long long t1 = clock64();
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc += acc8[i];
   if ((threadIdx.x & 31) == 0) cycles[blockIdx.x * NW + warp] = t1 - t0;
   sink[blockIdx.x * NW * 32 + threadIdx.x] = acc;
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -126,5 +133,6 @@ int main() {
   run("ld 4 x16 then wait", k_ld4<4>, 4, 64 * 32 * 4, it);
   run("ld 4 x16 then wait", k_ld4<8>, 8, 64 * 32 * 4, it);
   run("ld 4 x16 then wait", k_ld4<16>, 16, 64 * 32 * 4, it);
+  run("ld 4x32 cols (+wait each)", k_ld<16, 128>, 16, 128 * 32 * 4, it);
   return 0;
 }
