@@ -317,7 +317,14 @@ tod_status prep_tc(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     ref->ready = true;
   }
   TOD_TRY(ensure(ctx, B_EG, (size_t)std::max<int64_t>((n + 7) / 8, 1) * 8, &p));
-  cp->eg = static_cast<const double*>(p);
+  // Per-group residual bounds in the re-rank's UB and visit cut pay where the
+  // quantization residuals are large (bf16: C3 re-rank 28.7 -> 18.8 ms); with
+  // fp16's 8x smaller residuals they visit barely fewer groups and the per-
+  // candidate bound evaluation costs more than it saves (C2: 0.62 -> 0.75 ms).
+  // TOD_GROUP_EMAX (experiment knob) 1 / 0 forces them on / off.
+  bool use_eg = fmt == 2;
+  if (const char* e = getenv("TOD_GROUP_EMAX")) use_eg = atoi(e) != 0;
+  cp->eg = use_eg ? static_cast<const double*>(p) : nullptr;
   cp->ecol = B.e;
   const float* qsrc = self ? dX + a_row0 * d : dQ;
   TOD_CUDA(launch_prep_quant(qsrc, a_rows, d, mu, g, fmt, A, 1, st, launches));
