@@ -1,4 +1,5 @@
-// knn_tc4.cu — K2 main pass on CTA PAIRS (tcgen05 cta_group::2), dpad <= 64.
+// knn_tc4.cu — K2 main pass on CTA PAIRS (tcgen05 cta_group::2); dpad <= 64 with
+// the query tile resident, dpad > 64 K-pipelined (A and B slices streamed per K region).
 //
 // Same computation as knn_tc3.cu (the append-only threshold filter of the
 // two-pass candidate selection; arithmetic of Eq. (3)'s right-hand
@@ -65,14 +66,23 @@ struct Cfg4 {
   static constexpr int B_BYTES = NBH * (DPAD + 16) * 2;    // this CTA's half tile
   static constexpr int B_STRIDE = align_up(B_BYTES, 1024);
   static constexpr int B_EXTRA = NBH * NKB * RB;
+  // K-pipelined mode (dpad > 64): each CTA streams its own A slice and its half
+  // of the B slice of one 64-element K region (or of the 16-wide extra block)
+  // per ring stage: 32 KB per SM per region against the single-SM kernel's 48 KB
+  // (its 128 query rows + all 256 reference rows) -- the L2 -> SM operand traffic
+  // that bounds the single-SM K-pipelined pass at d = 512.
+  static constexpr bool KP = DPAD > 64;
+  static constexpr int KS_A = kBM * 128;
+  static constexpr int KS_BYTES = kBM * 128 + NBH * 128;
+  static constexpr int KX_BYTES = kBM * kExtraRB + NBH * kExtraRB;
 };
 
 template <int DPAD, int FW, int NB>
 __host__ __device__ constexpr int smem4(int nstage, int* off_b, int* off_p, int* off_bar) {
   using C = Cfg4<DPAD, NB>;
-  int o = C::A_STRIDE;
+  int o = C::KP ? 0 : C::A_STRIDE;
   *off_b = o;
-  o += nstage * C::B_STRIDE;
+  o += nstage * (C::KP ? align_up(C::KS_BYTES, 1024) : C::B_STRIDE);
   *off_p = o;
   o += FW * kPendRun * 32 * 8;
   *off_bar = o;
@@ -162,7 +172,108 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
   constexpr bool TRACE = (DBG & 8) != 0;  // profiling build only
   const bool tron = TRACE && trace != nullptr && blockIdx.x == 0;
 
-  if (warp == 0) {
+  if (warp == 0 && C::KP) {
+    // ------------------------------------------------ producer, K-pipelined
+    // (both CTAs: per K region, own query-tile slice + own half of the B slice)
+    constexpr int KSB = align_up(C::KS_BYTES, 1024);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t item = cid; item < n_items; item += ncl) {
+      const int64_t qtl = (item % n_qpairs) * 2 + rank;
+      const int c = (int)(item / n_qpairs);
+      TileSeqRT ts;
+      ts.begin(b_tiles, S, R, c, smode);
+      for (; ts.more(); ts.next()) {
+        const int64_t row0 = (int64_t)ts.t * NB + rank * NBH;
+        for (int kb = 0; kb <= C::NKB; ++kb) {
+          mbar_wait_cl_backoff(&empty[stage], phase ^ 1);
+          if (elect_one()) {
+            uint8_t* dst = sB + stage * KSB;
+            if (kb < C::NKB) {
+              mbar_arrive_expect_tx(&full[stage], C::KS_BYTES);
+              bulk_g2s(dst, a_img + kb * a_region + qtl * (int64_t)kBM * 128, kBM * 128, &full[stage]);
+              bulk_g2s(dst + C::KS_A, b_img + kb * b_region + row0 * 128, NBH * 128, &full[stage]);
+            } else {
+              mbar_arrive_expect_tx(&full[stage], C::KX_BYTES);
+              bulk_g2s(dst, a_img + a_extra + qtl * (int64_t)kBM * kExtraRB, kBM * kExtraRB,
+                       &full[stage]);
+              bulk_g2s(dst + kBM * kExtraRB, b_img + b_extra + row0 * kExtraRB, NBH * kExtraRB,
+                       &full[stage]);
+            }
+          }
+          __syncwarp();
+          if (++stage == nstage) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1 && leader && C::KP) {
+    // ------------------------------- MMA issuer (leader CTA), K-pipelined
+    constexpr uint32_t IDESC = idesc_f16(2 * kBM, NB, FMT == 1 ? 0u : 1u);
+    constexpr int KSB = align_up(C::KS_BYTES, 1024);
+    const uint32_t s_base = smem_u32(sB);
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    for (int64_t item = cid; item < n_items; item += ncl) {
+      const int c = (int)(item / n_qpairs);
+      TileSeqRT ts;
+      ts.begin(b_tiles, S, R, c, smode);
+      for (; ts.more(); ts.next()) {
+        mbar_wait_cl(&t_empty[acc], acc_phase ^ 1);
+        for (int kb = 0; kb <= C::NKB; ++kb) {
+          mbar_wait_cl(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = s_base + stage * KSB;
+          if (elect_one()) {
+            if (kb < C::NKB) {
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks)
+                tc_mma_f16_2cta(tmem_base + acc * NB, smem_desc(a0 + ks * 32, 8 * 128, 2),
+                                smem_desc(a0 + C::KS_A + ks * 32, 8 * 128, 2), IDESC,
+                                (kb > 0 || ks > 0) ? 1u : 0u);
+            } else {
+              tc_mma_f16_2cta(tmem_base + acc * NB, smem_desc(a0, 8 * kExtraRB, 6),
+                              smem_desc(a0 + kBM * kExtraRB, 8 * kExtraRB, 6), IDESC, 1u);
+              tc_commit_mc(&t_full[acc], 0x3);
+            }
+            tc_commit_mc(&empty[stage], 0x3);
+          }
+          __syncwarp();
+          if (++stage == nstage) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (++acc == NACC) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1 && C::KP) {
+    // ------------------- forwarder (CTA 1), K-pipelined: every stage landed
+    const uint32_t r_full = mapa_shared(smem_u32(full), 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t item = cid; item < n_items; item += ncl) {
+      const int c = (int)(item / n_qpairs);
+      TileSeqRT ts;
+      ts.begin(b_tiles, S, R, c, smode);
+      for (; ts.more(); ts.next()) {
+        for (int kb = 0; kb <= C::NKB; ++kb) {
+          mbar_wait_cl(&full[stage], phase);
+          if (lane == 0) mbar_arrive_cluster(r_full + stage * 8);
+          __syncwarp();
+          if (++stage == nstage) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 0) {
     // -------------------------------------------------------------- producer
     // (both CTAs: own query tile, own half of each reference tile)
     int stage = 0;
@@ -461,23 +572,32 @@ cudaError_t launch4(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
 // Measured on B200 (C2 d=32 / C3 d=64 shapes): the pair wins where the MMA is
 // long enough to cover the cross-SM release latency of the accumulators (d=64:
 // pass 1 130 vs 136 ms); at d <= 32 the single-SM kernel is faster (1.05 vs
-// 1.18 ms), so the pair is the default for dpad = 64 only.
+// 1.18 ms), so the pair is the default for dpad >= 64.
 int tc4_fits(int dpad, int parts) {
   if (parts != 4) return 0;
   switch (dpad) {
     case 16: return pick_stages4<16, 16, 256>() >= 3 && pick_stages4<16, 16, 160>() >= 3;
     case 32: return pick_stages4<32, 16, 256>() >= 3 && pick_stages4<32, 16, 160>() >= 3;
     case 64: return pick_stages4<64, 16, 256>() >= 3 && pick_stages4<64, 16, 160>() >= 3;
+    case 128: return pick_stages4<128, 16, 256>() >= 3;  // K-pipelined (256-column tiles only)
+    case 256: return pick_stages4<256, 16, 256>() >= 3;
+    case 512: return pick_stages4<512, 16, 256>() >= 3;
   }
   return 0;
 }
-int tc4_preferred(int dpad) { return dpad == 64; }
+// dpad > 64 (K-pipelined, measured at the C5 shape n = 5e5, d = 512, k = 50):
+// main kernel 236.8 -> 181.8 ms against the single-SM K-pipelined pass (the
+// per-SM operand stream per K region falls from 48 to 32 KB); d = 128 / 256 at
+// n = 2e5: 9.8 -> 7.5 / 17.2 -> 13.0 ms.
+int tc4_preferred(int dpad) { return dpad >= 64; }
 
 // MainPass.nb = 160: the three-accumulator ring (160-column tiles); else 256.
 template <int D, int FMT, int DBG, bool COL>
 cudaError_t launch4_nb(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                        bool self_join, const MainPass& m, int num_sms, cudaStream_t st) {
-  if (m.nb == 160) return launch4<D, FMT, DBG, 16, COL, 160, 3>(A, B, q_begin, q_count, self_join, m, num_sms, st);
+  if constexpr (D <= 64) {
+    if (m.nb == 160) return launch4<D, FMT, DBG, 16, COL, 160, 3>(A, B, q_begin, q_count, self_join, m, num_sms, st);
+  }
   return launch4<D, FMT, DBG, 16, COL, 256, 2>(A, B, q_begin, q_count, self_join, m, num_sms, st);
 }
 
@@ -505,6 +625,9 @@ cudaError_t launch_knn_tc4(const Image& A, const Image& B, int64_t q_begin, int6
     TOD_TC4_CASE(16)
     TOD_TC4_CASE(32)
     TOD_TC4_CASE(64)
+    TOD_TC4_CASE(128)
+    TOD_TC4_CASE(256)
+    TOD_TC4_CASE(512)
   }
 #undef TOD_TC4_CASE
   return cudaErrorInvalidValue;

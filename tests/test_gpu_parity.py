@@ -188,6 +188,20 @@ def test_pair_ring3_parity(pkg, n, d, k, fmt, col):
                                      "TOD_COLMODE": col}, main_kernel=4)
 
 
+@pytest.mark.parametrize("n,d,k,fmt,col", [
+    (12_000, 100, 12, "fp16", "0"),   # dpad 128, group candidates
+    (9_000, 200, 10, "fp16", "1"),    # dpad 256, column candidates
+    (9_000, 512, 20, "fp16", "1"),    # dpad 512 (C5 width)
+    (7_001, 512, 50, "fp16", "0"),    # dpad 512, k = 50, ragged n
+    (8_003, 128, 10, "bf16", "1"),    # bf16 (second tier)
+])
+def test_pair_kpipelined_parity(pkg, n, d, k, fmt, col):
+    # CTA-pair main pass, K-pipelined (dpad > 64): each SM streams its own A slice
+    # and half of each B slice per 64-wide K region (knn_tc4.cu KP mode)
+    _column_case(pkg, n, d, k, fmt, {"TOD_SAMPLE_V1": "0", "TOD_MAIN_PAIR": "1", "TOD_COLMODE": col},
+                 main_kernel=4)
+
+
 def _column_case(pkg, n, d, k, fmt, extra, main_kernel=None):
     # MainPass.colmode: the main pass appends each column below tau of a passing
     # group (the default for large n); forced on here at sizes the oracle checks
