@@ -59,6 +59,6 @@ def test_certificate_bound_on_product_kernel(pkg, d, fmt):
         pairs += w.numel()
         assert ratio <= 1.0, (name, fmt, d, ratio)
         # the kernel really is the production main pass
-        assert kern == (4 if d == 64 else 3)
+        assert kern == (4 if d >= 64 else 3)  # CTA pairs for dpad >= 64 (K-pipelined above 64)
     assert pairs >= 10_000_000
     print("dpad=%d %s: %d pairs, worst error / model = %.4f" % (K - 16, fmt, pairs, worst))

@@ -223,16 +223,21 @@ def _column_case(pkg, n, d, k, fmt, extra, main_kernel=None):
         assert res.stats["certified"] >= 0.99 * n, res.stats
 
 
+@pytest.mark.parametrize("pair", ["1", "0"])   # CTA-pair (default) / single-SM K-pipelined pass
 @pytest.mark.parametrize("n,d,k", [
     (3000, 200, 10),     # dpad 256, small n: two-pass forced (K-pipelined main pass)
     (12_000, 100, 12),   # dpad 128, K-pipelined two-pass
     (9000, 512, 20),     # dpad 512 (C5 width)
     (2000, 300, 50),     # C5's k
 ])
-def test_high_dimensional_parity(pkg, n, d, k):
+def test_high_dimensional_parity(pkg, n, d, k, pair):
     X = datagen.gaussian_mixture(n, d, seed=n + d)
-    with _ctx(pkg) as ctx:
-        res = ctx.knn(torch.from_numpy(X).cuda(), k)
+    os.environ["TOD_MAIN_PAIR"] = pair
+    try:
+        with _ctx(pkg) as ctx:
+            res = ctx.knn(torch.from_numpy(X).cuda(), k)
+    finally:
+        os.environ.pop("TOD_MAIN_PAIR", None)
     rows = np.arange(n) if n <= 3000 else np.random.default_rng(0).choice(n, 400, replace=False)
     _check_rows(res, X, k, np.sort(rows))
     assert res.stats["certified"] >= 0.95 * n, res.stats
