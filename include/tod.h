@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define TOD_ABI_VERSION 3
+#define TOD_ABI_VERSION 4
 
 /* Largest k (neighbours per row) this build serves; larger k -> TOD_E_UNSUPPORTED. */
 #define TOD_MAX_K 128
@@ -124,6 +124,8 @@ typedef struct {
                               (key-only pre-sample; the main-pass kernel over the sample tiles,
                               then over the others) */
   int32_t query_chunks;    /* query-row chunks the call was split into (workspace_bytes); 1 = none */
+  int64_t prebound_skipped;/* columns of visited groups the re-rank's per-column pre-bound excluded
+                              without their exact fp64 distance (ABI 4), summed over rows */
 } tod_stats;
 
 /* Per-neighbour and per-row outputs of the kNN functional operator (P:270,

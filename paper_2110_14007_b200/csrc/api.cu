@@ -326,6 +326,17 @@ tod_status prep_tc(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
   if (const char* e = getenv("TOD_GROUP_EMAX")) use_eg = atoi(e) != 0;
   cp->eg = use_eg ? static_cast<const double*>(p) : nullptr;
   cp->ecol = B.e;
+  // per-column pre-bound of the re-rank from the operand image (self-join):
+  // opt-in (TOD_RR_PREBOUND=1, experiment knob) -- it excludes 88-89 % of the
+  // visited groups' columns before their fp32 rows are gathered (C2: 169 of 192
+  // per row, C3: 267 of 299) but the extra dependent image read lengthens the
+  // latency-bound per-row chain: C2 re-rank 0.71 -> 1.00 ms, C3 20.9 -> 28.2 ms.
+  bool prebound = false;
+  if (const char* e = getenv("TOD_RR_PREBOUND")) prebound = self && atoi(e) != 0;
+  cp->bimg = prebound ? reinterpret_cast<const uint8_t*>(B.data) : nullptr;
+  cp->b_region = B.region_bytes();
+  cp->b_rb = B.rb;
+  cp->fmt = fmt;
   const float* qsrc = self ? dX + a_row0 * d : dQ;
   TOD_CUDA(launch_prep_quant(qsrc, a_rows, d, mu, g, fmt, A, 1, st, launches));
   cp->qa2 = A.a2 + (self ? q_begin - a_row0 : 0);
@@ -662,6 +673,7 @@ tod_status finish_rows(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ
     stats->cand_groups = (int64_t)h.counters[0];
     stats->visited_groups = (int64_t)h.counters[1];
     stats->cand_columns = (int64_t)h.counters[2];
+    stats->prebound_skipped = (int64_t)h.counters[3];
   }
   return TOD_OK;
 }
@@ -890,6 +902,7 @@ tod_status run_knn_auto(tod_ctx* ctx, const float* dX, int64_t n, const float* d
       acc.cand_groups += cs.cand_groups;
       acc.visited_groups += cs.visited_groups;
       acc.cand_columns += cs.cand_columns;
+      acc.prebound_skipped += cs.prebound_skipped;
       acc.max_abs_err = std::max(acc.max_abs_err, cs.max_abs_err);
     }
   }

@@ -126,7 +126,7 @@ struct SmallDev {
   int32_t fail_count;
   int32_t pad;
   double max_err;
-  unsigned long long counters[3];  // re-rank telemetry: staged groups, visited groups, kept columns
+  unsigned long long counters[4];  // re-rank telemetry: staged groups, visited groups, kept columns, pre-bound skips
 };
 
 // Reference-side prep shared by the query chunks of one call (automatic

@@ -152,6 +152,12 @@ struct CertParams {
   const double* ecol;    // per reference row: residual bound e_j (column candidates; nullable: eg/emax)
   int force_fail;        // TOD_F_NO_CERTIFY
   int colmode;           // two-pass candidates are single columns (MainPass.colmode), not 8-column groups
+  // The reference operand image (self-join, single process; nullable): the
+  // re-rank's per-column pre-bound reads xhat rows from it (DESIGN.md §5 "Re-rank").
+  const uint8_t* bimg;
+  size_t b_region;       // bytes per 64-element K region
+  int b_rb;              // bytes per row per region (128 / 64 / 32)
+  int fmt;               // 1 fp16, 2 bf16
 };
 struct KnnOutDev {
   int64_t* idx;

@@ -20,6 +20,8 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include <cuda_fp16.h>
+
 #include "internal.h"
 
 namespace tod {
@@ -529,9 +531,111 @@ __device__ __forceinline__ double d64_fixed(const double* __restrict__ xq, const
   return acc;
 }
 
+// ---- per-column pre-bound (DESIGN.md §5 "Re-rank"): before the exact O1 of a
+// visited group's column j, a lower bound on its D64 from the 16-bit operand
+// image alone -- R^ = ||xhat_i - xhat_j|| with both rows read from the image the
+// tensor core multiplied (half the bytes of the fp32 row), then the residuals
+// e_i, e_j, the scale and the oracle's own rounding exactly as in lb2_from_key.
+// It drops the group bound's accumulation term E_i and uses the column's own
+// distance instead of its group's minimum, so most columns of a visited group
+// are excluded without gathering their fp32 rows.  Only a VALID lower bound is
+// needed: a column is skipped iff the bound exceeds UB >= the k-th distance.
+template <int FMT>
+__device__ __forceinline__ float widen_img(uint32_t h) {
+  if constexpr (FMT == 2) return __uint_as_float(h << 16);  // bf16: exact
+  else return __half2float(__ushort_as_half((unsigned short)h));
+}
+// The 16-bit value of element c of image row r (swizzled K-major layout, prep.cu).
+__device__ __forceinline__ uint32_t img_elem(const CertParams& cp, int64_t r, int c) {
+  const int epr = cp.b_rb / 2;
+  const uint32_t M = (uint32_t)(cp.b_rb / 16 - 1);
+  const uint64_t o = (uint64_t)r * cp.b_rb + (uint64_t)(c % epr) * 2u;
+  const uint64_t phys = o ^ (((o >> 7) & M) << 4);
+  return *reinterpret_cast<const uint16_t*>(cp.bimg + (size_t)(c / epr) * cp.b_region + phys);
+}
+// The fp32 sum of (q - y)^2 over one image row, DP (= dpad) a compile-time
+// constant: every 16-byte chunk load in flight at once, four independent partial
+// sums (the bound below holds for any summation order of nonnegative terms).
+template <int FMT, int DP>
+__device__ __forceinline__ float img_dist2(const CertParams& cp, const float* qh, int64_t j) {
+  constexpr int RB = DP * 2 < 128 ? DP * 2 : 128;
+  constexpr int NREG = DP * 2 / RB;
+  constexpr int CPR = RB / 16;
+  const uint32_t x = (uint32_t)(((uint64_t)j * RB >> 7) & (uint64_t)(CPR - 1));
+  uint4 v[NREG * CPR];
+#pragma unroll
+  for (int kb = 0; kb < NREG; ++kb) {
+    const uint4* row = reinterpret_cast<const uint4*>(cp.bimg + (size_t)kb * cp.b_region +
+                                                      (size_t)j * RB);
+#pragma unroll
+    for (int k = 0; k < CPR; ++k) v[kb * CPR + k] = __ldg(row + (k ^ x));
+  }
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int k = 0; k < NREG * CPR; ++k) {
+    const uint32_t w4[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float d0 = qh[8 * k + 2 * t] - widen_img<FMT>(w4[t] & 0xFFFFu);
+      const float d1 = qh[8 * k + 2 * t + 1] - widen_img<FMT>(w4[t] >> 16);
+      a[t] = fmaf(d0, d0, a[t]);
+      a[t] = fmaf(d1, d1, a[t]);
+    }
+  }
+  return (a[0] + a[1]) + (a[2] + a[3]);
+}
+
+// Lower bound on D64(i, j) in original units (<= 0: none).  qh = xhat_i in fp32
+// (shared), ei = e_i.  fp32 sum of dpad terms fl(fl(q - y)^2 + acc), all >= 0:
+// acc <= Rhat^2 (1 + u)^2 (1 + gamma_dpad) <= Rhat^2 (1 + gamma_{dpad+3}) (+ underflow).
+template <int FMT, int DP = 0>
+__device__ __forceinline__ double lb2_col(const CertParams& cp, const float* qh, int64_t j,
+                                          double ei) {
+  const double u53 = 1.1102230246251565e-16;
+  if constexpr (DP > 0) {
+    const float acc = img_dist2<FMT, DP>(cp, qh, j);
+    const double D = (double)acc / (1.0 + gamma_up(DP + 3, 5.9604644775390625e-08)) -
+                     (DP + 3) * 1.1754943508222875e-38 /*2^-126*/;
+    if (!(D > 0.0)) return -1.0;
+    const double R = sqrt(D) * (1.0 - 2.0 * u53);
+    const double LB = (R - ei - cp.ecol[j]) * (1.0 - 8.0 * u53);
+    if (!(LB > 0.0)) return -1.0;
+    const double lbo = LB / cp.g->s;  // s = 2^e: exact
+    return lbo * lbo * (1.0 - 8.0 * u53) * (1.0 - gamma_up(cp.d + 2, u53));
+  }
+  const int nreg = cp.dpad * 2 / cp.b_rb;
+  const int cpr = cp.b_rb / 16;  // 16-byte chunks per row per region
+  const uint32_t x = (uint32_t)(((uint64_t)j * cp.b_rb >> 7) & (uint64_t)(cpr - 1));
+  float acc = 0.f;
+  for (int kb = 0; kb < nreg; ++kb) {
+    const uint4* row = reinterpret_cast<const uint4*>(cp.bimg + (size_t)kb * cp.b_region +
+                                                      (size_t)j * cp.b_rb);
+    const float* q = qh + kb * (cp.b_rb / 2);
+    for (int k = 0; k < cpr; ++k) {
+      const uint4 v = __ldg(row + (k ^ x));
+      const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float d0 = q[8 * k + 2 * t] - widen_img<FMT>(w4[t] & 0xFFFFu);
+        const float d1 = q[8 * k + 2 * t + 1] - widen_img<FMT>(w4[t] >> 16);
+        acc = fmaf(d0, d0, acc);
+        acc = fmaf(d1, d1, acc);
+      }
+    }
+  }
+  const double D = (double)acc / (1.0 + gamma_up(cp.dpad + 3, 5.9604644775390625e-08)) -
+                   (cp.dpad + 3) * 1.1754943508222875e-38 /*2^-126*/;
+  if (!(D > 0.0)) return -1.0;
+  const double R = sqrt(D) * (1.0 - 2.0 * u53);
+  const double LB = (R - ei - cp.ecol[j]) * (1.0 - 8.0 * u53);
+  if (!(LB > 0.0)) return -1.0;
+  const double lbo = LB / cp.g->s;  // s = 2^e: exact
+  return lbo * lbo * (1.0 - 8.0 * u53) * (1.0 - gamma_up(cp.d + 2, u53));
+}
+
 // Per-warp telemetry (one global atomic per warp at exit, not per row).
 struct RowTel {
-  unsigned long long G = 0, nv = 0, nc = 0;
+  unsigned long long G = 0, nv = 0, nc = 0, pre = 0;  // pre: columns the pre-bound excluded
   double maxerr = 0.0;
 };
 
@@ -551,12 +655,18 @@ __device__ __forceinline__ void rerank_groups_row(
   __shared__ int s_ci[kGrpWarps][kColMax];        //                    index
   __shared__ double s_tk[kGrpWarps][kMaxK];       // selected top-k
   __shared__ int s_ti[kGrpWarps][kMaxK];
+  __shared__ float s_qh[kGrpWarps][256];          // query row xhat (pre-bound; dpad <= 256)
   extern __shared__ double s_xq[];                // [warps][d] query row in fp64
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t gi = q_begin + r;
   const float* xi = self_join ? X + gi * d : Q + r * d;
   double* xq = s_xq + (size_t)w * d;
   for (int c = lane; c < d; c += 32) xq[c] = (double)xi[c];
+  const bool pre = cp.bimg != nullptr && self_join && cp.dpad <= 256;
+  float* qh = s_qh[w];
+  if (pre)
+    for (int c = lane; c < cp.dpad; c += 32)
+      qh[c] = cp.fmt == 2 ? widen_img<2>(img_elem(cp, gi, c)) : widen_img<1>(img_elem(cp, gi, c));
 
   float* gk = s_gk[w];
   int* gid = s_gi[w];
@@ -650,7 +760,20 @@ __device__ __forceinline__ void rerank_groups_row(
       j = g;
     }
     double key = CUDART_INF;
-    if (g >= 0 && j < n && !(self_join && j == gi)) {
+    bool live = g >= 0 && j < n && !(self_join && j == gi);
+    if (pre && st < gsteps) {
+      bool skip = false;
+      if (live) {
+        // d = dpad in {16, 32, 64} (DT > 0): the unrolled image read
+        constexpr int DP = DT <= 64 ? DT : 0;
+        const double lbc = cp.fmt == 2 ? lb2_col<2, DP>(cp, qh, j, cp.qe[r])
+                                       : lb2_col<1, DP>(cp, qh, j, cp.qe[r]);
+        skip = lbc > UB;  // provably not within the k nearest: no fp32 row gather, no O1
+      }
+      tel.pre += (unsigned long long)__popc(__ballot_sync(0xffffffffu, skip));
+      live = live && !skip;
+    }
+    if (live) {
       const float* xj = X + j * d;
       double acc = 0.0;  // O1, bit-identical to the oracle (no FMA, ascending c)
       if constexpr (DT > 0) {
@@ -826,6 +949,7 @@ __global__ void __launch_bounds__(kGrpWarps * 32, 4)
     if (tel.G) atomicAdd(counters + 0, tel.G);
     if (tel.nv) atomicAdd(counters + 1, tel.nv);
     if (tel.nc) atomicAdd(counters + 2, tel.nc);
+    if (tel.pre) atomicAdd(counters + 3, tel.pre);
   }
 }
 

@@ -57,7 +57,7 @@ class Stats(ctypes.Structure):
                 ("cand_groups", ctypes.c_int64), ("visited_groups", ctypes.c_int64),
                 ("cand_columns", ctypes.c_int64), ("ms_main_kernel", ctypes.c_float),
                 ("main_kernel", ctypes.c_int32), ("sample_pass", ctypes.c_int32),
-                ("query_chunks", ctypes.c_int32)]
+                ("query_chunks", ctypes.c_int32), ("prebound_skipped", ctypes.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -72,7 +72,7 @@ class KnnOut(ctypes.Structure):
 _lib = None
 
 
-ABI_VERSION = 3  # include/tod.h TOD_ABI_VERSION
+ABI_VERSION = 4  # include/tod.h TOD_ABI_VERSION
 
 
 def load_library(path: str = LIB_PATH):

@@ -223,6 +223,27 @@ def _column_case(pkg, n, d, k, fmt, extra, main_kernel=None):
         assert res.stats["certified"] >= 0.99 * n, res.stats
 
 
+@pytest.mark.parametrize("n,d,k,fmt", [
+    (20_000, 32, 20, "fp16"),
+    (20_000, 64, 10, "bf16"),
+    (7_777, 16, 8, "fp16"),
+    (9_000, 128, 10, "fp16"),    # generic (runtime-dpad) image read
+])
+def test_rerank_prebound_parity(pkg, n, d, k, fmt):
+    # the re-rank's per-column pre-bound from the operand image (opt-in): the
+    # columns it excludes must not change a single output
+    X = datagen.gaussian_mixture(n, d, seed=n + 3 * d)
+    os.environ["TOD_RR_PREBOUND"] = "1"
+    try:
+        with _ctx(pkg, fmt=fmt) as ctx:
+            res = ctx.knn(torch.from_numpy(X).cuda(), k)
+    finally:
+        os.environ.pop("TOD_RR_PREBOUND", None)
+    assert res.stats["prebound_skipped"] > 0, res.stats
+    rows = np.arange(n) if n <= 20_000 and d <= 64 else np.random.default_rng(2).choice(n, 500, replace=False)
+    _check_rows(res, X, k, np.sort(rows))
+
+
 @pytest.mark.parametrize("pair", ["1", "0"])   # CTA-pair (default) / single-SM K-pipelined pass
 @pytest.mark.parametrize("n,d,k", [
     (3000, 200, 10),     # dpad 256, small n: two-pass forced (K-pipelined main pass)

@@ -26,6 +26,7 @@ with T.Context(fmt=a.fmt, flags=T.F_TIMING) as ctx:
     st = r.stats
     n = max(st["rows"], 1)
     print("%s: main %.3f (kernel %.3f, K%d) cert %.3f fb %.3f ms | per row: staged %.1f visited %.1f "
-          "kept %.1f | certified %d/%d" % (os.path.basename(a.lib), st["ms_main"],
+          "kept %.1f pre-skipped %.1f | certified %d/%d" % (os.path.basename(a.lib), st["ms_main"],
           st.get("ms_main_kernel", 0), st.get("main_kernel", 0), st["ms_certify"], st["ms_fallback"],
-          st["cand_groups"] / n, st["visited_groups"] / n, st["cand_columns"] / n, st["certified"], n))
+          st["cand_groups"] / n, st["visited_groups"] / n, st["cand_columns"] / n,
+          st.get("prebound_skipped", 0) / n, st["certified"], n))
