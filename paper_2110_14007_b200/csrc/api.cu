@@ -447,8 +447,21 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
       const int nv = sm.parts * sm.samp_t;
       TOD_TRY(ensure(ctx, B_SAMP, (size_t)std::max<int64_t>(q_count, 1) * nv * 4, &p));
       sm.samp = static_cast<float*>(p);
-      TOD_CUDA(launch_knn_tc3(A, B, self ? q_begin : 0, q_count, self, plan.fmt, sm, ctx->num_sms,
-                              0, st, launches));
+      sm.tau_lists = 0;  // no thresholds in the sample pass
+      // dpad > 64 on CTA pairs: the K-pipelined pair kernel's key-only sample mode
+      // sweeps the same sample tiles (smode 1); else knn_tc3's sample mode
+      const char* sp = getenv("TOD_SAMPLE_PAIR");  // experiment knob 1 / 0
+      const bool samp4 = use4 && plan.dpad > 64 && (cands.dbg & 7) == 0 && !three &&
+                         (sp ? atoi(sp) != 0 : true);
+      if (samp4) {
+        sm.smode = 1;
+        sm.nb = 256;
+        TOD_CUDA(launch_knn_tc4(A, B, self ? q_begin : 0, q_count, self, plan.fmt, sm,
+                                ctx->num_sms, 0, st, launches));
+      } else {
+        TOD_CUDA(launch_knn_tc3(A, B, self ? q_begin : 0, q_count, self, plan.fmt, sm,
+                                ctx->num_sms, 0, st, launches));
+      }
       TOD_CUDA(launch_tau_combine(q_count, nv, std::min(nv, ja), sm.samp, cands.v, st, launches));
       cands.lists = 1;
       cands.kp = 0;

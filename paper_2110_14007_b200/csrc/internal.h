@@ -103,7 +103,7 @@ struct MainPass {
   int* cnt = nullptr;         // [q_count][parts] appended counts (may exceed cap = overflow)
   int cap = 0;
   int parts = 2;              // column parts per tile (one buffer per (row, part))
-  float* samp = nullptr;      // sample mode (knn_tc3 only): [q_count][parts][samp_t] smallest
+  float* samp = nullptr;      // sample mode (knn_tc3; knn_tc4 K-pipelined with smode 1): [q_count][parts][samp_t] smallest
                               // group minima over the sample tiles t = 0, R, 2R, ... (no appends)
   int samp_t = 4;             // 4 or 8
   int samp_acc = 0;           // sample mode: merge into the minima already in samp (ring of blocks)

@@ -110,7 +110,11 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float* v) {
   }
 }
 
-template <int DPAD, int FMT, int DBG, int FW, bool COL, int NB, int NACC>
+// SMP (4 or 8; K-pipelined pairs, dpad > 64): the key-only SAMPLE pass -- no
+// appends; each filter lane keeps the SMP smallest group minima of its (row,
+// part) over the tiles of the sweep (smode 1: the sample tiles) and writes them
+// to samp (knn_tc3.cu's sample mode on CTA pairs).
+template <int DPAD, int FMT, int DBG, int FW, bool COL, int NB, int NACC, int SMP = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
     k_knn_tc4(const uint8_t* __restrict__ a_img, size_t a_region, size_t a_extra,
               const uint8_t* __restrict__ b_img, size_t b_region, size_t b_extra, int64_t b_tiles,
@@ -118,7 +122,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
               int self_join, int S, int R, int nstage,
               const float* __restrict__ tau_v, int tau_lists,
               uint2* __restrict__ mbuf, int* __restrict__ mcnt, int cap, int64_t col0, int vote,
-              int smode, long long* __restrict__ trace) {
+              int smode, long long* __restrict__ trace, float* __restrict__ samp) {
   // trace (profiling, TOD_F_DEBUG_TRACE): the leader CTA of cluster 0, per tile,
   // the 16 clock64 stamps of knn_tc3.cu (tools/trace_main.py)
   constexpr int kTraceTiles = 2048;
@@ -464,6 +468,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
         }
         pa = pbase;
       };
+      constexpr int T = SMP > 0 ? SMP : 1;
+      float top[T];
+#pragma unroll
+      for (int i = 0; i < T; ++i) top[i] = CUDART_INF_F;
       TileSeqRT ts;
       ts.begin(b_tiles, S, R, c, smode);
       for (; ts.more(); ts.next()) {
@@ -516,6 +524,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
           for (int e = 0; e < BH; ++e)
             v[e] = (j0 + e == selfc || j0 + e >= n_ref) ? CUDART_INF_F : v[e];
         }
+        if constexpr (SMP > 0) {
+          // branch-free insertion of the part's group minima (new_i = min(r_i, max(r_i-1, x)))
+#pragma unroll
+          for (int g = 0; g < BH / 8; ++g) {
+            const float x = min8(v + 8 * g);
+#pragma unroll
+            for (int i = T - 1; i > 0; --i) top[i] = fminf(top[i], fmaxf(top[i - 1], x));
+            top[0] = fminf(top[0], x);
+          }
+          continue;
+        }
         auto reload = [=](int gg, float* c8) {
           tmem_ld8(taddr + 8 * gg, c8);
           tmem_ld_wait();
@@ -531,7 +550,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
                              release);  // col0 % 256 == 0
         if (tr) trace[(etr - 1) * 16 + 6] = clock64();
       }
-      flush();
+      if constexpr (SMP > 0) {
+        if (valid) {
+#pragma unroll
+          for (int i = 0; i < T; ++i) samp[(r * H + h) * T + i] = top[i];
+        }
+      } else {
+        flush();
+      }
     }
   }
   tc_fence_before();
@@ -542,7 +568,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + 32 * FW, 1)
   }
 }
 
-template <int DPAD, int FMT, int DBG, int FW, bool COL, int NB, int NACC>
+template <int DPAD, int FMT, int DBG, int FW, bool COL, int NB, int NACC, int SMP = 0>
 cudaError_t launch4(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                     bool self_join, const MainPass& m, int num_sms, cudaStream_t st) {
   const int nstage = pick_stages4<DPAD, FW, NB>();
@@ -550,7 +576,7 @@ cudaError_t launch4(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
   if (m.parts != FW / 4) return cudaErrorInvalidValue;
   int a, b, c;
   const int smem = smem4<DPAD, FW, NB>(nstage, &a, &b, &c);
-  auto kern = k_knn_tc4<DPAD, FMT, DBG, FW, COL, NB, NACC>;
+  auto kern = k_knn_tc4<DPAD, FMT, DBG, FW, COL, NB, NACC, SMP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t qt0 = q_begin / kBM;
@@ -563,7 +589,8 @@ cudaError_t launch4(const Image& A, const Image& B, int64_t q_begin, int64_t q_c
       reinterpret_cast<const uint8_t*>(A.data), A.region_bytes(), A.extra_offset(),
       reinterpret_cast<const uint8_t*>(B.data), B.region_bytes(), B.extra_offset(),
       (B.n + NB - 1) / NB, B.n, qt0, n_qpairs, q_begin, q_begin + q_count, self_join ? 1 : 0, m.S,
-      m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap, m.col0, m.vote, m.smode, m.trace);
+      m.R, nstage, m.tau_v, m.tau_lists, m.buf, m.cnt, m.cap, m.col0, m.vote, m.smode, m.trace,
+      m.samp);
   return cudaGetLastError();
 }
 
@@ -595,6 +622,15 @@ int tc4_preferred(int dpad) { return dpad >= 64; }
 template <int D, int FMT, int DBG, bool COL>
 cudaError_t launch4_nb(const Image& A, const Image& B, int64_t q_begin, int64_t q_count,
                        bool self_join, const MainPass& m, int num_sms, cudaStream_t st) {
+  if constexpr (D > 64 && DBG == 0 && !COL) {
+    if (m.samp) {  // key-only sample pass (smode 1), K-pipelined pairs
+      if (m.samp_acc || m.smode != 1) return cudaErrorInvalidValue;
+      return m.samp_t == 8
+                 ? launch4<D, FMT, 0, 16, false, 256, 2, 8>(A, B, q_begin, q_count, self_join, m, num_sms, st)
+                 : launch4<D, FMT, 0, 16, false, 256, 2, 4>(A, B, q_begin, q_count, self_join, m, num_sms, st);
+    }
+  }
+  if (m.samp) return cudaErrorInvalidValue;
   if constexpr (D <= 64) {
     if (m.nb == 160) return launch4<D, FMT, DBG, 16, COL, 160, 3>(A, B, q_begin, q_count, self_join, m, num_sms, st);
   }
