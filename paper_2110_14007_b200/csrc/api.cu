@@ -427,8 +427,13 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
                       tc4_fits(plan.dpad, tc3_parts(plan.dpad));
     const char* sv = getenv("TOD_SAMPLE_V1");
     const char* s3 = getenv("TOD_SAMPLE3");
-    const bool three = plan.two && use4 && (cands.dbg & 7) == 0 && !sv &&
-                       (s3 ? atoi(s3) != 0 : plan.dpad == 64);
+    // three-stage: d = 64 on CTA pairs; d <= 32 on the single-SM kernel from
+    // n = 3e5 (measured n = 1e6, d = 32: pass 1 103.0 -> 93.3 ms; at C2, n = 1e5,
+    // neutral: 1.355 vs 1.359 ms)
+    const bool three = plan.two && (cands.dbg & 7) == 0 && !sv &&
+                       ((use4 && (s3 ? atoi(s3) != 0 : plan.dpad == 64)) ||
+                        (!use4 && plan.dpad <= 32 && tc3_parts(plan.dpad) == 4 &&
+                         (s3 ? atoi(s3) != 0 : n >= 300000)));
     const bool samp_v1 = plan.two && !three && plan.dpad <= 128 &&
                          (sv ? atoi(sv) != 0 : plan.dpad == 64);
     if (plan.two) sample_pass = samp_v1 ? 1 : (three ? 3 : 2);
@@ -490,8 +495,12 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
         // stage 2: the sample tiles below tau0, appended; tau = their j-th smallest key
         MainPass mb = mp;
         mb.trace = nullptr;  // the profiling trace records the main sweep (stage 4)
-        TOD_CUDA(launch_knn_tc4(A, B, self ? q_begin : 0, q_count, self, plan.fmt, mb,
-                                ctx->num_sms, 0, st, launches));
+        if (use4)
+          TOD_CUDA(launch_knn_tc4(A, B, self ? q_begin : 0, q_count, self, plan.fmt, mb,
+                                  ctx->num_sms, 0, st, launches));
+        else
+          TOD_CUDA(launch_knn_tc3(A, B, self ? q_begin : 0, q_count, self, plan.fmt, mb,
+                                  ctx->num_sms, 0, st, launches));
         TOD_CUDA(launch_tau_from_appends(q_count, mp.parts, mp.cap, mp.cnt, mp.buf, jw, cands.v,
                                          st, launches));
         mp.smode = 0;

@@ -94,7 +94,8 @@ int pick_stages3() {
 }
 
 // MODE: 0 = main pass over every tile, 1 = main pass skipping the sample tiles
-// (t % R == 0), 4 / 8 = sample pass keeping that many minima per (row, part).
+// (t % R == 0), 2 = main pass over only the sample tiles, 4 / 8 = sample pass
+// keeping that many minima per (row, part).
 template <int DPAD, int FMT, int DBG, int FW, int MODE, bool COL>
 __global__ void __launch_bounds__(64 + 32 * FW, 1)
     k_knn_tc3(const uint8_t* __restrict__ a_img, size_t a_region, size_t a_extra,
@@ -116,6 +117,9 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
   using C = Cfg3<DPAD>;
   constexpr int SMP = MODE >= 4 ? MODE : 0;
   constexpr int SKIP = MODE == 1 ? 1 : 0;
+  // MODE 2: the main pass (appends) over ONLY the sample tiles t % R == 0
+  // (stage 2 of the three-stage selection)
+  constexpr int WALK = (SMP > 0 || MODE == 2) ? 1 : 0;
   constexpr int H = FW / 4;        // column parts per tile
   constexpr int BH = kBN / H;      // columns per filter warp per tile
   extern __shared__ uint8_t smem_raw[];
@@ -164,7 +168,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t qtl = item % n_qtiles;
       const int c = (int)(item / n_qtiles);
-      TileSeq<SMP, SKIP> ts;
+      TileSeq<WALK, SKIP> ts;
       ts.begin(b_tiles, S, R, c);
       for (; ts.more(); ts.next()) {
         const int64_t t = ts.t;
@@ -201,7 +205,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
     uint32_t phase = 0, acc_phase = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int c = (int)(item / n_qtiles);
-      TileSeq<SMP, SKIP> ts;
+      TileSeq<WALK, SKIP> ts;
       ts.begin(b_tiles, S, R, c);
       for (; ts.more(); ts.next()) {
         mbar_wait(&t_empty[acc], acc_phase ^ 1);
@@ -243,7 +247,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int64_t qtl = item % n_qtiles;
       const int c = (int)(item / n_qtiles);
-      TileSeq<SMP, SKIP> ts;
+      TileSeq<WALK, SKIP> ts;
       ts.begin(b_tiles, S, R, c);
       int issued = 0;
       bool a_done = false;
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
     int mtr = 0;
     for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int c = (int)(item / n_qtiles);
-      TileSeq<SMP, SKIP> ts;
+      TileSeq<WALK, SKIP> ts;
       ts.begin(b_tiles, S, R, c);
       mbar_wait(a_full, aphase);
       aphase ^= 1;
@@ -396,7 +400,7 @@ __global__ void __launch_bounds__(64 + 32 * FW, 1)
 #pragma unroll
       for (int i = 0; i < T; ++i)  // a ring of blocks accumulates over launches
         top[i] = (SMP && samp_acc && valid) ? samp[(r * H + h) * T + i] : CUDART_INF_F;
-      TileSeq<SMP, SKIP> ts;
+      TileSeq<WALK, SKIP> ts;
       ts.begin(b_tiles, S, R, c);
       for (; ts.more(); ts.next()) {
         const uint32_t acc = tcount & 1u;
@@ -627,6 +631,12 @@ cudaError_t launch_knn_tc3(const Image& A, const Image& B, int64_t q_begin, int6
   if (m.samp)                                                                                     \
     return fmt == 1 ? launch3<D, 1, 0, FW, 4>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
                     : launch3<D, 2, 0, FW, 4>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+  if (m.smode) {  /* three-stage, stage 2 (d <= 32 on the single-SM kernel) */                   \
+    if constexpr (D <= 32 && FW == 16)                                                           \
+      return fmt == 1 ? launch3<D, 1, 0, FW, 2>(A, B, q_begin, q_count, self_join, m, num_sms, st) \
+                      : launch3<D, 2, 0, FW, 2>(A, B, q_begin, q_count, self_join, m, num_sms, st); \
+    return cudaErrorInvalidValue;                                                                \
+  }                                                                                               \
   if (dbg & 4)                                                                                    \
     return fmt == 1 ? launch3<D, 1, 4, FW, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st)  \
                     : launch3<D, 2, 4, FW, 0>(A, B, q_begin, q_count, self_join, m, num_sms, st); \

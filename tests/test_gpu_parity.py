@@ -158,18 +158,26 @@ def test_column_candidates_parity(pkg, n, d, k, fmt, v1, pair):
     _column_case(pkg, n, d, k, fmt, {"TOD_SAMPLE_V1": v1, "TOD_MAIN_PAIR": pair})
 
 
-@pytest.mark.parametrize("n,d,k,fmt", [
-    (20_000, 64, 10, "fp16"),
-    (12_345, 64, 10, "bf16"),     # ragged tail, second tier
-    (17_001, 64, 20, "fp16"),
+@pytest.mark.parametrize("n,d,k,fmt,kern", [
+    (20_000, 64, 10, "fp16", 4),
+    (12_345, 64, 10, "bf16", 4),     # ragged tail, second tier
+    (17_001, 64, 20, "fp16", 4),
+    (20_000, 32, 20, "fp16", 3),     # d <= 32: the single-SM kernel's MODE 2 / MODE 1 sweeps
+    (12_345, 32, 10, "bf16", 3),
+    (9_001, 16, 8, "fp16", 3),
 ])
-def test_three_stage_selection_parity(pkg, n, d, k, fmt):
-    # the default at d = 64: key-only pre-sample (every 64th tile) -> the CTA-pair
-    # main pass over the sample tiles below tau0 -> tau -> the main pass over the rest
+def test_three_stage_selection_parity(pkg, n, d, k, fmt, kern):
+    # the default at d = 64 (and d <= 32 from n = 3e5; forced here): key-only
+    # pre-sample (every 64th tile) -> the main pass over the sample tiles below
+    # tau0 -> tau -> the main pass over the rest
     X = datagen.gaussian_mixture(n, d, seed=n + 11 * d)
-    with _ctx(pkg, fmt=fmt) as ctx:
-        res = ctx.knn(torch.from_numpy(X).cuda(), k)
-    assert res.stats["sample_pass"] == 3 and res.stats["main_kernel"] == 4, res.stats
+    os.environ["TOD_SAMPLE3"] = "1"
+    try:
+        with _ctx(pkg, fmt=fmt) as ctx:
+            res = ctx.knn(torch.from_numpy(X).cuda(), k)
+    finally:
+        os.environ.pop("TOD_SAMPLE3", None)
+    assert res.stats["sample_pass"] == 3 and res.stats["main_kernel"] == kern, res.stats
     _check_rows(res, X, k, np.arange(n))
     if fmt == "fp16":
         assert res.stats["certified"] >= 0.99 * n, res.stats
