@@ -430,8 +430,11 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
     // three-stage: d = 64 on CTA pairs; d <= 32 on the single-SM kernel from
     // n = 3e5 (measured n = 1e6, d = 32: pass 1 103.0 -> 93.3 ms; at C2, n = 1e5,
     // neutral: 1.355 vs 1.359 ms)
+    // dpad > 64 (K-pipelined pairs) also from n = 3e5 (C5 shape n = 5e5: pass 1
+    // 204 -> 187 ms; at n = 2000 the 1/64 pre-sample is too sparse: 71 % certified)
     const bool three = plan.two && (cands.dbg & 7) == 0 && !sv &&
-                       ((use4 && (s3 ? atoi(s3) != 0 : plan.dpad == 64)) ||
+                       ((use4 && (s3 ? atoi(s3) != 0
+                                     : (plan.dpad == 64 || (plan.dpad > 64 && n >= 300000)))) ||
                         (!use4 && plan.dpad <= 32 && tc3_parts(plan.dpad) == 4 &&
                          (s3 ? atoi(s3) != 0 : n >= 300000)));
     const bool samp_v1 = plan.two && !three && plan.dpad <= 128 &&
@@ -456,7 +459,7 @@ tod_status run_knn(tod_ctx* ctx, const float* dX, int64_t n, const float* dQ, in
       // dpad > 64 on CTA pairs: the K-pipelined pair kernel's key-only sample mode
       // sweeps the same sample tiles (smode 1); else knn_tc3's sample mode
       const char* sp = getenv("TOD_SAMPLE_PAIR");  // experiment knob 1 / 0
-      const bool samp4 = use4 && plan.dpad > 64 && (cands.dbg & 7) == 0 && !three &&
+      const bool samp4 = use4 && plan.dpad > 64 && (cands.dbg & 7) == 0 &&
                          (sp ? atoi(sp) != 0 : true);
       if (samp4) {
         sm.smode = 1;
