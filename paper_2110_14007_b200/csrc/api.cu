@@ -138,6 +138,7 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
       const int64_t want = (ctx->num_sms + units - 1) / units;
       if (want > p->main_S) p->main_S = (int)std::min<int64_t>(want, std::max<int64_t>(1, bt256 / 4));
     }
+    if (const char* e = getenv("TOD_MAIN_S")) p->main_S = std::max(1, atoi(e));  // experiment knob
     p->cap = roundup(std::max(64, 2 * (p->R - 1) * kps), 32);
     bt_v1 = (bt256 + p->R - 1) / p->R;
   }
