@@ -138,6 +138,23 @@ tod_status make_plan(tod_ctx* ctx, int64_t n_ref, int64_t q_count, int d, int k,
       const int64_t want = (ctx->num_sms + units - 1) / units;
       if (want > p->main_S) p->main_S = (int)std::min<int64_t>(want, std::max<int64_t>(1, bt256 / 4));
     }
+    {
+      // fill the last wave of the persistent grid: items = query tiles x S are
+      // dealt round-robin, so the makespan is ceil(items / grid) items of bt/S
+      // tiles; take the S in [S, S + 7] (>= 4 tiles per item) minimising
+      // ceil(Q S / G) / S.  C2 (782 query tiles on 148 SMs, last wave 42/148 at
+      // S = 1): S = 7, main kernel 1.180 -> 1.025 ms (tools/r02_s7.sh).
+      const int64_t Q = (q_count + 127) / 128, G = std::max(1, ctx->num_sms);
+      const int s0 = p->main_S;
+      double best = 1e300;
+      for (int s = s0; s <= s0 + 7 && (s == s0 || s <= bt256 / 4); ++s) {
+        const double v = (double)((Q * s + G - 1) / G) / s;
+        if (v < best - 1e-9) {
+          best = v;
+          p->main_S = s;
+        }
+      }
+    }
     if (const char* e = getenv("TOD_MAIN_S")) p->main_S = std::max(1, atoi(e));  // experiment knob
     p->cap = roundup(std::max(64, 2 * (p->R - 1) * kps), 32);
     bt_v1 = (bt256 + p->R - 1) / p->R;
